@@ -1,0 +1,175 @@
+/*
+ * jkcals.h — C ABI of the B200-native JK-CALS hot path.
+ *
+ * JK-CALS (Psarras, Karlsson, Bro, Bientinesi, "Accelerating jackknife resampling for the
+ * Canonical Polyadic Decomposition", arXiv 2112.03985), Alg. 3: all
+ * leave-one-out (LOO) CP submodels of a dense tensor T are fitted concurrently by ALS
+ * against the SAME full tensor. Submodel p's mode-0 factor carries a zero row at index p
+ * (Alg. 3 alg:cals_jk:multifactor0; §4.1 Case II), so one
+ * fused MTTKRP per mode (alg:cals_jk:mttkrp) serves every submodel; it is
+ * followed per submodel by the Hadamard of Gramians (alg:cals_jk:hadamard),
+ * the update U = M H^{-1} (alg:cals_jk:update), the re-zeroing of row p when
+ * n = 0 (alg:cals_jk:multifactor), and the submodel error with ||T_-p||^2
+ * (alg:cals_jk:error).
+ *
+ * Conventions
+ *   - 0-based indices; the sampled mode is mode 0 ("The samples are in the first mode",
+ *     PAPER.md:499). Submodel p leaves out slice p of mode 0.
+ *   - Tensors are dense FP64, generalised column-major (first index fastest), i.e. the
+ *     element (i_0..i_{N-1}) is at sum_k i_k prod_{m<k} I_m (Eq. 3).
+ *   - Host factor matrices crossing this ABI are column-major, rows x rank.
+ *   - Per-iteration semantics: after each update the
+ *     columns are normalised to unit 2-norm (lambda kept); Cholesky solve with a Jacobi
+ *     pseudoinverse fallback; error e = ||T_-p||^2 + sum(H .* V^T V) - 2 sum(V .* M)
+ *     (Alg. 3 error line with its sign corrected); fit = 1 - sqrt(max(e,0))/||T_-p||;
+ *     with tol > 0 a submodel stops once |fit - fit_prev| < tol (from its 2nd sweep).
+ *
+ * Ownership and threading
+ *   - Host inputs are only read during the call; host outputs are caller buffers.
+ *   - The caller owns the device WORKSPACE (e.g. a torch uint8 tensor) and the CUDA stream;
+ *     the tensor is copied into the workspace at create. destroy() frees only host state,
+ *     CUDA graphs and events, never the workspace.
+ *   - A handle is single-owner and not thread-safe. All device work is enqueued on the
+ *     handle's stream; calls that return host data synchronise that stream.
+ *
+ * Errors: every call returns a jkcals_status; jkcals_last_error() describes the last
+ * failure on a handle. Numerical failures are PER SUBMODEL and never fail a call: a
+ * failed Cholesky falls back to the pseudoinverse (JKCALS_F_PINV_FALLBACK); a non-finite
+ * error freezes the submodel (JKCALS_F_NONFINITE); a negative error below -1e-9 ||T_-p||^2
+ * sets JKCALS_F_BREAKDOWN.
+ */
+#ifndef JKCALS_H
+#define JKCALS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct jkcals_s *jkcals_t;
+
+typedef enum {
+  JKCALS_OK = 0,
+  JKCALS_E_ARG = -1,       /* invalid argument / precondition */
+  JKCALS_E_SHAPE = -2,     /* shape unsupported by the kernels (e.g. > 2^31 elements per index) */
+  JKCALS_E_STATE = -3,     /* call out of order (e.g. iterate before set_init) */
+  JKCALS_E_OOM = -4,       /* workspace too small */
+  JKCALS_E_CUDA = -5,      /* a CUDA runtime error (message in jkcals_last_error) */
+  JKCALS_E_NONFINITE = -6  /* non-finite value in the tensor or the initial model */
+} jkcals_status;
+
+typedef enum { JKCALS_FP64 = 0, JKCALS_FP32 = 1 } jkcals_precision;
+
+enum {
+  JKCALS_F_CONVERGED = 1,
+  JKCALS_F_PINV_FALLBACK = 2,
+  JKCALS_F_NONFINITE = 4,
+  JKCALS_F_BREAKDOWN = 8
+};
+
+#define JKCALS_MAX_MODES 8
+
+/* Bytes of device workspace needed by jkcals_create for these arguments on `device`.
+ * ndims in [3, 8]; dims[k] >= 1, dims[0] >= 2; rank >= 1; n_sub = sub_end - sub_begin >= 1;
+ * hist_cap >= 1 is the per-submodel error-history ring length. Returns 0 on bad arguments. */
+size_t jkcals_workspace_bytes(int ndims, const int64_t *dims, int rank, int64_t n_sub,
+                              jkcals_precision prec, int hist_cap, int device);
+
+/* Create a handle for submodels p in [sub_begin, sub_end) ⊆ [0, dims[0]) (a shard; the
+ * zero row of submodel p is at the GLOBAL index p). `tensor` is FP64 column-major with
+ * prod(dims) elements, on the host (tensor_is_device = 0) or device (1). `cuda_stream` is a
+ * cudaStream_t (NULL = legacy default stream). `workspace` is device memory of at least
+ * jkcals_workspace_bytes(...) bytes, 256-byte aligned. Computes ||T||^2 and the mode-0 slice
+ * norms (so ||T_-p||^2 = ||T||^2 - s_p). Errors: E_ARG, E_OOM, E_NONFINITE,
+ * E_CUDA. */
+/* On failure *out may still receive a handle so that jkcals_last_error() can be read; the
+ * caller must then jkcals_destroy() it. */
+jkcals_status jkcals_create(jkcals_t *out, int ndims, const int64_t *dims, int rank,
+                            int64_t sub_begin, int64_t sub_end, const double *tensor,
+                            int tensor_is_device, jkcals_precision prec, int device,
+                            void *cuda_stream, void *workspace, size_t workspace_bytes,
+                            int hist_cap);
+
+/* Warm start every submodel from the overall model P (Alg. 2 alg:jk:model_subsample,
+ * PAPER.md:331; Alg. 3 alg:start-jk-1..alg:stop-jk-1): P[n] is a host
+ * column-major dims[n] x rank array; block k of the mode-0 multi-factor gets row p_k
+ * zeroed. Resets fits, histories, flags and iteration counts. Errors: E_ARG, E_NONFINITE. */
+jkcals_status jkcals_set_init(jkcals_t h, const double *const *P);
+
+/* Optional per-submodel (re)initialisation, e.g. to resume: U is host column-major in the
+ * get_factors layout ((dims[0]-1) x rank for mode 0, row p absent; dims[mode] x rank else). */
+jkcals_status jkcals_set_init_submodel(jkcals_t h, int64_t p, int mode, const double *U);
+
+/* Run up to max_iters ALS sweeps of all active submodels (Alg. 3 repeat loop,
+ * PAPER.md:432-445). tol <= 0: exactly max_iters sweeps (the §5.1 protocol);
+ * tol > 0: submodels freeze as they converge and converged submodels are compacted out of
+ * the fused multi-factors; returns early once all have converged. *sweeps_done (may be
+ * NULL) receives the number of sweeps executed. Errors: E_STATE, E_ARG, E_CUDA. */
+jkcals_status jkcals_iterate(jkcals_t h, int max_iters, double tol, int *sweeps_done);
+
+/* Factors of submodel p (global index): mode 0 -> (dims[0]-1) x rank with row p DROPPED,
+ * mode n >= 1 -> dims[n] x rank; column-major, unit 2-norm columns. lambda (rank, may be
+ * NULL) holds the column norms of the LAST updated mode (mode ndims-1 after a sweep). */
+jkcals_status jkcals_get_factors(jkcals_t h, int64_t p, int mode, double *U, double *lambda);
+
+/* Debug/invariant view: submodel p's FULL block of the mode-`mode` multi-factor as it sits
+ * in the fused layout, dims[mode] x rank column-major. For mode 0 row p is the padded zero
+ * row, which must be exactly +0.0/-0.0 after every sweep (alg:cals_jk:multifactor). */
+jkcals_status jkcals_get_block(jkcals_t h, int64_t p, int mode, double *U);
+
+/* Per-submodel status, arrays of n_sub entries in submodel order (any may be NULL). */
+jkcals_status jkcals_get_status(jkcals_t h, double *fit, double *err, int *iters, int *flags);
+
+/* Error history of submodel p (oldest first): up to `cap` values; *count = number written. */
+jkcals_status jkcals_get_history(jkcals_t h, int64_t p, double *err, int cap, int *count);
+
+/* Jackknife mean and standard error of U_mode over this handle's submodels (mode >= 1):
+ * std = sqrt(((g-1)/g) sum_p (U_p - mean)^2), g = n_sub (Alg. 2 alg:jk:std, PAPER.md:339;
+ * estimator: DESIGN.md reading A11). Column-major dims[mode] x rank. Needs n_sub >= 2. */
+jkcals_status jkcals_get_jackknife_stats(jkcals_t h, int mode, double *mean, double *std);
+
+/* Local moments for cross-shard merging (Chan et al.): per element of U_mode the count,
+ * mean and sum of squared deviations M2 over this handle's submodels. mode >= 1. */
+jkcals_status jkcals_get_local_moments(jkcals_t h, int mode, double *count, double *mean,
+                                       double *m2);
+
+/* Instrumentation: when on, iterate() launches kernels eagerly (no CUDA graph) bracketed
+ * by CUDA events on the handle's stream and accumulates per-mode kernel times. */
+jkcals_status jkcals_set_instrument(jkcals_t h, int on);
+/* Accumulated per-mode kernel milliseconds (arrays of ndims) and launch count; resets. */
+jkcals_status jkcals_get_kernel_times(jkcals_t h, double *mttkrp_ms, double *epilogue_ms,
+                                      int64_t *mttkrp_launches);
+/* Algorithmic MTTKRP flops of one sweep with the current fused width: 2 * C * prod(dims) per
+ * mode, times ndims. */
+double jkcals_sweep_flops(jkcals_t h);
+/* Number of this library's kernels launched by one sweep (for bench accounting). */
+int jkcals_launches_per_sweep(jkcals_t h);
+
+const char *jkcals_last_error(jkcals_t h);
+void jkcals_destroy(jkcals_t h);
+
+/* ---- Stand-alone device operations (kernel-level parity tests and the roofline) ---- */
+
+/* Fused MTTKRP (Eq. 1 / Alg. 3 alg:cals_jk:mttkrp) on device data:
+ *   M(i, c) = sum_j T_(n)(i, j) * prod_{m != n} U_m(i_m(j), c),  c < C,
+ * T device FP64 column-major; U[m] device row-major dims[m] x ldu (C <= ldu; ldu % 8 == 0 and
+ * columns [C, round_up(C,128)) readable); M device row-major dims[n] x ldm. scratch is device
+ * memory of jkcals_mttkrp_scratch_bytes(...) bytes. Enqueued on `stream`; returns E_CUDA on a
+ * launch error. */
+size_t jkcals_mttkrp_scratch_bytes(int ndims, const int64_t *dims, int n, int64_t C, int device);
+jkcals_status jkcals_mttkrp(int ndims, const int64_t *dims, int n, const double *T,
+                            const double *const *U, int64_t C, int64_t ldu, double *M, int64_t ldm,
+                            void *scratch, size_t scratch_bytes, void *stream);
+
+/* Khatri-Rao generation (descending order of Eq. 1), materialised:
+ *   K(j, c) = prod_{m != n} U_m(i_m(j), c),  j in [0, prod_{m!=n} dims[m]) by Eq. 3, c < C,
+ * U[m] device row-major dims[m] x ldu; K device row-major J x ldk. HBM-write-bound. */
+jkcals_status jkcals_krp(int ndims, const int64_t *dims, int n, const double *const *U, int64_t C,
+                         int64_t ldu, double *K, int64_t ldk, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* JKCALS_H */

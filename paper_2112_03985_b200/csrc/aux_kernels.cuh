@@ -1,0 +1,180 @@
+// aux_kernels.cuh — the one-time and bookkeeping kernels around the hot loop:
+// slice norms (a0), warm-start broadcast (a0, Alg. 3 alg:start-jk-1..alg:stop-jk-1),
+// initial Gramians (a0/a3), factor extraction (a9), jackknife moments (a9, Alg. 2
+// alg:jk:std) and masked compaction of converged submodels (a8).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "epilogue.cuh"
+
+namespace jk {
+
+// (a0) mode-0 slice norms, pass 1: CTA b sums T(i0, j)^2 over its chunk of columns j of
+// T_(0) (column-major, so consecutive threads read consecutive i0: coalesced).
+__global__ void slice_norms_partial_kernel(const double* __restrict__ T, int64_t I0, int64_t J0,
+                                           int64_t chunk, double* __restrict__ part) {
+  const int64_t j0 = (int64_t)blockIdx.x * chunk, j1 = min(J0, j0 + chunk);
+  for (int64_t i = threadIdx.x; i < I0; i += blockDim.x) {
+    double s = 0.0;
+    for (int64_t j = j0; j < j1; ++j) {
+      double x = T[i + I0 * j];
+      s += x * x;
+    }
+    part[(int64_t)blockIdx.x * I0 + i] = s;
+  }
+}
+
+// pass 2 (single CTA): s_p = sum_b part[b][p] in order; ||T||^2 = sum_p s_p in order;
+// ||T_-p||^2 = ||T||^2 - s_p for every submodel.
+__global__ void slice_norms_final_kernel(const double* __restrict__ part, int nb, int64_t I0,
+                                         double* __restrict__ s, double* __restrict__ normT2,
+                                         const int64_t* __restrict__ pglob, int nsub,
+                                         double* __restrict__ normT2p) {
+  for (int64_t i = threadIdx.x; i < I0; i += blockDim.x) {
+    double acc = 0.0;
+    for (int b = 0; b < nb; ++b) acc += part[(int64_t)b * I0 + i];
+    s[i] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int64_t i = 0; i < I0; ++i) tot += s[i];
+    *normT2 = tot;
+    for (int q = 0; q < nsub; ++q) normT2p[q] = tot - s[pglob[q]];
+  }
+}
+
+// (a0) warm start: block k of the mode-n multi-factor = P_n (host col-major I x R staged on
+// the device); the mode-0 block k gets row p_k zeroed (Alg. 3 alg:cals_jk:multifactor0).
+// Columns [C, ldu) are zero (padding read by the KRP tiles).
+__global__ void broadcast_init_kernel(const double* __restrict__ P, int I, int R, int K, int64_t ldu,
+                                      double* __restrict__ U, int zero_rows,
+                                      const int* __restrict__ blk2sub, const int64_t* __restrict__ pglob) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)I * ldu) return;
+  const int i = (int)(e / ldu);
+  const int c = (int)(e % ldu);
+  double v = 0.0;
+  if (c < K * R) {
+    const int k = c / R, r = c % R;
+    v = P[i + (int64_t)I * r];
+    if (zero_rows && i == pglob[blk2sub[k]]) v = 0.0;
+  }
+  U[e] = v;
+}
+
+// one submodel's block from a host-provided col-major matrix (set_init_submodel): mode 0
+// arrives without row p, which is re-inserted as zeros.
+__global__ void set_block_kernel(const double* __restrict__ src, int I, int R, int64_t ldu, int blk,
+                                 int64_t pdrop, double* __restrict__ U) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= I * R) return;
+  const int i = e / R, r = e % R;
+  double v;
+  if (pdrop >= 0) {
+    const int rows = I - 1;
+    v = (i == pdrop) ? 0.0 : src[(i < pdrop ? i : i - 1) + (int64_t)rows * r];
+  } else {
+    v = src[i + (int64_t)I * r];
+  }
+  U[(int64_t)i * ldu + (int64_t)blk * R + r] = v;
+}
+
+// Gramian of one block (one CTA per live block): Gram_n^(sub) = U_blk^T U_blk.
+template <int RMAX>
+__global__ void __launch_bounds__(kEpiThreads) gram_kernel(const double* __restrict__ U, int I, int64_t ldu,
+                                                           int R, const int* __restrict__ blk2sub, int nsub,
+                                                           int n, double* __restrict__ gram) {
+  const int k = blockIdx.x, sub = blk2sub[k];
+  __shared__ double red[(kEpiThreads / 32 + 1) * (RMAX * RMAX + RMAX + 1)];
+  double g[RMAX * RMAX];
+#pragma unroll
+  for (int e = 0; e < RMAX * RMAX; ++e) g[e] = 0.0;
+  for (int i = threadIdx.x; i < I; i += kEpiThreads) {
+    const double* row = U + (int64_t)i * ldu + (int64_t)k * R;
+    double u[RMAX];
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) u[r] = r < R ? row[r] : 0.0;
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r)
+#pragma unroll
+      for (int q = 0; q < RMAX; ++q) g[r * RMAX + q] += u[r] * u[q];
+  }
+  block_sum<RMAX>(g, RMAX * RMAX, red);
+  const double* gt = red + (kEpiThreads / 32) * RMAX * RMAX;
+  for (int e = threadIdx.x; e < R * R; e += kEpiThreads)
+    gram[((int64_t)n * nsub + sub) * R * R + e] = gt[(e / R) * RMAX + (e % R)];
+}
+
+// reset per-submodel state at set_init
+__global__ void reset_state_kernel(int nsub, double* fit, double* fit_prev, double* err, int* iters, int* flags,
+                                   int* active) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nsub) return;
+  fit[q] = 0.0;
+  fit_prev[q] = 0.0;
+  err[q] = 0.0;
+  iters[q] = 0;
+  flags[q] = 0;
+  active[q] = 1;
+}
+
+// (a9) extract a row-major (stride ld) I x R block into a column-major output, dropping
+// row `drop` (the left-out sample's zero row in mode 0) when drop >= 0.
+__global__ void extract_kernel(const double* __restrict__ src, int64_t ld, int I, int R, int64_t drop,
+                               double* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int rows = drop >= 0 ? I - 1 : I;
+  if (e >= rows * R) return;
+  const int r = e / rows, io = e % rows;
+  const int i = (drop >= 0 && io >= drop) ? io + 1 : io;
+  out[e] = src[(int64_t)i * ld + r];
+}
+
+// (a9) per-element moments over the handle's submodels, fixed order (two-pass):
+// mean = sum/g, M2 = sum (x - mean)^2. src_off[q] / src_ld[q] locate submodel q's block
+// (row-major) relative to `base`. Output column-major I x R.
+__global__ void moments_kernel(const double* __restrict__ base, const int64_t* __restrict__ src_off,
+                               const int64_t* __restrict__ src_ld, int nsub, int I, int R,
+                               double* __restrict__ mean, double* __restrict__ m2) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= I * R) return;
+  const int r = e / I, i = e % I;
+  double s = 0.0;
+  for (int q = 0; q < nsub; ++q) s += base[src_off[q] + (int64_t)i * src_ld[q] + r];
+  const double mu = s / (double)nsub;
+  double ss = 0.0;
+  for (int q = 0; q < nsub; ++q) {
+    const double d = base[src_off[q] + (int64_t)i * src_ld[q] + r] - mu;
+    ss += d * d;
+  }
+  mean[e] = mu;
+  m2[e] = ss;
+}
+
+// (a8) store a converged block into the result store (row-major I x R per submodel).
+__global__ void store_block_kernel(const double* __restrict__ U, int I, int64_t ldu, int R, int blk,
+                                   double* __restrict__ dst) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= I * R) return;
+  const int i = e / R, r = e % R;
+  dst[e] = U[(int64_t)i * ldu + (int64_t)blk * R + r];
+}
+
+// (a8) masked compaction: gather the surviving blocks (old index map[k]) to the front of
+// the other multi-factor buffer; columns >= K_new*R become zero padding.
+__global__ void gather_blocks_kernel(const double* __restrict__ Uold, double* __restrict__ Unew, int I,
+                                     int64_t ldu, int R, const int* __restrict__ map, int Knew) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)I * ldu) return;
+  const int i = (int)(e / ldu), c = (int)(e % ldu);
+  double v = 0.0;
+  if (c < Knew * R) {
+    const int k = c / R, r = c % R;
+    v = Uold[(int64_t)i * ldu + (int64_t)map[k] * R + r];
+  }
+  Unew[e] = v;
+}
+
+}  // namespace jk

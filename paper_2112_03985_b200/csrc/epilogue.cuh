@@ -1,0 +1,325 @@
+// epilogue.cuh — per-submodel ALS update after the fused MTTKRP of mode n.
+//
+// One CTA per live submodel block k (sub = blk2sub[k]) does, in this order
+// (Alg. 3 lines alg:cals_jk:hadamard .. alg:cals_jk:error):
+//   H    = Hadamard over m != n of the cached Gramians Gram_m^(sub)          (a3)
+//   M    = fixed-order sum of the split-K / stream-K partial pieces         (a2 reduce)
+//   V    = M H^{-1}: Cholesky (thread 0), pinv fallback via Jacobi         (a4)
+//   n==0: V(p,:) = 0  (zero row of the left-out sample, alg:cals_jk:multifactor) (a5)
+//   lambda_r = ||V(:,r)||_2 ; U = V / lambda (lambda = 0 -> unchanged)       (a6)
+//   Gram_n^(sub) = U^T U (cached for the next modes)
+//   n==N-1: e = ||T_-p||^2 + sum(H .* V^T V) - 2 sum(V .* M); fit; history;
+//           convergence mask (|fit - fit_prev| < tol from sweep 2)          (a7)
+// Everything is summed in a fixed order, so results are run-to-run deterministic.
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "mttkrp.cuh"
+
+namespace jk {
+
+enum { F_CONVERGED = 1, F_PINV = 2, F_NONFINITE = 4, F_BREAKDOWN = 8 };
+
+struct EpiArgs {
+  int N, n, R;
+  int In;
+  int64_t ldu;
+  int nsub;                      // submodels of the handle (state arrays are indexed by sub)
+  double* U;                     // multi-factor of mode n (row-major In x ldu)
+  const int* blk2sub;            // live block -> submodel
+  const int64_t* pglob;          // submodel -> global left-out index p
+  const double* parts;           // partial pieces of the fused MTTKRP
+  const TileInfo* tinfo;
+  int BM, BN, nMt;
+  double* gram;                  // [N][nsub][R][R]
+  double* lambda;                // [nsub][R]
+  const double* normT2p;         // [nsub]  ||T_-p||^2
+  double* fit;                   // [nsub]
+  double* fit_prev;              // [nsub]
+  double* err;                   // [nsub]
+  int* iters;                    // [nsub]
+  int* flags;                    // [nsub]
+  int* active;                   // [nsub]
+  double* hist;                  // [nsub][hist_cap]
+  int hist_cap;
+  const double* tol;             // device scalar (graph-stable)
+  int* active_count;             // incremented at n == N-1 by still-active submodels
+};
+
+constexpr int kEpiThreads = 128;
+
+template <int RMAX>
+__device__ __forceinline__ void block_sum(double* vals, int cnt, double* red) {
+  // vals: per-thread array of cnt (<= RMAX*RMAX + RMAX + 1) values -> summed into red[0..cnt)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = kEpiThreads / 32;
+  for (int q = 0; q < cnt; ++q) {
+    double x = vals[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (lane == 0) red[warp * cnt + q] = x;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s += red[w * cnt + q];
+    red[NW * cnt + q] = s;
+  }
+  __syncthreads();
+}
+
+// Symmetric pseudoinverse by cyclic Jacobi (single thread, R <= RMAX).
+template <int RMAX>
+__device__ void jacobi_pinv(const double* H, int R, double* Hp, double rcond) {
+  double A[RMAX * RMAX], Q[RMAX * RMAX];
+  for (int e = 0; e < R * R; ++e) { A[e] = H[e]; Q[e] = 0.0; }
+  for (int i = 0; i < R; ++i) Q[i * R + i] = 1.0;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int i = 0; i < R; ++i)
+      for (int j = 0; j < R; ++j) {
+        double a = A[i * R + j];
+        tot += a * a;
+        if (i != j) off += a * a;
+      }
+    if (off <= 1e-30 * tot || off == 0.0) break;
+    for (int p = 0; p < R - 1; ++p)
+      for (int q = p + 1; q < R; ++q) {
+        double apq = A[p * R + q];
+        if (apq == 0.0) continue;
+        double theta = (A[q * R + q] - A[p * R + p]) / (2.0 * apq);
+        double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < R; ++k) {
+          double akp = A[k * R + p], akq = A[k * R + q];
+          A[k * R + p] = c * akp - s * akq;
+          A[k * R + q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < R; ++k) {
+          double apk = A[p * R + k], aqk = A[q * R + k];
+          A[p * R + k] = c * apk - s * aqk;
+          A[q * R + k] = s * apk + c * aqk;
+        }
+        for (int k = 0; k < R; ++k) {
+          double qkp = Q[k * R + p], qkq = Q[k * R + q];
+          Q[k * R + p] = c * qkp - s * qkq;
+          Q[k * R + q] = s * qkp + c * qkq;
+        }
+      }
+  }
+  double wmax = 0.0;
+  for (int i = 0; i < R; ++i) wmax = fmax(wmax, A[i * R + i]);
+  for (int e = 0; e < R * R; ++e) Hp[e] = 0.0;
+  for (int i = 0; i < R; ++i) {
+    double w = A[i * R + i];
+    if (!(w > rcond * wmax) || w <= 0.0) continue;
+    for (int a = 0; a < R; ++a)
+      for (int b = 0; b < R; ++b) Hp[a * R + b] += Q[a * R + i] * Q[b * R + i] / w;
+  }
+}
+
+template <int RMAX>
+__global__ void __launch_bounds__(kEpiThreads) als_epilogue_kernel(EpiArgs a) {
+  const int k = blockIdx.x;
+  const int sub = a.blk2sub[k];
+  if (!a.active[sub]) return;  // frozen (converged or failed)
+  const int R = a.R, n = a.n, N = a.N, tid = threadIdx.x;
+  const bool last = (n == N - 1);
+  const int64_t pzero = (n == 0) ? a.pglob[sub] : -1;
+  const int cb = k * R;
+
+  __shared__ double H[RMAX * RMAX];
+  __shared__ double Lf[RMAX * RMAX];       // Cholesky factor (row-major lower) or H^+
+  __shared__ int use_pinv;
+  __shared__ double red[(kEpiThreads / 32 + 1) * (RMAX * RMAX + RMAX + 1)];
+
+  // (a3) Hadamard of the cached Gramians of every other mode
+  for (int e = tid; e < R * R; e += kEpiThreads) {
+    double h = 1.0;
+    for (int m = 0; m < N; ++m)
+      if (m != n) h *= a.gram[((int64_t)m * a.nsub + sub) * R * R + e];
+    H[e] = h;
+  }
+  __syncthreads();
+  // (a4) Cholesky H = L L^T (textbook, no pivoting); pinv fallback
+  if (tid == 0) {
+    bool ok = true;
+    for (int j = 0; j < R && ok; ++j) {
+      double s = H[j * R + j];
+      for (int q = 0; q < j; ++q) s -= Lf[j * R + q] * Lf[j * R + q];
+      if (!(s > 0.0) || !isfinite(s)) { ok = false; break; }
+      Lf[j * R + j] = sqrt(s);
+      for (int i = j + 1; i < R; ++i) {
+        double t = H[i * R + j];
+        for (int q = 0; q < j; ++q) t -= Lf[i * R + q] * Lf[j * R + q];
+        Lf[i * R + j] = t / Lf[j * R + j];
+      }
+    }
+    use_pinv = ok ? 0 : 1;
+    if (!ok) {
+      jacobi_pinv<RMAX>(H, R, Lf, 1e-12);
+      a.flags[sub] |= F_PINV;
+    }
+  }
+  __syncthreads();
+  const bool pinv = use_pinv != 0;
+
+  // pass 1: reduce partials, solve, write V; accumulate column norms (and V^T V, V.M)
+  double cn[RMAX], vtv[RMAX * RMAX], cross = 0.0;
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) cn[r] = 0.0;
+#pragma unroll
+  for (int e = 0; e < RMAX * RMAX; ++e) vtv[e] = 0.0;
+
+  for (int i = tid; i < a.In; i += kEpiThreads) {
+    double m[RMAX], v[RMAX];
+    const int tn = i / a.BN;
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) {
+      m[r] = 0.0;
+      if (r < R) {
+        const int c = cb + r, tm = c / a.BM;
+        const TileInfo ti = a.tinfo[tn * a.nMt + tm];
+        const double* p = a.parts + (int64_t)ti.piece_base * a.BN * a.BM + (int64_t)(i - tn * a.BN) * a.BM + (c - tm * a.BM);
+        double s = 0.0;
+        for (int pc = 0; pc < ti.npieces; ++pc) s += p[(int64_t)pc * a.BN * a.BM];
+        m[r] = s;
+      }
+    }
+    if (i == pzero) {
+#pragma unroll
+      for (int r = 0; r < RMAX; ++r) v[r] = 0.0;
+    } else if (!pinv) {
+      double y[RMAX];
+#pragma unroll
+      for (int r = 0; r < RMAX; ++r) {
+        if (r < R) {
+          double t = m[r];
+#pragma unroll
+          for (int q = 0; q < r; ++q) t -= Lf[r * R + q] * y[q];
+          y[r] = t / Lf[r * R + r];
+        }
+      }
+#pragma unroll
+      for (int r = RMAX - 1; r >= 0; --r) {
+        if (r < R) {
+          double t = y[r];
+#pragma unroll
+          for (int q = r + 1; q < RMAX; ++q)
+            if (q < R) t -= Lf[q * R + r] * v[q];
+          v[r] = t / Lf[r * R + r];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < RMAX; ++r) {
+        if (r < R) {
+          double s = 0.0;
+#pragma unroll
+          for (int q = 0; q < RMAX; ++q)
+            if (q < R) s += m[q] * Lf[q * R + r];
+          v[r] = s;
+        }
+      }
+    }
+    double* urow = a.U + (int64_t)i * a.ldu + cb;
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) {
+      if (r < R) {
+        urow[r] = v[r];
+        cn[r] += v[r] * v[r];
+        if (last) {
+          cross += v[r] * m[r];
+#pragma unroll
+          for (int q = 0; q < RMAX; ++q)
+            if (q < R) vtv[r * RMAX + q] += v[r] * v[q];
+        }
+      }
+    }
+  }
+  // block reductions (fixed order)
+  double vals[RMAX * RMAX + RMAX + 1];
+  int cnt = 0;
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) vals[cnt++] = cn[r];
+  vals[cnt++] = cross;
+  if (last) {
+#pragma unroll
+    for (int e = 0; e < RMAX * RMAX; ++e) vals[cnt++] = vtv[e];
+  }
+  block_sum<RMAX>(vals, cnt, red);
+  constexpr int NW = kEpiThreads / 32;
+  const double* tot = red + NW * cnt;
+  double lam[RMAX];
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) lam[r] = (r < R) ? sqrt(tot[r]) : 0.0;
+  double quad = 0.0, crs = tot[RMAX];
+  if (last) {
+    for (int r = 0; r < R; ++r)
+      for (int q = 0; q < R; ++q) quad += H[r * R + q] * tot[RMAX + 1 + r * RMAX + q];
+  }
+  __syncthreads();  // everyone has read `red` before it is reused
+
+  // pass 2: normalise (a6) and accumulate the Gramian of the normalised block
+  double gr[RMAX * RMAX];
+#pragma unroll
+  for (int e = 0; e < RMAX * RMAX; ++e) gr[e] = 0.0;
+  for (int i = tid; i < a.In; i += kEpiThreads) {
+    double* urow = a.U + (int64_t)i * a.ldu + cb;
+    double uu[RMAX];
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) {
+      uu[r] = 0.0;
+      if (r < R) {
+        double x = urow[r];
+        uu[r] = lam[r] > 0.0 ? x / lam[r] : x;
+        urow[r] = uu[r];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r)
+#pragma unroll
+      for (int q = 0; q < RMAX; ++q)
+        if (r < R && q < R) gr[r * RMAX + q] += uu[r] * uu[q];
+  }
+  block_sum<RMAX>(gr, RMAX * RMAX, red);
+  const double* gt = red + NW * RMAX * RMAX;
+  for (int e = tid; e < R * R; e += kEpiThreads) {
+    int r = e / R, q = e % R;
+    a.gram[((int64_t)n * a.nsub + sub) * R * R + e] = gt[r * RMAX + q];
+  }
+  if (tid < R) a.lambda[(int64_t)sub * R + tid] = lam[tid];
+
+  if (last && tid == 0) {  // (a7) error, fit, history, convergence mask
+    const double nt2 = a.normT2p[sub];
+    const double e = nt2 + quad - 2.0 * crs;
+    int it = a.iters[sub] + 1;
+    a.iters[sub] = it;
+    a.err[sub] = e;
+    a.hist[(int64_t)sub * a.hist_cap + (it - 1) % a.hist_cap] = e;
+    int f = a.flags[sub];
+    bool act = true;
+    if (!isfinite(e)) {
+      f |= F_NONFINITE;
+      act = false;
+    } else {
+      if (e < -1e-9 * nt2) f |= F_BREAKDOWN;
+      const double fit = nt2 > 0.0 ? 1.0 - sqrt(fmax(e, 0.0)) / sqrt(nt2) : 0.0;
+      const double tol = *a.tol;
+      if (tol > 0.0 && it >= 2 && fabs(fit - a.fit_prev[sub]) < tol) {
+        f |= F_CONVERGED;
+        act = false;
+      }
+      a.fit[sub] = fit;
+      a.fit_prev[sub] = fit;
+    }
+    a.flags[sub] = f;
+    if (!act) a.active[sub] = 0;
+    else atomicAdd(a.active_count, 1);
+  }
+}
+
+}  // namespace jk

@@ -1,0 +1,1008 @@
+// jkcals.cu — host orchestration and C ABI (include/jkcals.h) of the B200 JK-CALS path.
+//
+// One handle = one shard of submodels on one GPU. The workspace (caller-owned, e.g. a torch
+// uint8 tensor) is carved by a deterministic bump layout; a sweep (N x [fused MTTKRP +
+// per-submodel epilogue]) is captured once into a CUDA graph and replayed max_iters times
+// (CS1 in SURVEY §3). With tol > 0 the host reads one int per sweep (active count) and, when
+// enough submodels have converged, compacts them out (a8) and re-captures the graph.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/jkcals.h"
+#include "aux_kernels.cuh"
+#include "epilogue.cuh"
+#include "mttkrp.cuh"
+
+using namespace jk;
+
+namespace {
+
+constexpr int kMaxNT = 16;
+constexpr size_t kAlign = 256;
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
+
+// ---------------------------------------------------------------- kernel dispatch tables
+typedef void (*MttkrpFn)(ModeView, const double*, MttkrpGeom, const TileInfo*, double*);
+
+template <int NT, int W>
+MttkrpFn mttkrp_ptr() { return mttkrp_dmma_kernel<NT, W>; }
+
+template <int W, int... NTs>
+struct Table {
+  static void fill(MttkrpFn* fns, size_t* smem) {
+    int i = 0;
+    ((fns[i] = mttkrp_ptr<NTs, W>(), smem[i] = MttkrpCfg<NTs, W>::kSmem, ++i), ...);
+  }
+};
+
+struct KernelInfo {
+  MttkrpFn fn[2][kMaxNT];  // [W==8][NT-1]
+  size_t smem[2][kMaxNT];
+  int occ[2][kMaxNT];
+  int nsm;
+};
+
+KernelInfo* kernel_info(int device, std::string* err) {
+  static KernelInfo info[16];
+  static bool ready[16] = {false};
+  if (device < 0 || device >= 16) return nullptr;
+  if (ready[device]) return &info[device];
+  KernelInfo& ki = info[device];
+  Table<4, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>::fill(ki.fn[0], ki.smem[0]);
+  Table<8, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>::fill(ki.fn[1], ki.smem[1]);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  cudaDeviceGetAttribute(&ki.nsm, cudaDevAttrMultiProcessorCount, device);
+  for (int w = 0; w < 2; ++w)
+    for (int t = 0; t < kMaxNT; ++t) {
+      cudaError_t e = cudaFuncSetAttribute(ki.fn[w][t], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)ki.smem[w][t]);
+      if (e != cudaSuccess) {
+        if (err) *err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e);
+        cudaSetDevice(prev);
+        return nullptr;
+      }
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ki.fn[w][t], (w ? 8 : 4) * 32, ki.smem[w][t]);
+      ki.occ[w][t] = std::max(1, occ);
+    }
+  cudaSetDevice(prev);
+  ready[device] = true;
+  return &ki;
+}
+
+// ---------------------------------------------------------------- per-mode plan
+struct ModePlan {
+  int NT = 1, W8 = 1, BM = 128, BN = 8, nMt = 1, nNt = 1, KT = 1, G = 1;
+  int64_t units = 1;
+  int ntiles = 1, npieces = 1;
+  std::vector<TileInfo> tinfo;
+};
+
+ModePlan make_plan(int64_t In, int64_t J, int64_t C, const KernelInfo& ki) {
+  ModePlan p;
+  int64_t nI8 = cdiv(In, 8);
+  p.nNt = (int)cdiv(nI8, kMaxNT);
+  p.NT = (int)cdiv(nI8, p.nNt);
+  p.BN = p.NT * 8;
+  p.W8 = (C > 64) ? 1 : 0;
+  p.BM = p.W8 ? 128 : 64;
+  p.nMt = (int)std::max<int64_t>(1, cdiv(C, p.BM));
+  p.KT = (int)cdiv(J, kBK);
+  p.ntiles = p.nMt * p.nNt;
+  p.units = (int64_t)p.ntiles * p.KT;
+  int64_t gmax = (int64_t)ki.nsm * ki.occ[p.W8][p.NT - 1];
+  p.G = (int)std::min<int64_t>(p.units, gmax);
+  std::vector<int> first(p.ntiles, -1), lastc(p.ntiles, -1);
+  for (int b = 0; b < p.G; ++b) {
+    int64_t u0 = (int64_t)b * p.units / p.G, u1 = (int64_t)(b + 1) * p.units / p.G;
+    if (u0 >= u1) continue;
+    int64_t t0 = u0 / p.KT, t1 = (u1 - 1) / p.KT;
+    for (int64_t t = t0; t <= t1; ++t) {
+      if (first[t] < 0) first[t] = b;
+      lastc[t] = b;
+    }
+  }
+  p.tinfo.resize(p.ntiles);
+  int base = 0;
+  for (int t = 0; t < p.ntiles; ++t) {
+    p.tinfo[t].first_cta = first[t];
+    p.tinfo[t].npieces = lastc[t] - first[t] + 1;
+    p.tinfo[t].piece_base = base;
+    p.tinfo[t].pad_ = 0;
+    base += p.tinfo[t].npieces;
+  }
+  p.npieces = base;
+  return p;
+}
+
+int64_t plan_parts_doubles(const ModePlan& p) { return (int64_t)p.npieces * p.BN * p.BM; }
+
+// upper bound over both warp variants, for workspace sizing
+void plan_bounds(int64_t In, int64_t J, int64_t C, const KernelInfo& ki, int64_t* parts, int* tiles) {
+  *parts = 0;
+  *tiles = 0;
+  for (int w8 = 0; w8 < 2; ++w8) {
+    int64_t nI8 = cdiv(In, 8);
+    int nNt = (int)cdiv(nI8, kMaxNT), NT = (int)cdiv(nI8, nNt);
+    int BM = w8 ? 128 : 64, BN = NT * 8;
+    int nMt = (int)std::max<int64_t>(1, cdiv(C, BM));
+    int64_t KT = cdiv(J, kBK);
+    int ntiles = nMt * nNt;
+    int64_t G = std::min<int64_t>((int64_t)ntiles * KT, (int64_t)ki.nsm * ki.occ[w8][NT - 1]);
+    *parts = std::max(*parts, (G + ntiles) * BN * BM);
+    *tiles = std::max(*tiles, ntiles);
+  }
+}
+
+// ---------------------------------------------------------------- workspace layout
+struct Layout {
+  size_t off = 0;
+  size_t take(size_t bytes) {
+    size_t o = off;
+    off = rup((int64_t)(off + bytes), kAlign);
+    return o;
+  }
+};
+
+struct Offsets {
+  size_t T, U[2][kMaxModes], Ures, parts, tinfo[kMaxModes], gram, lambda, normT2p, fit, fit_prev, err, hist,
+      slice, slice_part, stage, iters, flags, active, blk2sub, map, pglob, misc, srcoff, srcld;
+  int64_t parts_cap;
+  int tiles_cap;
+  int slice_nb;
+  int64_t stage_cap;
+  size_t total;
+};
+
+bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_cap, const KernelInfo& ki,
+                     Offsets* o) {
+  int64_t P = 1, sumI = 0, maxI = 0;
+  for (int k = 0; k < N; ++k) {
+    P *= dims[k];
+    sumI += dims[k];
+    maxI = std::max(maxI, dims[k]);
+  }
+  const int64_t C = nsub * R, ldu = rup(std::max<int64_t>(C, 1), 128);
+  Layout L;
+  o->T = L.take(P * 8);
+  for (int s = 0; s < 2; ++s)
+    for (int k = 0; k < N; ++k) o->U[s][k] = L.take(dims[k] * ldu * 8);
+  o->Ures = L.take(nsub * sumI * R * 8);
+  o->parts_cap = 0;
+  o->tiles_cap = 0;
+  for (int n = 0; n < N; ++n) {
+    int64_t pc;
+    int tc;
+    plan_bounds(dims[n], P / dims[n], C, ki, &pc, &tc);
+    o->parts_cap = std::max(o->parts_cap, pc);
+    o->tiles_cap = std::max(o->tiles_cap, tc);
+  }
+  o->parts = L.take(o->parts_cap * 8);
+  for (int n = 0; n < N; ++n) o->tinfo[n] = L.take((size_t)o->tiles_cap * sizeof(TileInfo));
+  o->gram = L.take((size_t)N * nsub * R * R * 8);
+  o->lambda = L.take(nsub * R * 8);
+  o->normT2p = L.take(nsub * 8);
+  o->fit = L.take(nsub * 8);
+  o->fit_prev = L.take(nsub * 8);
+  o->err = L.take(nsub * 8);
+  o->hist = L.take(nsub * (int64_t)hist_cap * 8);
+  o->slice = L.take(dims[0] * 8);
+  int64_t J0 = P / dims[0];
+  o->slice_nb = (int)std::min<int64_t>(J0, 2 * (int64_t)ki.nsm);
+  o->slice_part = L.take((int64_t)o->slice_nb * dims[0] * 8);
+  o->stage_cap = std::max<int64_t>(3 * maxI * R, 64);
+  o->stage = L.take(o->stage_cap * 8);
+  o->iters = L.take(nsub * 4);
+  o->flags = L.take(nsub * 4);
+  o->active = L.take(nsub * 4);
+  o->blk2sub = L.take(nsub * 4);
+  o->map = L.take(nsub * 4);
+  o->pglob = L.take(nsub * 8);
+  o->srcoff = L.take(nsub * 8);
+  o->srcld = L.take(nsub * 8);
+  o->misc = L.take(256);  // [0] normT2 (double), [8] tol (double), [16] active_count (int)
+  o->total = L.off + kAlign;  // slack for re-alignment of the caller's pointer
+  return true;
+}
+
+bool valid_dims(int N, const int64_t* dims, int R) {
+  if (N < 3 || N > JKCALS_MAX_MODES || !dims || R < 1 || R > 16) return false;
+  int64_t P = 1;
+  for (int k = 0; k < N; ++k) {
+    if (dims[k] < 1) return false;
+    P *= dims[k];
+    if (P > ((int64_t)1 << 40)) return false;
+  }
+  if (dims[0] < 2) return false;
+  for (int k = 0; k < N; ++k)
+    if (P / dims[k] >= ((int64_t)1 << 31)) return false;  // J_n indexes in int32
+  return true;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- the handle
+struct jkcals_s {
+  int N = 0;
+  int64_t dims[kMaxModes] = {0};
+  int R = 0;
+  int64_t sub_begin = 0, sub_end = 0;
+  int nsub = 0, K = 0, C = 0;
+  int64_t ldu = 0, P = 0;
+  int hist_cap = 1;
+  int device = 0;
+  cudaStream_t stream = nullptr;  // the caller's stream: all work is ordered on it
+  cudaStream_t cap = nullptr;     // private non-blocking stream used only for graph capture
+  cudaStream_t es = nullptr;      // stream the enqueue_* helpers target (stream, or cap while capturing)
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  Offsets off;
+  KernelInfo* ki = nullptr;
+  int cur = 0;
+  ModePlan plan[kMaxModes];
+  cudaGraphExec_t gexec = nullptr;
+  bool graph_ok = false;
+  bool inited = false;
+  bool ran = false;
+  double tol_host = 0.0;
+  int* pinned_count = nullptr;
+  std::vector<int> h_blk2sub, h_stored;
+  bool instrument = false;
+  cudaEvent_t ev[2 * 2 * kMaxModes + 2] = {};
+  double t_mttkrp[kMaxModes] = {0}, t_epi[kMaxModes] = {0};
+  int64_t launches = 0;
+  std::string err;
+
+  template <class T>
+  T* ptr(size_t o) { return reinterpret_cast<T*>(ws + o); }
+  double* U(int n) { return ptr<double>(off.U[cur][n]); }
+};
+
+namespace {
+
+jkcals_status fail(jkcals_t h, jkcals_status st, const char* fmt, ...) {
+  if (h) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    h->err = buf;
+  }
+  return st;
+}
+
+#define CKH(h, x)                                                                                       \
+  do {                                                                                                  \
+    cudaError_t e_ = (x);                                                                               \
+    if (e_ != cudaSuccess) return fail(h, JKCALS_E_CUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), \
+                                       __FILE__, __LINE__);                                             \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+ModeView make_view(jkcals_t h, int n, double* const* Uall) {
+  ModeView v;
+  v.N = h->N;
+  v.n = n;
+  v.nrest = h->N - 1;
+  v.In = (int)h->dims[n];
+  v.J = (int)(h->P / h->dims[n]);
+  int64_t L = 1;
+  for (int m = 0; m < n; ++m) L *= h->dims[m];
+  v.L = (int)L;
+  v.LIn = L * h->dims[n];
+  int q = 0;
+  for (int m = 0; m < h->N; ++m) {
+    if (m == n) continue;
+    v.rdim[q] = (int)h->dims[m];
+    v.U[q] = Uall[m];
+    ++q;
+  }
+  for (; q < kMaxModes - 1; ++q) {
+    v.rdim[q] = 1;
+    v.U[q] = nullptr;
+  }
+  return v;
+}
+
+jkcals_status replan(jkcals_t h) {
+  for (int n = 0; n < h->N; ++n) {
+    h->plan[n] = make_plan(h->dims[n], h->P / h->dims[n], h->C, *h->ki);
+    const ModePlan& p = h->plan[n];
+    if (plan_parts_doubles(p) > h->off.parts_cap || p.ntiles > h->off.tiles_cap)
+      return fail(h, JKCALS_E_OOM, "internal: plan exceeds workspace bounds");
+    CKH(h, cudaMemcpyAsync(h->ptr<TileInfo>(h->off.tinfo[n]), p.tinfo.data(), sizeof(TileInfo) * p.ntiles,
+                           cudaMemcpyHostToDevice, h->stream));
+  }
+  CKH(h, cudaStreamSynchronize(h->stream));  // tinfo host vectors may change on the next replan
+  if (h->gexec) {
+    cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+  }
+  h->graph_ok = false;
+  return JKCALS_OK;
+}
+
+template <int RMAX>
+void launch_epi(jkcals_t h, const EpiArgs& a) {
+  als_epilogue_kernel<RMAX><<<h->K, kEpiThreads, 0, h->es>>>(a);
+}
+
+jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
+  double* Uall[kMaxModes];
+  for (int m = 0; m < h->N; ++m) Uall[m] = h->U(m);
+  const ModePlan& p = h->plan[n];
+  ModeView v = make_view(h, n, Uall);
+  MttkrpGeom g;
+  g.C = h->C;
+  g.ldu = h->ldu;
+  g.nMt = p.nMt;
+  g.nNt = p.nNt;
+  g.KT = p.KT;
+  g.units = p.units;
+  g.G = p.G;
+  const TileInfo* ti = h->ptr<TileInfo>(h->off.tinfo[n]);
+  double* parts = h->ptr<double>(h->off.parts);
+  MttkrpFn fn = h->ki->fn[p.W8][p.NT - 1];
+  if (timed) CKH(h, cudaEventRecord(h->ev[4 * n + 0], h->es));
+  fn<<<p.G, (p.W8 ? 8 : 4) * 32, h->ki->smem[p.W8][p.NT - 1], h->es>>>(v, h->ptr<double>(h->off.T), g, ti,
+                                                                             parts);
+  CKH(h, cudaGetLastError());
+  if (timed) CKH(h, cudaEventRecord(h->ev[4 * n + 1], h->es));
+  EpiArgs a;
+  a.N = h->N;
+  a.n = n;
+  a.R = h->R;
+  a.In = (int)h->dims[n];
+  a.ldu = h->ldu;
+  a.nsub = h->nsub;
+  a.U = Uall[n];
+  a.blk2sub = h->ptr<int>(h->off.blk2sub);
+  a.pglob = h->ptr<int64_t>(h->off.pglob);
+  a.parts = parts;
+  a.tinfo = ti;
+  a.BM = p.BM;
+  a.BN = p.BN;
+  a.nMt = p.nMt;
+  a.gram = h->ptr<double>(h->off.gram);
+  a.lambda = h->ptr<double>(h->off.lambda);
+  a.normT2p = h->ptr<double>(h->off.normT2p);
+  a.fit = h->ptr<double>(h->off.fit);
+  a.fit_prev = h->ptr<double>(h->off.fit_prev);
+  a.err = h->ptr<double>(h->off.err);
+  a.iters = h->ptr<int>(h->off.iters);
+  a.flags = h->ptr<int>(h->off.flags);
+  a.active = h->ptr<int>(h->off.active);
+  a.hist = h->ptr<double>(h->off.hist);
+  a.hist_cap = h->hist_cap;
+  a.tol = reinterpret_cast<const double*>(h->ws + h->off.misc + 8);
+  a.active_count = reinterpret_cast<int*>(h->ws + h->off.misc + 16);
+  if (h->R <= 4) launch_epi<4>(h, a);
+  else if (h->R <= 8) launch_epi<8>(h, a);
+  else launch_epi<16>(h, a);
+  CKH(h, cudaGetLastError());
+  if (timed) CKH(h, cudaEventRecord(h->ev[4 * n + 2], h->es));
+  return JKCALS_OK;
+}
+
+jkcals_status enqueue_sweep(jkcals_t h, bool timed) {
+  CKH(h, cudaMemsetAsync(h->ws + h->off.misc + 16, 0, sizeof(int), h->es));
+  for (int n = 0; n < h->N; ++n) {
+    jkcals_status st = enqueue_mode(h, n, timed);
+    if (st != JKCALS_OK) return st;
+  }
+  return JKCALS_OK;
+}
+
+jkcals_status ensure_graph(jkcals_t h) {
+  if (h->graph_ok) return JKCALS_OK;
+  cudaGraph_t graph = nullptr;
+  // capture on a private stream (the caller's may be the legacy default stream, which
+  // cannot be captured); the instantiated graph is then launched on the caller's stream
+  CKH(h, cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
+  h->es = h->cap;
+  jkcals_status st = enqueue_sweep(h, false);
+  h->es = h->stream;
+  cudaError_t e = cudaStreamEndCapture(h->cap, &graph);
+  if (st != JKCALS_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return st;
+  }
+  if (e != cudaSuccess) return fail(h, JKCALS_E_CUDA, "graph capture: %s", cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&h->gexec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return fail(h, JKCALS_E_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  h->graph_ok = true;
+  return JKCALS_OK;
+}
+
+template <int RMAX>
+void launch_gram(jkcals_t h, int n) {
+  gram_kernel<RMAX><<<h->K, kEpiThreads, 0, h->stream>>>(h->U(n), (int)h->dims[n], h->ldu, h->R,
+                                                          h->ptr<int>(h->off.blk2sub), h->nsub, n,
+                                                          h->ptr<double>(h->off.gram));
+}
+
+jkcals_status compute_grams(jkcals_t h) {
+  for (int n = 0; n < h->N; ++n) {
+    if (h->R <= 4) launch_gram<4>(h, n);
+    else if (h->R <= 8) launch_gram<8>(h, n);
+    else launch_gram<16>(h, n);
+    CKH(h, cudaGetLastError());
+  }
+  return JKCALS_OK;
+}
+
+// (a8) compact: store converged live blocks, gather the active ones to the front.
+jkcals_status compact(jkcals_t h) {
+  std::vector<int> act(h->nsub);
+  CKH(h, cudaMemcpyAsync(act.data(), h->ptr<int>(h->off.active), sizeof(int) * h->nsub, cudaMemcpyDeviceToHost,
+                         h->stream));
+  CKH(h, cudaStreamSynchronize(h->stream));
+  int64_t sumI = 0;
+  for (int n = 0; n < h->N; ++n) sumI += h->dims[n];
+  std::vector<int> map;
+  for (int k = 0; k < h->K; ++k) {
+    int sub = h->h_blk2sub[k];
+    if (act[sub]) {
+      map.push_back(k);
+    } else if (!h->h_stored[sub]) {
+      int64_t o = 0;
+      for (int n = 0; n < h->N; ++n) {
+        int I = (int)h->dims[n];
+        double* dst = h->ptr<double>(h->off.Ures) + (int64_t)sub * sumI * h->R + o;
+        store_block_kernel<<<(int)cdiv((int64_t)I * h->R, 256), 256, 0, h->stream>>>(h->U(n), I, h->ldu, h->R, k,
+                                                                                     dst);
+        CKH(h, cudaGetLastError());
+        o += (int64_t)I * h->R;
+      }
+      h->h_stored[sub] = 1;
+    }
+  }
+  const int Knew = (int)map.size();
+  if (Knew == h->K) return JKCALS_OK;
+  std::vector<int> nb2s(std::max(Knew, 1));
+  for (int k = 0; k < Knew; ++k) nb2s[k] = h->h_blk2sub[map[k]];
+  if (Knew > 0) {
+    CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.map), map.data(), sizeof(int) * Knew, cudaMemcpyHostToDevice,
+                           h->stream));
+  }
+  const int other = h->cur ^ 1;
+  for (int n = 0; n < h->N; ++n) {
+    int64_t tot = h->dims[n] * h->ldu;
+    gather_blocks_kernel<<<(int)cdiv(tot, 256), 256, 0, h->stream>>>(
+        h->U(n), h->ptr<double>(h->off.U[other][n]), (int)h->dims[n], h->ldu, h->R, h->ptr<int>(h->off.map), Knew);
+    CKH(h, cudaGetLastError());
+  }
+  if (Knew > 0) {
+    CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.blk2sub), nb2s.data(), sizeof(int) * Knew, cudaMemcpyHostToDevice,
+                           h->stream));
+  }
+  CKH(h, cudaStreamSynchronize(h->stream));
+  h->cur = other;
+  h->h_blk2sub.assign(nb2s.begin(), nb2s.begin() + Knew);
+  h->K = Knew;
+  h->C = Knew * h->R;
+  if (Knew > 0) return replan(h);
+  return JKCALS_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+size_t jkcals_workspace_bytes(int ndims, const int64_t* dims, int rank, int64_t n_sub, jkcals_precision prec,
+                              int hist_cap, int device) {
+  if (!valid_dims(ndims, dims, rank) || n_sub < 1 || n_sub > dims[0] || hist_cap < 1) return 0;
+  if (prec != JKCALS_FP64) return 0;
+  if (n_sub * rank > (1 << 24)) return 0;
+  KernelInfo* ki = kernel_info(device, nullptr);
+  if (!ki) return 0;
+  Offsets o;
+  compute_offsets(ndims, dims, rank, n_sub, hist_cap, *ki, &o);
+  return o.total;
+}
+
+jkcals_status jkcals_create(jkcals_t* out, int ndims, const int64_t* dims, int rank, int64_t sub_begin,
+                            int64_t sub_end, const double* tensor, int tensor_is_device, jkcals_precision prec,
+                            int device, void* cuda_stream, void* workspace, size_t workspace_bytes, int hist_cap) {
+  if (!out) return JKCALS_E_ARG;
+  *out = nullptr;
+  if (!valid_dims(ndims, dims, rank) || !tensor || !workspace) return JKCALS_E_ARG;
+  if (sub_begin < 0 || sub_end > dims[0] || sub_end <= sub_begin || hist_cap < 1) return JKCALS_E_ARG;
+  if (prec != JKCALS_FP64) return JKCALS_E_ARG;  // FP32 path: not built in this round
+  DeviceGuard dg(device);
+  std::string kerr;
+  KernelInfo* ki = kernel_info(device, &kerr);
+  if (!ki) return JKCALS_E_CUDA;
+  jkcals_t h = new jkcals_s();
+  h->N = ndims;
+  for (int k = 0; k < ndims; ++k) h->dims[k] = dims[k];
+  h->R = rank;
+  h->sub_begin = sub_begin;
+  h->sub_end = sub_end;
+  h->nsub = (int)(sub_end - sub_begin);
+  h->K = h->nsub;
+  h->C = h->K * rank;
+  h->ldu = rup(std::max<int64_t>(h->C, 1), 128);
+  h->P = 1;
+  for (int k = 0; k < ndims; ++k) h->P *= dims[k];
+  h->hist_cap = hist_cap;
+  h->device = device;
+  h->stream = static_cast<cudaStream_t>(cuda_stream);
+  h->es = h->stream;
+  h->ki = ki;
+  compute_offsets(ndims, dims, rank, h->nsub, hist_cap, *ki, &h->off);
+  // align the caller's pointer
+  uintptr_t base = reinterpret_cast<uintptr_t>(workspace);
+  uintptr_t aligned = (base + kAlign - 1) & ~(uintptr_t)(kAlign - 1);
+  if (workspace_bytes < h->off.total) {
+    delete h;
+    return JKCALS_E_OOM;
+  }
+  h->ws = reinterpret_cast<char*>(aligned);
+  h->ws_bytes = workspace_bytes - (aligned - base);
+  *out = h;
+
+  CKH(h, cudaMallocHost(&h->pinned_count, sizeof(int)));
+  CKH(h, cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
+  for (auto& e : h->ev) CKH(h, cudaEventCreate(&e));
+  CKH(h, cudaMemcpyAsync(h->ptr<double>(h->off.T), tensor, sizeof(double) * h->P,
+                         tensor_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
+  std::vector<int64_t> pg(h->nsub);
+  std::vector<int> b2s(h->nsub);
+  for (int q = 0; q < h->nsub; ++q) {
+    pg[q] = sub_begin + q;
+    b2s[q] = q;
+  }
+  h->h_blk2sub = b2s;
+  h->h_stored.assign(h->nsub, 0);
+  CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.pglob), pg.data(), sizeof(int64_t) * h->nsub,
+                         cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.blk2sub), b2s.data(), sizeof(int) * h->nsub, cudaMemcpyHostToDevice,
+                         h->stream));
+  // (a0) slice norms, ||T||^2, ||T_-p||^2
+  const int64_t I0 = dims[0], J0 = h->P / I0;
+  const int nb = h->off.slice_nb;
+  const int64_t chunk = cdiv(J0, nb);
+  const int nb_eff = (int)cdiv(J0, chunk);
+  slice_norms_partial_kernel<<<nb_eff, 256, 0, h->stream>>>(h->ptr<double>(h->off.T), I0, J0, chunk,
+                                                             h->ptr<double>(h->off.slice_part));
+  CKH(h, cudaGetLastError());
+  slice_norms_final_kernel<<<1, 256, 0, h->stream>>>(h->ptr<double>(h->off.slice_part), nb_eff, I0,
+                                                     h->ptr<double>(h->off.slice),
+                                                     reinterpret_cast<double*>(h->ws + h->off.misc),
+                                                     h->ptr<int64_t>(h->off.pglob), h->nsub,
+                                                     h->ptr<double>(h->off.normT2p));
+  CKH(h, cudaGetLastError());
+  double nt2 = 0;
+  CKH(h, cudaMemcpyAsync(&nt2, h->ws + h->off.misc, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaStreamSynchronize(h->stream));
+  if (!std::isfinite(nt2)) return fail(h, JKCALS_E_NONFINITE, "tensor contains non-finite values");
+  jkcals_status st = replan(h);
+  if (st != JKCALS_OK) return st;
+  return JKCALS_OK;
+}
+
+jkcals_status jkcals_set_init(jkcals_t h, const double* const* P) {
+  if (!h || !P) return JKCALS_E_ARG;
+  DeviceGuard dg(h->device);
+  for (int n = 0; n < h->N; ++n) {
+    if (!P[n]) return fail(h, JKCALS_E_ARG, "P[%d] is NULL", n);
+    for (int64_t e = 0; e < h->dims[n] * h->R; ++e)
+      if (!std::isfinite(P[n][e])) return fail(h, JKCALS_E_NONFINITE, "P[%d] has a non-finite entry", n);
+  }
+  // full reset of the fused layout (undo any compaction)
+  bool relayout = (h->K != h->nsub) || (h->cur != 0);
+  h->cur = 0;
+  h->K = h->nsub;
+  h->C = h->K * h->R;
+  std::vector<int> b2s(h->nsub);
+  for (int q = 0; q < h->nsub; ++q) b2s[q] = q;
+  h->h_blk2sub = b2s;
+  h->h_stored.assign(h->nsub, 0);
+  CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.blk2sub), b2s.data(), sizeof(int) * h->nsub, cudaMemcpyHostToDevice,
+                         h->stream));
+  double* stage = h->ptr<double>(h->off.stage);
+  for (int n = 0; n < h->N; ++n) {
+    const int I = (int)h->dims[n];
+    CKH(h, cudaMemcpyAsync(stage, P[n], sizeof(double) * I * h->R, cudaMemcpyHostToDevice, h->stream));
+    int64_t tot = (int64_t)I * h->ldu;
+    broadcast_init_kernel<<<(int)cdiv(tot, 256), 256, 0, h->stream>>>(stage, I, h->R, h->K, h->ldu, h->U(n),
+                                                                      n == 0 ? 1 : 0, h->ptr<int>(h->off.blk2sub),
+                                                                      h->ptr<int64_t>(h->off.pglob));
+    CKH(h, cudaGetLastError());
+    CKH(h, cudaStreamSynchronize(h->stream));  // stage is reused by the next mode
+  }
+  jkcals_status st = compute_grams(h);
+  if (st != JKCALS_OK) return st;
+  reset_state_kernel<<<(int)cdiv(h->nsub, 256), 256, 0, h->stream>>>(
+      h->nsub, h->ptr<double>(h->off.fit), h->ptr<double>(h->off.fit_prev), h->ptr<double>(h->off.err),
+      h->ptr<int>(h->off.iters), h->ptr<int>(h->off.flags), h->ptr<int>(h->off.active));
+  CKH(h, cudaGetLastError());
+  CKH(h, cudaMemsetAsync(h->ptr<double>(h->off.hist), 0, sizeof(double) * h->nsub * (size_t)h->hist_cap, h->stream));
+  if (relayout) {
+    st = replan(h);
+    if (st != JKCALS_OK) return st;
+  }
+  CKH(h, cudaStreamSynchronize(h->stream));
+  h->inited = true;
+  h->ran = false;
+  return JKCALS_OK;
+}
+
+jkcals_status jkcals_set_init_submodel(jkcals_t h, int64_t p, int mode, const double* U) {
+  if (!h || !U || mode < 0 || mode >= h->N || p < h->sub_begin || p >= h->sub_end) return JKCALS_E_ARG;
+  if (!h->inited) return fail(h, JKCALS_E_STATE, "set_init must come first");
+  DeviceGuard dg(h->device);
+  const int sub = (int)(p - h->sub_begin);
+  int blk = -1;
+  for (int k = 0; k < h->K; ++k)
+    if (h->h_blk2sub[k] == sub) blk = k;
+  if (blk < 0) return fail(h, JKCALS_E_STATE, "submodel %lld was compacted out", (long long)p);
+  const int I = (int)h->dims[mode];
+  const int rows = mode == 0 ? I - 1 : I;
+  for (int64_t e = 0; e < (int64_t)rows * h->R; ++e)
+    if (!std::isfinite(U[e])) return fail(h, JKCALS_E_NONFINITE, "non-finite init");
+  double* stage = h->ptr<double>(h->off.stage);
+  CKH(h, cudaMemcpyAsync(stage, U, sizeof(double) * rows * h->R, cudaMemcpyHostToDevice, h->stream));
+  set_block_kernel<<<(int)cdiv((int64_t)I * h->R, 256), 256, 0, h->stream>>>(stage, I, h->R, h->ldu, blk,
+                                                                            mode == 0 ? p : -1, h->U(mode));
+  CKH(h, cudaGetLastError());
+  jkcals_status st = compute_grams(h);
+  if (st != JKCALS_OK) return st;
+  CKH(h, cudaStreamSynchronize(h->stream));
+  return JKCALS_OK;
+}
+
+jkcals_status jkcals_iterate(jkcals_t h, int max_iters, double tol, int* sweeps_done) {
+  if (!h || max_iters < 0) return JKCALS_E_ARG;
+  if (sweeps_done) *sweeps_done = 0;
+  if (!h->inited) return fail(h, JKCALS_E_STATE, "iterate before set_init");
+  DeviceGuard dg(h->device);
+  h->tol_host = tol;
+  CKH(h, cudaMemcpyAsync(h->ws + h->off.misc + 8, &h->tol_host, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  int it = 0;
+  for (; it < max_iters && h->K > 0; ++it) {
+    if (h->instrument) {
+      jkcals_status st = enqueue_sweep(h, true);
+      if (st != JKCALS_OK) return st;
+      CKH(h, cudaEventSynchronize(h->ev[4 * (h->N - 1) + 2]));
+      for (int n = 0; n < h->N; ++n) {
+        float a = 0, b = 0;
+        CKH(h, cudaEventElapsedTime(&a, h->ev[4 * n + 0], h->ev[4 * n + 1]));
+        CKH(h, cudaEventElapsedTime(&b, h->ev[4 * n + 1], h->ev[4 * n + 2]));
+        h->t_mttkrp[n] += a;
+        h->t_epi[n] += b;
+      }
+      h->launches += h->N;
+    } else {
+      jkcals_status st = ensure_graph(h);
+      if (st != JKCALS_OK) return st;
+      CKH(h, cudaGraphLaunch(h->gexec, h->stream));
+    }
+    if (tol > 0.0) {
+      CKH(h, cudaMemcpyAsync(h->pinned_count, h->ws + h->off.misc + 16, sizeof(int), cudaMemcpyDeviceToHost,
+                             h->stream));
+      CKH(h, cudaStreamSynchronize(h->stream));
+      const int nact = *h->pinned_count;
+      const int nconv = h->K - nact;
+      if (nact == 0 || (int64_t)nconv * h->R >= 64) {
+        jkcals_status st = compact(h);
+        if (st != JKCALS_OK) return st;
+      }
+    }
+  }
+  CKH(h, cudaStreamSynchronize(h->stream));
+  if (sweeps_done) *sweeps_done = it;
+  h->ran = true;
+  return JKCALS_OK;
+}
+
+static jkcals_status locate(jkcals_t h, int64_t p, int mode, const double** src, int64_t* ld, int* sub_out) {
+  const int sub = (int)(p - h->sub_begin);
+  *sub_out = sub;
+  if (h->h_stored[sub]) {
+    int64_t sumI = 0, o = 0;
+    for (int n = 0; n < h->N; ++n) sumI += h->dims[n];
+    for (int n = 0; n < mode; ++n) o += h->dims[n] * h->R;
+    *src = h->ptr<double>(h->off.Ures) + (int64_t)sub * sumI * h->R + o;
+    *ld = h->R;
+    return JKCALS_OK;
+  }
+  for (int k = 0; k < h->K; ++k)
+    if (h->h_blk2sub[k] == sub) {
+      *src = h->U(mode) + (int64_t)k * h->R;
+      *ld = h->ldu;
+      return JKCALS_OK;
+    }
+  return fail(h, JKCALS_E_STATE, "submodel %lld not found", (long long)p);
+}
+
+jkcals_status jkcals_get_factors(jkcals_t h, int64_t p, int mode, double* U, double* lambda) {
+  if (!h || !U || mode < 0 || mode >= h->N || p < h->sub_begin || p >= h->sub_end) return JKCALS_E_ARG;
+  if (!h->inited) return fail(h, JKCALS_E_STATE, "no model yet");
+  DeviceGuard dg(h->device);
+  const double* src;
+  int64_t ld;
+  int sub;
+  jkcals_status st = locate(h, p, mode, &src, &ld, &sub);
+  if (st != JKCALS_OK) return st;
+  const int I = (int)h->dims[mode];
+  const int rows = mode == 0 ? I - 1 : I;
+  double* stage = h->ptr<double>(h->off.stage);
+  extract_kernel<<<(int)cdiv((int64_t)rows * h->R, 256), 256, 0, h->stream>>>(src, ld, I, h->R, mode == 0 ? p : -1,
+                                                                              stage);
+  CKH(h, cudaGetLastError());
+  CKH(h, cudaMemcpyAsync(U, stage, sizeof(double) * rows * h->R, cudaMemcpyDeviceToHost, h->stream));
+  if (lambda)
+    CKH(h, cudaMemcpyAsync(lambda, h->ptr<double>(h->off.lambda) + (int64_t)sub * h->R, sizeof(double) * h->R,
+                           cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaStreamSynchronize(h->stream));
+  return JKCALS_OK;
+}
+
+jkcals_status jkcals_get_block(jkcals_t h, int64_t p, int mode, double* U) {
+  if (!h || !U || mode < 0 || mode >= h->N || p < h->sub_begin || p >= h->sub_end) return JKCALS_E_ARG;
+  if (!h->inited) return fail(h, JKCALS_E_STATE, "no model yet");
+  DeviceGuard dg(h->device);
+  const double* src;
+  int64_t ld;
+  int sub;
+  jkcals_status st = locate(h, p, mode, &src, &ld, &sub);
+  if (st != JKCALS_OK) return st;
+  const int I = (int)h->dims[mode];
+  double* stage = h->ptr<double>(h->off.stage);
+  extract_kernel<<<(int)cdiv((int64_t)I * h->R, 256), 256, 0, h->stream>>>(src, ld, I, h->R, -1, stage);
+  CKH(h, cudaGetLastError());
+  CKH(h, cudaMemcpyAsync(U, stage, sizeof(double) * I * h->R, cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaStreamSynchronize(h->stream));
+  return JKCALS_OK;
+}
+
+jkcals_status jkcals_get_status(jkcals_t h, double* fit, double* err, int* iters, int* flags) {
+  if (!h) return JKCALS_E_ARG;
+  DeviceGuard dg(h->device);
+  const size_t n = h->nsub;
+  if (fit) CKH(h, cudaMemcpyAsync(fit, h->ptr<double>(h->off.fit), 8 * n, cudaMemcpyDeviceToHost, h->stream));
+  if (err) CKH(h, cudaMemcpyAsync(err, h->ptr<double>(h->off.err), 8 * n, cudaMemcpyDeviceToHost, h->stream));
+  if (iters) CKH(h, cudaMemcpyAsync(iters, h->ptr<int>(h->off.iters), 4 * n, cudaMemcpyDeviceToHost, h->stream));
+  if (flags) CKH(h, cudaMemcpyAsync(flags, h->ptr<int>(h->off.flags), 4 * n, cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaStreamSynchronize(h->stream));
+  return JKCALS_OK;
+}
+
+jkcals_status jkcals_get_history(jkcals_t h, int64_t p, double* err, int cap, int* count) {
+  if (!h || !err || cap < 0 || p < h->sub_begin || p >= h->sub_end) return JKCALS_E_ARG;
+  DeviceGuard dg(h->device);
+  const int sub = (int)(p - h->sub_begin);
+  int it = 0;
+  CKH(h, cudaMemcpyAsync(&it, h->ptr<int>(h->off.iters) + sub, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  std::vector<double> ring(h->hist_cap);
+  CKH(h, cudaMemcpyAsync(ring.data(), h->ptr<double>(h->off.hist) + (int64_t)sub * h->hist_cap,
+                         sizeof(double) * h->hist_cap, cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaStreamSynchronize(h->stream));
+  int avail = std::min(it, h->hist_cap);
+  int nout = std::min(avail, cap);
+  // oldest first among the last `nout`
+  for (int q = 0; q < nout; ++q) {
+    int sweep = it - nout + q;  // 0-based sweep index
+    err[q] = ring[sweep % h->hist_cap];
+  }
+  if (count) *count = nout;
+  return JKCALS_OK;
+}
+
+static jkcals_status moments(jkcals_t h, int mode, double* mean_d, double* m2_d) {
+  std::vector<int64_t> off(h->nsub), ld(h->nsub);
+  for (int q = 0; q < h->nsub; ++q) {
+    const double* src;
+    int64_t l;
+    int sub;
+    jkcals_status st = locate(h, h->sub_begin + q, mode, &src, &l, &sub);
+    if (st != JKCALS_OK) return st;
+    off[q] = src - reinterpret_cast<const double*>(h->ws);
+    ld[q] = l;
+  }
+  CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.srcoff), off.data(), 8 * h->nsub, cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.srcld), ld.data(), 8 * h->nsub, cudaMemcpyHostToDevice, h->stream));
+  const int I = (int)h->dims[mode];
+  moments_kernel<<<(int)cdiv((int64_t)I * h->R, 128), 128, 0, h->stream>>>(
+      reinterpret_cast<const double*>(h->ws), h->ptr<int64_t>(h->off.srcoff), h->ptr<int64_t>(h->off.srcld),
+      h->nsub, I, h->R, mean_d, m2_d);
+  CKH(h, cudaGetLastError());
+  CKH(h, cudaStreamSynchronize(h->stream));  // off/ld host vectors go out of scope
+  return JKCALS_OK;
+}
+
+jkcals_status jkcals_get_local_moments(jkcals_t h, int mode, double* count, double* mean, double* m2) {
+  if (!h || !mean || !m2 || mode < 1 || mode >= h->N) return JKCALS_E_ARG;
+  if (!h->inited) return fail(h, JKCALS_E_STATE, "no model yet");
+  DeviceGuard dg(h->device);
+  const int64_t IR = h->dims[mode] * h->R;
+  double* stage = h->ptr<double>(h->off.stage);
+  jkcals_status st = moments(h, mode, stage, stage + IR);
+  if (st != JKCALS_OK) return st;
+  CKH(h, cudaMemcpyAsync(mean, stage, 8 * IR, cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaMemcpyAsync(m2, stage + IR, 8 * IR, cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaStreamSynchronize(h->stream));
+  if (count)
+    for (int64_t e = 0; e < IR; ++e) count[e] = (double)h->nsub;
+  return JKCALS_OK;
+}
+
+jkcals_status jkcals_get_jackknife_stats(jkcals_t h, int mode, double* mean, double* std_out) {
+  if (!h || !mean || !std_out || mode < 1 || mode >= h->N) return JKCALS_E_ARG;
+  if (h->nsub < 2) return fail(h, JKCALS_E_ARG, "jackknife statistics need >= 2 submodels");
+  const int64_t IR = h->dims[mode] * h->R;
+  std::vector<double> m2(IR);
+  jkcals_status st = jkcals_get_local_moments(h, mode, nullptr, mean, m2.data());
+  if (st != JKCALS_OK) return st;
+  const double g = (double)h->nsub;
+  for (int64_t e = 0; e < IR; ++e) std_out[e] = std::sqrt(((g - 1.0) / g) * m2[e]);
+  return JKCALS_OK;
+}
+
+jkcals_status jkcals_set_instrument(jkcals_t h, int on) {
+  if (!h) return JKCALS_E_ARG;
+  h->instrument = on != 0;
+  return JKCALS_OK;
+}
+
+jkcals_status jkcals_get_kernel_times(jkcals_t h, double* mttkrp_ms, double* epilogue_ms, int64_t* launches) {
+  if (!h) return JKCALS_E_ARG;
+  for (int n = 0; n < h->N; ++n) {
+    if (mttkrp_ms) mttkrp_ms[n] = h->t_mttkrp[n];
+    if (epilogue_ms) epilogue_ms[n] = h->t_epi[n];
+    h->t_mttkrp[n] = h->t_epi[n] = 0.0;
+  }
+  if (launches) *launches = h->launches;
+  h->launches = 0;
+  return JKCALS_OK;
+}
+
+double jkcals_sweep_flops(jkcals_t h) {
+  if (!h) return 0.0;
+  return 2.0 * (double)h->C * (double)h->P * (double)h->N;
+}
+
+int jkcals_launches_per_sweep(jkcals_t h) { return h ? 2 * h->N : 0; }
+
+const char* jkcals_last_error(jkcals_t h) { return h ? h->err.c_str() : "null handle"; }
+
+void jkcals_destroy(jkcals_t h) {
+  if (!h) return;
+  DeviceGuard dg(h->device);
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  if (h->pinned_count) cudaFreeHost(h->pinned_count);
+  if (h->cap) cudaStreamDestroy(h->cap);
+  delete h;
+}
+
+// ---------------------------------------------------------------- stand-alone ops
+size_t jkcals_mttkrp_scratch_bytes(int ndims, const int64_t* dims, int n, int64_t C, int device) {
+  if (!valid_dims(ndims, dims, 1) || n < 0 || n >= ndims || C < 1) return 0;
+  KernelInfo* ki = kernel_info(device, nullptr);
+  if (!ki) return 0;
+  int64_t P = 1;
+  for (int k = 0; k < ndims; ++k) P *= dims[k];
+  int64_t parts;
+  int tiles;
+  plan_bounds(dims[n], P / dims[n], C, *ki, &parts, &tiles);
+  return (size_t)parts * 8 + (size_t)rup(tiles * sizeof(TileInfo), kAlign) + kAlign;
+}
+
+jkcals_status jkcals_mttkrp(int ndims, const int64_t* dims, int n, const double* T, const double* const* U, int64_t C,
+                            int64_t ldu, double* M, int64_t ldm, void* scratch, size_t scratch_bytes, void* stream) {
+  if (!valid_dims(ndims, dims, 1) || n < 0 || n >= ndims || !T || !U || !M || C < 1 || ldu < C || ldm < C ||
+      (ldu % 8) != 0)
+    return JKCALS_E_ARG;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  KernelInfo* ki = kernel_info(dev, nullptr);
+  if (!ki) return JKCALS_E_CUDA;
+  if (scratch_bytes < jkcals_mttkrp_scratch_bytes(ndims, dims, n, C, dev)) return JKCALS_E_OOM;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int64_t P = 1;
+  for (int k = 0; k < ndims; ++k) P *= dims[k];
+  ModePlan p = make_plan(dims[n], P / dims[n], C, *ki);
+  uintptr_t base = (reinterpret_cast<uintptr_t>(scratch) + kAlign - 1) & ~(uintptr_t)(kAlign - 1);
+  TileInfo* ti = reinterpret_cast<TileInfo*>(base);
+  double* parts = reinterpret_cast<double*>(base + rup(p.ntiles * sizeof(TileInfo), kAlign));
+  if (cudaMemcpyAsync(ti, p.tinfo.data(), sizeof(TileInfo) * p.ntiles, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return JKCALS_E_CUDA;
+  ModeView v;
+  v.N = ndims;
+  v.n = n;
+  v.nrest = ndims - 1;
+  v.In = (int)dims[n];
+  v.J = (int)(P / dims[n]);
+  int64_t L = 1;
+  for (int m = 0; m < n; ++m) L *= dims[m];
+  v.L = (int)L;
+  v.LIn = L * dims[n];
+  int q = 0;
+  for (int m = 0; m < ndims; ++m) {
+    if (m == n) continue;
+    v.rdim[q] = (int)dims[m];
+    v.U[q] = U[m];
+    ++q;
+  }
+  for (; q < kMaxModes - 1; ++q) {
+    v.rdim[q] = 1;
+    v.U[q] = nullptr;
+  }
+  MttkrpGeom g;
+  g.C = (int)C;
+  g.ldu = ldu;
+  g.nMt = p.nMt;
+  g.nNt = p.nNt;
+  g.KT = p.KT;
+  g.units = p.units;
+  g.G = p.G;
+  ki->fn[p.W8][p.NT - 1]<<<p.G, (p.W8 ? 8 : 4) * 32, ki->smem[p.W8][p.NT - 1], s>>>(v, T, g, ti, parts);
+  if (cudaGetLastError() != cudaSuccess) return JKCALS_E_CUDA;
+  int64_t tot = dims[n] * C;
+  reduce_parts_kernel<<<(int)cdiv(tot, 256), 256, 0, s>>>(parts, ti, (int)dims[n], (int)C, p.BM, p.BN, p.nMt, M, ldm);
+  if (cudaGetLastError() != cudaSuccess) return JKCALS_E_CUDA;
+  // tinfo staging is pageable-host -> device: make sure the copy has consumed it
+  if (cudaStreamSynchronize(s) != cudaSuccess) return JKCALS_E_CUDA;
+  return JKCALS_OK;
+}
+
+jkcals_status jkcals_krp(int ndims, const int64_t* dims, int n, const double* const* U, int64_t C, int64_t ldu,
+                         double* K, int64_t ldk, void* stream) {
+  if (!valid_dims(ndims, dims, 1) || n < 0 || n >= ndims || !U || !K || C < 1 || ldu < C || ldk < C)
+    return JKCALS_E_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int64_t P = 1;
+  for (int k = 0; k < ndims; ++k) P *= dims[k];
+  ModeView v;
+  v.N = ndims;
+  v.n = n;
+  v.nrest = ndims - 1;
+  v.In = (int)dims[n];
+  v.J = (int)(P / dims[n]);
+  v.L = 1;
+  v.LIn = 0;
+  int q = 0;
+  for (int m = 0; m < ndims; ++m) {
+    if (m == n) continue;
+    v.rdim[q] = (int)dims[m];
+    v.U[q] = U[m];
+    ++q;
+  }
+  for (; q < kMaxModes - 1; ++q) {
+    v.rdim[q] = 1;
+    v.U[q] = nullptr;
+  }
+  dim3 grid((unsigned)cdiv(v.J, kKrpRows), (unsigned)cdiv(cdiv(C, 4), 256));
+  krp_gen_kernel<<<grid, 256, 0, s>>>(v, (int)C, ldu, K, ldk);
+  return cudaGetLastError() == cudaSuccess ? JKCALS_OK : JKCALS_E_CUDA;
+}
+
+}  // extern "C"

@@ -1,0 +1,80 @@
+"""Multi-GPU sharding of the submodels and cross-shard statistics.
+
+Submodels are independent ALS instances, so rank g of G fits the
+contiguous shard [floor(g I_0 / G), floor((g+1) I_0 / G)) against a full replica of T with
+NO per-iteration communication. The only collectives are end-of-run gathers over
+torch.distributed (NCCL on B200, gloo in CPU tests): per-element (count, mean, M2) of the
+jackknife factor moments, merged with Chan et al.'s pairwise formula, and the per-submodel
+fits / iteration counts.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def shard(I0, world, rank):
+    """Contiguous submodel range of `rank` out of `world` (global left-out indices)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    return (I0 * rank) // world, (I0 * (rank + 1)) // world
+
+
+def chan_merge(count_a, mean_a, m2_a, count_b, mean_b, m2_b):
+    """Merge two moment sets (Chan, Golub, LeVeque 1979): exact for any split."""
+    n = count_a + count_b
+    with np.errstate(invalid="ignore", divide="ignore"):
+        delta = mean_b - mean_a
+        wb = np.where(n > 0, count_b / np.where(n > 0, n, 1), 0.0)
+        mean = mean_a + delta * wb
+        m2 = m2_a + m2_b + delta * delta * count_a * wb
+    return n, mean, m2
+
+
+def merge_moments(parts):
+    """Fold a list of (count, mean, M2) in rank order."""
+    c, m, s = parts[0]
+    for cb, mb, sb in parts[1:]:
+        c, m, s = chan_merge(c, m, s, cb, mb, sb)
+    return c, m, s
+
+
+def jackknife_std(count, m2):
+    """Jackknife standard error sqrt(((g-1)/g) * M2)."""
+    g = count
+    return np.sqrt(np.where(g > 0, (g - 1) / np.where(g > 0, g, 1), 0.0) * m2)
+
+
+def allgather_moments(local, group=None):
+    """all_gather per-rank (count, mean, M2) arrays (same shape on every rank) and merge.
+    `local` is a tuple of numpy arrays; works for the nccl (cuda tensors) and gloo backends."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    stacked = torch.from_numpy(np.stack([np.asarray(a, dtype=np.float64) for a in local])).to(dev)
+    bufs = [torch.empty_like(stacked) for _ in range(world)]
+    dist.all_gather(bufs, stacked, group=group)
+    parts = [tuple(b.cpu().numpy()) for b in bufs]
+    return merge_moments(parts)
+
+
+def allgather_vector(vec, group=None):
+    """all_gather variable-length per-rank 1-D arrays (e.g. fits, iteration counts)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    v = torch.as_tensor(np.asarray(vec, dtype=np.float64), device=dev)
+    n = torch.tensor([v.numel()], dtype=torch.int64, device=dev)
+    ns = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(ns, n, group=group)
+    mx = int(max(int(x.item()) for x in ns))
+    pad = torch.zeros(mx, dtype=torch.float64, device=dev)
+    pad[: v.numel()] = v
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    return np.concatenate([b[: int(k.item())].cpu().numpy() for b, k in zip(bufs, ns)])

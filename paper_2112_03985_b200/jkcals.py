@@ -1,0 +1,281 @@
+"""Thin Python binding of the JK-CALS C ABI (include/jkcals.h).
+
+Argument marshalling only: every step of the hot path runs in libjkcals.so (CUDA,
+sm_100a). PyTorch provides device memory (the workspace), the CUDA stream and, in
+dist.py, process groups. There is no CPU fallback: if the library or a CUDA device
+is missing, every entry point raises.
+
+Names follow the paper (arXiv 2112.03985): T the target tensor, P the overall model
+(warm start), submodel p leaves out slice p of the sampled mode 0.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import _build
+
+FP64, FP32 = 0, 1
+F_CONVERGED, F_PINV_FALLBACK, F_NONFINITE, F_BREAKDOWN = 1, 2, 4, 8
+DEFAULT_TOL, DEFAULT_MAX_ITERS = 1e-6, 1000  # PAPER.md:596, 608 (§5.2 protocol)
+
+_STATUS = {0: "OK", -1: "E_ARG", -2: "E_SHAPE", -3: "E_STATE", -4: "E_OOM", -5: "E_CUDA", -6: "E_NONFINITE"}
+
+
+class JKCalsError(RuntimeError):
+    def __init__(self, status, msg=""):
+        super().__init__(f"jkcals {_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load libjkcals.so (building it first if the sources are newer)."""
+    global _lib
+    if _lib is None:
+        path = _build.LIB
+        if _build.stale():
+            path = _build.build()
+        L = ctypes.CDLL(path)
+        P, I, I64, D, SZ = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_size_t
+        sigs = {
+            "jkcals_workspace_bytes": (SZ, [I, P, I, I64, I, I, I]),
+            "jkcals_create": (I, [P, I, P, I, I64, I64, P, I, I, I, P, P, SZ, I]),
+            "jkcals_set_init": (I, [P, P]),
+            "jkcals_set_init_submodel": (I, [P, I64, I, P]),
+            "jkcals_iterate": (I, [P, I, D, P]),
+            "jkcals_get_factors": (I, [P, I64, I, P, P]),
+            "jkcals_get_block": (I, [P, I64, I, P]),
+            "jkcals_get_status": (I, [P, P, P, P, P]),
+            "jkcals_get_history": (I, [P, I64, P, I, P]),
+            "jkcals_get_jackknife_stats": (I, [P, I, P, P]),
+            "jkcals_get_local_moments": (I, [P, I, P, P, P]),
+            "jkcals_set_instrument": (I, [P, I]),
+            "jkcals_get_kernel_times": (I, [P, P, P, P]),
+            "jkcals_sweep_flops": (D, [P]),
+            "jkcals_launches_per_sweep": (I, [P]),
+            "jkcals_last_error": (ctypes.c_char_p, [P]),
+            "jkcals_destroy": (None, [P]),
+            "jkcals_mttkrp_scratch_bytes": (SZ, [I, P, I, I64, I]),
+            "jkcals_mttkrp": (I, [I, P, I, P, P, I64, I64, P, I64, P, SZ, P]),
+            "jkcals_krp": (I, [I, P, I, P, I64, I64, P, I64, P]),
+        }
+        for name, (res, args) in sigs.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+EXPORTED = [
+    "jkcals_workspace_bytes", "jkcals_create", "jkcals_set_init", "jkcals_set_init_submodel", "jkcals_iterate",
+    "jkcals_get_factors", "jkcals_get_block", "jkcals_get_status", "jkcals_get_history", "jkcals_get_jackknife_stats",
+    "jkcals_get_local_moments", "jkcals_set_instrument", "jkcals_get_kernel_times", "jkcals_sweep_flops",
+    "jkcals_launches_per_sweep", "jkcals_last_error", "jkcals_destroy", "jkcals_mttkrp_scratch_bytes",
+    "jkcals_mttkrp", "jkcals_krp",
+]
+
+
+def _i64(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int64))
+
+
+def _p(a):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise JKCalsError(-5, "no CUDA device: the JK-CALS path has no CPU fallback")
+    return torch
+
+
+def column_major_flat(T):
+    """Return (flat buffer, dims, is_device) with T's first index fastest (Eq. 3 layout)."""
+    try:
+        import torch
+        if isinstance(T, torch.Tensor):
+            dims = tuple(T.shape)
+            t = T.to(torch.float64).permute(*reversed(range(T.dim()))).contiguous().reshape(-1)
+            return t, dims, t.is_cuda
+    except ImportError:  # pragma: no cover
+        pass
+    a = np.asarray(T, dtype=np.float64)
+    dims = a.shape
+    return np.ravel(a, order="F"), dims, False
+
+
+class JKCals:
+    """One shard [sub_begin, sub_end) of the I_1 leave-one-out submodels on one GPU."""
+
+    def __init__(self, T, rank, sub_range=None, device=None, stream=None, hist_cap=None,
+                 precision=FP64, dims=None):
+        torch = _torch()
+        self._torch = torch
+        flat, tdims, is_dev = column_major_flat(T)
+        if dims is not None:
+            tdims = tuple(int(d) for d in dims)
+        self.dims = tuple(int(d) for d in tdims)
+        self.N, self.R = len(self.dims), int(rank)
+        if device is None:
+            device = flat.device.index if is_dev else torch.cuda.current_device()
+        self.device = int(device)
+        self.sub_begin, self.sub_end = (0, self.dims[0]) if sub_range is None else map(int, sub_range)
+        self.nsub = self.sub_end - self.sub_begin
+        self.hist_cap = int(hist_cap or DEFAULT_MAX_ITERS)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        L = lib()
+        d = _i64(self.dims)
+        nbytes = L.jkcals_workspace_bytes(self.N, _p(d), self.R, self.nsub, precision, self.hist_cap, self.device)
+        if nbytes == 0:
+            raise JKCalsError(-1, f"unsupported arguments dims={self.dims} rank={self.R} nsub={self.nsub}")
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{self.device}")
+        self._keep = flat
+        tptr = flat.data_ptr() if is_dev else flat.ctypes.data
+        h = ctypes.c_void_p()
+        st = L.jkcals_create(ctypes.byref(h), self.N, _p(d), self.R, self.sub_begin, self.sub_end,
+                             ctypes.c_void_p(tptr), 1 if is_dev else 0, precision, self.device,
+                             ctypes.c_void_p(self.stream.cuda_stream), ctypes.c_void_p(self.workspace.data_ptr()),
+                             nbytes, self.hist_cap)
+        self._h = h
+        if st != 0:
+            msg = L.jkcals_last_error(h).decode() if h.value else ""
+            self.close()
+            raise JKCalsError(st, msg)
+        self._keep = None  # the tensor now lives in the workspace
+
+    # ------------------------------------------------------------------ helpers
+    def _check(self, st):
+        if st != 0:
+            raise JKCalsError(st, lib().jkcals_last_error(self._h).decode())
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().jkcals_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ ABI
+    def set_init(self, P):
+        """Warm start from the overall model P = [U_1..U_N] (Alg. 2 alg:jk:model_subsample)."""
+        mats = [np.asfortranarray(np.asarray(p, dtype=np.float64)) for p in P]
+        for n, m in enumerate(mats):
+            if m.shape != (self.dims[n], self.R):
+                raise JKCalsError(-1, f"P[{n}] has shape {m.shape}, expected {(self.dims[n], self.R)}")
+        arr = (ctypes.c_void_p * self.N)(*[m.ctypes.data for m in mats])
+        self._check(lib().jkcals_set_init(self._h, arr))
+
+    def set_init_submodel(self, p, mode, U):
+        m = np.asfortranarray(np.asarray(U, dtype=np.float64))
+        self._check(lib().jkcals_set_init_submodel(self._h, int(p), int(mode), _p(m)))
+
+    def iterate(self, max_iters=DEFAULT_MAX_ITERS, tol=DEFAULT_TOL):
+        done = ctypes.c_int()
+        self._check(lib().jkcals_iterate(self._h, int(max_iters), float(tol), ctypes.byref(done)))
+        return done.value
+
+    def factors(self, p):
+        """Submodel p: ([U_0 ((I_0-1) x R, row p dropped), U_1, ...], lambda)."""
+        out, lam = [], np.zeros(self.R)
+        for n in range(self.N):
+            rows = self.dims[n] - 1 if n == 0 else self.dims[n]
+            U = np.zeros((rows, self.R), order="F")
+            self._check(lib().jkcals_get_factors(self._h, int(p), n, _p(U), _p(lam) if n == self.N - 1 else None))
+            out.append(U)
+        return out, lam
+
+    def block(self, p, mode):
+        """Submodel p's full fused block of mode `mode` (mode 0 keeps the zero row p)."""
+        U = np.zeros((self.dims[mode], self.R), order="F")
+        self._check(lib().jkcals_get_block(self._h, int(p), int(mode), _p(U)))
+        return U
+
+    def status(self):
+        fit, err = np.zeros(self.nsub), np.zeros(self.nsub)
+        it, fl = np.zeros(self.nsub, dtype=np.int32), np.zeros(self.nsub, dtype=np.int32)
+        self._check(lib().jkcals_get_status(self._h, _p(fit), _p(err), _p(it), _p(fl)))
+        return {"fit": fit, "err": err, "iters": it, "flags": fl}
+
+    def history(self, p, cap=None):
+        cap = cap or self.hist_cap
+        buf, cnt = np.zeros(cap), ctypes.c_int()
+        self._check(lib().jkcals_get_history(self._h, int(p), _p(buf), cap, ctypes.byref(cnt)))
+        return buf[: cnt.value]
+
+    def jackknife_stats(self, mode):
+        mean = np.zeros((self.dims[mode], self.R), order="F")
+        std = np.zeros((self.dims[mode], self.R), order="F")
+        self._check(lib().jkcals_get_jackknife_stats(self._h, int(mode), _p(mean), _p(std)))
+        return mean, std
+
+    def local_moments(self, mode):
+        shp = (self.dims[mode], self.R)
+        cnt, mean, m2 = (np.zeros(shp, order="F") for _ in range(3))
+        self._check(lib().jkcals_get_local_moments(self._h, int(mode), _p(cnt), _p(mean), _p(m2)))
+        return cnt, mean, m2
+
+    def set_instrument(self, on=True):
+        self._check(lib().jkcals_set_instrument(self._h, 1 if on else 0))
+
+    def kernel_times(self):
+        a, b, n = np.zeros(self.N), np.zeros(self.N), ctypes.c_int64()
+        self._check(lib().jkcals_get_kernel_times(self._h, _p(a), _p(b), ctypes.byref(n)))
+        return a, b, n.value
+
+    def sweep_flops(self):
+        return lib().jkcals_sweep_flops(self._h)
+
+    def launches_per_sweep(self):
+        return lib().jkcals_launches_per_sweep(self._h)
+
+
+# ---------------------------------------------------------------------- stand-alone ops
+def mttkrp(T_flat, dims, n, U, C):
+    """Fused MTTKRP on device tensors. T_flat: float64 cuda, column-major flat; U: list of
+    row-major (dims[m], ldu) float64 cuda tensors (U[n] may be any placeholder).
+    Returns M (dims[n], C) row-major torch tensor."""
+    torch = _torch()
+    L = lib()
+    d = _i64(dims)
+    ldu = U[(n + 1) % len(dims)].shape[1]
+    dev = T_flat.device.index
+    nb = L.jkcals_mttkrp_scratch_bytes(len(dims), _p(d), n, C, dev)
+    if nb == 0:
+        raise JKCalsError(-1, "unsupported mttkrp arguments")
+    scratch = torch.empty(nb, dtype=torch.uint8, device=T_flat.device)
+    M = torch.empty((dims[n], C), dtype=torch.float64, device=T_flat.device)
+    ptrs = (ctypes.c_void_p * len(dims))(*[u.data_ptr() for u in U])
+    st = L.jkcals_mttkrp(len(dims), _p(d), n, ctypes.c_void_p(T_flat.data_ptr()), ptrs, C, ldu,
+                         ctypes.c_void_p(M.data_ptr()), C, ctypes.c_void_p(scratch.data_ptr()), nb,
+                         ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+    if st != 0:
+        raise JKCalsError(st, "jkcals_mttkrp failed")
+    return M
+
+
+def krp(dims, n, U, C, out=None):
+    """Materialised Khatri-Rao product K (J_n, C) row-major on the device."""
+    torch = _torch()
+    d = _i64(dims)
+    J = int(np.prod([dims[m] for m in range(len(dims)) if m != n]))
+    ldu = U[(n + 1) % len(dims)].shape[1]
+    dev = U[(n + 1) % len(dims)].device
+    if out is None:
+        out = torch.empty((J, C), dtype=torch.float64, device=dev)
+    ptrs = (ctypes.c_void_p * len(dims))(*[u.data_ptr() for u in U])
+    st = lib().jkcals_krp(len(dims), _p(d), n, ptrs, C, ldu, ctypes.c_void_p(out.data_ptr()), out.shape[1],
+                          ctypes.c_void_p(torch.cuda.current_stream(dev.index).cuda_stream))
+    if st != 0:
+        raise JKCalsError(st, "jkcals_krp failed")
+    return out

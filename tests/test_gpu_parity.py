@@ -1,0 +1,250 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, element by element.
+
+Bar (BASELINE.json north_star): FP64 factors within 1e-10 relative Frobenius of the oracle
+from identical initial factors and a fixed sweep count. The per-sweep error is compared with
+|e_gpu - e_orc| <= 1e-9 |e_orc| + 1e-13 ||T_-p||^2 (e is a difference
+of O(||T||^2) terms, so its absolute rounding is O(eps ||T||^2)).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from synth import make_workload
+
+pytestmark = pytest.mark.gpu
+
+FTOL = 1e-10
+NCPU = os.cpu_count() or 1
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def run_gpu(w, sweeps, tol=0.0, sub_range=None, hist_cap=None, instrument=False):
+    from paper_2112_03985_b200 import JKCals
+    h = JKCals(w.T, w.R, sub_range=sub_range, hist_cap=hist_cap or max(sweeps, 1))
+    h.set_init(w.P)
+    if instrument:
+        h.set_instrument(True)
+    done = h.iterate(sweeps, tol)
+    return h, done
+
+
+def check_against_oracle(h, res, p_list, nt2p=None):
+    st = h.status()
+    for q, p in enumerate(p_list):
+        fac, lam = h.factors(p)
+        for n, (a, b) in enumerate(zip(fac, res.factors[q])):
+            assert rel(a, b) <= FTOL, (p, n, rel(a, b))
+        assert rel(lam, res.lam[q]) <= FTOL, (p, rel(lam, res.lam[q]))
+        hg, ho = h.history(p), res.history(q)
+        assert len(hg) == len(ho) == res.iters[q]
+        scale = nt2p[p] if nt2p is not None else abs(ho).max()
+        assert np.all(np.abs(hg - ho) <= 1e-9 * np.abs(ho) + 1e-13 * scale), (p, np.abs(hg - ho).max())
+        sub = p - h.sub_begin
+        assert st["iters"][sub] == res.iters[q]
+        assert (st["flags"][sub] & ~1) == (res.flags[q] & ~1), (p, st["flags"][sub], res.flags[q])
+        # padded-row invariant: row p of the mode-0 block is exactly zero
+        blk = h.block(p, 0)
+        assert np.all(blk[p] == 0.0)
+
+
+def nt2p_of(T):
+    n2 = O.norm_sq(T)
+    return n2 - O.slice_norms_sq(T, 0)
+
+
+# ---------------------------------------------------------------- kernel-level parity
+MTTKRP_CASES = [
+    ((10, 8, 6), 20), ((50, 50, 50), 50), ((50, 50, 50), 250), ((37, 23, 11), 129),
+    ((13, 7, 5, 3), 70), ((268, 30, 9), 33), ((5, 300, 4), 10), ((3, 2, 2), 1), ((17, 3, 4, 2, 3), 24),
+]
+
+
+@pytest.mark.parametrize("dims,C", MTTKRP_CASES)
+def test_mttkrp_kernel_vs_oracle(dims, C):
+    import torch
+    from paper_2112_03985_b200 import mttkrp
+    g = np.random.default_rng(sum(dims) + C)
+    T = np.asfortranarray(g.standard_normal(dims))
+    U = [g.standard_normal((I, C)) for I in dims]
+    ldu = ((C + 127) // 128) * 128
+    Ud = []
+    for u in U:
+        pad = np.zeros((u.shape[0], ldu))
+        pad[:, :C] = u
+        Ud.append(torch.from_numpy(pad).cuda())
+    Td = torch.from_numpy(np.ravel(T, order="F").copy()).cuda()
+    for n in range(len(dims)):
+        M = mttkrp(Td, dims, n, Ud, C).cpu().numpy()
+        ref = O.mttkrp(T, U, n)
+        scale = np.abs(ref).max()
+        assert np.allclose(M, ref, rtol=1e-12, atol=1e-12 * scale), (dims, C, n, np.abs(M - ref).max() / scale)
+
+
+def test_krp_kernel_vs_khatri_rao():
+    import torch
+    from paper_2112_03985_b200 import krp
+    g = np.random.default_rng(3)
+    dims, C = (7, 6, 5, 4), 13
+    U = [g.standard_normal((I, C)) for I in dims]
+    ldu = 16
+    Ud = []
+    for u in U:
+        pad = np.zeros((u.shape[0], ldu))
+        pad[:, :C] = u
+        Ud.append(torch.from_numpy(pad).cuda())
+    for n in range(4):
+        K = krp(dims, n, Ud, C).cpu().numpy()
+        rest = [m for m in range(4) if m != n]
+        ref = U[rest[0]]
+        for m in rest[1:]:
+            ref = O.khatri_rao(U[m], ref)  # descending KRP, earliest mode fastest (Eq. 1/3)
+        assert np.array_equal(K, ref) or np.allclose(K, ref, rtol=1e-15, atol=0)
+
+
+# ---------------------------------------------------------------- JK-CALS vs JK-ALS
+def test_tiny_all_submodels():
+    w = make_workload("tiny")
+    h, done = run_gpu(w, w.sweeps)
+    assert done == w.sweeps
+    res = O.jk_als(w.T, w.P, max_iters=w.sweeps, nthreads=NCPU)
+    check_against_oracle(h, res, range(10), nt2p_of(w.T))
+
+
+@pytest.mark.parametrize("R", [1, 2, 3, 4, 5])
+def test_syn50_all_submodels(R):
+    w = make_workload(f"syn50_r{R}")
+    h, _ = run_gpu(w, w.sweeps)
+    res = O.jk_als(w.T, w.P, max_iters=w.sweeps, nthreads=NCPU)
+    check_against_oracle(h, res, range(50), nt2p_of(w.T))
+
+
+def test_edge_two_samples_rank1():
+    w = make_workload(((2, 3, 4), 1, 1, 0.05, "syn", 30), seed=2)
+    h, _ = run_gpu(w, 30)
+    res = O.jk_als(w.T, w.P, max_iters=30)
+    check_against_oracle(h, res, range(2), nt2p_of(w.T))
+
+
+def test_edge_five_way_ragged():
+    w = make_workload(((9, 5, 3, 4, 2), 3, 3, 0.02, "syn", 25), seed=4)
+    h, _ = run_gpu(w, 25)
+    res = O.jk_als(w.T, w.P, max_iters=25, nthreads=NCPU)
+    check_against_oracle(h, res, range(9), nt2p_of(w.T))
+
+
+def test_sampled_large_configs_4way():
+    w = make_workload("4way")
+    h, _ = run_gpu(w, w.sweeps)
+    ps = [0, 1, 50, 99]
+    res = O.jk_als(w.T, w.P, p_list=ps, max_iters=w.sweeps, nthreads=NCPU)
+    check_against_oracle(h, res, ps, nt2p_of(w.T))
+
+
+@pytest.mark.parametrize("name", ["eem_r3", "eem_r5"])
+def test_sampled_eem(name):
+    w = make_workload(name)
+    h, _ = run_gpu(w, w.sweeps)
+    ps = [0, 133, 267]
+    res = O.jk_als(w.T, w.P, p_list=ps, max_iters=w.sweeps, nthreads=NCPU)
+    check_against_oracle(h, res, ps, nt2p_of(w.T))
+
+
+def test_sampled_syn200_bench_config():
+    w = make_workload("syn200")
+    h, _ = run_gpu(w, w.sweeps)
+    ps = [0, 1, 100, 199]
+    res = O.jk_als(w.T, w.P, p_list=ps, max_iters=w.sweeps, nthreads=NCPU)
+    check_against_oracle(h, res, ps, nt2p_of(w.T))
+
+
+# ---------------------------------------------------------------- modes of operation
+def test_tolerance_mode_and_compaction():
+    w = make_workload("syn50_r3")
+    h, done = run_gpu(w, 1000, tol=1e-6, hist_cap=1000)
+    res = O.jk_als(w.T, w.P, max_iters=1000, tol=1e-6, nthreads=NCPU)
+    assert done <= 1000
+    assert len(set(res.iters.tolist())) > 1  # submodels converge at different sweeps
+    check_against_oracle(h, res, range(50), nt2p_of(w.T))
+
+
+def test_shards_equal_full_and_merge():
+    from paper_2112_03985_b200.dist import jackknife_std, merge_moments
+    w = make_workload("syn50_r2")
+    full, _ = run_gpu(w, 40)
+    a, _ = run_gpu(w, 40, sub_range=(0, 20))
+    b, _ = run_gpu(w, 40, sub_range=(20, 50))
+    for p in range(50):
+        src = a if p < 20 else b
+        for x, y in zip(src.factors(p)[0], full.factors(p)[0]):
+            assert rel(x, y) <= 1e-13
+    for mode in (1, 2):
+        mean, std = full.jackknife_stats(mode)
+        c, m, s = merge_moments([a.local_moments(mode), b.local_moments(mode)])
+        assert np.allclose(m, mean, rtol=1e-13, atol=1e-15)
+        assert np.allclose(jackknife_std(c, s), std, rtol=1e-10, atol=1e-15)
+
+
+def test_jackknife_stats_vs_oracle():
+    w = make_workload("tiny")
+    h, _ = run_gpu(w, w.sweeps)
+    res = O.jk_als(w.T, w.P, max_iters=w.sweeps, nthreads=NCPU)
+    for mode in (1, 2):
+        X = np.stack([res.factors[q][mode] for q in range(10)])
+        m_o, s_o = O.jackknife_stats(X)
+        m_g, s_g = h.jackknife_stats(mode)
+        assert rel(m_g, m_o) <= FTOL and rel(s_g, s_o) <= 1e-8
+
+
+def test_pinv_fallback_is_per_submodel():
+    # a zero column in one submodel's mode-1 init makes its H singular; only
+    # that submodel takes the pseudoinverse path, and it still matches the oracle.
+    from paper_2112_03985_b200 import JKCals
+    w = make_workload("tiny")
+    h = JKCals(w.T, w.R, hist_cap=20)
+    h.set_init(w.P)
+    bad = w.P[1].copy()
+    bad[:, 1] = 0.0
+    h.set_init_submodel(3, 1, bad)
+    h.iterate(20, 0.0)
+    st = h.status()
+    assert st["flags"][3] & 2 and not np.any(np.delete(st["flags"], 3) & 2)
+    res = O.jk_als(w.T, w.P, p_list=[0, 5], max_iters=20)
+    check_against_oracle(h, res, [0, 5])
+    Pb = [w.P[0], bad, w.P[2]]
+    res3 = O.jk_als(w.T, Pb, p_list=[3], max_iters=20)
+    assert res3.flags[0] & 2
+    fac, _ = h.factors(3)
+    for a, b in zip(fac, res3.factors[0]):
+        assert rel(a, b) <= 1e-9
+
+
+def test_deterministic_and_graph_equals_eager():
+    w = make_workload("syn50_r2")
+    h1, _ = run_gpu(w, 15)
+    h2, _ = run_gpu(w, 15)
+    h3, _ = run_gpu(w, 15, instrument=True)
+    for p in (0, 17, 49):
+        for a, b, c in zip(h1.factors(p)[0], h2.factors(p)[0], h3.factors(p)[0]):
+            assert np.array_equal(a, b) and np.array_equal(a, c)
+    t_m, t_e, launches = h3.kernel_times()
+    assert launches == 15 * 3 and np.all(t_m > 0) and np.all(t_e > 0)
+
+
+def test_abi_errors():
+    from paper_2112_03985_b200 import JKCals, JKCalsError
+    w = make_workload("tiny")
+    h = JKCals(w.T, 2)
+    with pytest.raises(JKCalsError):
+        h.iterate(1, 0.0)  # before set_init -> E_STATE
+    with pytest.raises(JKCalsError):
+        h.set_init([np.full((10, 2), np.nan), w.P[1], w.P[2]])
+    with pytest.raises(JKCalsError):
+        JKCals(np.full((3, 3, 3), np.inf), 1)
+    with pytest.raises(JKCalsError):
+        JKCals(w.T, 2, sub_range=(4, 11))
