@@ -154,8 +154,8 @@ void jkcals_destroy(jkcals_t h);
 
 /* Fused MTTKRP (Eq. 1 / Alg. 3 alg:cals_jk:mttkrp) on device data:
  *   M(i, c) = sum_j T_(n)(i, j) * prod_{m != n} U_m(i_m(j), c),  c < C,
- * T device FP64 column-major; U[m] device row-major dims[m] x ldu (C <= ldu; ldu % 8 == 0 and
- * columns [C, round_up(C,128)) readable); M device row-major dims[n] x ldm. scratch is device
+ * T device FP64 column-major; U[m] device row-major dims[m] x ldu, 16-byte aligned, ldu even and
+ * ldu >= C (ldu >= C + 1 when C is odd); M device row-major dims[n] x ldm. scratch is device
  * memory of jkcals_mttkrp_scratch_bytes(...) bytes. Enqueued on `stream`; returns E_CUDA on a
  * launch error. */
 size_t jkcals_mttkrp_scratch_bytes(int ndims, const int64_t *dims, int n, int64_t C, int device);

@@ -24,30 +24,30 @@ using namespace jk;
 
 namespace {
 
-constexpr int kMaxNT = 16;
 constexpr size_t kAlign = 256;
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
 
 // ---------------------------------------------------------------- kernel dispatch tables
-typedef void (*MttkrpFn)(ModeView, const double*, MttkrpGeom, const TileInfo*, double*);
+typedef void (*MttkrpFn)(MttkrpView, const double*, MttkrpGeom, const TileInfo*, double*);
 
-template <int NT, int W>
-MttkrpFn mttkrp_ptr() { return mttkrp_dmma_kernel<NT, W>; }
+template <int NT, bool KM, int ST>
+size_t smem_of(int nslow) { return MttkrpCfg<NT, KM, ST>::smem_bytes(nslow); }
+typedef size_t (*SmemFn)(int);
 
-template <int W, int... NTs>
+template <bool KM, int ST, int... NTs>
 struct Table {
-  static void fill(MttkrpFn* fns, size_t* smem) {
+  static void fill(MttkrpFn* fns, SmemFn* sm) {
     int i = 0;
-    ((fns[i] = mttkrp_ptr<NTs, W>(), smem[i] = MttkrpCfg<NTs, W>::kSmem, ++i), ...);
+    ((fns[i] = mttkrp_dmma_kernel<NTs, KM, ST>, sm[i] = smem_of<NTs, KM, ST>, ++i), ...);
   }
 };
 
 struct KernelInfo {
-  MttkrpFn fn[2][kMaxNT];  // [W==8][NT-1]
-  size_t smem[2][kMaxNT];
-  int occ[2][kMaxNT];
+  MttkrpFn fn[2][2][kMaxNT];         // [KMAJOR][STAGES==4][NT-1]
+  SmemFn smem[2][2][kMaxNT];
+  int occ[2][2][kMaxNT][kMaxModes];  // [..][nslow]
   int nsm;
 };
 
@@ -57,51 +57,77 @@ KernelInfo* kernel_info(int device, std::string* err) {
   if (device < 0 || device >= 16) return nullptr;
   if (ready[device]) return &info[device];
   KernelInfo& ki = info[device];
-  Table<4, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>::fill(ki.fn[0], ki.smem[0]);
-  Table<8, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>::fill(ki.fn[1], ki.smem[1]);
+  Table<false, 2, 1, 2, 3, 4, 5, 6, 7, 8>::fill(ki.fn[0][0], ki.smem[0][0]);
+  Table<false, 4, 1, 2, 3, 4, 5, 6, 7, 8>::fill(ki.fn[0][1], ki.smem[0][1]);
+  Table<true, 2, 1, 2, 3, 4, 5, 6, 7, 8>::fill(ki.fn[1][0], ki.smem[1][0]);
+  Table<true, 4, 1, 2, 3, 4, 5, 6, 7, 8>::fill(ki.fn[1][1], ki.smem[1][1]);
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
   cudaDeviceGetAttribute(&ki.nsm, cudaDevAttrMultiProcessorCount, device);
-  for (int w = 0; w < 2; ++w)
-    for (int t = 0; t < kMaxNT; ++t) {
-      cudaError_t e = cudaFuncSetAttribute(ki.fn[w][t], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)ki.smem[w][t]);
-      if (e != cudaSuccess) {
-        if (err) *err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e);
-        cudaSetDevice(prev);
-        return nullptr;
+  for (int km = 0; km < 2; ++km)
+    for (int st = 0; st < 2; ++st)
+      for (int t = 0; t < kMaxNT; ++t) {
+        cudaError_t e = cudaFuncSetAttribute(ki.fn[km][st][t], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)ki.smem[km][st][t](kMaxModes - 2));
+        if (e != cudaSuccess) {
+          if (err) *err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e);
+          cudaSetDevice(prev);
+          return nullptr;
+        }
+        for (int ns = 1; ns <= kMaxModes - 2; ++ns) {
+          int occ = 0;
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ki.fn[km][st][t], kWarps * 32,
+                                                        ki.smem[km][st][t](ns));
+          ki.occ[km][st][t][ns] = std::max(1, occ);
+        }
       }
-      int occ = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ki.fn[w][t], (w ? 8 : 4) * 32, ki.smem[w][t]);
-      ki.occ[w][t] = std::max(1, occ);
-    }
   cudaSetDevice(prev);
   ready[device] = true;
   return &ki;
 }
 
 // ---------------------------------------------------------------- per-mode plan
+// q0 = fastest rest mode (mode 1 when n == 0, else mode 0); J' = product of the others.
+struct ModeGeo {
+  int64_t In, Iq0, Jp;
+  int q0, nslow;
+};
+
+ModeGeo mode_geo(int N, const int64_t* dims, int n) {
+  ModeGeo g;
+  g.In = dims[n];
+  g.q0 = (n == 0) ? 1 : 0;
+  g.Iq0 = dims[g.q0];
+  g.Jp = 1;
+  for (int m = 0; m < N; ++m)
+    if (m != n && m != g.q0) g.Jp *= dims[m];
+  g.nslow = N - 2;
+  return g;
+}
+
 struct ModePlan {
-  int NT = 1, W8 = 1, BM = 128, BN = 8, nMt = 1, nNt = 1, KT = 1, G = 1;
+  int NT = 1, KM = 0, ST4 = 1, BN = 8, nMt = 1, nNt = 1, KT = 1, G = 1;
   int64_t units = 1;
   int ntiles = 1, npieces = 1;
+  size_t smem = 0;
   std::vector<TileInfo> tinfo;
 };
 
-ModePlan make_plan(int64_t In, int64_t J, int64_t C, const KernelInfo& ki) {
+ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki) {
   ModePlan p;
-  int64_t nI8 = cdiv(In, 8);
+  int64_t nI8 = cdiv(mg.In, 8);
   p.nNt = (int)cdiv(nI8, kMaxNT);
   p.NT = (int)cdiv(nI8, p.nNt);
   p.BN = p.NT * 8;
-  p.W8 = (C > 64) ? 1 : 0;
-  p.BM = p.W8 ? 128 : 64;
-  p.nMt = (int)std::max<int64_t>(1, cdiv(C, p.BM));
-  p.KT = (int)cdiv(J, kBK);
+  p.KM = (n != 0) ? 1 : 0;
+  p.ST4 = (mg.Jp >= 3) ? 1 : 0;  // the U_q0 slab double buffer needs J' >= STAGES - 1
+  p.nMt = (int)std::max<int64_t>(1, cdiv(C, kBM));
+  p.KT = (int)(cdiv(mg.Iq0, kBK) * mg.Jp);
   p.ntiles = p.nMt * p.nNt;
   p.units = (int64_t)p.ntiles * p.KT;
-  int64_t gmax = (int64_t)ki.nsm * ki.occ[p.W8][p.NT - 1];
+  p.smem = ki.smem[p.KM][p.ST4][p.NT - 1](mg.nslow);
+  int64_t gmax = (int64_t)ki.nsm * ki.occ[p.KM][p.ST4][p.NT - 1][mg.nslow];
   p.G = (int)std::min<int64_t>(p.units, gmax);
   std::vector<int> first(p.ntiles, -1), lastc(p.ntiles, -1);
   for (int b = 0; b < p.G; ++b) {
@@ -126,23 +152,43 @@ ModePlan make_plan(int64_t In, int64_t J, int64_t C, const KernelInfo& ki) {
   return p;
 }
 
-int64_t plan_parts_doubles(const ModePlan& p) { return (int64_t)p.npieces * p.BN * p.BM; }
+int64_t plan_parts_doubles(const ModePlan& p) { return (int64_t)p.npieces * p.BN * kBM; }
 
-// upper bound over both warp variants, for workspace sizing
-void plan_bounds(int64_t In, int64_t J, int64_t C, const KernelInfo& ki, int64_t* parts, int* tiles) {
-  *parts = 0;
-  *tiles = 0;
-  for (int w8 = 0; w8 < 2; ++w8) {
-    int64_t nI8 = cdiv(In, 8);
-    int nNt = (int)cdiv(nI8, kMaxNT), NT = (int)cdiv(nI8, nNt);
-    int BM = w8 ? 128 : 64, BN = NT * 8;
-    int nMt = (int)std::max<int64_t>(1, cdiv(C, BM));
-    int64_t KT = cdiv(J, kBK);
-    int ntiles = nMt * nNt;
-    int64_t G = std::min<int64_t>((int64_t)ntiles * KT, (int64_t)ki.nsm * ki.occ[w8][NT - 1]);
-    *parts = std::max(*parts, (G + ntiles) * BN * BM);
-    *tiles = std::max(*tiles, ntiles);
+// upper bound for workspace sizing (any C' <= C)
+void plan_bounds(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, int64_t* parts, int* tiles) {
+  ModePlan p = make_plan(mg, n, C, ki);
+  *parts = (int64_t)(p.G + p.ntiles) * p.BN * kBM;
+  *tiles = p.ntiles;
+}
+
+MttkrpView make_mview(int N, const int64_t* dims, int n, const double* const* Uall) {
+  ModeGeo mg = mode_geo(N, dims, n);
+  MttkrpView v;
+  v.In = (int)mg.In;
+  v.Iq0 = (int)mg.Iq0;
+  v.nb0 = (int)cdiv(mg.Iq0, kBK);
+  v.Jp = (int)mg.Jp;
+  int64_t stride[kMaxModes];
+  stride[0] = 1;
+  for (int m = 1; m < N; ++m) stride[m] = stride[m - 1] * dims[m - 1];
+  v.stride_n = stride[n];
+  v.stride_q0 = stride[mg.q0];
+  v.nslow = N - 2;
+  v.Uq0 = Uall[mg.q0];
+  int s = 0;
+  for (int m = 0; m < N; ++m) {
+    if (m == n || m == mg.q0) continue;
+    v.sdim[s] = (int)dims[m];
+    v.sstride[s] = stride[m];
+    v.Us[s] = Uall[m];
+    ++s;
   }
+  for (; s < kMaxModes - 2; ++s) {
+    v.sdim[s] = 1;
+    v.sstride[s] = 0;
+    v.Us[s] = nullptr;
+  }
+  return v;
 }
 
 // ---------------------------------------------------------------- workspace layout
@@ -184,7 +230,7 @@ bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_c
   for (int n = 0; n < N; ++n) {
     int64_t pc;
     int tc;
-    plan_bounds(dims[n], P / dims[n], C, ki, &pc, &tc);
+    plan_bounds(mode_geo(N, dims, n), n, C, ki, &pc, &tc);
     o->parts_cap = std::max(o->parts_cap, pc);
     o->tiles_cap = std::max(o->tiles_cap, tc);
   }
@@ -301,34 +347,9 @@ struct DeviceGuard {
   }
 };
 
-ModeView make_view(jkcals_t h, int n, double* const* Uall) {
-  ModeView v;
-  v.N = h->N;
-  v.n = n;
-  v.nrest = h->N - 1;
-  v.In = (int)h->dims[n];
-  v.J = (int)(h->P / h->dims[n]);
-  int64_t L = 1;
-  for (int m = 0; m < n; ++m) L *= h->dims[m];
-  v.L = (int)L;
-  v.LIn = L * h->dims[n];
-  int q = 0;
-  for (int m = 0; m < h->N; ++m) {
-    if (m == n) continue;
-    v.rdim[q] = (int)h->dims[m];
-    v.U[q] = Uall[m];
-    ++q;
-  }
-  for (; q < kMaxModes - 1; ++q) {
-    v.rdim[q] = 1;
-    v.U[q] = nullptr;
-  }
-  return v;
-}
-
 jkcals_status replan(jkcals_t h) {
   for (int n = 0; n < h->N; ++n) {
-    h->plan[n] = make_plan(h->dims[n], h->P / h->dims[n], h->C, *h->ki);
+    h->plan[n] = make_plan(mode_geo(h->N, h->dims, n), n, h->C, *h->ki);
     const ModePlan& p = h->plan[n];
     if (plan_parts_doubles(p) > h->off.parts_cap || p.ntiles > h->off.tiles_cap)
       return fail(h, JKCALS_E_OOM, "internal: plan exceeds workspace bounds");
@@ -353,7 +374,7 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
   double* Uall[kMaxModes];
   for (int m = 0; m < h->N; ++m) Uall[m] = h->U(m);
   const ModePlan& p = h->plan[n];
-  ModeView v = make_view(h, n, Uall);
+  MttkrpView v = make_mview(h->N, h->dims, n, Uall);
   MttkrpGeom g;
   g.C = h->C;
   g.ldu = h->ldu;
@@ -364,9 +385,9 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
   g.G = p.G;
   const TileInfo* ti = h->ptr<TileInfo>(h->off.tinfo[n]);
   double* parts = h->ptr<double>(h->off.parts);
-  MttkrpFn fn = h->ki->fn[p.W8][p.NT - 1];
+  MttkrpFn fn = h->ki->fn[p.KM][p.ST4][p.NT - 1];
   if (timed) CKH(h, cudaEventRecord(h->ev[4 * n + 0], h->es));
-  fn<<<p.G, (p.W8 ? 8 : 4) * 32, h->ki->smem[p.W8][p.NT - 1], h->es>>>(v, h->ptr<double>(h->off.T), g, ti,
+  fn<<<p.G, kWarps * 32, p.smem, h->es>>>(v, h->ptr<double>(h->off.T), g, ti,
                                                                              parts);
   CKH(h, cudaGetLastError());
   if (timed) CKH(h, cudaEventRecord(h->ev[4 * n + 1], h->es));
@@ -382,7 +403,7 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
   a.pglob = h->ptr<int64_t>(h->off.pglob);
   a.parts = parts;
   a.tinfo = ti;
-  a.BM = p.BM;
+  a.BM = kBM;
   a.BN = p.BN;
   a.nMt = p.nMt;
   a.gram = h->ptr<double>(h->off.gram);
@@ -912,14 +933,14 @@ size_t jkcals_mttkrp_scratch_bytes(int ndims, const int64_t* dims, int n, int64_
   for (int k = 0; k < ndims; ++k) P *= dims[k];
   int64_t parts;
   int tiles;
-  plan_bounds(dims[n], P / dims[n], C, *ki, &parts, &tiles);
+  plan_bounds(mode_geo(ndims, dims, n), n, C, *ki, &parts, &tiles);
   return (size_t)parts * 8 + (size_t)rup(tiles * sizeof(TileInfo), kAlign) + kAlign;
 }
 
 jkcals_status jkcals_mttkrp(int ndims, const int64_t* dims, int n, const double* T, const double* const* U, int64_t C,
                             int64_t ldu, double* M, int64_t ldm, void* scratch, size_t scratch_bytes, void* stream) {
   if (!valid_dims(ndims, dims, 1) || n < 0 || n >= ndims || !T || !U || !M || C < 1 || ldu < C || ldm < C ||
-      (ldu % 8) != 0)
+      (ldu % 2) != 0 || (C % 2 == 1 && ldu < C + 1))
     return JKCALS_E_ARG;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -929,33 +950,13 @@ jkcals_status jkcals_mttkrp(int ndims, const int64_t* dims, int n, const double*
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int64_t P = 1;
   for (int k = 0; k < ndims; ++k) P *= dims[k];
-  ModePlan p = make_plan(dims[n], P / dims[n], C, *ki);
+  ModePlan p = make_plan(mode_geo(ndims, dims, n), n, C, *ki);
   uintptr_t base = (reinterpret_cast<uintptr_t>(scratch) + kAlign - 1) & ~(uintptr_t)(kAlign - 1);
   TileInfo* ti = reinterpret_cast<TileInfo*>(base);
   double* parts = reinterpret_cast<double*>(base + rup(p.ntiles * sizeof(TileInfo), kAlign));
   if (cudaMemcpyAsync(ti, p.tinfo.data(), sizeof(TileInfo) * p.ntiles, cudaMemcpyHostToDevice, s) != cudaSuccess)
     return JKCALS_E_CUDA;
-  ModeView v;
-  v.N = ndims;
-  v.n = n;
-  v.nrest = ndims - 1;
-  v.In = (int)dims[n];
-  v.J = (int)(P / dims[n]);
-  int64_t L = 1;
-  for (int m = 0; m < n; ++m) L *= dims[m];
-  v.L = (int)L;
-  v.LIn = L * dims[n];
-  int q = 0;
-  for (int m = 0; m < ndims; ++m) {
-    if (m == n) continue;
-    v.rdim[q] = (int)dims[m];
-    v.U[q] = U[m];
-    ++q;
-  }
-  for (; q < kMaxModes - 1; ++q) {
-    v.rdim[q] = 1;
-    v.U[q] = nullptr;
-  }
+  MttkrpView v = make_mview(ndims, dims, n, U);
   MttkrpGeom g;
   g.C = (int)C;
   g.ldu = ldu;
@@ -964,10 +965,10 @@ jkcals_status jkcals_mttkrp(int ndims, const int64_t* dims, int n, const double*
   g.KT = p.KT;
   g.units = p.units;
   g.G = p.G;
-  ki->fn[p.W8][p.NT - 1]<<<p.G, (p.W8 ? 8 : 4) * 32, ki->smem[p.W8][p.NT - 1], s>>>(v, T, g, ti, parts);
+  ki->fn[p.KM][p.ST4][p.NT - 1]<<<p.G, kWarps * 32, p.smem, s>>>(v, T, g, ti, parts);
   if (cudaGetLastError() != cudaSuccess) return JKCALS_E_CUDA;
   int64_t tot = dims[n] * C;
-  reduce_parts_kernel<<<(int)cdiv(tot, 256), 256, 0, s>>>(parts, ti, (int)dims[n], (int)C, p.BM, p.BN, p.nMt, M, ldm);
+  reduce_parts_kernel<<<(int)cdiv(tot, 256), 256, 0, s>>>(parts, ti, (int)dims[n], (int)C, p.BN, p.nMt, M, ldm);
   if (cudaGetLastError() != cudaSuccess) return JKCALS_E_CUDA;
   // tinfo staging is pageable-host -> device: make sure the copy has consumed it
   if (cudaStreamSynchronize(s) != cudaSuccess) return JKCALS_E_CUDA;

@@ -3,17 +3,22 @@
 // Computes, for one mode n (Alg. 3 alg:cals_jk:mttkrp; Eq. 1):
 //     M(i, c) = sum_j T_(n)(i, j) * KRP(j, c),   KRP(j, c) = prod_{m != n} U_m(i_m(j), c)
 // for all fused columns c of all active submodels at once (CALS fusion).
-// The KRP is generated tile by tile in shared memory and never touches HBM.
+// The KRP is never materialised: with q0 the fastest "rest" mode (Eq. 3 column order) and
+// j = i_q0 + I_q0 * j', every KRP row factors as U_q0(i_q0, c) * S_{j'}(c), where
+// S_{j'} = prod of the slower rest modes' rows. A k-tile is BK consecutive i_q0 at one j':
+// the A operand (KRP^T) of the tile is a BK x BM slab of U_q0 (staged once per i_q0 block and
+// reused for all J' tiles) scaled column-wise by one S row (N-2 factor rows, staged per tile).
 //
 // GEMM view: D[c][i] = sum_j A[c][j] * B[j][i] with A = KRP^T (C side = MMA "m"),
-// B = T_(n)^T (I_n side = MMA "n"), K = J_n. sm_100a has no FP64 tcgen05 kind, so the
-// contraction runs on mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4), which the microbenchmark in
-// tools/microbench_fp64.cu measured at 37.05 TFLOP/s on B200 (= the chip's FP64 peak).
+// B = T_(n)^T (I_n side = MMA "n"). sm_100a has no FP64 tcgen05 kind, so the contraction
+// runs on mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4), measured at 37.05 TFLOP/s on B200
+// (tools/microbench_fp64.cu), the chip's FP64 peak.
 //
-// Work decomposition: "stream-K". The (C/BM) x (I_n/BN) output tiles x (J/BK) k-tiles form
-// one linear unit space split evenly over G = #SMs x occupancy CTAs (one wave, balanced to
-// +-1 k-tile). A CTA whose range spans tiles writes one partial "piece" per tile; the
-// epilogue sums a tile's pieces in a fixed order (deterministic).
+// Data movement: every operand tile is moved by cp.async (LDGSTS, zero-fill for the ragged
+// edges) into a STAGES-deep shared-memory ring, one __syncthreads per k-tile; 2 CTAs/SM.
+// Work decomposition: "stream-K" -- the (C/BM) x (I_n/BN) output tiles x KT k-tiles form one
+// linear unit space split evenly over G = #SMs x occupancy CTAs (one wave); a CTA spanning
+// several tiles writes one partial "piece" per tile, summed in a fixed order later.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -21,22 +26,37 @@
 namespace jk {
 
 constexpr int kMaxModes = 8;
-constexpr int kBK = 16;  // k-tile depth (j values per shared-memory stage)
+constexpr int kBK = 16;      // k-tile depth (i_q0 values per tile)
+constexpr int kWarps = 8;    // warps per CTA; each warp owns 16 fused columns
+constexpr int kBM = kWarps * 16;
+constexpr int kBMP = kBM + 4;  // row pitch = 4 mod 16 doubles: conflict-free 64-bit fragment loads
+constexpr int kMaxNT = 8;    // n8 tiles per CTA (BN <= 64)
 
+// generic mode description (stand-alone KRP generator and host helpers)
 struct ModeView {
-  int N;                               // number of modes
-  int n;                               // the mode being updated
-  int nrest;                           // N - 1
-  int In;                              // I_n
-  int J;                               // prod_{m != n} I_m  (< 2^31, checked on the host)
-  int L;                               // prod_{m < n} I_m: stride of i_n in T
-  int64_t LIn;                         // L * I_n
-  int rdim[kMaxModes - 1];             // I_m of the modes m != n, ascending m
-  const double* U[kMaxModes - 1];      // multi-factor of mode m (row-major I_m x ldu)
+  int N, n, nrest;
+  int In;
+  int J;                            // prod_{m != n} I_m (< 2^31)
+  int L;                            // prod_{m < n} I_m
+  int64_t LIn;
+  int rdim[kMaxModes - 1];          // I_m of the modes m != n, ascending m
+  const double* U[kMaxModes - 1];   // their multi-factors (row-major I_m x ldu)
 };
 
-// Per output tile: the first CTA touching it, its number of partial pieces and the base
-// index of its pieces in the partial buffer.
+// mode description for the fused kernel (q0 = fastest rest mode, "slow" = the others)
+struct MttkrpView {
+  int In;                           // I_n
+  int Iq0;                          // I_q0
+  int nb0;                          // ceil(I_q0 / BK)
+  int Jp;                           // J' = prod of the slow rest modes
+  int64_t stride_n, stride_q0;      // T strides of modes n and q0
+  int nslow;                        // N - 2
+  int sdim[kMaxModes - 2];          // dims of the slow rest modes, ascending
+  int64_t sstride[kMaxModes - 2];   // their T strides
+  const double* Uq0;                // U_q0 (row-major I_q0 x ldu)
+  const double* Us[kMaxModes - 2];  // slow rest modes' U
+};
+
 struct TileInfo {
   int first_cta;
   int npieces;
@@ -45,21 +65,28 @@ struct TileInfo {
 };
 
 struct MttkrpGeom {
-  int C;          // fused width in use (columns >= C of U are zero up to round_up(C, BM))
-  int64_t ldu;    // row pitch of every U_m
+  int C;          // fused width in use
+  int64_t ldu;    // row pitch of every U_m (multiple of 128 doubles)
   int nMt, nNt;   // output tiles along C and along I_n
-  int KT;         // k-tiles: ceil(J / kBK)
+  int KT;         // k-tiles per output tile: nb0 * J'
   int64_t units;  // nMt * nNt * KT
   int G;          // CTAs launched
 };
 
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
-  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  int src_size = valid ? 8 : 0;  // src-size 0 => zero fill (OOB rows / tail j)
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_size));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(valid ? 16 : 0));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 __device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -67,64 +94,39 @@ __device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, do
                : "d"(a), "d"(b));
 }
 
-template <int NT, int WARPS>
+// Shared-memory layout of one CTA.
+//   Ub[2][BK][BMP]            U_q0 slab (double-buffered on b0 parity)
+//   per stage s: Bt[BK*BN-ish] T tile; Ss[nslow][BM] slow-mode rows
+// B layout: KMAJOR=false (n == 0: i_n contiguous in T) -> [k][BNP], BNP = 4 mod 16;
+//           KMAJOR=true  (n >= 1: i_q0 contiguous in T) -> [i][BKP], BKP = 20.
+template <int NT, bool KMAJOR, int STAGES>
 struct MttkrpCfg {
-  static constexpr int kThreads = WARPS * 32;
-  static constexpr int BM = WARPS * 16;                    // fused columns per CTA tile
-  static constexpr int BN = NT * 8;                        // rows of M (I_n) per CTA tile
-  static constexpr int BMP = BM + 8;                       // 64B-shifted rows: conflict-free
-  static constexpr int BNP = (NT % 2 == 0) ? BN + 8 : BN;  // row pitch = 8 mod 16 doubles
-  static constexpr size_t kSmemA = 2ull * kBK * BMP * sizeof(double);
-  static constexpr size_t kSmemB = 2ull * kBK * BNP * sizeof(double);
-  static constexpr size_t kSmemTab = 2ull * kBK * sizeof(int64_t) + 2ull * (kMaxModes - 1) * kBK * sizeof(int);
-  static constexpr size_t kSmem = kSmemA + kSmemB + kSmemTab;
+  static constexpr int BN = NT * 8;
+  static constexpr int BNP = BN + ((4 - BN % 16) + 16) % 16;  // BN rounded to 4 mod 16
+  static constexpr int BKP = kBK + 4;
+  static constexpr int kBTile = KMAJOR ? BN * BKP : kBK * BNP;  // doubles
+  static constexpr size_t kUb = 2ull * kBK * kBMP;              // doubles
+  static size_t smem_bytes(int nslow) {
+    return (kUb + (size_t)STAGES * ((size_t)kBTile + (size_t)nslow * kBM)) * sizeof(double);
+  }
 };
 
-// Build the per-k-tile index table: for each j of the tile, the T offset without the i_n
-// term (l + L*I_n*r with j = l + L*r, Eq. 3) and the row offsets i_m(j)*ldu into every U_m.
-__device__ __forceinline__ void build_table(const ModeView& v, int64_t ldu, int kt, int64_t* tofs,
-                                            int* koff) {
-  int t = threadIdx.x;
-  if (t < kBK) {
-    int j = kt * kBK + t;
-    if (j < v.J) {
-      int l = j % v.L, r = j / v.L;
-      tofs[t] = (int64_t)l + v.LIn * (int64_t)r;
-      int rem = j;
-#pragma unroll
-      for (int q = 0; q < kMaxModes - 1; ++q) {
-        if (q < v.nrest) {
-          int i = rem % v.rdim[q];
-          rem /= v.rdim[q];
-          koff[q * kBK + t] = i * (int)ldu;
-        }
-      }
-    } else {
-      tofs[t] = -1;
-#pragma unroll
-      for (int q = 0; q < kMaxModes - 1; ++q) koff[q * kBK + t] = 0;
-    }
-  }
-}
-
-template <int NT, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 1)
-    mttkrp_dmma_kernel(ModeView v, const double* __restrict__ T, MttkrpGeom g,
+template <int NT, bool KMAJOR, int STAGES>
+__global__ void __launch_bounds__(kWarps * 32, 2)
+    mttkrp_dmma_kernel(MttkrpView v, const double* __restrict__ T, MttkrpGeom g,
                        const TileInfo* __restrict__ tinfo, double* __restrict__ parts) {
-  using Cfg = MttkrpCfg<NT, WARPS>;
-  constexpr int BM = Cfg::BM, BN = Cfg::BN, BMP = Cfg::BMP, BNP = Cfg::BNP;
-  constexpr int THREADS = Cfg::kThreads;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* As = reinterpret_cast<double*>(smem_raw);                     // [2][BK][BMP]
-  double* Bs = As + 2 * kBK * BMP;                                      // [2][BK][BNP]
-  int64_t* tofs = reinterpret_cast<int64_t*>(Bs + 2 * kBK * BNP);       // [2][BK]
-  int* koff = reinterpret_cast<int*>(tofs + 2 * kBK);                   // [2][MAXM-1][BK]
+  using Cfg = MttkrpCfg<NT, KMAJOR, STAGES>;
+  constexpr int BN = Cfg::BN, BNP = Cfg::BNP, BKP = Cfg::BKP, BT = Cfg::kBTile;
+  constexpr int THREADS = kWarps * 32;
+  extern __shared__ __align__(16) double smem[];
+  double* Ub = smem;                                // [2][BK][BMP]
+  double* stage0 = smem + Cfg::kUb;                 // STAGES x (BT + nslow*BM)
+  const int stage_sz = BT + v.nslow * kBM;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int b = blockIdx.x;
   const int64_t u0 = (int64_t)b * g.units / g.G, u1 = (int64_t)(b + 1) * g.units / g.G;
-  const bool lmode = (v.L == 1);  // mode 0: i_n contiguous in T
 
   int64_t u = u0;
   while (u < u1) {
@@ -134,7 +136,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     const int kt1 = (int)(kt_end < (int64_t)g.KT ? kt_end : (int64_t)g.KT);
     u += kt1 - kt0;
     const int tm = t % g.nMt, tn = t / g.nMt;
-    const int c0 = tm * BM, i0 = tn * BN;
+    const int c0 = tm * kBM, i0 = tn * BN;
     const bool warp_live = (c0 + warp * 16) < g.C;
 
     double acc[2][NT][2];
@@ -143,81 +145,133 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 #pragma unroll
       for (int ni = 0; ni < NT; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
-    auto load_T = [&](int s) {
-      const int64_t* tf = tofs + s * kBK;
-      double* bs = Bs + s * kBK * BNP;
-      for (int e = tid; e < kBK * BN; e += THREADS) {
-        int k, i;
-        if (lmode) { k = e / BN; i = e % BN; } else { k = e % kBK; i = e / kBK; }
-        int gi = i0 + i;
-        int64_t off = tf[k];
-        bool valid = (gi < v.In) && (off >= 0);
-        const double* src = valid ? (T + off + (int64_t)v.L * gi) : T;
-        cp_async8(bs + k * BNP + i, src, valid);
-      }
-      cp_async_commit();
-    };
-    auto gen_A = [&](int s) {
-      const int* ko = koff + s * (kMaxModes - 1) * kBK;
-      double* as = As + s * kBK * BMP;
-      for (int e = tid; e < kBK * BM; e += THREADS) {
-        int k = e / BM, c = e % BM;
-        int gc = c0 + c;
-        double val = 0.0;
-        if (gc < g.C) {
-          val = 1.0;
-          // descending mode order of Eq. 1
+    // ---- loader state: next k-tile to load (b0 block of i_q0, j' multi-index)
+    int ld_kt = kt0;
+    int ld_b0 = kt0 / v.Jp, ld_jp = kt0 % v.Jp;
+    int sidx[kMaxModes - 2];
+    {
+      int rem = ld_jp;
 #pragma unroll
-          for (int q = kMaxModes - 2; q >= 0; --q)
-            if (q < v.nrest) val *= __ldg(v.U[q] + ko[q * kBK + k] + gc);
+      for (int s = 0; s < kMaxModes - 2; ++s)
+        if (s < v.nslow) { sidx[s] = rem % v.sdim[s]; rem /= v.sdim[s]; }
+    }
+    int loaded_b0 = -1;  // U_q0 slab most recently issued
+
+    auto issue_tile = [&](int slot) {
+      double* st = stage0 + slot * stage_sz;
+      double* Bt = st;
+      double* Ss = st + BT;
+      // U_q0 slab (only when the i_q0 block changes)
+      if (ld_b0 != loaded_b0) {
+        double* ub = Ub + (ld_b0 & 1) * (kBK * kBMP);
+        for (int e = tid; e < kBK * (kBM / 2); e += THREADS) {
+          const int k = e / (kBM / 2), c2 = (e % (kBM / 2)) * 2;
+          const int row = ld_b0 * kBK + k;
+          const bool ok = row < v.Iq0 && (c0 + c2) < g.C;
+          const double* src = ok ? v.Uq0 + (int64_t)row * g.ldu + c0 + c2 : v.Uq0;
+          cp_async16(ub + k * kBMP + c2, src, ok);
         }
-        as[k * BMP + c] = val;
+        loaded_b0 = ld_b0;
+      }
+      // slow-mode rows of S_{j'}
+      int64_t toff = (int64_t)ld_b0 * kBK * v.stride_q0;
+#pragma unroll
+      for (int s = 0; s < kMaxModes - 2; ++s) {
+        if (s < v.nslow) {
+          toff += (int64_t)sidx[s] * v.sstride[s];
+          const double* row = v.Us[s] + (int64_t)sidx[s] * g.ldu + c0;
+          for (int e = tid; e < kBM / 2; e += THREADS)
+            cp_async16(Ss + s * kBM + 2 * e, (c0 + 2 * e) < g.C ? row + 2 * e : v.Us[s], (c0 + 2 * e) < g.C);
+        }
+      }
+      // T tile: element (k, i) = T[toff + k*stride_q0 + (i0+i)*stride_n]
+      const int kvalid = v.Iq0 - ld_b0 * kBK;
+      if (!KMAJOR) {
+        for (int e = tid; e < kBK * BN; e += THREADS) {
+          const int k = e / BN, i = e % BN;
+          const bool ok = (k < kvalid) && (i0 + i < v.In);
+          const double* src = ok ? T + toff + (int64_t)k * v.stride_q0 + (int64_t)(i0 + i) * v.stride_n : T;
+          cp_async8(Bt + k * BNP + i, src, ok);
+        }
+      } else {
+        for (int e = tid; e < kBK * BN; e += THREADS) {
+          const int k = e % kBK, i = e / kBK;
+          const bool ok = (k < kvalid) && (i0 + i < v.In);
+          const double* src = ok ? T + toff + (int64_t)k * v.stride_q0 + (int64_t)(i0 + i) * v.stride_n : T;
+          cp_async8(Bt + i * BKP + k, src, ok);
+        }
+      }
+      // advance the loader to the next k-tile
+      ++ld_kt;
+      if (++ld_jp == v.Jp) {
+        ld_jp = 0;
+        ++ld_b0;
+      }
+#pragma unroll
+      for (int s = 0; s < kMaxModes - 2; ++s) {
+        if (s < v.nslow) {
+          if (++sidx[s] < v.sdim[s]) break;
+          sidx[s] = 0;
+        }
       }
     };
 
-    build_table(v, g.ldu, kt0, tofs, koff);
-    __syncthreads();
-    load_T(0);
-    gen_A(0);
+    // prologue: STAGES-1 tiles in flight
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (ld_kt < kt1) issue_tile(s);
+      cp_async_commit();
+    }
     for (int kt = kt0; kt < kt1; ++kt) {
-      const int s = (kt - kt0) & 1;
-      const bool more = (kt + 1) < kt1;
-      if (more) build_table(v, g.ldu, kt + 1, tofs + (s ^ 1) * kBK, koff + (s ^ 1) * (kMaxModes - 1) * kBK);
-      cp_async_wait_all();
+      const int slot = (kt - kt0) % STAGES;
+      cp_async_wait<STAGES - 2>();
       __syncthreads();
-      if (more) load_T(s ^ 1);
+      if (ld_kt < kt1) issue_tile((ld_kt - kt0) % STAGES);
+      cp_async_commit();
       if (warp_live) {
-        const double* as = As + s * kBK * BMP + warp * 16 + gid;
-        const double* bs = Bs + s * kBK * BNP + gid;
+        const double* st = stage0 + slot * stage_sz;
+        const double* Bt = st;
+        const double* Ss = st + BT;
+        const int b0 = kt / v.Jp;
+        const double* ub = Ub + (b0 & 1) * (kBK * kBMP) + warp * 16 + gid;
+        const int cl = warp * 16 + gid;
+        double s0 = Ss[cl], s1 = Ss[cl + 8];
+        for (int s = 1; s < v.nslow; ++s) {
+          s0 *= Ss[s * kBM + cl];
+          s1 *= Ss[s * kBM + cl + 8];
+        }
+        const int kvalid = v.Iq0 - b0 * kBK;
 #pragma unroll
         for (int kk = 0; kk < kBK / 4; ++kk) {
-          const int kr = kk * 4 + tig;
-          double a0 = as[kr * BMP], a1 = as[kr * BMP + 8];
+          if (kk * 4 < kvalid) {
+            const int kr = kk * 4 + tig;
+            const double a0 = ub[kr * kBMP] * s0;
+            const double a1 = ub[kr * kBMP + 8] * s1;
 #pragma unroll
-          for (int ni = 0; ni < NT; ++ni) {
-            if (i0 + ni * 8 < v.In) {
-              double bb = bs[kr * BNP + ni * 8];
-              dmma_m8n8k4(acc[0][ni][0], acc[0][ni][1], a0, bb);
-              dmma_m8n8k4(acc[1][ni][0], acc[1][ni][1], a1, bb);
+            for (int ni = 0; ni < NT; ++ni) {
+              if (i0 + ni * 8 < v.In) {
+                const double bb = KMAJOR ? Bt[(ni * 8 + gid) * BKP + kr] : Bt[kr * BNP + ni * 8 + gid];
+                dmma_m8n8k4(acc[0][ni][0], acc[0][ni][1], a0, bb);
+                dmma_m8n8k4(acc[1][ni][0], acc[1][ni][1], a1, bb);
+              }
             }
           }
         }
       }
-      if (more) gen_A(s ^ 1);
     }
-    __syncthreads();
+    cp_async_wait<0>();
+    __syncthreads();  // the next segment's prologue reuses every buffer
 
-    // partial piece of tile t written by this CTA
     const TileInfo ti = tinfo[t];
-    double* P = parts + ((int64_t)ti.piece_base + (b - ti.first_cta)) * (int64_t)(BN * BM);
+    double* P = parts + ((int64_t)ti.piece_base + (b - ti.first_cta)) * (int64_t)(BN * kBM);
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
       for (int ni = 0; ni < NT; ++ni) {
         const int cl = warp * 16 + mi * 8 + gid;
         const int il = ni * 8 + 2 * tig;
-        P[(int64_t)il * BM + cl] = acc[mi][ni][0];
-        P[(int64_t)(il + 1) * BM + cl] = acc[mi][ni][1];
+        P[(int64_t)il * kBM + cl] = acc[mi][ni][0];
+        P[(int64_t)(il + 1) * kBM + cl] = acc[mi][ni][1];
       }
   }
 }
@@ -225,21 +279,20 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 // Plain reduction of the partial pieces into a dense row-major M (stand-alone op only; the
 // JK-CALS path reduces inside the epilogue instead).
 __global__ void reduce_parts_kernel(const double* __restrict__ parts, const TileInfo* __restrict__ tinfo,
-                                    int In, int C, int BM, int BN, int nMt, double* __restrict__ M,
-                                    int64_t ldm) {
+                                    int In, int C, int BN, int nMt, double* __restrict__ M, int64_t ldm) {
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)In * C) return;
   int i = (int)(e / C), c = (int)(e % C);
-  int tn = i / BN, tm = c / BM;
+  int tn = i / BN, tm = c / kBM;
   TileInfo ti = tinfo[tn * nMt + tm];
-  const double* p = parts + (int64_t)ti.piece_base * BN * BM + (int64_t)(i - tn * BN) * BM + (c - tm * BM);
+  const double* p = parts + (int64_t)ti.piece_base * BN * kBM + (int64_t)(i - tn * BN) * kBM + (c - tm * kBM);
   double s = 0.0;
-  for (int pc = 0; pc < ti.npieces; ++pc) s += p[(int64_t)pc * BN * BM];
+  for (int pc = 0; pc < ti.npieces; ++pc) s += p[(int64_t)pc * BN * kBM];
   M[(int64_t)i * ldm + c] = s;
 }
 
 // Materialised Khatri-Rao generation (a1 in SURVEY §8a): K(j, c) = prod_{m != n} U_m(i_m(j), c),
-// row-major J x ldk. Each thread owns 4 consecutive columns and a run of kRows consecutive j,
+// row-major J x ldk. Each thread owns 4 consecutive columns and a run of kKrpRows consecutive j,
 // advancing the mixed-radix index incrementally; stores are 32-byte vectors (st.global.v4.f64).
 constexpr int kKrpRows = 64;
 __global__ void __launch_bounds__(256) krp_gen_kernel(ModeView v, int C, int64_t ldu, double* __restrict__ K,
@@ -282,7 +335,6 @@ __global__ void __launch_bounds__(256) krp_gen_kernel(ModeView v, int C, int64_t
       if (c + 2 < C) dst[2] = r2;
       if (c + 3 < C) dst[3] = r3;
     }
-    // mixed-radix increment (mode order ascending = Eq. 3 column order)
 #pragma unroll
     for (int q = 0; q < kMaxModes - 1; ++q) {
       if (q < v.nrest) {

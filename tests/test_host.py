@@ -41,11 +41,14 @@ def test_library_is_sm100a():
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _build.LIB], capture_output=True,
                          text=True).stdout
     assert "sm_100a" in out
-    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun",
-                           "_ZN2jk18mttkrp_dmma_kernelILi13ELi8EEEvNS_8ModeViewEPKdNS_10MttkrpGeomEPKNS_8TileInfoEPd",
-                           _build.LIB], capture_output=True, text=True).stdout
-    assert "DMMA" in sass  # FP64 tensor-pipe instruction in the hot kernel
-    assert "LDGSTS" in sass  # cp.async staging of the tensor tiles
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", _build.LIB], capture_output=True,
+                          text=True).stdout
+    funcs = sass.split("Function : ")
+    hot = [f for f in funcs if f.startswith("_ZN2jk18mttkrp_dmma_kernel")]
+    assert len(hot) == 32  # NT 1..8 x {n == 0, n >= 1} x {2, 4} stages
+    for f in hot:
+        assert "DMMA" in f     # FP64 tensor-pipe instruction in the hot kernel
+        assert "LDGSTS" in f   # cp.async staging of the operand tiles
 
 
 def test_no_cpu_fallback():
