@@ -122,7 +122,7 @@ __device__ void jacobi_pinv(const double* H, int R, double* Hp, double rcond) {
 }
 
 template <int RMAX>
-__global__ void __launch_bounds__(kEpiThreads) als_epilogue_kernel(EpiArgs a) {
+__global__ void __launch_bounds__(kEpiThreads) als_epilogue_rows_kernel(EpiArgs a) {
   const int k = blockIdx.x;
   const int sub = a.blk2sub[k];
   if (!a.active[sub]) return;  // frozen (converged or failed)
@@ -292,6 +292,198 @@ __global__ void __launch_bounds__(kEpiThreads) als_epilogue_kernel(EpiArgs a) {
     a.gram[((int64_t)n * a.nsub + sub) * R * R + e] = gt[r * RMAX + q];
   }
   if (tid < R) a.lambda[(int64_t)sub * R + tid] = lam[tid];
+
+  if (last && tid == 0) {  // (a7) error, fit, history, convergence mask
+    const double nt2 = a.normT2p[sub];
+    const double e = nt2 + quad - 2.0 * crs;
+    int it = a.iters[sub] + 1;
+    a.iters[sub] = it;
+    a.err[sub] = e;
+    a.hist[(int64_t)sub * a.hist_cap + (it - 1) % a.hist_cap] = e;
+    int f = a.flags[sub];
+    bool act = true;
+    if (!isfinite(e)) {
+      f |= F_NONFINITE;
+      act = false;
+    } else {
+      if (e < -1e-9 * nt2) f |= F_BREAKDOWN;
+      const double fit = nt2 > 0.0 ? 1.0 - sqrt(fmax(e, 0.0)) / sqrt(nt2) : 0.0;
+      const double tol = *a.tol;
+      if (tol > 0.0 && it >= 2 && fabs(fit - a.fit_prev[sub]) < tol) {
+        f |= F_CONVERGED;
+        act = false;
+      }
+      a.fit[sub] = fit;
+      a.fit_prev[sub] = fit;
+    }
+    a.flags[sub] = f;
+    if (!act) a.active[sub] = 0;
+    else atomicAdd(a.active_count, 1);
+  }
+}
+
+// Fast path (I_n * R small enough for shared memory): the same arithmetic as the row kernel
+// above -- identical per-row solve and fixed-order sums -- but with M and V staged in shared
+// memory so that the partial reduction, the solves and every reduction run with all threads.
+constexpr int kEpi2Threads = 256;
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// q-th quantity over rows: Q_q = sum_i f_q(i), one warp per quantity, fixed order
+// (lane-strided partial sums, then the shuffle tree).
+template <class F>
+__device__ __forceinline__ void warp_reduce_all(int nq, int In, double* out, F f) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int q = warp; q < nq; q += nw) {
+    double s = 0.0;
+    for (int i = lane; i < In; i += 32) s += f(q, i);
+    s = warp_sum(s);
+    if (lane == 0) out[q] = s;
+  }
+}
+
+template <int RMAX>
+__global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
+  const int k = blockIdx.x;
+  const int sub = a.blk2sub[k];
+  if (!a.active[sub]) return;  // frozen (converged or failed)
+  const int R = a.R, n = a.n, N = a.N, tid = threadIdx.x, In = a.In;
+  const bool last = (n == N - 1);
+  const int64_t pzero = (n == 0) ? a.pglob[sub] : -1;
+  const int cb = k * R;
+
+  __shared__ double H[RMAX * RMAX];
+  __shared__ double Lf[RMAX * RMAX];
+  __shared__ double red[RMAX * RMAX + RMAX + 1];
+  __shared__ double lam_s[RMAX];
+  __shared__ int use_pinv;
+  extern __shared__ double dyn[];
+  double* Ms = dyn;             // [In][R]
+  double* Vs = dyn + In * R;    // [In][R]
+
+  // (a3) Hadamard of the cached Gramians of every other mode
+  for (int e = tid; e < R * R; e += blockDim.x) {
+    double h = 1.0;
+    for (int m = 0; m < N; ++m)
+      if (m != n) h *= a.gram[((int64_t)m * a.nsub + sub) * R * R + e];
+    H[e] = h;
+  }
+  // (a2) fixed-order sum of the partial pieces of this submodel's R columns
+  for (int e = tid; e < In * R; e += blockDim.x) {
+    const int i = e / R, r = e % R;
+    const int c = cb + r, tn = i / a.BN, tm = c / a.BM;
+    const TileInfo ti = a.tinfo[tn * a.nMt + tm];
+    const double* p = a.parts + (int64_t)ti.piece_base * a.BN * a.BM + (int64_t)(i - tn * a.BN) * a.BM + (c - tm * a.BM);
+    double s = 0.0;
+    for (int pc = 0; pc < ti.npieces; ++pc) s += p[(int64_t)pc * a.BN * a.BM];
+    Ms[e] = s;
+  }
+  __syncthreads();
+  // (a4) Cholesky H = L L^T (textbook, no pivoting); Jacobi pinv fallback
+  if (tid == 0) {
+    bool ok = true;
+    for (int j = 0; j < R && ok; ++j) {
+      double s = H[j * R + j];
+      for (int q = 0; q < j; ++q) s -= Lf[j * R + q] * Lf[j * R + q];
+      if (!(s > 0.0) || !isfinite(s)) { ok = false; break; }
+      Lf[j * R + j] = sqrt(s);
+      for (int i = j + 1; i < R; ++i) {
+        double t = H[i * R + j];
+        for (int q = 0; q < j; ++q) t -= Lf[i * R + q] * Lf[j * R + q];
+        Lf[i * R + j] = t / Lf[j * R + j];
+      }
+    }
+    use_pinv = ok ? 0 : 1;
+    if (!ok) {
+      jacobi_pinv<RMAX>(H, R, Lf, 1e-12);
+      a.flags[sub] |= F_PINV;
+    }
+  }
+  __syncthreads();
+  const bool pinv = use_pinv != 0;
+  // (a4/a5) per-row solve V(i,:) = M(i,:) H^{-1}; the left-out row p of mode 0 is zero
+  for (int i = tid; i < In; i += blockDim.x) {
+    double m[RMAX], v[RMAX];
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) m[r] = (r < R) ? Ms[i * R + r] : 0.0;
+    if (i == pzero) {
+#pragma unroll
+      for (int r = 0; r < RMAX; ++r) v[r] = 0.0;
+    } else if (!pinv) {
+      double y[RMAX];
+#pragma unroll
+      for (int r = 0; r < RMAX; ++r) {
+        if (r < R) {
+          double t = m[r];
+#pragma unroll
+          for (int q = 0; q < r; ++q) t -= Lf[r * R + q] * y[q];
+          y[r] = t / Lf[r * R + r];
+        }
+      }
+#pragma unroll
+      for (int r = RMAX - 1; r >= 0; --r) {
+        if (r < R) {
+          double t = y[r];
+#pragma unroll
+          for (int q = r + 1; q < RMAX; ++q)
+            if (q < R) t -= Lf[q * R + r] * v[q];
+          v[r] = t / Lf[r * R + r];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < RMAX; ++r) {
+        if (r < R) {
+          double s = 0.0;
+#pragma unroll
+          for (int q = 0; q < RMAX; ++q)
+            if (q < R) s += m[q] * Lf[q * R + r];
+          v[r] = s;
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r)
+      if (r < R) Vs[i * R + r] = v[r];
+  }
+  __syncthreads();
+  // reductions: column norms (R), then if last: V.M (1) and V^T V (R*R)
+  const int nq = last ? R + 1 + R * R : R;
+  warp_reduce_all(nq, In, red, [&](int q, int i) -> double {
+    if (q < R) { const double x = Vs[i * R + q]; return x * x; }
+    if (q == R) {
+      double s = 0.0;
+      for (int r = 0; r < R; ++r) s += Vs[i * R + r] * Ms[i * R + r];
+      return s;
+    }
+    const int e = q - R - 1;
+    return Vs[i * R + e / R] * Vs[i * R + e % R];
+  });
+  __syncthreads();
+  if (tid < R) lam_s[tid] = sqrt(red[tid]);
+  double quad = 0.0, crs = 0.0;
+  if (last && tid == 0) {
+    crs = red[R];
+    for (int e = 0; e < R * R; ++e) quad += H[e] * red[R + 1 + e];
+  }
+  __syncthreads();
+  // (a6) normalise; write the block of the multi-factor; keep U in Ms for the Gramian
+  for (int e = tid; e < In * R; e += blockDim.x) {
+    const int i = e / R, r = e % R;
+    const double lm = lam_s[r], x = Vs[e];
+    const double uu = lm > 0.0 ? x / lm : x;
+    Ms[e] = uu;
+    a.U[(int64_t)i * a.ldu + cb + r] = uu;
+  }
+  __syncthreads();
+  warp_reduce_all(R * R, In, red, [&](int q, int i) -> double { return Ms[i * R + q / R] * Ms[i * R + q % R]; });
+  __syncthreads();
+  for (int e = tid; e < R * R; e += blockDim.x) a.gram[((int64_t)n * a.nsub + sub) * R * R + e] = red[e];
+  if (tid < R) a.lambda[(int64_t)sub * R + tid] = lam_s[tid];
 
   if (last && tid == 0) {  // (a7) error, fit, history, convergence mask
     const double nt2 = a.normT2p[sub];

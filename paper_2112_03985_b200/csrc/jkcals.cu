@@ -367,7 +367,17 @@ jkcals_status replan(jkcals_t h) {
 
 template <int RMAX>
 void launch_epi(jkcals_t h, const EpiArgs& a) {
-  als_epilogue_kernel<RMAX><<<h->K, kEpiThreads, 0, h->es>>>(a);
+  const size_t dyn = (size_t)2 * a.In * a.R * sizeof(double);
+  constexpr size_t kMaxDyn = 96 * 1024;
+  static unsigned attr_mask = 0;  // per RMAX instantiation and device
+  if (!(attr_mask & (1u << (h->device & 31)))) {
+    cudaFuncSetAttribute(als_epilogue_kernel<RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDyn);
+    attr_mask |= 1u << (h->device & 31);
+  }
+  if (dyn <= kMaxDyn)
+    als_epilogue_kernel<RMAX><<<h->K, kEpi2Threads, dyn, h->es>>>(a);
+  else
+    als_epilogue_rows_kernel<RMAX><<<h->K, kEpiThreads, 0, h->es>>>(a);
 }
 
 jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {

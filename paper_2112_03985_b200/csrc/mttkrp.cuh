@@ -216,6 +216,11 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
       }
     };
 
+    // consumer state: i_q0 block / j' of the tile being computed; valid n8 tiles
+    int cmp_b0 = kt0 / v.Jp, cmp_jp = kt0 % v.Jp;
+    const int nvalid_n = (v.In - i0 + 7) / 8;
+    const bool full_n = nvalid_n >= NT;
+
     // prologue: STAGES-1 tiles in flight
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
@@ -232,31 +237,55 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
         const double* st = stage0 + slot * stage_sz;
         const double* Bt = st;
         const double* Ss = st + BT;
-        const int b0 = kt / v.Jp;
-        const double* ub = Ub + (b0 & 1) * (kBK * kBMP) + warp * 16 + gid;
+        const double* ub = Ub + (cmp_b0 & 1) * (kBK * kBMP) + warp * 16 + gid;
         const int cl = warp * 16 + gid;
         double s0 = Ss[cl], s1 = Ss[cl + 8];
         for (int s = 1; s < v.nslow; ++s) {
           s0 *= Ss[s * kBM + cl];
           s1 *= Ss[s * kBM + cl + 8];
         }
-        const int kvalid = v.Iq0 - b0 * kBK;
+        // A fragments of the whole k-tile: KRP^T(c, k) = U_q0(k, c) * S_{j'}(c)
+        double a[kBK / 4][2];
 #pragma unroll
         for (int kk = 0; kk < kBK / 4; ++kk) {
-          if (kk * 4 < kvalid) {
+          const int kr = kk * 4 + tig;
+          a[kk][0] = ub[kr * kBMP] * s0;
+          a[kk][1] = ub[kr * kBMP + 8] * s1;
+        }
+        const int kvalid = v.Iq0 - cmp_b0 * kBK;
+        if (kvalid >= kBK && full_n) {
+          // interior tile: no predicates around the MMAs
+#pragma unroll
+          for (int kk = 0; kk < kBK / 4; ++kk) {
             const int kr = kk * 4 + tig;
-            const double a0 = ub[kr * kBMP] * s0;
-            const double a1 = ub[kr * kBMP + 8] * s1;
 #pragma unroll
             for (int ni = 0; ni < NT; ++ni) {
-              if (i0 + ni * 8 < v.In) {
-                const double bb = KMAJOR ? Bt[(ni * 8 + gid) * BKP + kr] : Bt[kr * BNP + ni * 8 + gid];
-                dmma_m8n8k4(acc[0][ni][0], acc[0][ni][1], a0, bb);
-                dmma_m8n8k4(acc[1][ni][0], acc[1][ni][1], a1, bb);
+              const double bb = KMAJOR ? Bt[(ni * 8 + gid) * BKP + kr] : Bt[kr * BNP + ni * 8 + gid];
+              dmma_m8n8k4(acc[0][ni][0], acc[0][ni][1], a[kk][0], bb);
+              dmma_m8n8k4(acc[1][ni][0], acc[1][ni][1], a[kk][1], bb);
+            }
+          }
+        } else {
+          // ragged edge: skip whole k4 steps / n8 tiles outside the tensor (warp-uniform)
+#pragma unroll
+          for (int kk = 0; kk < kBK / 4; ++kk) {
+            if (kk * 4 < kvalid) {
+              const int kr = kk * 4 + tig;
+#pragma unroll
+              for (int ni = 0; ni < NT; ++ni) {
+                if (ni < nvalid_n) {
+                  const double bb = KMAJOR ? Bt[(ni * 8 + gid) * BKP + kr] : Bt[kr * BNP + ni * 8 + gid];
+                  dmma_m8n8k4(acc[0][ni][0], acc[0][ni][1], a[kk][0], bb);
+                  dmma_m8n8k4(acc[1][ni][0], acc[1][ni][1], a[kk][1], bb);
+                }
               }
             }
           }
         }
+      }
+      if (++cmp_jp == v.Jp) {
+        cmp_jp = 0;
+        ++cmp_b0;
       }
     }
     cp_async_wait<0>();
