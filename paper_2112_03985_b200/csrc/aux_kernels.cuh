@@ -12,13 +12,13 @@ namespace jk {
 
 // (a0) mode-0 slice norms, pass 1: CTA b sums T(i0, j)^2 over its chunk of columns j of
 // T_(0) (column-major, so consecutive threads read consecutive i0: coalesced).
-__global__ void slice_norms_partial_kernel(const double* __restrict__ T, int64_t I0, int64_t J0,
+__global__ void slice_norms_partial_kernel(const double* __restrict__ T, int64_t I0, int64_t ld, int64_t J0,
                                            int64_t chunk, double* __restrict__ part) {
   const int64_t j0 = (int64_t)blockIdx.x * chunk, j1 = min(J0, j0 + chunk);
   for (int64_t i = threadIdx.x; i < I0; i += blockDim.x) {
     double s = 0.0;
     for (int64_t j = j0; j < j1; ++j) {
-      double x = T[i + I0 * j];
+      double x = T[i + ld * j];
       s += x * x;
     }
     part[(int64_t)blockIdx.x * I0 + i] = s;

@@ -5,6 +5,8 @@
 // per-submodel epilogue]) is captured once into a CUDA graph and replayed max_iters times
 // (CS1 in SURVEY §3). With tol > 0 the host reads one int per sweep (active count) and, when
 // enough submodels have converged, compacts them out (a8) and re-captures the graph.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -30,7 +32,7 @@ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
 
 // ---------------------------------------------------------------- kernel dispatch tables
-typedef void (*MttkrpFn)(MttkrpView, const double*, MttkrpGeom, const TileInfo*, double*);
+typedef void (*MttkrpFn)(const CUtensorMap, const CUtensorMap, MttkrpView, MttkrpGeom, const TileInfo*, double*);
 
 template <int NT, bool KM, int ST>
 size_t smem_of(int nslow) { return MttkrpCfg<NT, KM, ST>::smem_bytes(nslow); }
@@ -168,27 +170,92 @@ MttkrpView make_mview(int N, const int64_t* dims, int n, const double* const* Ua
   v.Iq0 = (int)mg.Iq0;
   v.nb0 = (int)cdiv(mg.Iq0, kBK);
   v.Jp = (int)mg.Jp;
-  int64_t stride[kMaxModes];
-  stride[0] = 1;
-  for (int m = 1; m < N; ++m) stride[m] = stride[m - 1] * dims[m - 1];
-  v.stride_n = stride[n];
-  v.stride_q0 = stride[mg.q0];
+  // slow modes merged into <= 2 runs: n == 0 -> one run (modes 2..N-1);
+  // n >= 1 -> run A = modes 1..n-1, run B = modes n+1..N-1 (j' = jA + runA * jB, Eq. 3 order)
+  int64_t runA = 1;
+  if (n == 0) {
+    for (int m = 2; m < N; ++m) runA *= dims[m];
+  } else {
+    for (int m = 1; m < n; ++m) runA *= dims[m];
+  }
+  v.runA = (int)runA;
   v.nslow = N - 2;
-  v.Uq0 = Uall[mg.q0];
   int s = 0;
   for (int m = 0; m < N; ++m) {
     if (m == n || m == mg.q0) continue;
     v.sdim[s] = (int)dims[m];
-    v.sstride[s] = stride[m];
     v.Us[s] = Uall[m];
     ++s;
   }
   for (; s < kMaxModes - 2; ++s) {
     v.sdim[s] = 1;
-    v.sstride[s] = 0;
     v.Us[s] = nullptr;
   }
   return v;
+}
+
+// ---------------------------------------------------------------- TMA descriptors
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// T (FP64, column-major, mode-0 pitch I0p even so that every stride is a multiple of 16 B)
+// viewed for mode n as a 4-D box source with non-decreasing strides:
+//   n == 0: (i_0 [In], i_1 [q0], modes 2.. [run], 1)       box (BNP, 16, 1, 1)
+//   n >= 1: (i_0 [q0], modes 1..n-1 [runA], i_n, modes n+1.. [runB])   box (20, 1, BN, 1)
+bool make_tmap_T(CUtensorMap* tm, const double* T, int N, const int64_t* dims, int64_t I0p, int n, int BN, int BNP) {
+  auto enc = encode_fn();
+  if (!enc) return false;
+  int64_t st[kMaxModes + 1];
+  st[0] = 1;
+  st[1] = I0p;
+  for (int m = 2; m <= N; ++m) st[m] = st[m - 1] * dims[m - 1];
+  const int64_t total = st[N];
+  cuuint64_t gdim[4], gstr[3];
+  cuuint32_t box[4], est[4] = {1, 1, 1, 1};
+  if (n == 0) {
+    int64_t run = 1;
+    for (int m = 2; m < N; ++m) run *= dims[m];
+    gdim[0] = dims[0]; gdim[1] = dims[1]; gdim[2] = run; gdim[3] = 1;
+    gstr[0] = st[1] * 8; gstr[1] = st[2] * 8; gstr[2] = total * 8;
+    box[0] = BNP; box[1] = kBK; box[2] = 1; box[3] = 1;
+  } else {
+    int64_t runA = 1, runB = 1;
+    for (int m = 1; m < n; ++m) runA *= dims[m];
+    for (int m = n + 1; m < N; ++m) runB *= dims[m];
+    gdim[0] = dims[0]; gdim[1] = runA; gdim[2] = dims[n]; gdim[3] = runB;
+    gstr[0] = st[1] * 8; gstr[1] = st[n] * 8; gstr[2] = (n + 1 < N ? st[n + 1] : total) * 8;
+    box[0] = kBK + 4; box[1] = 1; box[2] = BN; box[3] = 1;
+  }
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(T), gdim, gstr, box, est,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// U_q0 (row-major rows x ldu): 2-D box (BMP columns, BK rows); OOB rows/columns read as zero.
+bool make_tmap_U(CUtensorMap* tm, const double* U, int64_t rows, int64_t ldu) {
+  auto enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t gdim[2] = {(cuuint64_t)ldu, (cuuint64_t)rows}, gstr[1] = {(cuuint64_t)ldu * 8};
+  cuuint32_t box[2] = {(cuuint32_t)kBMP, (cuuint32_t)kBK}, est[2] = {1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(U), gdim, gstr, box, est,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int bnp_of(int NT) {
+  const int BN = NT * 8;
+  return BN + ((4 - BN % 16) + 16) % 16;
 }
 
 // ---------------------------------------------------------------- workspace layout
@@ -221,7 +288,7 @@ bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_c
   }
   const int64_t C = nsub * R, ldu = rup(std::max<int64_t>(C, 1), 128);
   Layout L;
-  o->T = L.take(P * 8);
+  o->T = L.take(rup(dims[0], 2) * (P / dims[0]) * 8);  // mode-0 pitch padded to even (TMA strides)
   for (int s = 0; s < 2; ++s)
     for (int k = 0; k < N; ++k) o->U[s][k] = L.take(dims[k] * ldu * 8);
   o->Ures = L.take(nsub * sumI * R * 8);
@@ -285,7 +352,7 @@ struct jkcals_s {
   int R = 0;
   int64_t sub_begin = 0, sub_end = 0;
   int nsub = 0, K = 0, C = 0;
-  int64_t ldu = 0, P = 0;
+  int64_t ldu = 0, P = 0, I0p = 0;
   int hist_cap = 1;
   int device = 0;
   cudaStream_t stream = nullptr;  // the caller's stream: all work is ordered on it
@@ -297,6 +364,8 @@ struct jkcals_s {
   KernelInfo* ki = nullptr;
   int cur = 0;
   ModePlan plan[kMaxModes];
+  CUtensorMap tmT[kMaxModes];
+  CUtensorMap tmU[2][kMaxModes];
   cudaGraphExec_t gexec = nullptr;
   bool graph_ok = false;
   bool inited = false;
@@ -355,6 +424,13 @@ jkcals_status replan(jkcals_t h) {
       return fail(h, JKCALS_E_OOM, "internal: plan exceeds workspace bounds");
     CKH(h, cudaMemcpyAsync(h->ptr<TileInfo>(h->off.tinfo[n]), p.tinfo.data(), sizeof(TileInfo) * p.ntiles,
                            cudaMemcpyHostToDevice, h->stream));
+    // TMA descriptors: the tensor view of mode n and the U_q0 slab source of both U buffer sets
+    if (!make_tmap_T(&h->tmT[n], h->ptr<double>(h->off.T), h->N, h->dims, h->I0p, n, p.BN, bnp_of(p.NT)))
+      return fail(h, JKCALS_E_CUDA, "cuTensorMapEncodeTiled failed for the tensor view of mode %d", n);
+    const int q0 = (n == 0) ? 1 : 0;
+    for (int set = 0; set < 2; ++set)
+      if (!make_tmap_U(&h->tmU[set][n], h->ptr<double>(h->off.U[set][q0]), h->dims[q0], h->ldu))
+        return fail(h, JKCALS_E_CUDA, "cuTensorMapEncodeTiled failed for U_%d", q0);
   }
   CKH(h, cudaStreamSynchronize(h->stream));  // tinfo host vectors may change on the next replan
   if (h->gexec) {
@@ -397,7 +473,7 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
   double* parts = h->ptr<double>(h->off.parts);
   MttkrpFn fn = h->ki->fn[p.KM][p.ST4][p.NT - 1];
   if (timed) CKH(h, cudaEventRecord(h->ev[4 * n + 0], h->es));
-  fn<<<p.G, kWarps * 32, p.smem, h->es>>>(v, h->ptr<double>(h->off.T), g, ti,
+  fn<<<p.G, kWarps * 32, p.smem, h->es>>>(h->tmT[n], h->tmU[h->cur][n], v, g, ti,
                                                                              parts);
   CKH(h, cudaGetLastError());
   if (timed) CKH(h, cudaEventRecord(h->ev[4 * n + 1], h->es));
@@ -580,6 +656,7 @@ jkcals_status jkcals_create(jkcals_t* out, int ndims, const int64_t* dims, int r
   h->ldu = rup(std::max<int64_t>(h->C, 1), 128);
   h->P = 1;
   for (int k = 0; k < ndims; ++k) h->P *= dims[k];
+  h->I0p = rup(dims[0], 2);
   h->hist_cap = hist_cap;
   h->device = device;
   h->stream = static_cast<cudaStream_t>(cuda_stream);
@@ -600,8 +677,12 @@ jkcals_status jkcals_create(jkcals_t* out, int ndims, const int64_t* dims, int r
   CKH(h, cudaMallocHost(&h->pinned_count, sizeof(int)));
   CKH(h, cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
   for (auto& e : h->ev) CKH(h, cudaEventCreate(&e));
-  CKH(h, cudaMemcpyAsync(h->ptr<double>(h->off.T), tensor, sizeof(double) * h->P,
-                         tensor_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
+  // T into the workspace with its mode-0 pitch padded to I0p (zero pad row when I0 is odd)
+  if (h->I0p != dims[0])
+    CKH(h, cudaMemsetAsync(h->ptr<double>(h->off.T), 0, sizeof(double) * h->I0p * (h->P / dims[0]), h->stream));
+  CKH(h, cudaMemcpy2DAsync(h->ptr<double>(h->off.T), sizeof(double) * h->I0p, tensor, sizeof(double) * dims[0],
+                           sizeof(double) * dims[0], h->P / dims[0],
+                           tensor_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
   std::vector<int64_t> pg(h->nsub);
   std::vector<int> b2s(h->nsub);
   for (int q = 0; q < h->nsub; ++q) {
@@ -619,7 +700,7 @@ jkcals_status jkcals_create(jkcals_t* out, int ndims, const int64_t* dims, int r
   const int nb = h->off.slice_nb;
   const int64_t chunk = cdiv(J0, nb);
   const int nb_eff = (int)cdiv(J0, chunk);
-  slice_norms_partial_kernel<<<nb_eff, 256, 0, h->stream>>>(h->ptr<double>(h->off.T), I0, J0, chunk,
+  slice_norms_partial_kernel<<<nb_eff, 256, 0, h->stream>>>(h->ptr<double>(h->off.T), I0, h->I0p, J0, chunk,
                                                              h->ptr<double>(h->off.slice_part));
   CKH(h, cudaGetLastError());
   slice_norms_final_kernel<<<1, 256, 0, h->stream>>>(h->ptr<double>(h->off.slice_part), nb_eff, I0,
@@ -944,7 +1025,13 @@ size_t jkcals_mttkrp_scratch_bytes(int ndims, const int64_t* dims, int n, int64_
   int64_t parts;
   int tiles;
   plan_bounds(mode_geo(ndims, dims, n), n, C, *ki, &parts, &tiles);
-  return (size_t)parts * 8 + (size_t)rup(tiles * sizeof(TileInfo), kAlign) + kAlign;
+  // + staged copies: T with an even mode-0 pitch, every U_m with pitch round_up(C, 128)
+  int64_t sumI = 0;
+  for (int k = 0; k < ndims; ++k) sumI += dims[k];
+  const int64_t ldp = rup(C, 128);
+  return (size_t)rup(parts * 8, kAlign) + (size_t)rup(tiles * sizeof(TileInfo), kAlign) +
+         (size_t)rup(rup(dims[0], 2) * (P / dims[0]) * 8, kAlign) + (size_t)ndims * kAlign +
+         (size_t)sumI * ldp * 8 + kAlign;
 }
 
 jkcals_status jkcals_mttkrp(int ndims, const int64_t* dims, int n, const double* T, const double* const* U, int64_t C,
@@ -963,19 +1050,41 @@ jkcals_status jkcals_mttkrp(int ndims, const int64_t* dims, int n, const double*
   ModePlan p = make_plan(mode_geo(ndims, dims, n), n, C, *ki);
   uintptr_t base = (reinterpret_cast<uintptr_t>(scratch) + kAlign - 1) & ~(uintptr_t)(kAlign - 1);
   TileInfo* ti = reinterpret_cast<TileInfo*>(base);
-  double* parts = reinterpret_cast<double*>(base + rup(p.ntiles * sizeof(TileInfo), kAlign));
+  base += rup(p.ntiles * sizeof(TileInfo), kAlign);
+  double* parts = reinterpret_cast<double*>(base);
+  base += rup(plan_parts_doubles(p) * 8, kAlign);
+  // stage T (even mode-0 pitch) and U (pitch round_up(C,128), zero padding) for the TMA views
+  const int64_t I0p = rup(dims[0], 2), J0 = P / dims[0], ldp = rup(C, 128);
+  double* Tp = reinterpret_cast<double*>(base);
+  base += rup(I0p * J0 * 8, kAlign);
+  if (cudaMemsetAsync(Tp, 0, I0p * J0 * 8, s) != cudaSuccess ||
+      cudaMemcpy2DAsync(Tp, I0p * 8, T, dims[0] * 8, dims[0] * 8, J0, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return JKCALS_E_CUDA;
+  double* Up[kMaxModes];
+  for (int m = 0; m < ndims; ++m) {
+    Up[m] = reinterpret_cast<double*>(base);
+    base += rup(dims[m] * ldp * 8, kAlign);
+    if (m == n) continue;
+    if (cudaMemsetAsync(Up[m], 0, dims[m] * ldp * 8, s) != cudaSuccess ||
+        cudaMemcpy2DAsync(Up[m], ldp * 8, U[m], ldu * 8, C * 8, dims[m], cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      return JKCALS_E_CUDA;
+  }
   if (cudaMemcpyAsync(ti, p.tinfo.data(), sizeof(TileInfo) * p.ntiles, cudaMemcpyHostToDevice, s) != cudaSuccess)
     return JKCALS_E_CUDA;
-  MttkrpView v = make_mview(ndims, dims, n, U);
+  MttkrpView v = make_mview(ndims, dims, n, Up);
+  CUtensorMap tmT, tmU;
+  const int q0 = (n == 0) ? 1 : 0;
+  if (!make_tmap_T(&tmT, Tp, ndims, dims, I0p, n, p.BN, bnp_of(p.NT)) || !make_tmap_U(&tmU, Up[q0], dims[q0], ldp))
+    return JKCALS_E_CUDA;
   MttkrpGeom g;
   g.C = (int)C;
-  g.ldu = ldu;
+  g.ldu = ldp;
   g.nMt = p.nMt;
   g.nNt = p.nNt;
   g.KT = p.KT;
   g.units = p.units;
   g.G = p.G;
-  ki->fn[p.KM][p.ST4][p.NT - 1]<<<p.G, kWarps * 32, p.smem, s>>>(v, T, g, ti, parts);
+  ki->fn[p.KM][p.ST4][p.NT - 1]<<<p.G, kWarps * 32, p.smem, s>>>(tmT, tmU, v, g, ti, parts);
   if (cudaGetLastError() != cudaSuccess) return JKCALS_E_CUDA;
   int64_t tot = dims[n] * C;
   reduce_parts_kernel<<<(int)cdiv(tot, 256), 256, 0, s>>>(parts, ti, (int)dims[n], (int)C, p.BN, p.nMt, M, ldm);

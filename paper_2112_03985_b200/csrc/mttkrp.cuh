@@ -14,12 +14,15 @@
 // runs on mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4), measured at 37.05 TFLOP/s on B200
 // (tools/microbench_fp64.cu), the chip's FP64 peak.
 //
-// Data movement: every operand tile is moved by cp.async (LDGSTS, zero-fill for the ragged
-// edges) into a STAGES-deep shared-memory ring, one __syncthreads per k-tile; 2 CTAs/SM.
+// Data movement: one thread per CTA issues, per k-tile, a 4-D TMA box of T (zero-filled at the
+// ragged edges), 1-D bulk copies of the N-2 slow-mode factor rows and, when the i_q0 block
+// changes, a 2-D TMA box of the U_q0 slab, all completing on the stage's mbarrier; a
+// STAGES-deep shared-memory ring keeps STAGES-1 k-tiles in flight; 2 CTAs/SM.
 // Work decomposition: "stream-K" -- the (C/BM) x (I_n/BN) output tiles x KT k-tiles form one
 // linear unit space split evenly over G = #SMs x occupancy CTAs (one wave); a CTA spanning
 // several tiles writes one partial "piece" per tile, summed in a fixed order later.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -49,12 +52,10 @@ struct MttkrpView {
   int Iq0;                          // I_q0
   int nb0;                          // ceil(I_q0 / BK)
   int Jp;                           // J' = prod of the slow rest modes
-  int64_t stride_n, stride_q0;      // T strides of modes n and q0
+  int runA;                         // j' = jA + runA * jB (slow modes merged into <= 2 runs for TMA)
   int nslow;                        // N - 2
   int sdim[kMaxModes - 2];          // dims of the slow rest modes, ascending
-  int64_t sstride[kMaxModes - 2];   // their T strides
-  const double* Uq0;                // U_q0 (row-major I_q0 x ldu)
-  const double* Us[kMaxModes - 2];  // slow rest modes' U
+  const double* Us[kMaxModes - 2];  // slow rest modes' U (row-major I x ldu)
 };
 
 struct TileInfo {
@@ -76,17 +77,47 @@ struct MttkrpGeom {
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
-               "r"(valid ? 8 : 0));
+
+// ---- mbarrier / TMA / bulk-copy primitives (PTX ISA 8.x, sm_90+; SASS UTMALDG / UBLKCP / SYNCS)
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
 }
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
-               "r"(valid ? 16 : 0));
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, int x0, int x1, int x2, int x3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];\n" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(x0), "r"(x1), "r"(x2), "r"(x3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int x0, int x1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(tm), "r"(x0), "r"(x1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 
 __device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -94,39 +125,56 @@ __device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, do
                : "d"(a), "d"(b));
 }
 
-// Shared-memory layout of one CTA.
-//   Ub[2][BK][BMP]            U_q0 slab (double-buffered on b0 parity)
-//   per stage s: Bt[BK*BN-ish] T tile; Ss[nslow][BM] slow-mode rows
-// B layout: KMAJOR=false (n == 0: i_n contiguous in T) -> [k][BNP], BNP = 4 mod 16;
-//           KMAJOR=true  (n >= 1: i_q0 contiguous in T) -> [i][BKP], BKP = 20.
+// Shared-memory layout of one CTA (every buffer 128-byte aligned for TMA):
+//   Ub[2][BK][BMP]                       U_q0 slab, double-buffered on b0 parity (2-D TMA, box 132 x 16)
+//   STAGES x { Bt (T tile, 4-D TMA box), Ss[nslow][BM] (slow-mode rows, 1-D bulk copies) }
+//   full[STAGES] mbarriers
+// B layout: KMAJOR=false (n == 0: i_n contiguous in T) -> Bt[k][BNP], box (BNP, 16), BNP = 4 mod 16;
+//           KMAJOR=true  (n >= 1: i_q0 contiguous in T) -> Bt[i][BKP], box (20, BN), BKP = 20.
+// The 4-double over-fetch of each box row makes the row pitch 4 mod 16 doubles, so the 64-bit
+// fragment loads of a half-warp hit 16 distinct bank pairs.
 template <int NT, bool KMAJOR, int STAGES>
 struct MttkrpCfg {
   static constexpr int BN = NT * 8;
-  static constexpr int BNP = BN + ((4 - BN % 16) + 16) % 16;  // BN rounded to 4 mod 16
+  static constexpr int BNP = BN + ((4 - BN % 16) + 16) % 16;  // BN rounded up to 4 mod 16
   static constexpr int BKP = kBK + 4;
-  static constexpr int kBTile = KMAJOR ? BN * BKP : kBK * BNP;  // doubles
+  static constexpr int kBTile = KMAJOR ? BN * BKP : kBK * BNP;  // doubles (= TMA box volume)
+  static constexpr unsigned kTBytes = kBTile * 8u;
   static constexpr size_t kUb = 2ull * kBK * kBMP;              // doubles
-  static size_t smem_bytes(int nslow) {
-    return (kUb + (size_t)STAGES * ((size_t)kBTile + (size_t)nslow * kBM)) * sizeof(double);
+  __host__ __device__ static size_t stage_doubles(int nslow) { return (size_t)kBTile + (size_t)nslow * kBM; }
+  __host__ __device__ static size_t smem_bytes(int nslow) {
+    return 128 + (kUb + (size_t)STAGES * stage_doubles(nslow)) * sizeof(double) + STAGES * sizeof(uint64_t);
   }
 };
 
 template <int NT, bool KMAJOR, int STAGES>
 __global__ void __launch_bounds__(kWarps * 32, 2)
-    mttkrp_dmma_kernel(MttkrpView v, const double* __restrict__ T, MttkrpGeom g,
-                       const TileInfo* __restrict__ tinfo, double* __restrict__ parts) {
+    mttkrp_dmma_kernel(const __grid_constant__ CUtensorMap tmT, const __grid_constant__ CUtensorMap tmU,
+                       MttkrpView v, MttkrpGeom g, const TileInfo* __restrict__ tinfo, double* __restrict__ parts) {
   using Cfg = MttkrpCfg<NT, KMAJOR, STAGES>;
   constexpr int BN = Cfg::BN, BNP = Cfg::BNP, BKP = Cfg::BKP, BT = Cfg::kBTile;
-  constexpr int THREADS = kWarps * 32;
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ unsigned char smem_raw[];
+  double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   double* Ub = smem;                                // [2][BK][BMP]
   double* stage0 = smem + Cfg::kUb;                 // STAGES x (BT + nslow*BM)
-  const int stage_sz = BT + v.nslow * kBM;
+  const int stage_sz = (int)Cfg::stage_doubles(v.nslow);
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + (size_t)STAGES * stage_sz);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int b = blockIdx.x;
   const int64_t u0 = (int64_t)b * g.units / g.G, u1 = (int64_t)(b + 1) * g.units / g.G;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  unsigned git = 0;     // consumer: tiles consumed by this CTA (ring slot + phase)
+  unsigned ld_git = 0;  // producer (thread 0): tiles issued by this CTA
+  const unsigned s_bytes = (unsigned)v.nslow * kBM * 8u;
 
   int64_t u = u0;
   while (u < u1) {
@@ -145,68 +193,46 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
 #pragma unroll
       for (int ni = 0; ni < NT; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
-    // ---- loader state: next k-tile to load (b0 block of i_q0, j' multi-index)
-    int ld_kt = kt0;
-    int ld_b0 = kt0 / v.Jp, ld_jp = kt0 % v.Jp;
+    // ---- producer state (thread 0): next k-tile to load
+    int ld_kt = kt0, ld_b0 = 0, ld_jp = 0, ld_ja = 0, ld_jb = 0, loaded_b0 = -1;
     int sidx[kMaxModes - 2];
-    {
+    if (tid == 0) {
+      ld_b0 = kt0 / v.Jp;
+      ld_jp = kt0 % v.Jp;
+      ld_ja = ld_jp % v.runA;
+      ld_jb = ld_jp / v.runA;
       int rem = ld_jp;
 #pragma unroll
       for (int s = 0; s < kMaxModes - 2; ++s)
         if (s < v.nslow) { sidx[s] = rem % v.sdim[s]; rem /= v.sdim[s]; }
     }
-    int loaded_b0 = -1;  // U_q0 slab most recently issued
-
-    auto issue_tile = [&](int slot) {
-      double* st = stage0 + slot * stage_sz;
-      double* Bt = st;
-      double* Ss = st + BT;
-      // U_q0 slab (only when the i_q0 block changes)
-      if (ld_b0 != loaded_b0) {
-        double* ub = Ub + (ld_b0 & 1) * (kBK * kBMP);
-        for (int e = tid; e < kBK * (kBM / 2); e += THREADS) {
-          const int k = e / (kBM / 2), c2 = (e % (kBM / 2)) * 2;
-          const int row = ld_b0 * kBK + k;
-          const bool ok = row < v.Iq0 && (c0 + c2) < g.C;
-          const double* src = ok ? v.Uq0 + (int64_t)row * g.ldu + c0 + c2 : v.Uq0;
-          cp_async16(ub + k * kBMP + c2, src, ok);
-        }
+    auto issue_tile = [&]() {
+      const int slot = (int)(ld_git % STAGES);
+      double* st = stage0 + (size_t)slot * stage_sz;
+      uint64_t* bar = &full[slot];
+      const bool new_slab = (ld_b0 != loaded_b0);
+      mbar_expect_tx(bar, Cfg::kTBytes + s_bytes + (new_slab ? (unsigned)(kBK * kBMP * 8) : 0u));
+      if (new_slab) {  // U_q0 rows [b0*BK, b0*BK+BK) x columns [c0, c0+BMP): OOB rows are zero
+        tma_load_2d(Ub + (ld_b0 & 1) * (kBK * kBMP), &tmU, c0, ld_b0 * kBK, bar);
         loaded_b0 = ld_b0;
       }
-      // slow-mode rows of S_{j'}
-      int64_t toff = (int64_t)ld_b0 * kBK * v.stride_q0;
+      if (KMAJOR) tma_load_4d(st, &tmT, ld_b0 * kBK, ld_ja, i0, ld_jb, bar);  // view (q0, runA, n, runB)
+      else tma_load_4d(st, &tmT, i0, ld_b0 * kBK, ld_ja, ld_jb, bar);
 #pragma unroll
-      for (int s = 0; s < kMaxModes - 2; ++s) {
-        if (s < v.nslow) {
-          toff += (int64_t)sidx[s] * v.sstride[s];
-          const double* row = v.Us[s] + (int64_t)sidx[s] * g.ldu + c0;
-          for (int e = tid; e < kBM / 2; e += THREADS)
-            cp_async16(Ss + s * kBM + 2 * e, (c0 + 2 * e) < g.C ? row + 2 * e : v.Us[s], (c0 + 2 * e) < g.C);
-        }
-      }
-      // T tile: element (k, i) = T[toff + k*stride_q0 + (i0+i)*stride_n]
-      const int kvalid = v.Iq0 - ld_b0 * kBK;
-      if (!KMAJOR) {
-        for (int e = tid; e < kBK * BN; e += THREADS) {
-          const int k = e / BN, i = e % BN;
-          const bool ok = (k < kvalid) && (i0 + i < v.In);
-          const double* src = ok ? T + toff + (int64_t)k * v.stride_q0 + (int64_t)(i0 + i) * v.stride_n : T;
-          cp_async8(Bt + k * BNP + i, src, ok);
-        }
-      } else {
-        for (int e = tid; e < kBK * BN; e += THREADS) {
-          const int k = e % kBK, i = e / kBK;
-          const bool ok = (k < kvalid) && (i0 + i < v.In);
-          const double* src = ok ? T + toff + (int64_t)k * v.stride_q0 + (int64_t)(i0 + i) * v.stride_n : T;
-          cp_async8(Bt + i * BKP + k, src, ok);
-        }
-      }
-      // advance the loader to the next k-tile
+      for (int s = 0; s < kMaxModes - 2; ++s)
+        if (s < v.nslow) bulk_load(st + BT + s * kBM, v.Us[s] + (int64_t)sidx[s] * g.ldu + c0, kBM * 8u, bar);
+      // advance to the next k-tile (j' fastest, then the i_q0 block)
       ++ld_kt;
+      ++ld_git;
       if (++ld_jp == v.Jp) {
         ld_jp = 0;
         ++ld_b0;
       }
+      if (++ld_ja == v.runA) {
+        ld_ja = 0;
+        ++ld_jb;
+      }
+      if (ld_jp == 0) ld_jb = 0;
 #pragma unroll
       for (int s = 0; s < kMaxModes - 2; ++s) {
         if (s < v.nslow) {
@@ -216,25 +242,23 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
       }
     };
 
-    // consumer state: i_q0 block / j' of the tile being computed; valid n8 tiles
+    if (tid == 0) {
+#pragma unroll 1
+      for (int s = 0; s < STAGES - 1; ++s)
+        if (ld_kt < kt1) issue_tile();
+    }
     int cmp_b0 = kt0 / v.Jp, cmp_jp = kt0 % v.Jp;
     const int nvalid_n = (v.In - i0 + 7) / 8;
     const bool full_n = nvalid_n >= NT;
 
-    // prologue: STAGES-1 tiles in flight
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-      if (ld_kt < kt1) issue_tile(s);
-      cp_async_commit();
-    }
     for (int kt = kt0; kt < kt1; ++kt) {
-      const int slot = (kt - kt0) % STAGES;
-      cp_async_wait<STAGES - 2>();
-      __syncthreads();
-      if (ld_kt < kt1) issue_tile((ld_kt - kt0) % STAGES);
-      cp_async_commit();
+      __syncthreads();  // every warp is done with tile kt-1: its slot may be refilled
+      if (tid == 0 && ld_kt < kt1) issue_tile();
+      const int slot = (int)(git % STAGES);
+      mbar_wait(&full[slot], (git / STAGES) & 1u);
+      ++git;
       if (warp_live) {
-        const double* st = stage0 + slot * stage_sz;
+        const double* st = stage0 + (size_t)slot * stage_sz;
         const double* Bt = st;
         const double* Ss = st + BT;
         const double* ub = Ub + (cmp_b0 & 1) * (kBK * kBMP) + warp * 16 + gid;
@@ -288,7 +312,6 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
         ++cmp_b0;
       }
     }
-    cp_async_wait<0>();
     __syncthreads();  // the next segment's prologue reuses every buffer
 
     const TileInfo ti = tinfo[t];

@@ -48,7 +48,8 @@ def test_library_is_sm100a():
     assert len(hot) == 32  # NT 1..8 x {n == 0, n >= 1} x {2, 4} stages
     for f in hot:
         assert "DMMA" in f     # FP64 tensor-pipe instruction in the hot kernel
-        assert "LDGSTS" in f   # cp.async staging of the operand tiles
+        assert "UTMALDG" in f  # TMA (cp.async.bulk.tensor) staging of the tensor tiles
+        assert "UBLKCP" in f   # bulk copies of the Khatri-Rao factor rows
 
 
 def test_no_cpu_fallback():
