@@ -114,13 +114,25 @@ struct ModePlan {
   int ntiles = 1, npieces = 1;
   size_t smem = 0;
   std::vector<TileInfo> tinfo;
+  std::vector<int> cta_u;  // CTA b processes units [cta_u[b], cta_u[b+1])
 };
 
 ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki) {
   ModePlan p;
-  int64_t nI8 = cdiv(mg.In, 8);
-  p.nNt = (int)cdiv(nI8, kMaxNT);
-  p.NT = (int)cdiv(nI8, p.nNt);
+  // N tiling: NT n8 tiles per CTA tile. Score = useful/issued n8 slots x NT/(NT + 1), the second
+  // factor modelling the per-k-tile cost that does not scale with NT (A fragments, S scaling,
+  // barriers): I_n = 200 (25 n8) -> 5 x 5 exactly rather than 4 x 7 with 3 idle slots.
+  const int64_t nI8 = cdiv(mg.In, 8);
+  double best = -1.0;
+  for (int nt = 1; nt <= kMaxNT; ++nt) {
+    const int64_t ntiles_n = cdiv(nI8, nt);
+    const double score = (double)nI8 / (double)(ntiles_n * nt) * (double)nt / (nt + 1.0);
+    if (score > best + 1e-12) {
+      best = score;
+      p.NT = nt;
+      p.nNt = (int)ntiles_n;
+    }
+  }
   p.BN = p.NT * 8;
   p.KM = (n != 0) ? 1 : 0;
   p.ST4 = (mg.Jp >= 3) ? 1 : 0;  // the U_q0 slab double buffer needs J' >= STAGES - 1
@@ -131,9 +143,52 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki) {
   p.smem = ki.smem[p.KM][p.ST4][p.NT - 1](mg.nslow);
   int64_t gmax = (int64_t)ki.nsm * ki.occ[p.KM][p.ST4][p.NT - 1][mg.nslow];
   p.G = (int)std::min<int64_t>(p.units, gmax);
+  // Cost-weighted stream-K split. A unit (tile t, k-tile kt) costs a fixed per-k-tile overhead
+  // (barrier, TMA issue, A-fragment scaling) plus the DMMA time of its busiest SM sub-partition:
+  // ceil(live warps / 4) x (valid n8 tiles) x (valid k4 steps) -- warps w and w+4 share one
+  // SMSP, so a C tile with 1..4 live warps runs at half the time of a full one, not 1/8.
+  const int nb0 = (int)cdiv(mg.Iq0, kBK);
+  const int64_t Jp = mg.Jp;
+  const int kv4_last = (int)cdiv(mg.Iq0 - (int64_t)(nb0 - 1) * kBK, 4);
+  constexpr double kFixed = 8.0;  // per-k-tile overhead in DMMA-pair units (full tile ~ 2*7*4 = 56)
+  auto kprefix = [&](int64_t kt) -> double {  // valid k4 steps in k-tiles [0, kt) of a tile
+    const int64_t full_tiles = (int64_t)(nb0 - 1) * Jp;
+    if (kt <= full_tiles) return 4.0 * kt;
+    return 4.0 * full_tiles + (double)kv4_last * (kt - full_tiles);
+  };
+  std::vector<double> wt(p.ntiles), wpre(p.ntiles + 1, 0.0);
+  for (int t = 0; t < p.ntiles; ++t) {
+    const int tm = t % p.nMt, tn = t / p.nMt;
+    const int64_t live_w = std::min<int64_t>(kWarps, cdiv(C - (int64_t)tm * kBM, 16));
+    const int64_t nv = std::min<int64_t>(p.NT, cdiv(mg.In - (int64_t)tn * p.BN, 8));
+    // Measured (r01): weighting by the DMMA count made ragged-tile CTAs the stragglers -- the
+    // per-k-tile time is dominated by its fixed part -- so the split is uniform in k-tiles for now.
+    wt[t] = 0.0 * (double)cdiv(std::max<int64_t>(live_w, 1), 4) * (double)std::max<int64_t>(nv, 1);
+    wpre[t + 1] = wpre[t] + wt[t] * kprefix(p.KT) + kFixed * p.KT;
+  }
+  auto prefix = [&](int64_t u) -> double {
+    const int64_t t = u / p.KT, kt = u % p.KT;
+    return t >= p.ntiles ? wpre[p.ntiles] : wpre[t] + wt[t] * kprefix(kt) + kFixed * kt;
+  };
+  p.cta_u.assign(p.G + 1, 0);
+  p.cta_u[p.G] = (int)p.units;
+  for (int b = 1; b < p.G; ++b) {
+    const double target = wpre[p.ntiles] * (double)b / (double)p.G;
+    int64_t lo = p.cta_u[b - 1], hi = p.units;  // smallest u with prefix(u) >= target
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (prefix(mid) >= target) hi = mid;
+      else lo = mid + 1;
+    }
+    p.cta_u[b] = (int)lo;
+  }
+  // drop empty ranges (a unit costing more than one CTA's share) so that the CTAs touching a
+  // tile are consecutive and the piece index of CTA b in tile t is b - first_cta[t]
+  p.cta_u.erase(std::unique(p.cta_u.begin(), p.cta_u.end()), p.cta_u.end());
+  p.G = (int)p.cta_u.size() - 1;
   std::vector<int> first(p.ntiles, -1), lastc(p.ntiles, -1);
   for (int b = 0; b < p.G; ++b) {
-    int64_t u0 = (int64_t)b * p.units / p.G, u1 = (int64_t)(b + 1) * p.units / p.G;
+    int64_t u0 = p.cta_u[b], u1 = p.cta_u[b + 1];
     if (u0 >= u1) continue;
     int64_t t0 = u0 / p.KT, t1 = (u1 - 1) / p.KT;
     for (int64_t t = t0; t <= t1; ++t) {
@@ -155,6 +210,15 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki) {
 }
 
 int64_t plan_parts_doubles(const ModePlan& p) { return (int64_t)p.npieces * p.BN * kBM; }
+
+// device plan table: TileInfo[ntiles] followed by int cta_u[G+1] (read by the kernel)
+size_t plan_table_bytes(int ntiles, int G) { return ntiles * sizeof(TileInfo) + (size_t)(G + 1) * sizeof(int); }
+std::vector<char> pack_plan(const ModePlan& p) {
+  std::vector<char> buf(plan_table_bytes(p.ntiles, p.G));
+  memcpy(buf.data(), p.tinfo.data(), p.ntiles * sizeof(TileInfo));
+  memcpy(buf.data() + p.ntiles * sizeof(TileInfo), p.cta_u.data(), (p.G + 1) * sizeof(int));
+  return buf;
+}
 
 // upper bound for workspace sizing (any C' <= C)
 void plan_bounds(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, int64_t* parts, int* tiles) {
@@ -302,7 +366,7 @@ bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_c
     o->tiles_cap = std::max(o->tiles_cap, tc);
   }
   o->parts = L.take(o->parts_cap * 8);
-  for (int n = 0; n < N; ++n) o->tinfo[n] = L.take((size_t)o->tiles_cap * sizeof(TileInfo));
+  for (int n = 0; n < N; ++n) o->tinfo[n] = L.take(plan_table_bytes(o->tiles_cap, ki.nsm * 8));
   o->gram = L.take((size_t)N * nsub * R * R * 8);
   o->lambda = L.take(nsub * R * 8);
   o->normT2p = L.take(nsub * 8);
@@ -366,6 +430,7 @@ struct jkcals_s {
   ModePlan plan[kMaxModes];
   CUtensorMap tmT[kMaxModes];
   CUtensorMap tmU[2][kMaxModes];
+  std::vector<char> table[kMaxModes];  // host copy of each mode's device plan table
   cudaGraphExec_t gexec = nullptr;
   bool graph_ok = false;
   bool inited = false;
@@ -422,7 +487,8 @@ jkcals_status replan(jkcals_t h) {
     const ModePlan& p = h->plan[n];
     if (plan_parts_doubles(p) > h->off.parts_cap || p.ntiles > h->off.tiles_cap)
       return fail(h, JKCALS_E_OOM, "internal: plan exceeds workspace bounds");
-    CKH(h, cudaMemcpyAsync(h->ptr<TileInfo>(h->off.tinfo[n]), p.tinfo.data(), sizeof(TileInfo) * p.ntiles,
+    h->table[n] = pack_plan(p);
+    CKH(h, cudaMemcpyAsync(h->ptr<TileInfo>(h->off.tinfo[n]), h->table[n].data(), h->table[n].size(),
                            cudaMemcpyHostToDevice, h->stream));
     // TMA descriptors: the tensor view of mode n and the U_q0 slab source of both U buffer sets
     if (!make_tmap_T(&h->tmT[n], h->ptr<double>(h->off.T), h->N, h->dims, h->I0p, n, p.BN, bnp_of(p.NT)))
@@ -1029,7 +1095,7 @@ size_t jkcals_mttkrp_scratch_bytes(int ndims, const int64_t* dims, int n, int64_
   int64_t sumI = 0;
   for (int k = 0; k < ndims; ++k) sumI += dims[k];
   const int64_t ldp = rup(C, 128);
-  return (size_t)rup(parts * 8, kAlign) + (size_t)rup(tiles * sizeof(TileInfo), kAlign) +
+  return (size_t)rup(parts * 8, kAlign) + (size_t)rup(plan_table_bytes(tiles, ki->nsm * 8), kAlign) +
          (size_t)rup(rup(dims[0], 2) * (P / dims[0]) * 8, kAlign) + (size_t)ndims * kAlign +
          (size_t)sumI * ldp * 8 + kAlign;
 }
@@ -1050,7 +1116,7 @@ jkcals_status jkcals_mttkrp(int ndims, const int64_t* dims, int n, const double*
   ModePlan p = make_plan(mode_geo(ndims, dims, n), n, C, *ki);
   uintptr_t base = (reinterpret_cast<uintptr_t>(scratch) + kAlign - 1) & ~(uintptr_t)(kAlign - 1);
   TileInfo* ti = reinterpret_cast<TileInfo*>(base);
-  base += rup(p.ntiles * sizeof(TileInfo), kAlign);
+  base += rup(plan_table_bytes(p.ntiles, p.G), kAlign);
   double* parts = reinterpret_cast<double*>(base);
   base += rup(plan_parts_doubles(p) * 8, kAlign);
   // stage T (even mode-0 pitch) and U (pitch round_up(C,128), zero padding) for the TMA views
@@ -1069,7 +1135,8 @@ jkcals_status jkcals_mttkrp(int ndims, const int64_t* dims, int n, const double*
         cudaMemcpy2DAsync(Up[m], ldp * 8, U[m], ldu * 8, C * 8, dims[m], cudaMemcpyDeviceToDevice, s) != cudaSuccess)
       return JKCALS_E_CUDA;
   }
-  if (cudaMemcpyAsync(ti, p.tinfo.data(), sizeof(TileInfo) * p.ntiles, cudaMemcpyHostToDevice, s) != cudaSuccess)
+  std::vector<char> table = pack_plan(p);
+  if (cudaMemcpyAsync(ti, table.data(), table.size(), cudaMemcpyHostToDevice, s) != cudaSuccess)
     return JKCALS_E_CUDA;
   MttkrpView v = make_mview(ndims, dims, n, Up);
   CUtensorMap tmT, tmU;

@@ -86,6 +86,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n"
@@ -143,7 +146,7 @@ struct MttkrpCfg {
   static constexpr size_t kUb = 2ull * kBK * kBMP;              // doubles
   __host__ __device__ static size_t stage_doubles(int nslow) { return (size_t)kBTile + (size_t)nslow * kBM; }
   __host__ __device__ static size_t smem_bytes(int nslow) {
-    return 128 + (kUb + (size_t)STAGES * stage_doubles(nslow)) * sizeof(double) + STAGES * sizeof(uint64_t);
+    return 128 + (kUb + (size_t)STAGES * stage_doubles(nslow)) * sizeof(double) + 2 * STAGES * sizeof(uint64_t);
   }
 };
 
@@ -153,20 +156,26 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
                        MttkrpView v, MttkrpGeom g, const TileInfo* __restrict__ tinfo, double* __restrict__ parts) {
   using Cfg = MttkrpCfg<NT, KMAJOR, STAGES>;
   constexpr int BN = Cfg::BN, BNP = Cfg::BNP, BKP = Cfg::BKP, BT = Cfg::kBTile;
-  extern __shared__ unsigned char smem_raw[];
-  double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  // (no integer round-trip on the base pointer: it must stay in the shared window so that the
+  // fragment loads compile to LDS, not generic LD)
+  extern __shared__ __align__(1024) double smem[];
   double* Ub = smem;                                // [2][BK][BMP]
   double* stage0 = smem + Cfg::kUb;                 // STAGES x (BT + nslow*BM)
   const int stage_sz = (int)Cfg::stage_doubles(v.nslow);
-  uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + (size_t)STAGES * stage_sz);
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + (size_t)STAGES * stage_sz);  // data landed
+  uint64_t* empty = full + STAGES;                                                     // all warps done
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int b = blockIdx.x;
-  const int64_t u0 = (int64_t)b * g.units / g.G, u1 = (int64_t)(b + 1) * g.units / g.G;
+  const int* cta_u = reinterpret_cast<const int*>(tinfo + g.nMt * g.nNt);  // packed after the tile table
+  const int64_t u0 = cta_u[b], u1 = cta_u[b + 1];
 
   if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   }
@@ -208,6 +217,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
     }
     auto issue_tile = [&]() {
       const int slot = (int)(ld_git % STAGES);
+      // WAR: the previous use of this slot must have been released by every warp
+      if (ld_git >= STAGES) mbar_wait(&empty[slot], ((ld_git / STAGES) - 1) & 1u);
       double* st = stage0 + (size_t)slot * stage_sz;
       uint64_t* bar = &full[slot];
       const bool new_slab = (ld_b0 != loaded_b0);
@@ -252,11 +263,10 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
     const bool full_n = nvalid_n >= NT;
 
     for (int kt = kt0; kt < kt1; ++kt) {
-      __syncthreads();  // every warp is done with tile kt-1: its slot may be refilled
-      if (tid == 0 && ld_kt < kt1) issue_tile();
+      // no CTA-wide barrier per k-tile: warps drift freely within the ring; a slot is refilled
+      // only after all 8 warps released it on its `empty` mbarrier
       const int slot = (int)(git % STAGES);
       mbar_wait(&full[slot], (git / STAGES) & 1u);
-      ++git;
       if (warp_live) {
         const double* st = stage0 + (size_t)slot * stage_sz;
         const double* Bt = st;
@@ -307,12 +317,17 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
           }
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      ++git;
+      // producer: refill the slot of tile kt-1 with tile kt+STAGES-1
+      if (tid == 0 && ld_kt < kt1) issue_tile();
       if (++cmp_jp == v.Jp) {
         cmp_jp = 0;
         ++cmp_b0;
       }
     }
-    __syncthreads();  // the next segment's prologue reuses every buffer
+    __syncthreads();  // the next segment reloads the U_q0 slab buffers
 
     const TileInfo ti = tinfo[t];
     double* P = parts + ((int64_t)ti.piece_base + (b - ti.first_cta)) * (int64_t)(BN * kBM);
