@@ -147,7 +147,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="syn200")
-    ap.add_argument("--ref-sweeps", type=int, default=3, help="sweeps per oracle sample step")
+    ap.add_argument("--ref-sweeps", type=int, default=30, help="sweeps per oracle sample step (~10 s on 16 cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
