@@ -79,7 +79,7 @@ KernelInfo* kernel_info(int device, std::string* err) {
         }
         for (int ns = 1; ns <= kMaxModes - 2; ++ns) {
           int occ = 0;
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ki.fn[km][st][t], kWarps * 32,
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ki.fn[km][st][t], (kWarps + 1) * 32,
                                                         ki.smem[km][st][t](ns));
           ki.occ[km][st][t][ns] = std::max(1, occ);
         }
@@ -539,7 +539,7 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
   double* parts = h->ptr<double>(h->off.parts);
   MttkrpFn fn = h->ki->fn[p.KM][p.ST4][p.NT - 1];
   if (timed) CKH(h, cudaEventRecord(h->ev[4 * n + 0], h->es));
-  fn<<<p.G, kWarps * 32, p.smem, h->es>>>(h->tmT[n], h->tmU[h->cur][n], v, g, ti,
+  fn<<<p.G, (kWarps + 1) * 32, p.smem, h->es>>>(h->tmT[n], h->tmU[h->cur][n], v, g, ti,
                                                                              parts);
   CKH(h, cudaGetLastError());
   if (timed) CKH(h, cudaEventRecord(h->ev[4 * n + 1], h->es));
@@ -1151,7 +1151,7 @@ jkcals_status jkcals_mttkrp(int ndims, const int64_t* dims, int n, const double*
   g.KT = p.KT;
   g.units = p.units;
   g.G = p.G;
-  ki->fn[p.KM][p.ST4][p.NT - 1]<<<p.G, kWarps * 32, p.smem, s>>>(tmT, tmU, v, g, ti, parts);
+  ki->fn[p.KM][p.ST4][p.NT - 1]<<<p.G, (kWarps + 1) * 32, p.smem, s>>>(tmT, tmU, v, g, ti, parts);
   if (cudaGetLastError() != cudaSuccess) return JKCALS_E_CUDA;
   int64_t tot = dims[n] * C;
   reduce_parts_kernel<<<(int)cdiv(tot, 256), 256, 0, s>>>(parts, ti, (int)dims[n], (int)C, p.BN, p.nMt, M, ldm);

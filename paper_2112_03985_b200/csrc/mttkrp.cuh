@@ -151,7 +151,7 @@ struct MttkrpCfg {
 };
 
 template <int NT, bool KMAJOR, int STAGES>
-__global__ void __launch_bounds__(kWarps * 32, 2)
+__global__ void __maxnreg__(112)
     mttkrp_dmma_kernel(const __grid_constant__ CUtensorMap tmT, const __grid_constant__ CUtensorMap tmU,
                        MttkrpView v, MttkrpGeom g, const TileInfo* __restrict__ tinfo, double* __restrict__ parts) {
   using Cfg = MttkrpCfg<NT, KMAJOR, STAGES>;
@@ -163,10 +163,9 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
   double* stage0 = smem + Cfg::kUb;                 // STAGES x (BT + nslow*BM)
   const int stage_sz = (int)Cfg::stage_doubles(v.nslow);
   uint64_t* full = reinterpret_cast<uint64_t*>(stage0 + (size_t)STAGES * stage_sz);  // data landed
-  uint64_t* empty = full + STAGES;                                                     // all warps done
+  uint64_t* empty = full + STAGES;                                                     // consumers done
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int gid = lane >> 2, tig = lane & 3;
   const int b = blockIdx.x;
   const int* cta_u = reinterpret_cast<const int*>(tinfo + g.nMt * g.nNt);  // packed after the tile table
   const int64_t u0 = cta_u[b], u1 = cta_u[b + 1];
@@ -181,12 +180,76 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
   }
   __syncthreads();
 
-  unsigned git = 0;     // consumer: tiles consumed by this CTA (ring slot + phase)
-  unsigned ld_git = 0;  // producer (thread 0): tiles issued by this CTA
-  const unsigned s_bytes = (unsigned)v.nslow * kBM * 8u;
+  // =========================== producer warp (warp kWarps, one lane) ===========================
+  if (warp == kWarps) {
+    if (lane != 0) return;
+    const unsigned s_bytes = (unsigned)v.nslow * kBM * 8u;
+    unsigned ld_git = 0;  // tiles issued by this CTA (ring slot + phase)
+    for (int64_t u = u0; u < u1;) {
+      const int t = (int)(u / g.KT);
+      const int kt0 = (int)(u % g.KT);
+      const int64_t kt_end = (int64_t)kt0 + (u1 - u);
+      const int kt1 = (int)(kt_end < (int64_t)g.KT ? kt_end : (int64_t)g.KT);
+      u += kt1 - kt0;
+      const int tm = t % g.nMt, tn = t / g.nMt;
+      const int c0 = tm * kBM, i0 = tn * BN;
+      // a new segment reloads the U_q0 slab buffers: wait until every issued tile is consumed
+      for (unsigned q = (ld_git >= (unsigned)STAGES ? ld_git - STAGES + 1 : 0); q < ld_git; ++q)
+        mbar_wait(&empty[q % STAGES], (q / STAGES) & 1u);
+      int ld_b0 = kt0 / v.Jp, ld_jp = kt0 % v.Jp, loaded_b0 = -1;
+      int ld_ja = ld_jp % v.runA, ld_jb = ld_jp / v.runA;
+      int sidx[kMaxModes - 2];
+      {
+        int rem = ld_jp;
+#pragma unroll
+        for (int s = 0; s < kMaxModes - 2; ++s)
+          if (s < v.nslow) { sidx[s] = rem % v.sdim[s]; rem /= v.sdim[s]; }
+      }
+#pragma unroll 1
+      for (int kt = kt0; kt < kt1; ++kt) {
+        const int slot = (int)(ld_git % STAGES);
+        // WAR: the previous use of this slot must have been released by every consumer warp
+        if (ld_git >= (unsigned)STAGES) mbar_wait(&empty[slot], ((ld_git / STAGES) - 1) & 1u);
+        double* st = stage0 + (size_t)slot * stage_sz;
+        uint64_t* bar = &full[slot];
+        const bool new_slab = (ld_b0 != loaded_b0);
+        mbar_expect_tx(bar, Cfg::kTBytes + s_bytes + (new_slab ? (unsigned)(kBK * kBMP * 8) : 0u));
+        if (new_slab) {  // U_q0 rows [b0*BK, b0*BK+BK) x columns [c0, c0+BMP): OOB rows are zero
+          tma_load_2d(Ub + (ld_b0 & 1) * (kBK * kBMP), &tmU, c0, ld_b0 * kBK, bar);
+          loaded_b0 = ld_b0;
+        }
+        if (KMAJOR) tma_load_4d(st, &tmT, ld_b0 * kBK, ld_ja, i0, ld_jb, bar);  // view (q0, runA, n, runB)
+        else tma_load_4d(st, &tmT, i0, ld_b0 * kBK, ld_ja, ld_jb, bar);
+#pragma unroll
+        for (int s = 0; s < kMaxModes - 2; ++s)
+          if (s < v.nslow) bulk_load(st + BT + s * kBM, v.Us[s] + (int64_t)sidx[s] * g.ldu + c0, kBM * 8u, bar);
+        // advance to the next k-tile (j' fastest, then the i_q0 block)
+        ++ld_git;
+        if (++ld_jp == v.Jp) {
+          ld_jp = 0;
+          ++ld_b0;
+        }
+        if (++ld_ja == v.runA) {
+          ld_ja = 0;
+          ++ld_jb;
+        }
+        if (ld_jp == 0) ld_jb = 0;
+#pragma unroll
+        for (int s = 0; s < kMaxModes - 2; ++s) {
+          if (s < v.nslow) {
+            if (++sidx[s] < v.sdim[s]) break;
+            sidx[s] = 0;
+          }
+        }
+      }
+    }
+    return;
+  }
 
-  int64_t u = u0;
-  while (u < u1) {
+  // =========================== consumer warps 0..kWarps-1 ===========================
+  const int gid = lane >> 2, tig = lane & 3;
+  unsigned git = 0;  // tiles consumed by this CTA (ring slot + phase)
+  for (int64_t u = u0; u < u1;) {
     const int t = (int)(u / g.KT);
     const int kt0 = (int)(u % g.KT);
     const int64_t kt_end = (int64_t)kt0 + (u1 - u);
@@ -202,69 +265,11 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
 #pragma unroll
       for (int ni = 0; ni < NT; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
-    // ---- producer state (thread 0): next k-tile to load
-    int ld_kt = kt0, ld_b0 = 0, ld_jp = 0, ld_ja = 0, ld_jb = 0, loaded_b0 = -1;
-    int sidx[kMaxModes - 2];
-    if (tid == 0) {
-      ld_b0 = kt0 / v.Jp;
-      ld_jp = kt0 % v.Jp;
-      ld_ja = ld_jp % v.runA;
-      ld_jb = ld_jp / v.runA;
-      int rem = ld_jp;
-#pragma unroll
-      for (int s = 0; s < kMaxModes - 2; ++s)
-        if (s < v.nslow) { sidx[s] = rem % v.sdim[s]; rem /= v.sdim[s]; }
-    }
-    auto issue_tile = [&]() {
-      const int slot = (int)(ld_git % STAGES);
-      // WAR: the previous use of this slot must have been released by every warp
-      if (ld_git >= STAGES) mbar_wait(&empty[slot], ((ld_git / STAGES) - 1) & 1u);
-      double* st = stage0 + (size_t)slot * stage_sz;
-      uint64_t* bar = &full[slot];
-      const bool new_slab = (ld_b0 != loaded_b0);
-      mbar_expect_tx(bar, Cfg::kTBytes + s_bytes + (new_slab ? (unsigned)(kBK * kBMP * 8) : 0u));
-      if (new_slab) {  // U_q0 rows [b0*BK, b0*BK+BK) x columns [c0, c0+BMP): OOB rows are zero
-        tma_load_2d(Ub + (ld_b0 & 1) * (kBK * kBMP), &tmU, c0, ld_b0 * kBK, bar);
-        loaded_b0 = ld_b0;
-      }
-      if (KMAJOR) tma_load_4d(st, &tmT, ld_b0 * kBK, ld_ja, i0, ld_jb, bar);  // view (q0, runA, n, runB)
-      else tma_load_4d(st, &tmT, i0, ld_b0 * kBK, ld_ja, ld_jb, bar);
-#pragma unroll
-      for (int s = 0; s < kMaxModes - 2; ++s)
-        if (s < v.nslow) bulk_load(st + BT + s * kBM, v.Us[s] + (int64_t)sidx[s] * g.ldu + c0, kBM * 8u, bar);
-      // advance to the next k-tile (j' fastest, then the i_q0 block)
-      ++ld_kt;
-      ++ld_git;
-      if (++ld_jp == v.Jp) {
-        ld_jp = 0;
-        ++ld_b0;
-      }
-      if (++ld_ja == v.runA) {
-        ld_ja = 0;
-        ++ld_jb;
-      }
-      if (ld_jp == 0) ld_jb = 0;
-#pragma unroll
-      for (int s = 0; s < kMaxModes - 2; ++s) {
-        if (s < v.nslow) {
-          if (++sidx[s] < v.sdim[s]) break;
-          sidx[s] = 0;
-        }
-      }
-    };
-
-    if (tid == 0) {
-#pragma unroll 1
-      for (int s = 0; s < STAGES - 1; ++s)
-        if (ld_kt < kt1) issue_tile();
-    }
     int cmp_b0 = kt0 / v.Jp, cmp_jp = kt0 % v.Jp;
     const int nvalid_n = (v.In - i0 + 7) / 8;
     const bool full_n = nvalid_n >= NT;
 
     for (int kt = kt0; kt < kt1; ++kt) {
-      // no CTA-wide barrier per k-tile: warps drift freely within the ring; a slot is refilled
-      // only after all 8 warps released it on its `empty` mbarrier
       const int slot = (int)(git % STAGES);
       mbar_wait(&full[slot], (git / STAGES) & 1u);
       if (warp_live) {
@@ -320,14 +325,11 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
       ++git;
-      // producer: refill the slot of tile kt-1 with tile kt+STAGES-1
-      if (tid == 0 && ld_kt < kt1) issue_tile();
       if (++cmp_jp == v.Jp) {
         cmp_jp = 0;
         ++cmp_b0;
       }
     }
-    __syncthreads();  // the next segment reloads the U_q0 slab buffers
 
     const TileInfo ti = tinfo[t];
     double* P = parts + ((int64_t)ti.piece_base + (b - ti.first_cta)) * (int64_t)(BN * kBM);
