@@ -126,7 +126,11 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki) {
   double best = -1.0;
   for (int nt = 1; nt <= kMaxNT; ++nt) {
     const int64_t ntiles_n = cdiv(nI8, nt);
-    const double score = (double)nI8 / (double)(ntiles_n * nt) * (double)nt / (nt + 1.0);
+    // variants that fit 2 CTAs/SM (<= 96 regs: NT <= 6) hide the per-k-tile latency better:
+    // measured +7 % on syn200 (r01), modelled as a 1.08 factor
+    const int km = (n != 0) ? 1 : 0, st4 = (mg.Jp >= 3) ? 1 : 0;
+    const double occ_bonus = ki.occ[km][st4][nt - 1][mg.nslow] >= 2 ? 1.08 : 1.0;
+    const double score = (double)nI8 / (double)(ntiles_n * nt) * (double)nt / (nt + 1.0) * occ_bonus;
     if (score > best + 1e-12) {
       best = score;
       p.NT = nt;

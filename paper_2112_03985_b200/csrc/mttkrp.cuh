@@ -151,7 +151,7 @@ struct MttkrpCfg {
 };
 
 template <int NT, bool KMAJOR, int STAGES>
-__global__ void __maxnreg__(112)
+__global__ void __maxnreg__(NT <= 6 ? 96 : 112)
     mttkrp_dmma_kernel(const __grid_constant__ CUtensorMap tmT, const __grid_constant__ CUtensorMap tmU,
                        MttkrpView v, MttkrpGeom g, const TileInfo* __restrict__ tinfo, double* __restrict__ parts) {
   using Cfg = MttkrpCfg<NT, KMAJOR, STAGES>;
