@@ -73,7 +73,7 @@ __device__ __forceinline__ void block_sum(double* vals, int cnt, double* red) {
 
 // Symmetric pseudoinverse by cyclic Jacobi (single thread, R <= RMAX).
 template <int RMAX>
-__device__ void jacobi_pinv(const double* H, int R, double* Hp, double rcond) {
+__device__ __noinline__ void jacobi_pinv(const double* H, int R, double* Hp, double rcond) {
   double A[RMAX * RMAX], Q[RMAX * RMAX];
   for (int e = 0; e < R * R; ++e) { A[e] = H[e]; Q[e] = 0.0; }
   for (int i = 0; i < R; ++i) Q[i * R + i] = 1.0;
@@ -357,29 +357,40 @@ __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
   const int cb = k * R;
 
   __shared__ double H[RMAX * RMAX];
-  __shared__ double Lf[RMAX * RMAX];
+  __shared__ double Lf[RMAX * RMAX];   // Cholesky factor (row-major lower) or H^+
+  __shared__ double Linv[RMAX];        // 1 / L(j,j)
   __shared__ double red[RMAX * RMAX + RMAX + 1];
-  __shared__ double lam_s[RMAX];
+  __shared__ double lam_s[RMAX], ilam_s[RMAX];
   __shared__ int use_pinv;
   extern __shared__ double dyn[];
   double* Ms = dyn;             // [In][R]
   double* Vs = dyn + In * R;    // [In][R]
 
   // (a3) Hadamard of the cached Gramians of every other mode
-  for (int e = tid; e < R * R; e += blockDim.x) {
+  if (tid < R * R) {
     double h = 1.0;
     for (int m = 0; m < N; ++m)
-      if (m != n) h *= a.gram[((int64_t)m * a.nsub + sub) * R * R + e];
-    H[e] = h;
+      if (m != n) h *= a.gram[((int64_t)m * a.nsub + sub) * R * R + tid];
+    H[tid] = h;
   }
-  // (a2) fixed-order sum of the partial pieces of this submodel's R columns
+  // (a2) fixed-order sum of the partial pieces of this submodel's R columns; the loads of a
+  // chunk of 8 pieces are issued together (memory-level parallelism), the adds stay in order
+  const int64_t piece = (int64_t)a.BN * a.BM;
   for (int e = tid; e < In * R; e += blockDim.x) {
     const int i = e / R, r = e % R;
     const int c = cb + r, tn = i / a.BN, tm = c / a.BM;
     const TileInfo ti = a.tinfo[tn * a.nMt + tm];
-    const double* p = a.parts + (int64_t)ti.piece_base * a.BN * a.BM + (int64_t)(i - tn * a.BN) * a.BM + (c - tm * a.BM);
+    const double* p = a.parts + (int64_t)ti.piece_base * piece + (int64_t)(i - tn * a.BN) * a.BM + (c - tm * a.BM);
     double s = 0.0;
-    for (int pc = 0; pc < ti.npieces; ++pc) s += p[(int64_t)pc * a.BN * a.BM];
+    int pc = 0;
+    for (; pc + 8 <= ti.npieces; pc += 8) {
+      double x[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) x[q] = __ldcg(p + (int64_t)(pc + q) * piece);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s += x[q];
+    }
+    for (; pc < ti.npieces; ++pc) s += __ldcg(p + (int64_t)pc * piece);
     Ms[e] = s;
   }
   __syncthreads();
@@ -390,11 +401,13 @@ __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
       double s = H[j * R + j];
       for (int q = 0; q < j; ++q) s -= Lf[j * R + q] * Lf[j * R + q];
       if (!(s > 0.0) || !isfinite(s)) { ok = false; break; }
-      Lf[j * R + j] = sqrt(s);
+      const double d = sqrt(s), id = 1.0 / d;
+      Lf[j * R + j] = d;
+      Linv[j] = id;
       for (int i = j + 1; i < R; ++i) {
         double t = H[i * R + j];
         for (int q = 0; q < j; ++q) t -= Lf[i * R + q] * Lf[j * R + q];
-        Lf[i * R + j] = t / Lf[j * R + j];
+        Lf[i * R + j] = t * id;
       }
     }
     use_pinv = ok ? 0 : 1;
@@ -421,7 +434,7 @@ __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
           double t = m[r];
 #pragma unroll
           for (int q = 0; q < r; ++q) t -= Lf[r * R + q] * y[q];
-          y[r] = t / Lf[r * R + r];
+          y[r] = t * Linv[r];
         }
       }
 #pragma unroll
@@ -431,7 +444,7 @@ __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
 #pragma unroll
           for (int q = r + 1; q < RMAX; ++q)
             if (q < R) t -= Lf[q * R + r] * v[q];
-          v[r] = t / Lf[r * R + r];
+          v[r] = t * Linv[r];
         }
       }
     } else {
@@ -464,25 +477,28 @@ __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
     return Vs[i * R + e / R] * Vs[i * R + e % R];
   });
   __syncthreads();
-  if (tid < R) lam_s[tid] = sqrt(red[tid]);
+  if (tid < R) {
+    const double lm = sqrt(red[tid]);
+    lam_s[tid] = lm;
+    ilam_s[tid] = lm > 0.0 ? 1.0 / lm : 1.0;
+  }
+  __syncthreads();
+  // (a6) normalise; write the block of the multi-factor; keep U in Ms for the Gramian
+  for (int e = tid; e < In * R; e += blockDim.x) {
+    const int i = e / R, r = e % R;
+    const double uu = Vs[e] * ilam_s[r];
+    Ms[e] = uu;
+    a.U[(int64_t)i * a.ldu + cb + r] = uu;
+  }
   double quad = 0.0, crs = 0.0;
   if (last && tid == 0) {
     crs = red[R];
     for (int e = 0; e < R * R; ++e) quad += H[e] * red[R + 1 + e];
   }
   __syncthreads();
-  // (a6) normalise; write the block of the multi-factor; keep U in Ms for the Gramian
-  for (int e = tid; e < In * R; e += blockDim.x) {
-    const int i = e / R, r = e % R;
-    const double lm = lam_s[r], x = Vs[e];
-    const double uu = lm > 0.0 ? x / lm : x;
-    Ms[e] = uu;
-    a.U[(int64_t)i * a.ldu + cb + r] = uu;
-  }
-  __syncthreads();
   warp_reduce_all(R * R, In, red, [&](int q, int i) -> double { return Ms[i * R + q / R] * Ms[i * R + q % R]; });
   __syncthreads();
-  for (int e = tid; e < R * R; e += blockDim.x) a.gram[((int64_t)n * a.nsub + sub) * R * R + e] = red[e];
+  if (tid < R * R) a.gram[((int64_t)n * a.nsub + sub) * R * R + tid] = red[tid];
   if (tid < R) a.lambda[(int64_t)sub * R + tid] = lam_s[tid];
 
   if (last && tid == 0) {  // (a7) error, fit, history, convergence mask
