@@ -238,9 +238,9 @@ def main():
         hh.set_init(w.P)
         hh.iterate(w.sweeps, 0.0)
         out = 0
-        for p in range(sb, se):
-            fac, lam = hh.factors(p)
-            out += sum(f.nbytes for f in fac) + lam.nbytes
+        for m in range(len(w.dims)):  # every submodel's factors, one batched D2H per mode
+            U_all, lam = hh.all_factors(m)
+            out += U_all.nbytes + (lam.nbytes if m == len(w.dims) - 1 else 0)
         for m in range(1, len(w.dims)):
             mom = hh.local_moments(m)
             out += sum(x.nbytes for x in mom)

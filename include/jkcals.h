@@ -114,6 +114,11 @@ jkcals_status jkcals_iterate(jkcals_t h, int max_iters, double tol, int *sweeps_
  * NULL) holds the column norms of the LAST updated mode (mode ndims-1 after a sweep). */
 jkcals_status jkcals_get_factors(jkcals_t h, int64_t p, int mode, double *U, double *lambda);
 
+/* Factors of ALL this handle's submodels for one mode in one call: U receives n_sub blocks in
+ * submodel order, each in the get_factors layout ((dims[0]-1) x rank for mode 0 with row p
+ * dropped; dims[mode] x rank otherwise), column-major; lambda (n_sub x rank, may be NULL). */
+jkcals_status jkcals_get_all_factors(jkcals_t h, int mode, double *U, double *lambda);
+
 /* Debug/invariant view: submodel p's FULL block of the mode-`mode` multi-factor as it sits
  * in the fused layout, dims[mode] x rank column-major. For mode 0 row p is the padded zero
  * row, which must be exactly +0.0/-0.0 after every sweep (alg:cals_jk:multifactor). */

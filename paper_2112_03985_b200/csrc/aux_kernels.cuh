@@ -132,6 +132,22 @@ __global__ void extract_kernel(const double* __restrict__ src, int64_t ld, int I
   out[e] = src[(int64_t)i * ld + r];
 }
 
+// (a9) every submodel's mode block at once: out[q] = column-major rows x R block of submodel q
+// (mode 0: the left-out row p_q dropped), q in submodel order.
+__global__ void extract_all_kernel(const double* __restrict__ base, const int64_t* __restrict__ src_off,
+                                   const int64_t* __restrict__ src_ld, int nsub, int I, int R, int drop,
+                                   const int64_t* __restrict__ pglob, double* __restrict__ out) {
+  const int rows = drop ? I - 1 : I;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)nsub * rows * R) return;
+  const int q = (int)(e / ((int64_t)rows * R));
+  const int rem = (int)(e % ((int64_t)rows * R));
+  const int r = rem / rows, io = rem % rows;
+  const int64_t p = drop ? pglob[q] : -1;
+  const int i = (drop && io >= p) ? io + 1 : io;
+  out[e] = base[src_off[q] + (int64_t)i * src_ld[q] + r];
+}
+
 // (a9) per-element moments over the handle's submodels, fixed order (two-pass):
 // mean = sum/g, M2 = sum (x - mean)^2. src_off[q] / src_ld[q] locate submodel q's block
 // (row-major) relative to `base`. Output column-major I x R.

@@ -124,6 +124,9 @@ __device__ __noinline__ void jacobi_pinv(const double* H, int R, double* Hp, dou
 template <int RMAX>
 __global__ void __launch_bounds__(kEpiThreads) als_epilogue_rows_kernel(EpiArgs a) {
   const int k = blockIdx.x;
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the MTTKRP grid has completed
+  asm volatile("griddepcontrol.launch_dependents;\n" :::);
+  if (a.n == 0 && k == 0 && threadIdx.x == 0) *a.active_count = 0;  // per-sweep counter reset
   const int sub = a.blk2sub[k];
   if (!a.active[sub]) return;  // frozen (converged or failed)
   const int R = a.R, n = a.n, N = a.N, tid = threadIdx.x;
@@ -327,10 +330,76 @@ __global__ void __launch_bounds__(kEpiThreads) als_epilogue_rows_kernel(EpiArgs 
 // memory so that the partial reduction, the solves and every reduction run with all threads.
 constexpr int kEpi2Threads = 256;
 
+#ifdef JK_EPI_PROF
+#define EPI_PROBE(i)                                                                              \
+  do {                                                                                            \
+    if (threadIdx.x == 0) {                                                                       \
+      unsigned long long t_;                                                                      \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                      \
+      epi_ts_[(i)] = t_;                                                                          \
+    }                                                                                             \
+  } while (0)
+#define EPI_PROBE_DUMP()                                                                          \
+  do {                                                                                            \
+    if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))                     \
+      printf("EPI blk %d n %d: %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", blockIdx.x,   \
+             a.n, epi_ts_[1] - epi_ts_[0], epi_ts_[2] - epi_ts_[0], epi_ts_[3] - epi_ts_[0],       \
+             epi_ts_[4] - epi_ts_[0], epi_ts_[5] - epi_ts_[0], epi_ts_[6] - epi_ts_[0],            \
+             epi_ts_[7] - epi_ts_[0], 0ull, 0ull, 0ull);                                                           \
+  } while (0)
+#else
+#define EPI_PROBE(i) do {} while (0)
+#define EPI_PROBE_DUMP() do {} while (0)
+#endif
+
+
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
   return x;
+}
+
+
+template <int J, int Q>
+__device__ __forceinline__ void sum_pieces(const EpiArgs& a, int cb, int R, int In, double* Ms) {
+  const int64_t piece = (int64_t)a.BN * a.BM;
+  const int T = blockDim.x;
+  for (int e0 = threadIdx.x; e0 < In * R; e0 += J * T) {
+    const double* p[J];
+    int np[J];
+    double s[J];
+    int npmax = 0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int e = e0 + j * T;
+      s[j] = 0.0;
+      np[j] = 0;
+      p[j] = a.parts;
+      if (e < In * R) {
+        const int i = e / R, r = e % R;
+        const int c = cb + r, tn = i / a.BN, tm = c / a.BM;
+        const TileInfo ti = a.tinfo[tn * a.nMt + tm];
+        p[j] = a.parts + (int64_t)ti.piece_base * piece + (int64_t)(i - tn * a.BN) * a.BM + (c - tm * a.BM);
+        np[j] = ti.npieces;
+        npmax = max(npmax, ti.npieces);
+      }
+    }
+    for (int pc = 0; pc < npmax; pc += Q) {
+      double x[J][Q];
+#pragma unroll
+      for (int j = 0; j < J; ++j)
+#pragma unroll
+        for (int q = 0; q < Q; ++q) x[j][q] = (pc + q < np[j]) ? __ldcg(p[j] + (int64_t)(pc + q) * piece) : 0.0;
+#pragma unroll
+      for (int j = 0; j < J; ++j)
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+          if (pc + q < np[j]) s[j] += x[j][q];
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j)
+      if (e0 + j * T < In * R) Ms[e0 + j * T] = s[j];
+  }
 }
 
 // q-th quantity over rows: Q_q = sum_i f_q(i), one warp per quantity, fixed order
@@ -348,10 +417,21 @@ __device__ __forceinline__ void warp_reduce_all(int nq, int In, double* out, F f
 
 template <int RMAX>
 __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
+  constexpr int NQ = RMAX * (RMAX + 1) / 2;  // upper triangle of V^T V
   const int k = blockIdx.x;
+#ifdef JK_EPI_PROF
+  __shared__ unsigned long long epi_ts_[16];
+#endif
+  EPI_PROBE(0);
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the MTTKRP grid has completed
+  asm volatile("griddepcontrol.launch_dependents;\n" :::);
+  EPI_PROBE(1);
+  if (a.n == 0 && k == 0 && threadIdx.x == 0) *a.active_count = 0;  // per-sweep counter reset
   const int sub = a.blk2sub[k];
   if (!a.active[sub]) return;  // frozen (converged or failed)
   const int R = a.R, n = a.n, N = a.N, tid = threadIdx.x, In = a.In;
+  const int lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kEpi2Threads / 32;
   const bool last = (n == N - 1);
   const int64_t pzero = (n == 0) ? a.pglob[sub] : -1;
   const int cb = k * R;
@@ -359,8 +439,9 @@ __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
   __shared__ double H[RMAX * RMAX];
   __shared__ double Lf[RMAX * RMAX];   // Cholesky factor (row-major lower) or H^+
   __shared__ double Linv[RMAX];        // 1 / L(j,j)
-  __shared__ double red[RMAX * RMAX + RMAX + 1];
-  __shared__ double lam_s[RMAX], ilam_s[RMAX];
+  __shared__ double red[NW][NQ + 1];
+  __shared__ double tot[NQ + 1];
+  __shared__ double ilam_s[RMAX];
   __shared__ int use_pinv;
   extern __shared__ double dyn[];
   double* Ms = dyn;             // [In][R]
@@ -373,52 +454,60 @@ __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
       if (m != n) h *= a.gram[((int64_t)m * a.nsub + sub) * R * R + tid];
     H[tid] = h;
   }
-  // (a2) fixed-order sum of the partial pieces of this submodel's R columns; the loads of a
-  // chunk of 8 pieces are issued together (memory-level parallelism), the adds stay in order
-  const int64_t piece = (int64_t)a.BN * a.BM;
-  for (int e = tid; e < In * R; e += blockDim.x) {
-    const int i = e / R, r = e % R;
-    const int c = cb + r, tn = i / a.BN, tm = c / a.BM;
-    const TileInfo ti = a.tinfo[tn * a.nMt + tm];
-    const double* p = a.parts + (int64_t)ti.piece_base * piece + (int64_t)(i - tn * a.BN) * a.BM + (c - tm * a.BM);
-    double s = 0.0;
-    int pc = 0;
-    for (; pc + 8 <= ti.npieces; pc += 8) {
-      double x[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) x[q] = __ldcg(p + (int64_t)(pc + q) * piece);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) s += x[q];
-    }
-    for (; pc < ti.npieces; ++pc) s += __ldcg(p + (int64_t)pc * piece);
-    Ms[e] = s;
-  }
+  // (a2) fixed-order sum of the partial pieces of this submodel's R columns: J elements per
+  // thread x Q pieces = 16 independent loads in flight; the adds of each element stay in order
+  if (In * R <= kEpi2Threads) sum_pieces<1, 16>(a, cb, R, In, Ms);
+  else sum_pieces<4, 4>(a, cb, R, In, Ms);
   __syncthreads();
-  // (a4) Cholesky H = L L^T (textbook, no pivoting); Jacobi pinv fallback
+  EPI_PROBE(2);
+  // (a4) Cholesky H = L L^T (textbook, no pivoting) in registers of thread 0; pinv fallback
   if (tid == 0) {
+    double L[RMAX][RMAX];
     bool ok = true;
-    for (int j = 0; j < R && ok; ++j) {
-      double s = H[j * R + j];
-      for (int q = 0; q < j; ++q) s -= Lf[j * R + q] * Lf[j * R + q];
-      if (!(s > 0.0) || !isfinite(s)) { ok = false; break; }
-      const double d = sqrt(s), id = 1.0 / d;
-      Lf[j * R + j] = d;
-      Linv[j] = id;
-      for (int i = j + 1; i < R; ++i) {
-        double t = H[i * R + j];
-        for (int q = 0; q < j; ++q) t -= Lf[i * R + q] * Lf[j * R + q];
-        Lf[i * R + j] = t * id;
+#pragma unroll
+    for (int j = 0; j < RMAX; ++j) {
+      if (j < R && ok) {
+        double s = H[j * R + j];
+#pragma unroll
+        for (int q = 0; q < j; ++q) s -= L[j][q] * L[j][q];
+        if (!(s > 0.0) || !isfinite(s)) {
+          ok = false;
+        } else {
+          const double d = sqrt(s), id = 1.0 / d;
+          L[j][j] = d;
+          Linv[j] = id;
+#pragma unroll
+          for (int i = j + 1; i < RMAX; ++i) {
+            if (i < R) {
+              double t = H[i * R + j];
+#pragma unroll
+              for (int q = 0; q < j; ++q) t -= L[i][q] * L[j][q];
+              L[i][j] = t * id;
+            }
+          }
+        }
       }
     }
     use_pinv = ok ? 0 : 1;
-    if (!ok) {
+    if (ok) {
+#pragma unroll
+      for (int i = 0; i < RMAX; ++i)
+#pragma unroll
+        for (int j = 0; j <= i; ++j)
+          if (i < R) Lf[i * R + j] = L[i][j];
+    } else {
       jacobi_pinv<RMAX>(H, R, Lf, 1e-12);
       a.flags[sub] |= F_PINV;
     }
   }
   __syncthreads();
+  EPI_PROBE(3);
   const bool pinv = use_pinv != 0;
-  // (a4/a5) per-row solve V(i,:) = M(i,:) H^{-1}; the left-out row p of mode 0 is zero
+  // (a4/a5) per-row solve V(i,:) = M(i,:) H^{-1} (the left-out row p of mode 0 is zero) and,
+  // in the same pass, this thread's share of V^T V (upper triangle) and of V.M
+  double acc[NQ + 1];
+#pragma unroll
+  for (int q = 0; q <= NQ; ++q) acc[q] = 0.0;
   for (int i = tid; i < In; i += blockDim.x) {
     double m[RMAX], v[RMAX];
 #pragma unroll
@@ -430,6 +519,7 @@ __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
       double y[RMAX];
 #pragma unroll
       for (int r = 0; r < RMAX; ++r) {
+        y[r] = 0.0;
         if (r < R) {
           double t = m[r];
 #pragma unroll
@@ -439,6 +529,7 @@ __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
       }
 #pragma unroll
       for (int r = RMAX - 1; r >= 0; --r) {
+        v[r] = 0.0;
         if (r < R) {
           double t = y[r];
 #pragma unroll
@@ -450,58 +541,64 @@ __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
     } else {
 #pragma unroll
       for (int r = 0; r < RMAX; ++r) {
-        if (r < R) {
-          double s = 0.0;
+        double s = 0.0;
 #pragma unroll
-          for (int q = 0; q < RMAX; ++q)
-            if (q < R) s += m[q] * Lf[q * R + r];
-          v[r] = s;
-        }
+        for (int q = 0; q < RMAX; ++q)
+          if (q < R && r < R) s += m[q] * Lf[q * R + r];
+        v[r] = s;
       }
     }
+    int q = 0;
 #pragma unroll
-    for (int r = 0; r < RMAX; ++r)
+    for (int r = 0; r < RMAX; ++r) {
       if (r < R) Vs[i * R + r] = v[r];
-  }
-  __syncthreads();
-  // reductions: column norms (R), then if last: V.M (1) and V^T V (R*R)
-  const int nq = last ? R + 1 + R * R : R;
-  warp_reduce_all(nq, In, red, [&](int q, int i) -> double {
-    if (q < R) { const double x = Vs[i * R + q]; return x * x; }
-    if (q == R) {
-      double s = 0.0;
-      for (int r = 0; r < R; ++r) s += Vs[i * R + r] * Ms[i * R + r];
-      return s;
+#pragma unroll
+      for (int c = r; c < RMAX; ++c, ++q) acc[q] += v[r] * v[c];
     }
-    const int e = q - R - 1;
-    return Vs[i * R + e / R] * Vs[i * R + e % R];
-  });
-  __syncthreads();
-  if (tid < R) {
-    const double lm = sqrt(red[tid]);
-    lam_s[tid] = lm;
-    ilam_s[tid] = lm > 0.0 ? 1.0 / lm : 1.0;
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) acc[NQ] += v[r] * m[r];
+  }
+  // block reduction of the NQ+1 quantities in a fixed order (shuffle tree, then warps in order)
+#pragma unroll
+  for (int q = 0; q <= NQ; ++q) {
+    const double x = warp_sum(acc[q]);
+    if (lane == 0) red[warp][q] = x;
   }
   __syncthreads();
-  // (a6) normalise; write the block of the multi-factor; keep U in Ms for the Gramian
+  EPI_PROBE(4);
+  for (int q = tid; q <= NQ; q += blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s += red[w][q];
+    tot[q] = s;
+  }
+  __syncthreads();
+  EPI_PROBE(5);
+  // (a6) lambda_r = ||V(:,r)||, U = V / lambda; Gram of U = (V^T V) / (lambda lambda^T)
+  auto vtv = [&](int r, int c) -> double {  // index into the packed upper triangle
+    const int lo = r < c ? r : c, hi = r < c ? c : r;
+    return tot[lo * RMAX - lo * (lo - 1) / 2 + (hi - lo)];
+  };
+  if (tid < R) {
+    const double lm = sqrt(vtv(tid, tid));
+    ilam_s[tid] = lm > 0.0 ? 1.0 / lm : 1.0;
+    a.lambda[(int64_t)sub * R + tid] = lm;
+  }
+  __syncthreads();
   for (int e = tid; e < In * R; e += blockDim.x) {
     const int i = e / R, r = e % R;
-    const double uu = Vs[e] * ilam_s[r];
-    Ms[e] = uu;
-    a.U[(int64_t)i * a.ldu + cb + r] = uu;
+    a.U[(int64_t)i * a.ldu + cb + r] = Vs[e] * ilam_s[r];
   }
-  double quad = 0.0, crs = 0.0;
-  if (last && tid == 0) {
-    crs = red[R];
-    for (int e = 0; e < R * R; ++e) quad += H[e] * red[R + 1 + e];
+  if (tid < R * R) {
+    const int r = tid / R, c = tid % R;
+    a.gram[((int64_t)n * a.nsub + sub) * R * R + tid] = vtv(r, c) * ilam_s[r] * ilam_s[c];
   }
-  __syncthreads();
-  warp_reduce_all(R * R, In, red, [&](int q, int i) -> double { return Ms[i * R + q / R] * Ms[i * R + q % R]; });
-  __syncthreads();
-  if (tid < R * R) a.gram[((int64_t)n * a.nsub + sub) * R * R + tid] = red[tid];
-  if (tid < R) a.lambda[(int64_t)sub * R + tid] = lam_s[tid];
-
+  EPI_PROBE(6);
   if (last && tid == 0) {  // (a7) error, fit, history, convergence mask
+    double quad = 0.0;
+    for (int r = 0; r < R; ++r)
+      for (int c = 0; c < R; ++c) quad += H[r * R + c] * vtv(r, c);
+    const double crs = tot[NQ];
     const double nt2 = a.normT2p[sub];
     const double e = nt2 + quad - 2.0 * crs;
     int it = a.iters[sub] + 1;
@@ -528,6 +625,8 @@ __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
     if (!act) a.active[sub] = 0;
     else atomicAdd(a.active_count, 1);
   }
+  EPI_PROBE(7);
+  EPI_PROBE_DUMP();
 }
 
 }  // namespace jk

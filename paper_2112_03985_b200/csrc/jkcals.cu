@@ -146,6 +146,10 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki) {
   p.units = (int64_t)p.ntiles * p.KT;
   p.smem = ki.smem[p.KM][p.ST4][p.NT - 1](mg.nslow);
   int64_t gmax = (int64_t)ki.nsm * ki.occ[p.KM][p.ST4][p.NT - 1][mg.nslow];
+  // at most kMaxPieces partial pieces per output tile: small problems (few tiles) would
+  // otherwise write and re-read a BN x BM piece per CTA for ~1 k-tile of work each
+  constexpr int64_t kMaxPieces = 48;
+  gmax = std::min<int64_t>(gmax, kMaxPieces * p.ntiles);
   p.G = (int)std::min<int64_t>(p.units, gmax);
   // Cost-weighted stream-K split. A unit (tile t, k-tile kt) costs a fixed per-k-tile overhead
   // (barrier, TMA issue, A-fragment scaling) plus the DMMA time of its busiest SM sub-partition:
@@ -382,7 +386,7 @@ bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_c
   int64_t J0 = P / dims[0];
   o->slice_nb = (int)std::min<int64_t>(J0, 2 * (int64_t)ki.nsm);
   o->slice_part = L.take((int64_t)o->slice_nb * dims[0] * 8);
-  o->stage_cap = std::max<int64_t>(3 * maxI * R, 64);
+  o->stage_cap = std::max<int64_t>(std::max<int64_t>(3 * maxI * R, nsub * maxI * R), 64);
   o->stage = L.take(o->stage_cap * 8);
   o->iters = L.take(nsub * 4);
   o->flags = L.take(nsub * 4);
@@ -443,6 +447,7 @@ struct jkcals_s {
   int* pinned_count = nullptr;
   std::vector<int> h_blk2sub, h_stored;
   bool instrument = false;
+  bool pdl = true;  // programmatic dependent launch between the sweep's kernels
   cudaEvent_t ev[2 * 2 * kMaxModes + 2] = {};
   double t_mttkrp[kMaxModes] = {0}, t_epi[kMaxModes] = {0};
   int64_t launches = 0;
@@ -512,7 +517,7 @@ jkcals_status replan(jkcals_t h) {
 }
 
 template <int RMAX>
-void launch_epi(jkcals_t h, const EpiArgs& a) {
+void launch_epi(jkcals_t h, const EpiArgs& a, bool pdl) {
   const size_t dyn = (size_t)2 * a.In * a.R * sizeof(double);
   constexpr size_t kMaxDyn = 96 * 1024;
   static unsigned attr_mask = 0;  // per RMAX instantiation and device
@@ -520,10 +525,23 @@ void launch_epi(jkcals_t h, const EpiArgs& a) {
     cudaFuncSetAttribute(als_epilogue_kernel<RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDyn);
     attr_mask |= 1u << (h->device & 31);
   }
-  if (dyn <= kMaxDyn)
-    als_epilogue_kernel<RMAX><<<h->K, kEpi2Threads, dyn, h->es>>>(a);
-  else
-    als_epilogue_rows_kernel<RMAX><<<h->K, kEpiThreads, 0, h->es>>>(a);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.gridDim = dim3(h->K);
+  cfg.stream = h->es;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (dyn <= kMaxDyn) {
+    cfg.blockDim = dim3(kEpi2Threads);
+    cfg.dynamicSmemBytes = dyn;
+    cudaLaunchKernelEx(&cfg, als_epilogue_kernel<RMAX>, a);
+  } else {
+    cfg.blockDim = dim3(kEpiThreads);
+    cfg.dynamicSmemBytes = 0;
+    cudaLaunchKernelEx(&cfg, als_epilogue_rows_kernel<RMAX>, a);
+  }
 }
 
 jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
@@ -543,8 +561,21 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
   double* parts = h->ptr<double>(h->off.parts);
   MttkrpFn fn = h->ki->fn[p.KM][p.ST4][p.NT - 1];
   if (timed) CKH(h, cudaEventRecord(h->ev[4 * n + 0], h->es));
-  fn<<<p.G, (kWarps + 1) * 32, p.smem, h->es>>>(h->tmT[n], h->tmU[h->cur][n], v, g, ti,
-                                                                             parts);
+  {
+    // programmatic dependent launch: this grid may start (prologue) while the previous kernel
+    // drains; the kernel waits (griddepcontrol.wait) before touching its inputs
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = (h->pdl && !timed) ? 1 : 0;
+    cfg.gridDim = dim3(p.G);
+    cfg.blockDim = dim3((kWarps + 1) * 32);
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = h->es;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CKH(h, cudaLaunchKernelEx(&cfg, fn, h->tmT[n], h->tmU[h->cur][n], v, g, ti, parts));
+  }
   CKH(h, cudaGetLastError());
   if (timed) CKH(h, cudaEventRecord(h->ev[4 * n + 1], h->es));
   EpiArgs a;
@@ -575,16 +606,19 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
   a.hist_cap = h->hist_cap;
   a.tol = reinterpret_cast<const double*>(h->ws + h->off.misc + 8);
   a.active_count = reinterpret_cast<int*>(h->ws + h->off.misc + 16);
-  if (h->R <= 4) launch_epi<4>(h, a);
-  else if (h->R <= 8) launch_epi<8>(h, a);
-  else launch_epi<16>(h, a);
+  const bool pdl = h->pdl && !timed;
+  if (h->R <= 2) launch_epi<2>(h, a, pdl);
+  else if (h->R <= 4) launch_epi<4>(h, a, pdl);
+  else if (h->R <= 6) launch_epi<6>(h, a, pdl);
+  else if (h->R <= 8) launch_epi<8>(h, a, pdl);
+  else launch_epi<16>(h, a, pdl);
   CKH(h, cudaGetLastError());
   if (timed) CKH(h, cudaEventRecord(h->ev[4 * n + 2], h->es));
   return JKCALS_OK;
 }
 
 jkcals_status enqueue_sweep(jkcals_t h, bool timed) {
-  CKH(h, cudaMemsetAsync(h->ws + h->off.misc + 16, 0, sizeof(int), h->es));
+  // (the per-sweep active counter is reset by the mode-0 epilogue, so a sweep is kernels only)
   for (int n = 0; n < h->N; ++n) {
     jkcals_status st = enqueue_mode(h, n, timed);
     if (st != JKCALS_OK) return st;
@@ -946,6 +980,30 @@ jkcals_status jkcals_get_factors(jkcals_t h, int64_t p, int mode, double* U, dou
   return JKCALS_OK;
 }
 
+static jkcals_status build_src_table(jkcals_t h, int mode);
+
+jkcals_status jkcals_get_all_factors(jkcals_t h, int mode, double* U, double* lambda) {
+  if (!h || !U || mode < 0 || mode >= h->N) return JKCALS_E_ARG;
+  if (!h->inited) return fail(h, JKCALS_E_STATE, "no model yet");
+  DeviceGuard dg(h->device);
+  jkcals_status st = build_src_table(h, mode);
+  if (st != JKCALS_OK) return st;
+  const int I = (int)h->dims[mode];
+  const int rows = mode == 0 ? I - 1 : I;
+  const int64_t tot = (int64_t)h->nsub * rows * h->R;
+  double* stage = h->ptr<double>(h->off.stage);
+  extract_all_kernel<<<(int)cdiv(tot, 256), 256, 0, h->stream>>>(
+      reinterpret_cast<const double*>(h->ws), h->ptr<int64_t>(h->off.srcoff), h->ptr<int64_t>(h->off.srcld), h->nsub, I,
+      h->R, mode == 0 ? 1 : 0, h->ptr<int64_t>(h->off.pglob), stage);
+  CKH(h, cudaGetLastError());
+  CKH(h, cudaMemcpyAsync(U, stage, sizeof(double) * tot, cudaMemcpyDeviceToHost, h->stream));
+  if (lambda)
+    CKH(h, cudaMemcpyAsync(lambda, h->ptr<double>(h->off.lambda), sizeof(double) * h->nsub * h->R,
+                           cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaStreamSynchronize(h->stream));
+  return JKCALS_OK;
+}
+
 jkcals_status jkcals_get_block(jkcals_t h, int64_t p, int mode, double* U) {
   if (!h || !U || mode < 0 || mode >= h->N || p < h->sub_begin || p >= h->sub_end) return JKCALS_E_ARG;
   if (!h->inited) return fail(h, JKCALS_E_STATE, "no model yet");
@@ -997,7 +1055,8 @@ jkcals_status jkcals_get_history(jkcals_t h, int64_t p, double* err, int cap, in
   return JKCALS_OK;
 }
 
-static jkcals_status moments(jkcals_t h, int mode, double* mean_d, double* m2_d) {
+// device table locating every submodel's mode-`mode` block (live multi-factor or result store)
+static jkcals_status build_src_table(jkcals_t h, int mode) {
   std::vector<int64_t> off(h->nsub), ld(h->nsub);
   for (int q = 0; q < h->nsub; ++q) {
     const double* src;
@@ -1010,6 +1069,13 @@ static jkcals_status moments(jkcals_t h, int mode, double* mean_d, double* m2_d)
   }
   CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.srcoff), off.data(), 8 * h->nsub, cudaMemcpyHostToDevice, h->stream));
   CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.srcld), ld.data(), 8 * h->nsub, cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaStreamSynchronize(h->stream));  // off/ld are host temporaries
+  return JKCALS_OK;
+}
+
+static jkcals_status moments(jkcals_t h, int mode, double* mean_d, double* m2_d) {
+  jkcals_status st = build_src_table(h, mode);
+  if (st != JKCALS_OK) return st;
   const int I = (int)h->dims[mode];
   moments_kernel<<<(int)cdiv((int64_t)I * h->R, 128), 128, 0, h->stream>>>(
       reinterpret_cast<const double*>(h->ws), h->ptr<int64_t>(h->off.srcoff), h->ptr<int64_t>(h->off.srcld),

@@ -179,6 +179,11 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   }
   __syncthreads();
+  // programmatic dependent launch: everything above overlapped the previous kernel's tail;
+  // U and the partial buffer are only touched after the previous grid has fully completed.
+  // The dependent epilogue grid may be scheduled right away (its CTAs wait likewise).
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" :::);
 
   // =========================== producer warp (warp kWarps, one lane) ===========================
   if (warp == kWarps) {

@@ -50,6 +50,7 @@ def lib():
             "jkcals_iterate": (I, [P, I, D, P]),
             "jkcals_get_factors": (I, [P, I64, I, P, P]),
             "jkcals_get_block": (I, [P, I64, I, P]),
+            "jkcals_get_all_factors": (I, [P, I, P, P]),
             "jkcals_get_status": (I, [P, P, P, P, P]),
             "jkcals_get_history": (I, [P, I64, P, I, P]),
             "jkcals_get_jackknife_stats": (I, [P, I, P, P]),
@@ -74,7 +75,7 @@ def lib():
 
 EXPORTED = [
     "jkcals_workspace_bytes", "jkcals_create", "jkcals_set_init", "jkcals_set_init_submodel", "jkcals_iterate",
-    "jkcals_get_factors", "jkcals_get_block", "jkcals_get_status", "jkcals_get_history", "jkcals_get_jackknife_stats",
+    "jkcals_get_factors", "jkcals_get_all_factors", "jkcals_get_block", "jkcals_get_status", "jkcals_get_history", "jkcals_get_jackknife_stats",
     "jkcals_get_local_moments", "jkcals_set_instrument", "jkcals_get_kernel_times", "jkcals_sweep_flops",
     "jkcals_launches_per_sweep", "jkcals_last_error", "jkcals_destroy", "jkcals_mttkrp_scratch_bytes",
     "jkcals_mttkrp", "jkcals_krp",
@@ -194,6 +195,15 @@ class JKCals:
             self._check(lib().jkcals_get_factors(self._h, int(p), n, _p(U), _p(lam) if n == self.N - 1 else None))
             out.append(U)
         return out, lam
+
+    def all_factors(self, mode):
+        """Every submodel's mode-`mode` factor at once: array (n_sub, rows, R) (row p dropped in
+        mode 0) and lambda (n_sub, R)."""
+        rows = self.dims[mode] - 1 if mode == 0 else self.dims[mode]
+        U = np.zeros((self.nsub, self.R, rows))  # C order: per submodel a column-major rows x R
+        lam = np.zeros((self.nsub, self.R))
+        self._check(lib().jkcals_get_all_factors(self._h, int(mode), _p(U), _p(lam)))
+        return np.ascontiguousarray(U.transpose(0, 2, 1)), lam
 
     def block(self, p, mode):
         """Submodel p's full fused block of mode `mode` (mode 0 keeps the zero row p)."""

@@ -190,6 +190,17 @@ def test_shards_equal_full_and_merge():
         assert np.allclose(jackknife_std(c, s), std, rtol=1e-10, atol=1e-15)
 
 
+def test_all_factors_equals_per_submodel():
+    w = make_workload("tiny")
+    h, _ = run_gpu(w, 12)
+    for mode in range(3):
+        U_all, lam_all = h.all_factors(mode)
+        for p in range(10):
+            fac, lam = h.factors(p)
+            assert np.array_equal(U_all[p], fac[mode])
+            assert np.array_equal(lam_all[p], lam)
+
+
 def test_jackknife_stats_vs_oracle():
     w = make_workload("tiny")
     h, _ = run_gpu(w, w.sweeps)
