@@ -21,6 +21,7 @@
 #include "aux_kernels.cuh"
 #include "epilogue.cuh"
 #include "mttkrp.cuh"
+#include "mttkrp_tf32.cuh"
 
 using namespace jk;
 
@@ -67,6 +68,15 @@ KernelInfo* kernel_info(int device, std::string* err) {
   cudaGetDevice(&prev);
   cudaSetDevice(device);
   cudaDeviceGetAttribute(&ki.nsm, cudaDevAttrMultiProcessorCount, device);
+  {
+    cudaError_t e = cudaFuncSetAttribute(mttkrp_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)tf_smem_bytes(kTfMaxN, kMaxModes - 2));
+    if (e != cudaSuccess) {
+      if (err) *err = std::string("cudaFuncSetAttribute(tf32): ") + cudaGetErrorString(e);
+      cudaSetDevice(prev);
+      return nullptr;
+    }
+  }
   for (int km = 0; km < 2; ++km)
     for (int st = 0; st < 2; ++st)
       for (int t = 0; t < kMaxNT; ++t) {
@@ -115,10 +125,63 @@ struct ModePlan {
   size_t smem = 0;
   std::vector<TileInfo> tinfo;
   std::vector<int> cta_u;  // CTA b processes units [cta_u[b], cta_u[b+1])
+  int tf32 = 0;
 };
 
-ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki) {
+// stream-K CTA ranges, per-tile piece bookkeeping (shared by the FP64 and TF32 plans).
+// CTA b processes units [cta_u[b], cta_u[b+1]) of the (tile, k-tile) space, split uniformly.
+// (r01 measurement: weighting units by their DMMA count made the CTAs on ragged tiles the
+// stragglers -- the per-k-tile time is dominated by its fixed part -- so the split is uniform.)
+void finish_plan(ModePlan& p, const ModeGeo& mg) {
+  (void)mg;
+  p.cta_u.assign(p.G + 1, 0);
+  for (int b = 0; b <= p.G; ++b) p.cta_u[b] = (int)((int64_t)b * p.units / p.G);
+  // drop empty ranges so that the CTAs touching a tile are consecutive and the piece index of
+  // CTA b in tile t is b - first_cta[t]
+  p.cta_u.erase(std::unique(p.cta_u.begin(), p.cta_u.end()), p.cta_u.end());
+  p.G = (int)p.cta_u.size() - 1;
+  std::vector<int> first(p.ntiles, -1), lastc(p.ntiles, -1);
+  for (int b = 0; b < p.G; ++b) {
+    int64_t u0 = p.cta_u[b], u1 = p.cta_u[b + 1];
+    if (u0 >= u1) continue;
+    int64_t t0 = u0 / p.KT, t1 = (u1 - 1) / p.KT;
+    for (int64_t t = t0; t <= t1; ++t) {
+      if (first[t] < 0) first[t] = b;
+      lastc[t] = b;
+    }
+  }
+  p.tinfo.resize(p.ntiles);
+  int base = 0;
+  for (int t = 0; t < p.ntiles; ++t) {
+    p.tinfo[t].first_cta = first[t];
+    p.tinfo[t].npieces = lastc[t] - first[t] + 1;
+    p.tinfo[t].piece_base = base;
+    p.tinfo[t].pad_ = 0;
+    base += p.tinfo[t].npieces;
+  }
+  p.npieces = base;
+}
+
+
+ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bool tf32 = false) {
   ModePlan p;
+  if (tf32) {
+    // FP32 (3xTF32 tcgen05) path: UMMA M = 128 fused columns, N = whole I_n up to 256 per tile
+    p.tf32 = 1;
+    p.nNt = (int)cdiv(mg.In, kTfMaxN);
+    p.BN = (int)rup(cdiv(mg.In, p.nNt), 16);
+    p.NT = p.BN / 8;
+    p.KM = 1;
+    p.ST4 = 1;
+    p.nMt = (int)std::max<int64_t>(1, cdiv(C, kBM));
+    p.KT = (int)(cdiv(mg.Iq0, kTfBK) * mg.Jp);
+    p.ntiles = p.nMt * p.nNt;
+    p.units = (int64_t)p.ntiles * p.KT;
+    p.smem = tf_smem_bytes(p.BN, mg.nslow);
+    p.G = (int)std::min<int64_t>(p.units, std::min<int64_t>((int64_t)ki.nsm, 48 * (int64_t)p.ntiles));
+    finish_plan(p, mg);
+    return p;
+  }
   // N tiling: NT n8 tiles per CTA tile. Score = useful/issued n8 slots x NT/(NT + 1), the second
   // factor modelling the per-k-tile cost that does not scale with NT (A fragments, S scaling,
   // barriers): I_n = 200 (25 n8) -> 5 x 5 exactly rather than 4 x 7 with 3 idle slots.
@@ -151,69 +214,7 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki) {
   constexpr int64_t kMaxPieces = 48;
   gmax = std::min<int64_t>(gmax, kMaxPieces * p.ntiles);
   p.G = (int)std::min<int64_t>(p.units, gmax);
-  // Cost-weighted stream-K split. A unit (tile t, k-tile kt) costs a fixed per-k-tile overhead
-  // (barrier, TMA issue, A-fragment scaling) plus the DMMA time of its busiest SM sub-partition:
-  // ceil(live warps / 4) x (valid n8 tiles) x (valid k4 steps) -- warps w and w+4 share one
-  // SMSP, so a C tile with 1..4 live warps runs at half the time of a full one, not 1/8.
-  const int nb0 = (int)cdiv(mg.Iq0, kBK);
-  const int64_t Jp = mg.Jp;
-  const int kv4_last = (int)cdiv(mg.Iq0 - (int64_t)(nb0 - 1) * kBK, 4);
-  constexpr double kFixed = 8.0;  // per-k-tile overhead in DMMA-pair units (full tile ~ 2*7*4 = 56)
-  auto kprefix = [&](int64_t kt) -> double {  // valid k4 steps in k-tiles [0, kt) of a tile
-    const int64_t full_tiles = (int64_t)(nb0 - 1) * Jp;
-    if (kt <= full_tiles) return 4.0 * kt;
-    return 4.0 * full_tiles + (double)kv4_last * (kt - full_tiles);
-  };
-  std::vector<double> wt(p.ntiles), wpre(p.ntiles + 1, 0.0);
-  for (int t = 0; t < p.ntiles; ++t) {
-    const int tm = t % p.nMt, tn = t / p.nMt;
-    const int64_t live_w = std::min<int64_t>(kWarps, cdiv(C - (int64_t)tm * kBM, 16));
-    const int64_t nv = std::min<int64_t>(p.NT, cdiv(mg.In - (int64_t)tn * p.BN, 8));
-    // Measured (r01): weighting by the DMMA count made ragged-tile CTAs the stragglers -- the
-    // per-k-tile time is dominated by its fixed part -- so the split is uniform in k-tiles for now.
-    wt[t] = 0.0 * (double)cdiv(std::max<int64_t>(live_w, 1), 4) * (double)std::max<int64_t>(nv, 1);
-    wpre[t + 1] = wpre[t] + wt[t] * kprefix(p.KT) + kFixed * p.KT;
-  }
-  auto prefix = [&](int64_t u) -> double {
-    const int64_t t = u / p.KT, kt = u % p.KT;
-    return t >= p.ntiles ? wpre[p.ntiles] : wpre[t] + wt[t] * kprefix(kt) + kFixed * kt;
-  };
-  p.cta_u.assign(p.G + 1, 0);
-  p.cta_u[p.G] = (int)p.units;
-  for (int b = 1; b < p.G; ++b) {
-    const double target = wpre[p.ntiles] * (double)b / (double)p.G;
-    int64_t lo = p.cta_u[b - 1], hi = p.units;  // smallest u with prefix(u) >= target
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) / 2;
-      if (prefix(mid) >= target) hi = mid;
-      else lo = mid + 1;
-    }
-    p.cta_u[b] = (int)lo;
-  }
-  // drop empty ranges (a unit costing more than one CTA's share) so that the CTAs touching a
-  // tile are consecutive and the piece index of CTA b in tile t is b - first_cta[t]
-  p.cta_u.erase(std::unique(p.cta_u.begin(), p.cta_u.end()), p.cta_u.end());
-  p.G = (int)p.cta_u.size() - 1;
-  std::vector<int> first(p.ntiles, -1), lastc(p.ntiles, -1);
-  for (int b = 0; b < p.G; ++b) {
-    int64_t u0 = p.cta_u[b], u1 = p.cta_u[b + 1];
-    if (u0 >= u1) continue;
-    int64_t t0 = u0 / p.KT, t1 = (u1 - 1) / p.KT;
-    for (int64_t t = t0; t <= t1; ++t) {
-      if (first[t] < 0) first[t] = b;
-      lastc[t] = b;
-    }
-  }
-  p.tinfo.resize(p.ntiles);
-  int base = 0;
-  for (int t = 0; t < p.ntiles; ++t) {
-    p.tinfo[t].first_cta = first[t];
-    p.tinfo[t].npieces = lastc[t] - first[t] + 1;
-    p.tinfo[t].piece_base = base;
-    p.tinfo[t].pad_ = 0;
-    base += p.tinfo[t].npieces;
-  }
-  p.npieces = base;
+  finish_plan(p, mg);
   return p;
 }
 
@@ -229,8 +230,9 @@ std::vector<char> pack_plan(const ModePlan& p) {
 }
 
 // upper bound for workspace sizing (any C' <= C)
-void plan_bounds(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, int64_t* parts, int* tiles) {
-  ModePlan p = make_plan(mg, n, C, ki);
+void plan_bounds(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, int64_t* parts, int* tiles,
+                 bool tf32 = false) {
+  ModePlan p = make_plan(mg, n, C, ki, tf32);
   *parts = (int64_t)(p.G + p.ntiles) * p.BN * kBM;
   *tiles = p.ntiles;
 }
@@ -314,6 +316,21 @@ bool make_tmap_T(CUtensorMap* tm, const double* T, int N, const int64_t* dims, i
 }
 
 // U_q0 (row-major rows x ldu): 2-D box (BMP columns, BK rows); OOB rows/columns read as zero.
+// FP32 hi/lo copy viewed as (q0 [contiguous], runA, n, runB), box (16, 1, BN, 1) with the 64-byte
+// swizzle that the UMMA K-major SWIZZLE_64B operand layout expects.
+bool make_tmap_T32(CUtensorMap* tm, const float* T, const int64_t gdim_in[4], const int64_t gstride_elems[3], int BN) {
+  auto enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t gdim[4], gstr[3];
+  for (int d = 0; d < 4; ++d) gdim[d] = (cuuint64_t)gdim_in[d];
+  for (int d = 0; d < 3; ++d) gstr[d] = (cuuint64_t)gstride_elems[d] * 4;
+  cuuint32_t box[4] = {(cuuint32_t)kTfBK, 1, (cuuint32_t)BN, 1}, est[4] = {1, 1, 1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(T), gdim, gstr, box, est,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 bool make_tmap_U(CUtensorMap* tm, const double* U, int64_t rows, int64_t ldu) {
   auto enc = encode_fn();
   if (!enc) return false;
@@ -341,7 +358,7 @@ struct Layout {
 };
 
 struct Offsets {
-  size_t T, U[2][kMaxModes], Ures, parts, tinfo[kMaxModes], gram, lambda, normT2p, fit, fit_prev, err, hist,
+  size_t T, T32hi, T32lo, T1hi, T1lo, U[2][kMaxModes], Ures, parts, tinfo[kMaxModes], gram, lambda, normT2p, fit, fit_prev, err, hist,
       slice, slice_part, stage, iters, flags, active, blk2sub, map, pglob, misc, srcoff, srcld;
   int64_t parts_cap;
   int tiles_cap;
@@ -351,7 +368,7 @@ struct Offsets {
 };
 
 bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_cap, const KernelInfo& ki,
-                     Offsets* o) {
+                     Offsets* o, bool tf32 = false) {
   int64_t P = 1, sumI = 0, maxI = 0;
   for (int k = 0; k < N; ++k) {
     P *= dims[k];
@@ -361,6 +378,13 @@ bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_c
   const int64_t C = nsub * R, ldu = rup(std::max<int64_t>(C, 1), 128);
   Layout L;
   o->T = L.take(rup(dims[0], 2) * (P / dims[0]) * 8);  // mode-0 pitch padded to even (TMA strides)
+  o->T32hi = o->T32lo = o->T1hi = o->T1lo = 0;
+  if (tf32) {  // FP32 hi/lo copies (16-byte strides): original layout and modes (1,0,2,..) permuted
+    o->T32hi = L.take(rup(dims[0], 4) * (P / dims[0]) * 4);
+    o->T32lo = L.take(rup(dims[0], 4) * (P / dims[0]) * 4);
+    o->T1hi = L.take(rup(dims[1], 4) * (P / dims[1]) * 4);
+    o->T1lo = L.take(rup(dims[1], 4) * (P / dims[1]) * 4);
+  }
   for (int s = 0; s < 2; ++s)
     for (int k = 0; k < N; ++k) o->U[s][k] = L.take(dims[k] * ldu * 8);
   o->Ures = L.take(nsub * sumI * R * 8);
@@ -369,7 +393,7 @@ bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_c
   for (int n = 0; n < N; ++n) {
     int64_t pc;
     int tc;
-    plan_bounds(mode_geo(N, dims, n), n, C, ki, &pc, &tc);
+    plan_bounds(mode_geo(N, dims, n), n, C, ki, &pc, &tc, tf32);
     o->parts_cap = std::max(o->parts_cap, pc);
     o->tiles_cap = std::max(o->tiles_cap, tc);
   }
@@ -439,6 +463,8 @@ struct jkcals_s {
   CUtensorMap tmT[kMaxModes];
   CUtensorMap tmU[2][kMaxModes];
   std::vector<char> table[kMaxModes];  // host copy of each mode's device plan table
+  int tf32 = 0;                        // precision JKCALS_FP32: 3xTF32 tcgen05 MTTKRP
+  CUtensorMap tmThi[kMaxModes], tmTlo[kMaxModes];
   cudaGraphExec_t gexec = nullptr;
   bool graph_ok = false;
   bool inited = false;
@@ -492,7 +518,7 @@ struct DeviceGuard {
 
 jkcals_status replan(jkcals_t h) {
   for (int n = 0; n < h->N; ++n) {
-    h->plan[n] = make_plan(mode_geo(h->N, h->dims, n), n, h->C, *h->ki);
+    h->plan[n] = make_plan(mode_geo(h->N, h->dims, n), n, h->C, *h->ki, h->tf32 != 0);
     const ModePlan& p = h->plan[n];
     if (plan_parts_doubles(p) > h->off.parts_cap || p.ntiles > h->off.tiles_cap)
       return fail(h, JKCALS_E_OOM, "internal: plan exceeds workspace bounds");
@@ -506,6 +532,27 @@ jkcals_status replan(jkcals_t h) {
     for (int set = 0; set < 2; ++set)
       if (!make_tmap_U(&h->tmU[set][n], h->ptr<double>(h->off.U[set][q0]), h->dims[q0], h->ldu))
         return fail(h, JKCALS_E_CUDA, "cuTensorMapEncodeTiled failed for U_%d", q0);
+    if (h->tf32) {
+      int64_t gd[4], gs[3];
+      if (n == 0) {  // permuted copy (i_1, i_0, rest): q0 = i_1 contiguous, n = i_0
+        const int64_t ld1 = rup(h->dims[1], 4), rest = h->P / (h->dims[0] * h->dims[1]);
+        gd[0] = h->dims[1]; gd[1] = 1; gd[2] = h->dims[0]; gd[3] = rest;
+        gs[0] = ld1; gs[1] = ld1; gs[2] = ld1 * h->dims[0];
+        if (!make_tmap_T32(&h->tmThi[n], h->ptr<float>(h->off.T1hi), gd, gs, p.BN) ||
+            !make_tmap_T32(&h->tmTlo[n], h->ptr<float>(h->off.T1lo), gd, gs, p.BN))
+          return fail(h, JKCALS_E_CUDA, "cuTensorMapEncodeTiled failed for the fp32 view of mode 0");
+      } else {
+        const int64_t ld0 = rup(h->dims[0], 4);
+        int64_t runA = 1, runB = 1, st_n = ld0;
+        for (int m = 1; m < n; ++m) { runA *= h->dims[m]; st_n *= h->dims[m]; }
+        for (int m = n + 1; m < h->N; ++m) runB *= h->dims[m];
+        gd[0] = h->dims[0]; gd[1] = runA; gd[2] = h->dims[n]; gd[3] = runB;
+        gs[0] = ld0; gs[1] = st_n; gs[2] = st_n * h->dims[n];
+        if (!make_tmap_T32(&h->tmThi[n], h->ptr<float>(h->off.T32hi), gd, gs, p.BN) ||
+            !make_tmap_T32(&h->tmTlo[n], h->ptr<float>(h->off.T32lo), gd, gs, p.BN))
+          return fail(h, JKCALS_E_CUDA, "cuTensorMapEncodeTiled failed for the fp32 view of mode %d", n);
+      }
+    }
   }
   CKH(h, cudaStreamSynchronize(h->stream));  // tinfo host vectors may change on the next replan
   if (h->gexec) {
@@ -559,9 +606,32 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
   g.G = p.G;
   const TileInfo* ti = h->ptr<TileInfo>(h->off.tinfo[n]);
   double* parts = h->ptr<double>(h->off.parts);
-  MttkrpFn fn = h->ki->fn[p.KM][p.ST4][p.NT - 1];
   if (timed) CKH(h, cudaEventRecord(h->ev[4 * n + 0], h->es));
-  {
+  if (h->tf32) {
+    TfGeom tg;
+    tg.C = h->C;
+    tg.ldu = h->ldu;
+    tg.nMt = p.nMt;
+    tg.nNt = p.nNt;
+    tg.BN = p.BN;
+    tg.KT = p.KT;
+    tg.units = p.units;
+    tg.G = p.G;
+    if (n == 0) v.runA = 1;  // the n = 0 fp32 view carries j' in its runB coordinate
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = (h->pdl && !timed) ? 1 : 0;
+    cfg.gridDim = dim3(p.G);
+    cfg.blockDim = dim3(kTfThreads);
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = h->es;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CKH(h, cudaLaunchKernelEx(&cfg, mttkrp_tf32_kernel, h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v, tg, ti,
+                              parts));
+  } else {
+    MttkrpFn fn = h->ki->fn[p.KM][p.ST4][p.NT - 1];
     // programmatic dependent launch: this grid may start (prologue) while the previous kernel
     // drains; the kernel waits (griddepcontrol.wait) before touching its inputs
     cudaLaunchConfig_t cfg = {};
@@ -727,12 +797,12 @@ extern "C" {
 size_t jkcals_workspace_bytes(int ndims, const int64_t* dims, int rank, int64_t n_sub, jkcals_precision prec,
                               int hist_cap, int device) {
   if (!valid_dims(ndims, dims, rank) || n_sub < 1 || n_sub > dims[0] || hist_cap < 1) return 0;
-  if (prec != JKCALS_FP64) return 0;
+  if (prec != JKCALS_FP64 && prec != JKCALS_FP32) return 0;
   if (n_sub * rank > (1 << 24)) return 0;
   KernelInfo* ki = kernel_info(device, nullptr);
   if (!ki) return 0;
   Offsets o;
-  compute_offsets(ndims, dims, rank, n_sub, hist_cap, *ki, &o);
+  compute_offsets(ndims, dims, rank, n_sub, hist_cap, *ki, &o, prec == JKCALS_FP32);
   return o.total;
 }
 
@@ -743,7 +813,7 @@ jkcals_status jkcals_create(jkcals_t* out, int ndims, const int64_t* dims, int r
   *out = nullptr;
   if (!valid_dims(ndims, dims, rank) || !tensor || !workspace) return JKCALS_E_ARG;
   if (sub_begin < 0 || sub_end > dims[0] || sub_end <= sub_begin || hist_cap < 1) return JKCALS_E_ARG;
-  if (prec != JKCALS_FP64) return JKCALS_E_ARG;  // FP32 path: not built in this round
+  if (prec != JKCALS_FP64 && prec != JKCALS_FP32) return JKCALS_E_ARG;
   DeviceGuard dg(device);
   std::string kerr;
   KernelInfo* ki = kernel_info(device, &kerr);
@@ -766,7 +836,8 @@ jkcals_status jkcals_create(jkcals_t* out, int ndims, const int64_t* dims, int r
   h->stream = static_cast<cudaStream_t>(cuda_stream);
   h->es = h->stream;
   h->ki = ki;
-  compute_offsets(ndims, dims, rank, h->nsub, hist_cap, *ki, &h->off);
+  h->tf32 = (prec == JKCALS_FP32) ? 1 : 0;
+  compute_offsets(ndims, dims, rank, h->nsub, hist_cap, *ki, &h->off, h->tf32 != 0);
   // align the caller's pointer
   uintptr_t base = reinterpret_cast<uintptr_t>(workspace);
   uintptr_t aligned = (base + kAlign - 1) & ~(uintptr_t)(kAlign - 1);
@@ -817,6 +888,21 @@ jkcals_status jkcals_create(jkcals_t* out, int ndims, const int64_t* dims, int r
   CKH(h, cudaMemcpyAsync(&nt2, h->ws + h->off.misc, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   CKH(h, cudaStreamSynchronize(h->stream));
   if (!std::isfinite(nt2)) return fail(h, JKCALS_E_NONFINITE, "tensor contains non-finite values");
+  if (h->tf32) {  // FP32 hi/lo copies of T for the 3xTF32 path (original + modes-(1,0) permuted)
+    const int64_t I1 = dims[1], rest = h->P / (dims[0] * dims[1]);
+    const int64_t ld0 = rup(dims[0], 4), ld1 = rup(dims[1], 4);
+    CKH(h, cudaMemsetAsync(h->ptr<float>(h->off.T32hi), 0, ld0 * (h->P / dims[0]) * 4, h->stream));
+    CKH(h, cudaMemsetAsync(h->ptr<float>(h->off.T32lo), 0, ld0 * (h->P / dims[0]) * 4, h->stream));
+    CKH(h, cudaMemsetAsync(h->ptr<float>(h->off.T1hi), 0, ld1 * (h->P / dims[1]) * 4, h->stream));
+    CKH(h, cudaMemsetAsync(h->ptr<float>(h->off.T1lo), 0, ld1 * (h->P / dims[1]) * 4, h->stream));
+    const int nbk = (int)cdiv(h->P, 256);
+    split_tf32_kernel<<<nbk, 256, 0, h->stream>>>(h->ptr<double>(h->off.T), dims[0], h->I0p, I1, rest, 0, ld0,
+                                                  h->ptr<float>(h->off.T32hi), h->ptr<float>(h->off.T32lo));
+    CKH(h, cudaGetLastError());
+    split_tf32_kernel<<<nbk, 256, 0, h->stream>>>(h->ptr<double>(h->off.T), dims[0], h->I0p, I1, rest, 1, ld1,
+                                                  h->ptr<float>(h->off.T1hi), h->ptr<float>(h->off.T1lo));
+    CKH(h, cudaGetLastError());
+  }
   jkcals_status st = replan(h);
   if (st != JKCALS_OK) return st;
   return JKCALS_OK;

@@ -1,0 +1,401 @@
+// mttkrp_tf32.cuh — the FP32 path of the fused KRP + MTTKRP on the 5th-generation tensor cores
+// (tcgen05.mma kind::tf32, accumulators in TMEM), FP32-accurate via the 3xTF32 split.
+//
+// Same product as mttkrp.cuh (Alg. 3 alg:cals_jk:mttkrp; Eq. 1):
+//     D[c][i] = sum_j KRP(j, c) * T_(n)(i, j)   (M = fused columns c, N = I_n, K = J_n)
+// Every operand x is split x = hi + lo with hi = x truncated to TF32 (10-bit mantissa) and
+// lo = x - hi, and D += A_hi B_hi^T + A_hi B_lo^T + A_lo B_hi^T (the lo*lo term is below FP32
+// rounding) — "3xTF32", which a single TF32 pass would fail (1.5e-4 > 1e-4).
+//
+// Roles (one CTA per SM, 6 warps):
+//   warps 0-3  A producers: build the KRP^T tile of a k-step in shared memory, already split into
+//              hi/lo and laid out in the UMMA K-major SWIZZLE_64B canonical layout, from the
+//              U_q0 slab (TMA) scaled by the S_{j'} row (bulk copies) -- the KRP never hits HBM;
+//              at the end of an output tile they drain the TMEM accumulator (tcgen05.ld) into
+//              the FP64 partial-piece buffer consumed by the same epilogue as the FP64 path.
+//   warp 4     TMA producer (one lane): T_hi / T_lo boxes (4-D tensor maps, 64-B swizzle), the
+//              S rows and the U_q0 slab, all on the stage's mbarrier.
+//   warp 5     MMA issuer (one lane): 3 x (BK/8) tcgen05.mma per k-tile, tcgen05.commit to the
+//              stage's `empty` barrier and, per output tile, to `acc_full`.
+// T is stored as FP32 hi/lo copies (built once at create): the original layout for n >= 1
+// (i_0 contiguous) and a mode-(1,0,2,..) permuted copy for n = 0 so that B is always K-major.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "mttkrp.cuh"
+
+namespace jk {
+
+constexpr int kTfBK = 16;         // k (i_q0 values) per stage: one 64-byte swizzle atom of fp32
+constexpr int kTfStages = 3;
+constexpr int kTfAWarps = 4;      // A producers / epilogue (TMEM lane quadrants 0..3)
+constexpr int kTfDWarps = 4;      // TMEM drain warps (4..7: lane quadrants warp % 4)
+constexpr int kTfThreads = (kTfAWarps + kTfDWarps + 2) * 32;
+constexpr int kTfTmaWarp = kTfAWarps + kTfDWarps, kTfMmaWarp = kTfTmaWarp + 1;
+constexpr int kTfMaxN = 256;      // UMMA N (fp32 accumulator columns) per output tile
+constexpr uint32_t kTfTmemCols = 512;  // two accumulator buffers of kTfMaxN columns
+// FP32 accumulation chains are cut every kTfChunk k-tiles (768 products x 3): the TMEM buffer is
+// drained into the FP64 partial piece while the MMAs continue in the other buffer.
+constexpr int kTfChunk = 48;
+
+struct TfGeom {
+  int C;          // fused width in use
+  int64_t ldu;    // pitch of the FP64 multi-factors (multiple of 128)
+  int nMt, nNt;   // output tiles (C / 128, I_n / BN)
+  int BN;         // UMMA N of an output tile (multiple of 16, <= 256)
+  int KT;         // k-tiles per output tile (nb0 * J')
+  int64_t units;
+  int G;
+};
+
+__host__ __device__ constexpr size_t tf_stage_bytes(int BN, int nslow) {
+  return 2u * 128u * 64u + 2u * (size_t)BN * 64u + (size_t)nslow * kBM * 8u;
+}
+__host__ __device__ constexpr size_t tf_slab_bytes() { return 2ull * kBK * kBMP * 8ull; }
+__host__ __device__ constexpr size_t tf_smem_bytes(int BN, int nslow) {
+  // 1 KB alignment slack + slab + stages + barriers (3 per stage + 2) + TMEM address
+  return 1024 + tf_slab_bytes() + kTfStages * tf_stage_bytes(BN, nslow) + (3 * kTfStages + 4) * 8 + 16;
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_64B, 8-row groups of 64-byte rows (SBO 512 B)
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1u << 16) | ((uint64_t)(512u >> 4) << 32) |
+         ((uint64_t)1u << 46) | ((uint64_t)4u << 61);
+}
+// instruction descriptor: D fp32, A/B tf32, both K-major, M = 128, N = BN
+__device__ __forceinline__ uint32_t umma_idesc_tf32(int BN) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((128u >> 4) << 24);
+}
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// mbarrier wait that traps (illegal-instruction error) instead of spinning forever if the
+// barrier never completes -- a protocol bug must not hang the GPU
+__device__ __forceinline__ void mbar_wait_safe(uint64_t* bar, unsigned parity) {
+  uint32_t done = 0;
+  for (uint64_t it = 0; it < (1ull << 26); ++it) {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+  }
+  __trap();
+}
+
+__device__ __forceinline__ uint32_t tf32_trunc(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
+
+template <int NSTEP>  // 32 lanes x NSTEP fp32 columns
+__device__ __forceinline__ void tmem_ld_32x32b(uint32_t taddr, float* v) {
+  static_assert(NSTEP == 16, "");
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(r[q]);
+}
+
+__global__ void __launch_bounds__(kTfThreads, 1)
+    mttkrp_tf32_kernel(const __grid_constant__ CUtensorMap tmThi, const __grid_constant__ CUtensorMap tmTlo,
+                       const __grid_constant__ CUtensorMap tmU, MttkrpView v, TfGeom g,
+                       const TileInfo* __restrict__ tinfo, double* __restrict__ parts) {
+  extern __shared__ __align__(1024) unsigned char tsm[];
+  unsigned char* base = tsm;  // dynamic smem is 1 KB aligned (__align__(1024) on the declaration)
+  double* Ub = reinterpret_cast<double*>(base);                                   // [2][BK][BMP] fp64
+  unsigned char* stages = base + tf_slab_bytes();
+  const size_t stage_sz = tf_stage_bytes(g.BN, v.nslow);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kTfStages * stage_sz);
+  uint64_t* fullB = bars;                      // TMA data landed (count 1 + tx)
+  uint64_t* fullA = bars + kTfStages;          // A tile written (count kTfAWarps)
+  uint64_t* empty = bars + 2 * kTfStages;      // MMAs of the stage done (tcgen05.commit)
+  uint64_t* acc_full = bars + 3 * kTfStages;   // [2] accumulator buffer holds a finished chunk
+  uint64_t* acc_empty = acc_full + 2;          // [2] accumulator buffer drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int b = blockIdx.x;
+  const int* cta_u = reinterpret_cast<const int*>(tinfo + g.nMt * g.nNt);
+  const int64_t u0 = cta_u[b], u1 = cta_u[b + 1];
+  const int BN = g.BN;
+
+  auto stA_hi = [&](int s) { return stages + s * stage_sz; };
+  auto stA_lo = [&](int s) { return stages + s * stage_sz + 128 * 64; };
+  auto stB_hi = [&](int s) { return stages + s * stage_sz + 2 * 128 * 64; };
+  auto stB_lo = [&](int s) { return stages + s * stage_sz + 2 * 128 * 64 + (size_t)BN * 64; };
+  auto stS = [&](int s) { return reinterpret_cast<double*>(stages + s * stage_sz + 2 * 128 * 64 + 2 * (size_t)BN * 64); };
+
+  if (tid == 0) {
+    for (int s = 0; s < kTfStages; ++s) {
+      mbar_init(&fullB[s], 1);
+      mbar_init(&fullA[s], kTfAWarps);
+      mbar_init(&empty[s], 1);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&acc_full[q], 1);
+      mbar_init(&acc_empty[q], kTfDWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  if (warp == 0) {  // TMEM accumulator: 128 lanes x 256 fp32 columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "n"(kTfTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" :::);
+
+  if (warp == kTfTmaWarp) {
+    // ======================= TMA producer =======================
+    if (lane == 0) {
+      const unsigned s_bytes = (unsigned)v.nslow * kBM * 8u;
+      const unsigned t_bytes = 2u * (unsigned)BN * 64u;
+      unsigned ld_git = 0;
+      for (int64_t u = u0; u < u1;) {
+        const int t = (int)(u / g.KT);
+        const int kt0 = (int)(u % g.KT);
+        const int64_t kt_end = (int64_t)kt0 + (u1 - u);
+        const int kt1 = (int)(kt_end < (int64_t)g.KT ? kt_end : (int64_t)g.KT);
+        u += kt1 - kt0;
+        const int tm = t % g.nMt, tn = t / g.nMt;
+        const int c0 = tm * kBM, i0 = tn * BN;
+        for (unsigned q = (ld_git >= (unsigned)kTfStages ? ld_git - kTfStages + 1 : 0); q < ld_git; ++q)
+          mbar_wait_safe(&empty[q % kTfStages], (q / kTfStages) & 1u);
+        int ld_b0 = kt0 / v.Jp, ld_jp = kt0 % v.Jp, loaded_b0 = -1;
+        int ld_ja = ld_jp % v.runA, ld_jb = ld_jp / v.runA;
+        int sidx[kMaxModes - 2];
+        {
+          int rem = ld_jp;
+#pragma unroll
+          for (int s = 0; s < kMaxModes - 2; ++s)
+            if (s < v.nslow) { sidx[s] = rem % v.sdim[s]; rem /= v.sdim[s]; }
+        }
+#pragma unroll 1
+        for (int kt = kt0; kt < kt1; ++kt) {
+          const int slot = (int)(ld_git % kTfStages);
+          if (ld_git >= (unsigned)kTfStages) mbar_wait_safe(&empty[slot], ((ld_git / kTfStages) - 1) & 1u);
+          uint64_t* bar = &fullB[slot];
+          const bool new_slab = (ld_b0 != loaded_b0);
+          mbar_expect_tx(bar, t_bytes + s_bytes + (new_slab ? (unsigned)(kBK * kBMP * 8) : 0u));
+          if (new_slab) {
+            tma_load_2d(Ub + (ld_b0 & 1) * (kBK * kBMP), &tmU, c0, ld_b0 * kBK, bar);
+            loaded_b0 = ld_b0;
+          }
+          // view (q0, runA, n, runB) for every mode (the n = 0 view is the permuted copy)
+          tma_load_4d(stB_hi(slot), &tmThi, ld_b0 * kTfBK, ld_ja, i0, ld_jb, bar);
+          tma_load_4d(stB_lo(slot), &tmTlo, ld_b0 * kTfBK, ld_ja, i0, ld_jb, bar);
+#pragma unroll
+          for (int s = 0; s < kMaxModes - 2; ++s)
+            if (s < v.nslow)
+              bulk_load(stS(slot) + s * kBM, v.Us[s] + (int64_t)sidx[s] * g.ldu + c0, kBM * 8u, bar);
+          ++ld_git;
+          if (++ld_jp == v.Jp) {
+            ld_jp = 0;
+            ++ld_b0;
+          }
+          if (++ld_ja == v.runA) {
+            ld_ja = 0;
+            ++ld_jb;
+          }
+          if (ld_jp == 0) ld_jb = 0;
+#pragma unroll
+          for (int s = 0; s < kMaxModes - 2; ++s) {
+            if (s < v.nslow) {
+              if (++sidx[s] < v.sdim[s]) break;
+              sidx[s] = 0;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == kTfMmaWarp) {
+    // ======================= MMA issuer =======================
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_tf32(BN);
+      unsigned git = 0, gc = 0;  // k-tiles consumed, chunks issued (accumulator buffer = gc & 1)
+      for (int64_t u = u0; u < u1;) {
+        const int kt0 = (int)(u % g.KT);
+        const int64_t kt_end = (int64_t)kt0 + (u1 - u);
+        const int kt1 = (int)(kt_end < (int64_t)g.KT ? kt_end : (int64_t)g.KT);
+        u += kt1 - kt0;
+        int cmp_b0 = kt0 / v.Jp, cmp_jp = kt0 % v.Jp;
+        bool first = true;
+        uint32_t dacc = tmem;
+        for (int kt = kt0; kt < kt1; ++kt) {
+          const int cpos = (kt - kt0) % kTfChunk;
+          if (cpos == 0) {  // new chunk: its accumulator buffer must have been drained
+            if (gc >= 2) mbar_wait_safe(&acc_empty[gc & 1], ((gc >> 1) - 1) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            dacc = tmem + (gc & 1) * kTfMaxN;
+            first = true;
+          }
+          const int slot = (int)(git % kTfStages);
+          mbar_wait_safe(&fullB[slot], (git / kTfStages) & 1u);
+          mbar_wait_safe(&fullA[slot], (git / kTfStages) & 1u);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          const int kvalid = v.Iq0 - cmp_b0 * kTfBK;
+          const int nks = kvalid >= kTfBK ? kTfBK / 8 : (kvalid + 7) / 8;
+          const uint32_t ahi = smem_u32(stA_hi(slot)), alo = smem_u32(stA_lo(slot));
+          const uint32_t bhi = smem_u32(stB_hi(slot)), blo = smem_u32(stB_lo(slot));
+          for (int kk = 0; kk < nks; ++kk) {
+            const uint32_t ko = kk * 32;  // 8 tf32 = 32 bytes along K inside the 64-byte atom
+            umma_tf32(dacc, umma_desc_sw64(alo + ko), umma_desc_sw64(bhi + ko), idesc, first ? 0u : 1u);
+            first = false;
+            umma_tf32(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(blo + ko), idesc, 1u);
+            umma_tf32(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(bhi + ko), idesc, 1u);
+          }
+          umma_commit(&empty[slot]);  // frees the stage once these MMAs have read it
+          ++git;
+          if (cpos == kTfChunk - 1 || kt == kt1 - 1) {
+            umma_commit(&acc_full[gc & 1]);  // chunk complete -> drain warps
+            ++gc;
+          }
+          if (++cmp_jp == v.Jp) {
+            cmp_jp = 0;
+            ++cmp_b0;
+          }
+        }
+      }
+    }
+  } else if (warp >= kTfAWarps) {
+    // ======================= TMEM drain warps (4..7) =======================
+    const int quad = warp & 3;               // TMEM lane quadrant of this warp
+    const int row = quad * 32 + lane;        // fused column c0 + row <-> TMEM lane
+    unsigned gc = 0;
+    for (int64_t u = u0; u < u1;) {
+      const int t = (int)(u / g.KT);
+      const int kt0 = (int)(u % g.KT);
+      const int64_t kt_end = (int64_t)kt0 + (u1 - u);
+      const int kt1 = (int)(kt_end < (int64_t)g.KT ? kt_end : (int64_t)g.KT);
+      u += kt1 - kt0;
+      const TileInfo ti = tinfo[t];
+      double* P = parts + ((int64_t)ti.piece_base + (b - ti.first_cta)) * (int64_t)(BN * kBM) + row;
+      const int nch = (kt1 - kt0 + kTfChunk - 1) / kTfChunk;
+      for (int ch = 0; ch < nch; ++ch, ++gc) {
+        mbar_wait_safe(&acc_full[gc & 1], (gc >> 1) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16) + (gc & 1) * kTfMaxN;
+        // BN is a multiple of 16; 32 columns per round keep 32 independent loads in flight
+        for (int col = 0; col < BN; col += 32) {
+          const bool two = col + 16 < BN;
+          float vals[32];
+          tmem_ld_32x32b<16>(lane_base + (uint32_t)col, vals);
+          if (two) tmem_ld_32x32b<16>(lane_base + (uint32_t)col + 16, vals + 16);
+          double* Pc = P + (int64_t)col * kBM;
+          if (ch == 0) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (q < 16 || two) Pc[(int64_t)q * kBM] = (double)vals[q];
+          } else {
+            double old[32];
+#pragma unroll
+            for (int q = 0; q < 32; ++q) old[q] = (q < 16 || two) ? __ldcg(Pc + (int64_t)q * kBM) : 0.0;
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (q < 16 || two) Pc[(int64_t)q * kBM] = old[q] + (double)vals[q];
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[gc & 1]);
+      }
+    }
+  } else {
+    // ======================= A producers (warps 0-3) =======================
+    const int row = tid;  // fused column c0 + row of the A tile (and TMEM lane)
+    unsigned git = 0;
+    for (int64_t u = u0; u < u1;) {
+      const int t = (int)(u / g.KT);
+      const int kt0 = (int)(u % g.KT);
+      const int64_t kt_end = (int64_t)kt0 + (u1 - u);
+      const int kt1 = (int)(kt_end < (int64_t)g.KT ? kt_end : (int64_t)g.KT);
+      u += kt1 - kt0;
+      const int tm = t % g.nMt;
+      const int c0 = tm * kBM;
+      const bool live = (c0 + row) < g.C;
+      int cmp_b0 = kt0 / v.Jp, cmp_jp = kt0 % v.Jp;
+      // swizzled (SWIZZLE_64B, K-major) byte offset of this row's 16-byte chunk ch
+      const uint32_t rbase = (uint32_t)(row >> 3) * 512u + (uint32_t)(row & 7) * 64u;
+      const uint32_t sw = (uint32_t)((row & 7) >> 1) & 3u;
+      for (int kt = kt0; kt < kt1; ++kt) {
+        const int slot = (int)(git % kTfStages);
+        if (git >= (unsigned)kTfStages) mbar_wait_safe(&empty[slot], ((git / kTfStages) - 1) & 1u);
+        mbar_wait_safe(&fullB[slot], (git / kTfStages) & 1u);
+        const double* Ss = stS(slot);
+        double s = 0.0;
+        if (live) {
+          s = Ss[row];
+          for (int q = 1; q < v.nslow; ++q) s *= Ss[q * kBM + row];
+        }
+        const double* ub = Ub + (cmp_b0 & 1) * (kBK * kBMP) + row;
+        unsigned char* ah = stA_hi(slot) + rbase;
+        unsigned char* al = stA_lo(slot) + rbase;
+#pragma unroll
+        for (int ch = 0; ch < kTfBK / 4; ++ch) {
+          float4 h4, l4;
+          float* hp = &h4.x;
+          float* lp = &l4.x;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float a = (float)(ub[(ch * 4 + e) * kBMP] * s);  // KRP^T(c, k) = U_q0(k, c) * S(c)
+            const uint32_t hb = tf32_trunc(a);
+            hp[e] = __uint_as_float(hb);
+            lp[e] = a - __uint_as_float(hb);
+          }
+          const uint32_t off = ((uint32_t)ch ^ sw) * 16u;
+          *reinterpret_cast<float4*>(ah + off) = h4;
+          *reinterpret_cast<float4*>(al + off) = l4;
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> tensor core
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&fullA[slot]);
+        ++git;
+        if (++cmp_jp == v.Jp) {
+          cmp_jp = 0;
+          ++cmp_b0;
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(kTfTmemCols));
+  }
+}
+
+// FP32 hi/lo copies of T for the TF32 path. dst layout: dims permuted by `perm01` (swap modes 0
+// and 1 when set), first-dim pitch ld_dst (multiple of 4 floats => 16-byte TMA strides).
+__global__ void split_tf32_kernel(const double* __restrict__ T, int64_t I0, int64_t I0p, int64_t I1, int64_t rest,
+                                  int perm01, int64_t ld_dst, float* __restrict__ hi, float* __restrict__ lo) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= I0 * I1 * rest) return;
+  const int64_t i0 = e % I0, i1 = (e / I0) % I1, r = e / (I0 * I1);
+  const double x = T[i0 + I0p * (i1 + I1 * r)];
+  const float h = __uint_as_float(__float_as_uint((float)x) & 0xFFFFE000u);
+  const float l = (float)(x - (double)h);
+  const int64_t d = perm01 ? (i1 + ld_dst * (i0 + I0 * r)) : (i0 + ld_dst * (i1 + I1 * r));
+  hi[d] = h;
+  lo[d] = l;
+}
+
+}  // namespace jk

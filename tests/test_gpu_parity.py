@@ -259,3 +259,38 @@ def test_abi_errors():
         JKCals(np.full((3, 3, 3), np.inf), 1)
     with pytest.raises(JKCalsError):
         JKCals(w.T, 2, sub_range=(4, 11))
+
+
+# ---------------------------------------------------------------- FP32 path (3xTF32 tcgen05)
+FTOL32 = 1e-4  # north_star: the FP32 path matches the FP64 oracle to 1e-4 relative Frobenius
+
+
+def run_gpu32(w, sweeps, sub_range=None):
+    from paper_2112_03985_b200 import JKCals
+    from paper_2112_03985_b200.jkcals import FP32
+    h = JKCals(w.T, w.R, sub_range=sub_range, hist_cap=max(sweeps, 1), precision=FP32)
+    h.set_init(w.P)
+    h.iterate(sweeps, 0.0)
+    return h
+
+
+def check32(h, res, p_list):
+    worst = 0.0
+    for q, p in enumerate(p_list):
+        fac, lam = h.factors(p)
+        for a, b in zip(fac, res.factors[q]):
+            worst = max(worst, rel(a, b))
+        worst = max(worst, rel(lam, res.lam[q]))
+        assert np.all(h.block(p, 0)[p] == 0.0)
+    assert worst <= FTOL32, worst
+    return worst
+
+
+@pytest.mark.parametrize("name,ps", [("tiny", None), ("syn50_r5", None), ("4way", [0, 1, 50, 99])])
+def test_fp32_path_vs_oracle(name, ps):
+    w = make_workload(name)
+    sweeps = min(w.sweeps, 50) if name == "4way" else w.sweeps
+    h = run_gpu32(w, sweeps)
+    p_list = list(range(w.dims[0])) if ps is None else ps
+    res = O.jk_als(w.T, w.P, p_list=p_list, max_iters=sweeps, nthreads=NCPU)
+    check32(h, res, p_list)

@@ -7,8 +7,9 @@ from synth import make_workload
 
 name = sys.argv[1] if len(sys.argv) > 1 else "syn200"
 sweeps = int(sys.argv[2]) if len(sys.argv) > 2 else 100
+prec = 1 if (len(sys.argv) > 3 and sys.argv[3] == "fp32") else 0
 w = make_workload(name)
-h = JKCals(w.T, w.R, hist_cap=sweeps)
+h = JKCals(w.T, w.R, hist_cap=sweeps, precision=prec)
 h.set_init(w.P); h.iterate(3, 0.0)
 h.set_init(w.P)
 torch.cuda.synchronize()
@@ -16,7 +17,7 @@ s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True
 s.record(h.stream); h.iterate(sweeps, 0.0); e.record(h.stream); e.synchronize()
 ms = s.elapsed_time(e)
 fl = h.sweep_flops()
-print(f"{name}: {sweeps} sweeps {ms:.2f} ms, {ms/sweeps*1e3:.1f} us/sweep, MTTKRP-flop rate {fl*sweeps/(ms*1e-3)/1e12:.2f} TF/s")
+print(f"{name}{' fp32' if prec else ''}: {sweeps} sweeps {ms:.2f} ms, {ms/sweeps*1e3:.1f} us/sweep, MTTKRP-flop rate {fl*sweeps/(ms*1e-3)/1e12:.2f} TF/s")
 h.set_init(w.P); h.set_instrument(True); h.iterate(10, 0.0)
 tm, te, n = h.kernel_times()
 P = float(np.prod(w.dims)); C = w.R * w.dims[0]
