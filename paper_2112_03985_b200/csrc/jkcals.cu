@@ -28,6 +28,7 @@ using namespace jk;
 namespace {
 
 constexpr size_t kAlign = 256;
+constexpr size_t kTfSmemMax = 227 * 1024;  // opt-in dynamic shared memory per CTA on sm_100
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
@@ -69,8 +70,10 @@ KernelInfo* kernel_info(int device, std::string* err) {
   cudaSetDevice(device);
   cudaDeviceGetAttribute(&ki.nsm, cudaDevAttrMultiProcessorCount, device);
   {
-    cudaError_t e = cudaFuncSetAttribute(mttkrp_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)tf_smem_bytes(kTfMaxN, kMaxModes - 2));
+    cudaError_t e = cudaFuncSetAttribute(mttkrp_tf32_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kTfSmemMax);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(mttkrp_tf32_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTfSmemMax);
     if (e != cudaSuccess) {
       if (err) *err = std::string("cudaFuncSetAttribute(tf32): ") + cudaGetErrorString(e);
       cudaSetDevice(prev);
@@ -172,12 +175,12 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
     p.BN = (int)rup(cdiv(mg.In, p.nNt), 16);
     p.NT = p.BN / 8;
     p.KM = 1;
-    p.ST4 = 1;
     p.nMt = (int)std::max<int64_t>(1, cdiv(C, kBM));
     p.KT = (int)(cdiv(mg.Iq0, kTfBK) * mg.Jp);
     p.ntiles = p.nMt * p.nNt;
     p.units = (int64_t)p.ntiles * p.KT;
-    p.smem = tf_smem_bytes(p.BN, mg.nslow);
+    p.ST4 = tf_smem_bytes(p.BN, mg.nslow, 4) <= kTfSmemMax ? 1 : 0;  // 4-stage ring when it fits
+    p.smem = tf_smem_bytes(p.BN, mg.nslow, p.ST4 ? 4 : 3);
     p.G = (int)std::min<int64_t>(p.units, std::min<int64_t>((int64_t)ki.nsm, 48 * (int64_t)p.ntiles));
     finish_plan(p, mg);
     return p;
@@ -628,8 +631,12 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     cfg.stream = h->es;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CKH(h, cudaLaunchKernelEx(&cfg, mttkrp_tf32_kernel, h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v, tg, ti,
-                              parts));
+    if (p.ST4)
+      CKH(h, cudaLaunchKernelEx(&cfg, mttkrp_tf32_kernel<4>, h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v, tg, ti,
+                                parts));
+    else
+      CKH(h, cudaLaunchKernelEx(&cfg, mttkrp_tf32_kernel<3>, h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v, tg, ti,
+                                parts));
   } else {
     MttkrpFn fn = h->ki->fn[p.KM][p.ST4][p.NT - 1];
     // programmatic dependent launch: this grid may start (prologue) while the previous kernel

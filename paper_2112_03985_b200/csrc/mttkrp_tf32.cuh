@@ -29,7 +29,6 @@
 namespace jk {
 
 constexpr int kTfBK = 16;         // k (i_q0 values) per stage: one 64-byte swizzle atom of fp32
-constexpr int kTfStages = 3;
 constexpr int kTfAWarps = 4;      // A producers / epilogue (TMEM lane quadrants 0..3)
 constexpr int kTfDWarps = 4;      // TMEM drain warps (4..7: lane quadrants warp % 4)
 constexpr int kTfThreads = (kTfAWarps + kTfDWarps + 2) * 32;
@@ -54,9 +53,9 @@ __host__ __device__ constexpr size_t tf_stage_bytes(int BN, int nslow) {
   return 2u * 128u * 64u + 2u * (size_t)BN * 64u + (size_t)nslow * kBM * 8u;
 }
 __host__ __device__ constexpr size_t tf_slab_bytes() { return 2ull * kBK * kBMP * 8ull; }
-__host__ __device__ constexpr size_t tf_smem_bytes(int BN, int nslow) {
-  // 1 KB alignment slack + slab + stages + barriers (3 per stage + 2) + TMEM address
-  return 1024 + tf_slab_bytes() + kTfStages * tf_stage_bytes(BN, nslow) + (3 * kTfStages + 4) * 8 + 16;
+__host__ __device__ constexpr size_t tf_smem_bytes(int BN, int nslow, int stages) {
+  // 1 KB alignment slack + slab + stages + barriers (3 per stage + 4) + TMEM address
+  return 1024 + tf_slab_bytes() + stages * tf_stage_bytes(BN, nslow) + (3 * stages + 4) * 8 + 16;
 }
 
 // UMMA shared-memory descriptor: K-major, SWIZZLE_64B, 8-row groups of 64-byte rows (SBO 512 B)
@@ -109,6 +108,7 @@ __device__ __forceinline__ void tmem_ld_32x32b(uint32_t taddr, float* v) {
   for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(r[q]);
 }
 
+template <int kTfStages>
 __global__ void __launch_bounds__(kTfThreads, 1)
     mttkrp_tf32_kernel(const __grid_constant__ CUtensorMap tmThi, const __grid_constant__ CUtensorMap tmTlo,
                        const __grid_constant__ CUtensorMap tmU, MttkrpView v, TfGeom g,
@@ -194,6 +194,10 @@ __global__ void __launch_bounds__(kTfThreads, 1)
           if (ld_git >= (unsigned)kTfStages) mbar_wait_safe(&empty[slot], ((ld_git / kTfStages) - 1) & 1u);
           uint64_t* bar = &fullB[slot];
           const bool new_slab = (ld_b0 != loaded_b0);
+          if (new_slab && v.Jp < kTfStages - 1) {  // short i_q0 blocks: drain before reusing a slab buffer
+            for (unsigned q = (ld_git >= (unsigned)kTfStages ? ld_git - kTfStages + 1 : 0); q < ld_git; ++q)
+              mbar_wait_safe(&empty[q % kTfStages], (q / kTfStages) & 1u);
+          }
           mbar_expect_tx(bar, t_bytes + s_bytes + (new_slab ? (unsigned)(kBK * kBMP * 8) : 0u));
           if (new_slab) {
             tma_load_2d(Ub + (ld_b0 & 1) * (kBK * kBMP), &tmU, c0, ld_b0 * kBK, bar);
