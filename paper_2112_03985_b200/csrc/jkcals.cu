@@ -179,8 +179,9 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
     p.KT = (int)(cdiv(mg.Iq0, kTfBK) * mg.Jp);
     p.ntiles = p.nMt * p.nNt;
     p.units = (int64_t)p.ntiles * p.KT;
-    p.ST4 = tf_smem_bytes(p.BN, mg.nslow, 4) <= kTfSmemMax ? 1 : 0;  // 4-stage ring when it fits
-    p.smem = tf_smem_bytes(p.BN, mg.nslow, p.ST4 ? 4 : 3);
+    // 4-stage ring when it fits (r01: deeper rings measured slower), else 3
+    p.ST4 = tf_smem_bytes(p.BN, mg.nslow, 4) <= kTfSmemMax ? 4 : 3;
+    p.smem = tf_smem_bytes(p.BN, mg.nslow, p.ST4);
     p.G = (int)std::min<int64_t>(p.units, std::min<int64_t>((int64_t)ki.nsm, 48 * (int64_t)p.ntiles));
     finish_plan(p, mg);
     return p;
@@ -631,7 +632,8 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     cfg.stream = h->es;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (p.ST4)
+    tg.stages = p.ST4;
+    if (p.ST4 == 4)
       CKH(h, cudaLaunchKernelEx(&cfg, mttkrp_tf32_kernel<4>, h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v, tg, ti,
                                 parts));
     else

@@ -29,8 +29,8 @@
 namespace jk {
 
 constexpr int kTfBK = 16;         // k (i_q0 values) per stage: one 64-byte swizzle atom of fp32
-constexpr int kTfAWarps = 4;      // A producers / epilogue (TMEM lane quadrants 0..3)
-constexpr int kTfDWarps = 4;      // TMEM drain warps (4..7: lane quadrants warp % 4)
+constexpr int kTfAWarps = 8;      // A producers: thread = (row of the A tile, half of the k-tile)
+constexpr int kTfDWarps = 4;      // TMEM drain warps (8..11: lane quadrants warp % 4)
 constexpr int kTfThreads = (kTfAWarps + kTfDWarps + 2) * 32;
 constexpr int kTfTmaWarp = kTfAWarps + kTfDWarps, kTfMmaWarp = kTfTmaWarp + 1;
 constexpr int kTfMaxN = 256;      // UMMA N (fp32 accumulator columns) per output tile
@@ -38,6 +38,7 @@ constexpr uint32_t kTfTmemCols = 512;  // two accumulator buffers of kTfMaxN col
 // FP32 accumulation chains are cut every kTfChunk k-tiles (768 products x 3): the TMEM buffer is
 // drained into the FP64 partial piece while the MMAs continue in the other buffer.
 constexpr int kTfChunk = 48;
+constexpr int kTfMaxStages = 8;
 
 struct TfGeom {
   int C;          // fused width in use
@@ -47,6 +48,7 @@ struct TfGeom {
   int KT;         // k-tiles per output tile (nb0 * J')
   int64_t units;
   int G;
+  int stages;     // shared-memory ring depth (as many as fit, <= kTfMaxStages)
 };
 
 __host__ __device__ constexpr size_t tf_stage_bytes(int BN, int nslow) {
@@ -55,7 +57,7 @@ __host__ __device__ constexpr size_t tf_stage_bytes(int BN, int nslow) {
 __host__ __device__ constexpr size_t tf_slab_bytes() { return 2ull * kBK * kBMP * 8ull; }
 __host__ __device__ constexpr size_t tf_smem_bytes(int BN, int nslow, int stages) {
   // 1 KB alignment slack + slab + stages + barriers (3 per stage + 4) + TMEM address
-  return 1024 + tf_slab_bytes() + stages * tf_stage_bytes(BN, nslow) + (3 * stages + 4) * 8 + 16;
+  return 1024 + tf_slab_bytes() + stages * tf_stage_bytes(BN, nslow) + (4 * stages + 4) * 8 + 16;
 }
 
 // UMMA shared-memory descriptor: K-major, SWIZZLE_64B, 8-row groups of 64-byte rows (SBO 512 B)
@@ -124,7 +126,8 @@ __global__ void __launch_bounds__(kTfThreads, 1)
   uint64_t* empty = bars + 2 * kTfStages;      // MMAs of the stage done (tcgen05.commit)
   uint64_t* acc_full = bars + 3 * kTfStages;   // [2] accumulator buffer holds a finished chunk
   uint64_t* acc_empty = acc_full + 2;          // [2] accumulator buffer drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* fullS = acc_empty + 2;             // [STAGES] S rows (+ U_q0 slab) landed: A may start
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fullS + kTfStages);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int b = blockIdx.x;
@@ -141,6 +144,7 @@ __global__ void __launch_bounds__(kTfThreads, 1)
   if (tid == 0) {
     for (int s = 0; s < kTfStages; ++s) {
       mbar_init(&fullB[s], 1);
+      mbar_init(&fullS[s], 1);
       mbar_init(&fullA[s], kTfAWarps);
       mbar_init(&empty[s], 1);
     }
@@ -198,18 +202,21 @@ __global__ void __launch_bounds__(kTfThreads, 1)
             for (unsigned q = (ld_git >= (unsigned)kTfStages ? ld_git - kTfStages + 1 : 0); q < ld_git; ++q)
               mbar_wait_safe(&empty[q % kTfStages], (q / kTfStages) & 1u);
           }
-          mbar_expect_tx(bar, t_bytes + s_bytes + (new_slab ? (unsigned)(kBK * kBMP * 8) : 0u));
+          uint64_t* sbar = &fullS[slot];
+          // the A producers only need the slow-mode rows and the U_q0 slab: their own barrier, issued first
+          mbar_expect_tx(sbar, s_bytes + (new_slab ? (unsigned)(kBK * kBMP * 8) : 0u));
           if (new_slab) {
-            tma_load_2d(Ub + (ld_b0 & 1) * (kBK * kBMP), &tmU, c0, ld_b0 * kBK, bar);
+            tma_load_2d(Ub + (ld_b0 & 1) * (kBK * kBMP), &tmU, c0, ld_b0 * kBK, sbar);
             loaded_b0 = ld_b0;
           }
-          // view (q0, runA, n, runB) for every mode (the n = 0 view is the permuted copy)
-          tma_load_4d(stB_hi(slot), &tmThi, ld_b0 * kTfBK, ld_ja, i0, ld_jb, bar);
-          tma_load_4d(stB_lo(slot), &tmTlo, ld_b0 * kTfBK, ld_ja, i0, ld_jb, bar);
 #pragma unroll
           for (int s = 0; s < kMaxModes - 2; ++s)
             if (s < v.nslow)
-              bulk_load(stS(slot) + s * kBM, v.Us[s] + (int64_t)sidx[s] * g.ldu + c0, kBM * 8u, bar);
+              bulk_load(stS(slot) + s * kBM, v.Us[s] + (int64_t)sidx[s] * g.ldu + c0, kBM * 8u, sbar);
+          mbar_expect_tx(bar, t_bytes);
+          // view (q0, runA, n, runB) for every mode (the n = 0 view is the permuted copy)
+          tma_load_4d(stB_hi(slot), &tmThi, ld_b0 * kTfBK, ld_ja, i0, ld_jb, bar);
+          tma_load_4d(stB_lo(slot), &tmTlo, ld_b0 * kTfBK, ld_ja, i0, ld_jb, bar);
           ++ld_git;
           if (++ld_jp == v.Jp) {
             ld_jp = 0;
@@ -323,8 +330,9 @@ __global__ void __launch_bounds__(kTfThreads, 1)
       }
     }
   } else {
-    // ======================= A producers (warps 0-3) =======================
-    const int row = tid;  // fused column c0 + row of the A tile (and TMEM lane)
+    // ======================= A producers (warps 0-7) =======================
+    const int row = tid & (kBM - 1);  // fused column c0 + row of the A tile
+    const int kh = tid >> 7;          // which half of the k-tile (chunks 2kh, 2kh+1)
     unsigned git = 0;
     for (int64_t u = u0; u < u1;) {
       const int t = (int)(u / g.KT);
@@ -339,27 +347,38 @@ __global__ void __launch_bounds__(kTfThreads, 1)
       // swizzled (SWIZZLE_64B, K-major) byte offset of this row's 16-byte chunk ch
       const uint32_t rbase = (uint32_t)(row >> 3) * 512u + (uint32_t)(row & 7) * 64u;
       const uint32_t sw = (uint32_t)((row & 7) >> 1) & 3u;
+      // this thread's 8 U_q0 values (its row, its k half) stay in registers for the J' tiles of
+      // an i_q0 block; they are re-read from the FP64 slab only when the block changes
+      float uv[8];
+      int uv_b0 = -1;
       for (int kt = kt0; kt < kt1; ++kt) {
         const int slot = (int)(git % kTfStages);
         if (git >= (unsigned)kTfStages) mbar_wait_safe(&empty[slot], ((git / kTfStages) - 1) & 1u);
-        mbar_wait_safe(&fullB[slot], (git / kTfStages) & 1u);
+        mbar_wait_safe(&fullS[slot], (git / kTfStages) & 1u);
         const double* Ss = stS(slot);
-        double s = 0.0;
+        float s = 0.0f;
         if (live) {
-          s = Ss[row];
-          for (int q = 1; q < v.nslow; ++q) s *= Ss[q * kBM + row];
+          double sd = Ss[row];
+          for (int q = 1; q < v.nslow; ++q) sd *= Ss[q * kBM + row];
+          s = (float)sd;
         }
-        const double* ub = Ub + (cmp_b0 & 1) * (kBK * kBMP) + row;
+        if (uv_b0 != cmp_b0) {
+          const double* ub = Ub + (cmp_b0 & 1) * (kBK * kBMP) + row;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) uv[e] = (float)ub[(kh * 8 + e) * kBMP];
+          uv_b0 = cmp_b0;
+        }
         unsigned char* ah = stA_hi(slot) + rbase;
         unsigned char* al = stA_lo(slot) + rbase;
 #pragma unroll
-        for (int ch = 0; ch < kTfBK / 4; ++ch) {
+        for (int cc = 0; cc < 2; ++cc) {
+          const int ch = kh * 2 + cc;
           float4 h4, l4;
           float* hp = &h4.x;
           float* lp = &l4.x;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float a = (float)(ub[(ch * 4 + e) * kBMP] * s);  // KRP^T(c, k) = U_q0(k, c) * S(c)
+            const float a = uv[cc * 4 + e] * s;  // KRP^T(c, k) = U_q0(k, c) * S(c), FP32 product
             const uint32_t hb = tf32_trunc(a);
             hp[e] = __uint_as_float(hb);
             lp[e] = a - __uint_as_float(hb);
