@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -74,6 +75,10 @@ KernelInfo* kernel_info(int device, std::string* err) {
                                          (int)kTfSmemMax);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(mttkrp_tf32_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTfSmemMax);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(mttkrp_tf32_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTfSmemMax);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(mttkrp_tf32_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTfSmemMax);
     if (e != cudaSuccess) {
       if (err) *err = std::string("cudaFuncSetAttribute(tf32): ") + cudaGetErrorString(e);
       cudaSetDevice(prev);
@@ -179,8 +184,11 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
     p.KT = (int)(cdiv(mg.Iq0, kTfBK) * mg.Jp);
     p.ntiles = p.nMt * p.nNt;
     p.units = (int64_t)p.ntiles * p.KT;
-    // 4-stage ring when it fits (r01: deeper rings measured slower), else 3
-    p.ST4 = tf_smem_bytes(p.BN, mg.nslow, 4) <= kTfSmemMax ? 4 : 3;
+    // deepest ring of {8, 6, 4, 3} stages that fits (env JKCALS_TF32_MAX_STAGES caps it, for tuning)
+    static int cap = [] { const char* e = getenv("JKCALS_TF32_MAX_STAGES"); return e ? atoi(e) : 8; }();
+    p.ST4 = 3;
+    for (int st : {8, 6, 4})
+      if (st <= cap && tf_smem_bytes(p.BN, mg.nslow, st) <= kTfSmemMax) { p.ST4 = st; break; }
     p.smem = tf_smem_bytes(p.BN, mg.nslow, p.ST4);
     p.G = (int)std::min<int64_t>(p.units, std::min<int64_t>((int64_t)ki.nsm, 48 * (int64_t)p.ntiles));
     finish_plan(p, mg);
@@ -633,7 +641,13 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     tg.stages = p.ST4;
-    if (p.ST4 == 4)
+    if (p.ST4 == 8)
+      CKH(h, cudaLaunchKernelEx(&cfg, mttkrp_tf32_kernel<8>, h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v, tg, ti,
+                                parts));
+    else if (p.ST4 == 6)
+      CKH(h, cudaLaunchKernelEx(&cfg, mttkrp_tf32_kernel<6>, h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v, tg, ti,
+                                parts));
+    else if (p.ST4 == 4)
       CKH(h, cudaLaunchKernelEx(&cfg, mttkrp_tf32_kernel<4>, h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v, tg, ti,
                                 parts));
     else

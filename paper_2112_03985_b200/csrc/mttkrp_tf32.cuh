@@ -94,6 +94,17 @@ __device__ __forceinline__ void mbar_wait_safe(uint64_t* bar, unsigned parity) {
   __trap();
 }
 
+// one lane of a converged warp (lane 0 when all are active): issue slot for single-thread
+// instructions while the whole warp walks the loop, so that every operand stays warp-uniform
+// (uniform registers for tcgen05.mma / TMA, no per-lane serialisation loops)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .b32 r;\n.reg .pred p;\nelect.sync r|p, 0xffffffff;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ uint32_t tf32_trunc(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
 
 template <int NSTEP>  // 32 lanes x NSTEP fp32 columns
@@ -168,8 +179,8 @@ __global__ void __launch_bounds__(kTfThreads, 1)
   asm volatile("griddepcontrol.launch_dependents;\n" :::);
 
   if (warp == kTfTmaWarp) {
-    // ======================= TMA producer =======================
-    if (lane == 0) {
+    // ======================= TMA producer (whole warp walks the loop, one elected lane issues) ===
+    {
       const unsigned s_bytes = (unsigned)v.nslow * kBM * 8u;
       const unsigned t_bytes = 2u * (unsigned)BN * 64u;
       unsigned ld_git = 0;
@@ -203,20 +214,21 @@ __global__ void __launch_bounds__(kTfThreads, 1)
               mbar_wait_safe(&empty[q % kTfStages], (q / kTfStages) & 1u);
           }
           uint64_t* sbar = &fullS[slot];
-          // the A producers only need the slow-mode rows and the U_q0 slab: their own barrier, issued first
-          mbar_expect_tx(sbar, s_bytes + (new_slab ? (unsigned)(kBK * kBMP * 8) : 0u));
-          if (new_slab) {
-            tma_load_2d(Ub + (ld_b0 & 1) * (kBK * kBMP), &tmU, c0, ld_b0 * kBK, sbar);
-            loaded_b0 = ld_b0;
-          }
+          if (elect_one()) {
+            // the A producers only need the slow-mode rows and the U_q0 slab: their own barrier
+            mbar_expect_tx(sbar, s_bytes + (new_slab ? (unsigned)(kBK * kBMP * 8) : 0u));
+            if (new_slab) tma_load_2d(Ub + (ld_b0 & 1) * (kBK * kBMP), &tmU, c0, ld_b0 * kBK, sbar);
 #pragma unroll
-          for (int s = 0; s < kMaxModes - 2; ++s)
-            if (s < v.nslow)
-              bulk_load(stS(slot) + s * kBM, v.Us[s] + (int64_t)sidx[s] * g.ldu + c0, kBM * 8u, sbar);
-          mbar_expect_tx(bar, t_bytes);
-          // view (q0, runA, n, runB) for every mode (the n = 0 view is the permuted copy)
-          tma_load_4d(stB_hi(slot), &tmThi, ld_b0 * kTfBK, ld_ja, i0, ld_jb, bar);
-          tma_load_4d(stB_lo(slot), &tmTlo, ld_b0 * kTfBK, ld_ja, i0, ld_jb, bar);
+            for (int s = 0; s < kMaxModes - 2; ++s)
+              if (s < v.nslow)
+                bulk_load(stS(slot) + s * kBM, v.Us[s] + (int64_t)sidx[s] * g.ldu + c0, kBM * 8u, sbar);
+            mbar_expect_tx(bar, t_bytes);
+            // view (q0, runA, n, runB) for every mode (the n = 0 view is the permuted copy)
+            tma_load_4d(stB_hi(slot), &tmThi, ld_b0 * kTfBK, ld_ja, i0, ld_jb, bar);
+            tma_load_4d(stB_lo(slot), &tmTlo, ld_b0 * kTfBK, ld_ja, i0, ld_jb, bar);
+          }
+          __syncwarp();
+          if (new_slab) loaded_b0 = ld_b0;
           ++ld_git;
           if (++ld_jp == v.Jp) {
             ld_jp = 0;
@@ -238,8 +250,8 @@ __global__ void __launch_bounds__(kTfThreads, 1)
       }
     }
   } else if (warp == kTfMmaWarp) {
-    // ======================= MMA issuer =======================
-    if (lane == 0) {
+    // ======================= MMA issuer (whole warp walks the loop, one elected lane issues) ===
+    {
       const uint32_t idesc = umma_idesc_tf32(BN);
       unsigned git = 0, gc = 0;  // k-tiles consumed, chunks issued (accumulator buffer = gc & 1)
       for (int64_t u = u0; u < u1;) {
@@ -266,19 +278,21 @@ __global__ void __launch_bounds__(kTfThreads, 1)
           const int nks = kvalid >= kTfBK ? kTfBK / 8 : (kvalid + 7) / 8;
           const uint32_t ahi = smem_u32(stA_hi(slot)), alo = smem_u32(stA_lo(slot));
           const uint32_t bhi = smem_u32(stB_hi(slot)), blo = smem_u32(stB_lo(slot));
-          for (int kk = 0; kk < nks; ++kk) {
-            const uint32_t ko = kk * 32;  // 8 tf32 = 32 bytes along K inside the 64-byte atom
-            umma_tf32(dacc, umma_desc_sw64(alo + ko), umma_desc_sw64(bhi + ko), idesc, first ? 0u : 1u);
-            first = false;
-            umma_tf32(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(blo + ko), idesc, 1u);
-            umma_tf32(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(bhi + ko), idesc, 1u);
+          if (elect_one()) {
+            for (int kk = 0; kk < nks; ++kk) {
+              const uint32_t ko = kk * 32;  // 8 tf32 = 32 bytes along K inside the 64-byte atom
+              umma_tf32(dacc, umma_desc_sw64(alo + ko), umma_desc_sw64(bhi + ko), idesc, first ? 0u : 1u);
+              first = false;
+              umma_tf32(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(blo + ko), idesc, 1u);
+              umma_tf32(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(bhi + ko), idesc, 1u);
+            }
+            umma_commit(&empty[slot]);  // frees the stage once these MMAs have read it
+            if (cpos == kTfChunk - 1 || kt == kt1 - 1) umma_commit(&acc_full[gc & 1]);  // -> drain warps
           }
-          umma_commit(&empty[slot]);  // frees the stage once these MMAs have read it
+          __syncwarp();
+          first = false;
           ++git;
-          if (cpos == kTfChunk - 1 || kt == kt1 - 1) {
-            umma_commit(&acc_full[gc & 1]);  // chunk complete -> drain warps
-            ++gc;
-          }
+          if (cpos == kTfChunk - 1 || kt == kt1 - 1) ++gc;
           if (++cmp_jp == v.Jp) {
             cmp_jp = 0;
             ++cmp_b0;
