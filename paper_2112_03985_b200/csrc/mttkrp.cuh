@@ -122,6 +122,17 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
       : "memory");
 }
 
+// one lane of a converged warp (lane 0 when all are active): issue slot for single-thread
+// instructions while the whole warp walks the loop, so that every operand stays warp-uniform
+// (uniform registers for tcgen05.mma / TMA, no per-lane serialisation loops)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .b32 r;\n.reg .pred p;\nelect.sync r|p, 0xffffffff;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
@@ -186,6 +197,8 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
   asm volatile("griddepcontrol.launch_dependents;\n" :::);
 
   // =========================== producer warp (warp kWarps, one lane) ===========================
+  // (r01: a warp-uniform loop with elect.sync measured no faster here -- the FP64 kernel is
+  // DMMA-bound -- and 12 % slower on the 4-way config, so the lane-0 producer stays)
   if (warp == kWarps) {
     if (lane != 0) return;
     const unsigned s_bytes = (unsigned)v.nslow * kBM * 8u;
@@ -218,16 +231,17 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
         double* st = stage0 + (size_t)slot * stage_sz;
         uint64_t* bar = &full[slot];
         const bool new_slab = (ld_b0 != loaded_b0);
-        mbar_expect_tx(bar, Cfg::kTBytes + s_bytes + (new_slab ? (unsigned)(kBK * kBMP * 8) : 0u));
-        if (new_slab) {  // U_q0 rows [b0*BK, b0*BK+BK) x columns [c0, c0+BMP): OOB rows are zero
-          tma_load_2d(Ub + (ld_b0 & 1) * (kBK * kBMP), &tmU, c0, ld_b0 * kBK, bar);
-          loaded_b0 = ld_b0;
-        }
-        if (KMAJOR) tma_load_4d(st, &tmT, ld_b0 * kBK, ld_ja, i0, ld_jb, bar);  // view (q0, runA, n, runB)
-        else tma_load_4d(st, &tmT, i0, ld_b0 * kBK, ld_ja, ld_jb, bar);
+        {
+          mbar_expect_tx(bar, Cfg::kTBytes + s_bytes + (new_slab ? (unsigned)(kBK * kBMP * 8) : 0u));
+          // U_q0 rows [b0*BK, b0*BK+BK) x columns [c0, c0+BMP): OOB rows are zero
+          if (new_slab) tma_load_2d(Ub + (ld_b0 & 1) * (kBK * kBMP), &tmU, c0, ld_b0 * kBK, bar);
+          if (KMAJOR) tma_load_4d(st, &tmT, ld_b0 * kBK, ld_ja, i0, ld_jb, bar);  // view (q0, runA, n, runB)
+          else tma_load_4d(st, &tmT, i0, ld_b0 * kBK, ld_ja, ld_jb, bar);
 #pragma unroll
-        for (int s = 0; s < kMaxModes - 2; ++s)
-          if (s < v.nslow) bulk_load(st + BT + s * kBM, v.Us[s] + (int64_t)sidx[s] * g.ldu + c0, kBM * 8u, bar);
+          for (int s = 0; s < kMaxModes - 2; ++s)
+            if (s < v.nslow) bulk_load(st + BT + s * kBM, v.Us[s] + (int64_t)sidx[s] * g.ldu + c0, kBM * 8u, bar);
+        }
+        if (new_slab) loaded_b0 = ld_b0;
         // advance to the next k-tile (j' fastest, then the i_q0 block)
         ++ld_git;
         if (++ld_jp == v.Jp) {

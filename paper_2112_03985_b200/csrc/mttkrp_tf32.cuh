@@ -94,17 +94,6 @@ __device__ __forceinline__ void mbar_wait_safe(uint64_t* bar, unsigned parity) {
   __trap();
 }
 
-// one lane of a converged warp (lane 0 when all are active): issue slot for single-thread
-// instructions while the whole warp walks the loop, so that every operand stays warp-uniform
-// (uniform registers for tcgen05.mma / TMA, no per-lane serialisation loops)
-__device__ __forceinline__ bool elect_one() {
-  uint32_t pred = 0;
-  asm volatile(
-      "{\n.reg .b32 r;\n.reg .pred p;\nelect.sync r|p, 0xffffffff;\nselp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(pred));
-  return pred != 0;
-}
-
 __device__ __forceinline__ uint32_t tf32_trunc(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
 
 template <int NSTEP>  // 32 lanes x NSTEP fp32 columns
