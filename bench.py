@@ -35,6 +35,9 @@ METRIC = "jackknife s to fit all I1 submodels (fixed iters); MTTKRP TFLOP/s vs p
 # no FP64 entry, so the measured pipe peak is the denominator (the stricter of the two).
 FP64_PEAK_TFLOPS = 37.05
 FP64_DGEMM_TFLOPS = 35.45
+# TF32 dense tensor peak for the FP32 path's roofline: MEASURED_PEAKS.json bf16 (1678 TF/s burst)
+# x the guide's nominal tf32/bf16 ratio (1.1 / 2.25 PFLOP/s); 3xTF32 issues 3 MMAs per FP32 product
+TF32_PEAK_TFLOPS = round(1678.0 * 1.1 / 2.25, 1)
 
 
 def dist_env():
@@ -149,6 +152,7 @@ def main():
     ap.add_argument("--config", default="syn200")
     ap.add_argument("--ref-sweeps", type=int, default=30, help="sweeps per oracle sample step (~10 s on 16 cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the supplementary FP32-path measurement")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -255,6 +259,39 @@ def main():
         e2e = float(t.item())
 
     launches_per_step = (2 * len(w.dims) + 1) + h.launches_per_sweep() * w.sweeps
+
+    # --- supplementary: the optional FP32 path (3xTF32 on tcgen05, FP64 epilogue), same workload
+    fp32 = None
+    if not args.no_fp32:
+        from paper_2112_03985_b200.jkcals import FP32
+        h32 = JKCals(Td, w.R, sub_range=(sb, se), hist_cap=w.sweeps, dims=w.dims, precision=FP32)
+        for _ in range(2):
+            h32.set_init(w.P)
+            h32.iterate(w.sweeps, 0.0)
+        t32 = 0.0
+        for _ in range(max(2, min(args.steps, 3))):
+            flush.random_(0, 255)
+            barrier()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(h32.stream)
+            h32.set_init(w.P)
+            h32.iterate(w.sweeps, 0.0)
+            e.record(h32.stream)
+            e.synchronize()
+            t32 += s.elapsed_time(e)
+        t32 /= max(2, min(args.steps, 3))
+        h32.set_init(w.P)
+        h32.set_instrument(True)
+        h32.iterate(w.sweeps, 0.0)
+        tm32, te32, nl32 = h32.kernel_times()
+        ach32 = flops_launch / (float(tm32.sum()) / nl32 * 1e-3) / 1e12
+        fp32 = {"value": round(t32 / 1e3, 5), "unit": "s", "dtype": "f32 (3xTF32 tcgen05 MTTKRP, f64 epilogue)",
+                "mttkrp_tflops_fp32_equiv": round(ach32, 2),
+                "roofline": {"bound": "tensor", "achieved": round(3 * ach32, 2), "unit": "TFLOP/s (tf32 MMA)",
+                             "peak": TF32_PEAK_TFLOPS, "frac": round(3 * ach32 / TF32_PEAK_TFLOPS, 4),
+                             "peak_source": "measured bf16 cuBLAS 1678 TF/s x nominal tf32/bf16 ratio 1.1/2.25"},
+                "parity_bar": "1e-4 relative Frobenius vs the FP64 oracle"}
+        h32.close()
     line = None
     if rank == 0:
         cpu = None
@@ -282,6 +319,7 @@ def main():
             "e2e": {"value": round(e2e, 4), "unit": "s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches_per_step * args.steps),
+            "fp32_path": fp32,
             "clocks": {"sm_mhz": csum["sm_mhz"], "sm_max_mhz": csum["sm_max_mhz"], "reasons": csum["reasons"]},
         }
         print(json.dumps(line), flush=True)
