@@ -271,6 +271,17 @@ void orc_slice_norms_sq(int N, const int64_t *dims, const double *T, int mode, d
   }
 }
 
+/* delete-d variant: drop every element with p0 <= i_mode < p1. */
+void orc_remove_slices(int N, const int64_t *dims, const double *T, int mode, int64_t p0, int64_t p1,
+                       double *out) {
+  int64_t total = prod_dims(N, dims), w = 0;
+  int64_t idx[16] = {0}; /* N <= 16 */
+  for (int64_t lin = 0; lin < total; ++lin) {
+    if (idx[mode] < p0 || idx[mode] >= p1) out[w++] = T[lin];
+    next_index(N, dims, idx);
+  }
+}
+
 /* Alg. 2 alg:jk:tensor_subsample: drop every element with i_mode == p,
  * keeping the remaining elements in their column-major order. */
 void orc_remove_slice(int N, const int64_t *dims, const double *T, int mode, int64_t p,
@@ -376,8 +387,9 @@ typedef struct {
   const double *T;
   int R;
   const double *const *P;
-  const int64_t *p_list;
+  const int64_t *p_list;  /* group indices g: rows [g*d, min(g*d + d, I_0)) of mode 0 */
   int64_t np;
+  int64_t d;
   int max_iters;
   double tol;
   double *out_U, *out_lambda, *out_err;
@@ -389,27 +401,28 @@ typedef struct {
 static void jk_one(jk_job *J, int64_t q) {
   int N = J->N, R = J->R;
   const int64_t *dims = J->dims;
-  int64_t p = J->p_list[q];
+  const int64_t p0 = J->p_list[q] * J->d;
+  const int64_t p1 = (p0 + J->d < dims[0]) ? p0 + J->d : dims[0];  /* removed rows [p0, p1) */
   int64_t sub_dims[16];
   for (int k = 0; k < N; ++k) sub_dims[k] = dims[k];
-  sub_dims[0] = dims[0] - 1;
+  sub_dims[0] = dims[0] - (p1 - p0);
   int64_t sub_total = prod_dims(N, sub_dims);
   double *Tp = malloc(sizeof(double) * (size_t)sub_total);
-  orc_remove_slice(N, dims, J->T, 0, p, Tp); /* alg:jk:tensor_subsample */
+  orc_remove_slices(N, dims, J->T, 0, p0, p1, Tp); /* alg:jk:tensor_subsample (delete-d) */
   double *U[16];
-  int64_t stride = 0;
-  for (int k = 0; k < N; ++k) stride += sub_dims[k] * R;
+  int64_t stride = R * (dims[0] - 1); /* fixed slot size: mode 0 of any group has <= I_0 - 1 rows */
+  for (int k = 1; k < N; ++k) stride += sub_dims[k] * R;
   double *outq = J->out_U + q * stride;
   int64_t off = 0;
   for (int k = 0; k < N; ++k) {
     U[k] = outq + off;
     off += sub_dims[k] * R;
   }
-  /* alg:jk:model_subsample: U_0 = P_0 with row p removed; U_n = P_n */
+  /* alg:jk:model_subsample: U_0 = P_0 with the group's rows removed; U_n = P_n */
   for (int r = 0; r < R; ++r) {
     int64_t w = 0;
     for (int64_t i = 0; i < dims[0]; ++i)
-      if (i != p) U[0][w++ + sub_dims[0] * r] = J->P[0][i + dims[0] * r];
+      if (i < p0 || i >= p1) U[0][w++ + sub_dims[0] * r] = J->P[0][i + dims[0] * r];
   }
   for (int k = 1; k < N; ++k) memcpy(U[k], J->P[k], sizeof(double) * (size_t)(dims[k] * R));
   int iters = 0;
@@ -435,11 +448,21 @@ static void *jk_worker(void *arg) {
 int orc_jk_als(int N, const int64_t *dims, const double *T, int R, const double *const *P,
                const int64_t *p_list, int64_t np, int max_iters, double tol, int nthreads,
                double *out_U, double *out_lambda, double *out_err, int *out_iters, int *out_flags) {
-  if (N < 2 || N > 16 || dims[0] < 2 || R < 1 || max_iters < 1) return -1;
-  for (int64_t q = 0; q < np; ++q)
-    if (p_list[q] < 0 || p_list[q] >= dims[0]) return -1;
-  for (int64_t q = 0; q < np * max_iters; ++q) out_err[q] = NAN;
-  jk_job J = {N, dims, T, R, P, p_list, np, max_iters, tol, out_U, out_lambda, out_err,
+  return orc_jk_als_d(N, dims, T, R, P, 1, p_list, np, max_iters, tol, nthreads, out_U, out_lambda, out_err,
+                      out_iters, out_flags);
+}
+
+int orc_jk_als_d(int N, const int64_t *dims, const double *T, int R, const double *const *P, int64_t d,
+                 const int64_t *g_list, int64_t ng, int max_iters, double tol, int nthreads, double *out_U,
+                 double *out_lambda, double *out_err, int *out_iters, int *out_flags) {
+  if (N < 2 || N > 16 || dims[0] < 2 || R < 1 || max_iters < 1 || d < 1 || 2 * d > dims[0]) return -1;
+  const int64_t ngroups = (dims[0] + d - 1) / d;
+  for (int64_t q = 0; q < ng; ++q)
+    if (g_list[q] < 0 || g_list[q] >= ngroups) return -1;
+  for (int64_t q = 0; q < ng * max_iters; ++q) out_err[q] = NAN;
+  int64_t np = ng;
+  const int64_t *p_list = g_list;
+  jk_job J = {N, dims, T, R, P, p_list, np, d, max_iters, tol, out_U, out_lambda, out_err,
               out_iters, out_flags, 0, PTHREAD_MUTEX_INITIALIZER};
   if (nthreads < 1) nthreads = 1;
   if (nthreads > np) nthreads = (int)(np > 0 ? np : 1);

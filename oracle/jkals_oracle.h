@@ -84,6 +84,16 @@ int orc_jk_als(int N, const int64_t *dims, const double *T, int R, const double 
                const int64_t *p_list, int64_t np, int max_iters, double tol, int nthreads,
                double *out_U, double *out_lambda, double *out_err, int *out_iters, int *out_flags);
 
+/* Delete-d jackknife: group g leaves out rows
+ * [g*d, min(g*d + d, I_0)) of mode 0 (ceil(I_0/d) contiguous groups, the last one possibly
+ * smaller); 1 <= d <= I_0/2. Same outputs as orc_jk_als, indexed by position
+ * q in g_list; the mode-0 block of group q has I_0 - |group| rows (slot stride as for d = 1). */
+int orc_jk_als_d(int N, const int64_t *dims, const double *T, int R, const double *const *P, int64_t d,
+                 const int64_t *g_list, int64_t ng, int max_iters, double tol, int nthreads, double *out_U,
+                 double *out_lambda, double *out_err, int *out_iters, int *out_flags);
+void orc_remove_slices(int N, const int64_t *dims, const double *T, int mode, int64_t p0, int64_t p1,
+                       double *out);
+
 /* Jackknife mean and standard error over g submodels (alg:jk:std;
  * estimator reading SURVEY §8c A11): X is g blocks of len doubles;
  * std = sqrt(((g-1)/g) * sum_p (X_p - mean)^2). Returns -1 if g < 2. */

@@ -57,6 +57,8 @@ def lib():
             "orc_explicit_residual": (D, [I, P, P, P, P, I]),
             "orc_cp_als": (I, [I, P, P, I, P, P, I, D, P, P]),
             "orc_jk_als": (I, [I, P, P, I, P, P, I64, I, D, I, P, P, P, P, P]),
+            "orc_jk_als_d": (I, [I, P, P, I, P, I64, P, I64, I, D, I, P, P, P, P, P]),
+            "orc_remove_slices": (None, [I, P, P, I, I64, I64, P]),
             "orc_jackknife_stats": (I, [I64, I64, P, P, P]),
         }
         for name, (res, args) in sig.items():
@@ -171,6 +173,22 @@ def remove_slice(T, mode, p):
     return out
 
 
+def remove_slices(T, mode, p0, p1):
+    """Delete-d tensor subsample: drop slices p0 <= i_mode < p1."""
+    T = _f64(T)
+    d = _dims(T.shape)
+    shp = list(T.shape)
+    shp[mode] -= p1 - p0
+    out = np.zeros(shp, order="F")
+    lib().orc_remove_slices(len(d), _p(d), _p(T), mode, p0, p1, _p(out))
+    return out
+
+
+def delete_d_groups(I, d):
+    """ceil(I/d) contiguous groups of mode-0 indices, the last possibly smaller."""
+    return [list(range(g * d, min(g * d + d, I))) for g in range((I + d - 1) // d)]
+
+
 def cp_error(normT2, H, M, V):
     H, M, V = _f64(H), _f64(M), _f64(V)
     return lib().orc_cp_error(normT2, _p(H), _p(M), _p(V), V.shape[0], V.shape[1])
@@ -204,12 +222,13 @@ def cp_als(T, U0, max_iters, tol=0.0):
 class JKResult:
     """Per-submodel outputs of JK-ALS, indexed by position q in p_list."""
 
-    def __init__(self, dims, R, p_list, U, lam, err, iters, flags):
-        self.dims, self.R, self.p_list = list(dims), R, list(p_list)
+    def __init__(self, dims, R, p_list, U, lam, err, iters, flags, d=1):
+        self.dims, self.R, self.p_list, self.d = list(dims), R, list(p_list), d
         self.lam, self.err, self.iters, self.flags = lam, err, iters, flags
-        rows = [dims[0] - 1] + list(dims[1:])
         self.factors = []
-        for q in range(len(p_list)):
+        for q, g in enumerate(p_list):
+            size = min(g * d + d, dims[0]) - g * d
+            rows = [dims[0] - size] + list(dims[1:])
             off, fs = 0, []
             for r_ in rows:
                 fs.append(U[q, off:off + r_ * R].reshape((r_, R), order="F"))
@@ -243,6 +262,34 @@ def jk_als(T, P, p_list=None, max_iters=100, tol=0.0, nthreads=None):
     if rc != 0:
         raise ValueError("orc_jk_als rejected its arguments")
     return JKResult(d.tolist(), R, pl.tolist(), U, lam, err, iters, flags)
+
+
+def jk_als_d(T, P, d, g_list=None, max_iters=100, tol=0.0, nthreads=None):
+    """Delete-d JK-ALS: group g removes mode-0 rows [g*d, min(g*d+d, I_0))."""
+    T = _f64(T)
+    P = [_f64(u) for u in P]
+    dims = _dims(T.shape)
+    R = P[0].shape[1]
+    if d < 1:
+        raise ValueError("delete-d needs d >= 1")
+    ngroups = (int(dims[0]) + d - 1) // d
+    if g_list is None:
+        g_list = range(ngroups)
+    gl = np.ascontiguousarray(np.asarray(list(g_list), dtype=np.int64))
+    ng = len(gl)
+    stride = R * (int(dims[0]) - 1 + int(dims[1:].sum()))
+    U = np.zeros((max(ng, 1), stride))
+    lam = np.zeros((max(ng, 1), R))
+    err = np.zeros((max(ng, 1), max_iters))
+    iters = np.zeros(max(ng, 1), dtype=np.int32)
+    flags = np.zeros(max(ng, 1), dtype=np.int32)
+    if nthreads is None:
+        nthreads = os.cpu_count() or 1
+    rc = lib().orc_jk_als_d(len(dims), _p(dims), _p(T), R, _ptr_array(P), d, _p(gl), ng, max_iters,
+                            tol, nthreads, _p(U), _p(lam), _p(err), _p(iters), _p(flags))
+    if rc != 0:
+        raise ValueError("orc_jk_als_d rejected its arguments")
+    return JKResult(dims.tolist(), R, gl.tolist(), U, lam, err, iters, flags, d=d)
 
 
 def jackknife_stats(X):

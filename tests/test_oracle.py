@@ -312,3 +312,106 @@ def test_jk_cals_equals_jk_als_theorem():
         for n in (1, 2):
             assert np.allclose(U[p][n], a[n], rtol=1e-10, atol=1e-12)
         assert np.allclose(errs[p], res.history(p), rtol=1e-9)
+
+
+# ---------------------------------------------------------------- delete-d jackknife (§4.2)
+def test_delete_d_groups_partition():
+    # ceil(I/d) contiguous disjoint groups covering 0..I-1
+    for I, d in [(10, 1), (10, 3), (7, 2), (50, 5), (9, 4)]:
+        G = O.delete_d_groups(I, d)
+        assert len(G) == -(-I // d)
+        assert sum(G, []) == list(range(I))
+        assert all(len(g) == d for g in G[:-1]) and 1 <= len(G[-1]) <= d
+
+
+def test_remove_slices_matches_numpy_delete():
+    # PAPER.md:416-417 (delete-d subsample) against numpy.delete (library routine)
+    T = rng(21).standard_normal((9, 4, 3))
+    T = np.asfortranarray(T)
+    for p0, p1 in [(0, 2), (3, 6), (8, 9)]:
+        out = O.remove_slices(T, 0, p0, p1)
+        assert np.array_equal(out, np.delete(T, range(p0, p1), axis=0))
+    assert np.array_equal(O.remove_slices(T, 0, 4, 5), O.remove_slice(T, 0, 4))
+
+
+def test_jk_als_d1_is_leave_one_out():
+    # d = 1 is leave-one-out: identical submodels, bit for bit
+    w = make_workload("tiny")
+    a = O.jk_als(w.T, w.P, max_iters=12, nthreads=2)
+    b = O.jk_als_d(w.T, w.P, 1, max_iters=12, nthreads=2)
+    assert np.array_equal(a.err, b.err) and np.array_equal(a.lam, b.lam)
+    for fa, fb in zip(a.factors, b.factors):
+        for x, y in zip(fa, fb):
+            assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("d", [2, 3, 5])
+def test_jk_als_d_matches_manual_group_removal(d):
+    # Alg. 2 with a group of d rows removed: each group's
+    # submodel is cp_als on numpy-deleted T and P_0 (independent of orc_remove_slices)
+    w = make_workload("tiny")   # I_0 = 10: d = 3 leaves a ragged last group of 1
+    res = O.jk_als_d(w.T, w.P, d, max_iters=15, nthreads=3)
+    G = O.delete_d_groups(10, d)
+    assert len(res.factors) == len(G)
+    for q, g in enumerate(G):
+        Tp = np.asfortranarray(np.delete(w.T, g, axis=0))
+        Pp = [np.delete(w.P[0], g, axis=0)] + w.P[1:]
+        U, lam, hist, _, _ = O.cp_als(Tp, Pp, 15)
+        assert res.factors[q][0].shape == (10 - len(g), w.R)
+        for a, b in zip(res.factors[q], U):
+            assert np.array_equal(a, b)
+        assert np.array_equal(res.history(q), hist)
+
+
+def test_jk_als_d_rejects_bad_d():
+    # d <= I/2 and group indices < ceil(I/d)
+    w = make_workload("tiny")
+    for d in (0, 6):
+        with pytest.raises(ValueError):
+            O.jk_als_d(w.T, w.P, d, max_iters=2)
+    with pytest.raises(ValueError):
+        O.jk_als_d(w.T, w.P, 3, g_list=[4], max_iters=2)
+
+
+def _numpy_jk_cals_d(T, P, d, sweeps):
+    """Test-only delete-d JK-CALS: pad and re-zero d rows per group."""
+    dims = T.shape
+    N, I0, R = len(dims), dims[0], P[0].shape[1]
+    G = [list(range(g * d, min(g * d + d, I0))) for g in range(-(-I0 // d))]
+    U = [[p.copy() for p in P] for _ in G]
+    for q, g in enumerate(G):
+        U[q][0][g] = 0.0
+    errs = np.zeros((len(G), sweeps))
+    for it in range(sweeps):
+        for n in range(N):
+            Tn = np_unfold(T, n)
+            for q, g in enumerate(G):
+                M = Tn @ np_krp([U[q][m] for m in range(N) if m != n])
+                H = np.ones((R, R))
+                for m in range(N):
+                    if m != n:
+                        H *= U[q][m].T @ U[q][m]
+                V = M @ np.linalg.inv(H)
+                if n == 0:
+                    V[g] = 0.0
+                U[q][n] = V / np.linalg.norm(V, axis=0)
+                if n == N - 1:
+                    n2p = np.sum(T * T) - np.sum(T[g] ** 2)
+                    errs[q, it] = n2p + np.sum(H * (V.T @ V)) - 2 * np.sum(V * M)
+    return G, U, errs
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_delete_d_jk_cals_equals_jk_als(d):
+    # §4.2 "pad and periodically zero out d rows" (PAPER.md:416-417) reaches the delete-d
+    # JK-ALS submodels (the §4.1 theorem with E_p deleting d rows); I_0 = 7 gives a ragged group
+    w = make_workload(((7, 6, 5), 2, 2, 0.05, "syn", 12), seed=9)
+    res = O.jk_als_d(w.T, w.P, d, max_iters=12)
+    G, U, errs = _numpy_jk_cals_d(w.T, w.P, d, 12)
+    for q, g in enumerate(G):
+        a = res.factors[q]
+        assert np.all(U[q][0][g] == 0.0)
+        assert np.allclose(np.delete(U[q][0], g, axis=0), a[0], rtol=1e-10, atol=1e-12)
+        for n in (1, 2):
+            assert np.allclose(U[q][n], a[n], rtol=1e-10, atol=1e-12)
+        assert np.allclose(errs[q], res.history(q), rtol=1e-9)
