@@ -92,6 +92,20 @@ jkcals_status jkcals_create(jkcals_t *out, int ndims, const int64_t *dims, int r
                             void *cuda_stream, void *workspace, size_t workspace_bytes,
                             int hist_cap);
 
+/* Delete-d jackknife ("pad and periodically zero out d rows"; flop ratio
+ * PAPER.md:453-476): the I_0 samples form ceil(I_0/d) contiguous groups, group g leaving out
+ * rows [g*d, min(g*d + d, I_0)) of mode 0 (the last group is smaller when d does not divide
+ * I_0). 1 <= d <= I_0/2 (d = 1 is jkcals_create exactly).
+ * [sub_begin, sub_end) ⊆ [0, ceil(I_0/d)) are GROUP indices, and every `p` argument of the
+ * calls below then names a group: its mode-0 factor has I_0 - |group| rows, its error uses
+ * ||T_-g||^2 = ||T||^2 - sum_{i in group} s_i. n_sub for jkcals_workspace_bytes is
+ * sub_end - sub_begin. Other arguments and errors as jkcals_create (E_ARG for a bad d). */
+jkcals_status jkcals_create_d(jkcals_t *out, int ndims, const int64_t *dims, int rank, int64_t d,
+                              int64_t sub_begin, int64_t sub_end, const double *tensor,
+                              int tensor_is_device, jkcals_precision prec, int device,
+                              void *cuda_stream, void *workspace, size_t workspace_bytes,
+                              int hist_cap);
+
 /* Warm start every submodel from the overall model P (Alg. 2 alg:jk:model_subsample,
  * PAPER.md:331; Alg. 3 alg:start-jk-1..alg:stop-jk-1): P[n] is a host
  * column-major dims[n] x rank array; block k of the mode-0 multi-factor gets row p_k
@@ -99,7 +113,8 @@ jkcals_status jkcals_create(jkcals_t *out, int ndims, const int64_t *dims, int r
 jkcals_status jkcals_set_init(jkcals_t h, const double *const *P);
 
 /* Optional per-submodel (re)initialisation, e.g. to resume: U is host column-major in the
- * get_factors layout ((dims[0]-1) x rank for mode 0, row p absent; dims[mode] x rank else). */
+ * get_factors layout ((dims[0]-1) x rank for mode 0, row p absent; dims[mode] x rank else;
+ * delete-d: (dims[0]-|group p|) x rank for mode 0, the group's rows absent). */
 jkcals_status jkcals_set_init_submodel(jkcals_t h, int64_t p, int mode, const double *U);
 
 /* Run up to max_iters ALS sweeps of all active submodels (Alg. 3 repeat loop,
@@ -109,14 +124,16 @@ jkcals_status jkcals_set_init_submodel(jkcals_t h, int64_t p, int mode, const do
  * NULL) receives the number of sweeps executed. Errors: E_STATE, E_ARG, E_CUDA. */
 jkcals_status jkcals_iterate(jkcals_t h, int max_iters, double tol, int *sweeps_done);
 
-/* Factors of submodel p (global index): mode 0 -> (dims[0]-1) x rank with row p DROPPED,
+/* Factors of submodel p (global index): mode 0 -> (dims[0]-1) x rank with row p DROPPED
+ * (delete-d: (dims[0]-|group p|) x rank with the group's rows dropped),
  * mode n >= 1 -> dims[n] x rank; column-major, unit 2-norm columns. lambda (rank, may be
  * NULL) holds the column norms of the LAST updated mode (mode ndims-1 after a sweep). */
 jkcals_status jkcals_get_factors(jkcals_t h, int64_t p, int mode, double *U, double *lambda);
 
 /* Factors of ALL this handle's submodels for one mode in one call: U receives n_sub blocks in
  * submodel order, each in the get_factors layout ((dims[0]-1) x rank for mode 0 with row p
- * dropped; dims[mode] x rank otherwise), column-major; lambda (n_sub x rank, may be NULL). */
+ * dropped; dims[mode] x rank otherwise), column-major, packed back to back (delete-d with a
+ * ragged last group: that block has dims[0]-|group| rows); lambda (n_sub x rank, may be NULL). */
 jkcals_status jkcals_get_all_factors(jkcals_t h, int mode, double *U, double *lambda);
 
 /* Debug/invariant view: submodel p's FULL block of the mode-`mode` multi-factor as it sits

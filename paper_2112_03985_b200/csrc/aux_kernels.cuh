@@ -26,10 +26,11 @@ __global__ void slice_norms_partial_kernel(const double* __restrict__ T, int64_t
 }
 
 // pass 2 (single CTA): s_p = sum_b part[b][p] in order; ||T||^2 = sum_p s_p in order;
-// ||T_-p||^2 = ||T||^2 - s_p for every submodel.
+// ||T_-p||^2 = ||T||^2 - s_p for every submodel; delete-d:
+// ||T_-g||^2 = ||T||^2 - sum_{i in group} s_i.
 __global__ void slice_norms_final_kernel(const double* __restrict__ part, int nb, int64_t I0,
                                          double* __restrict__ s, double* __restrict__ normT2,
-                                         const int64_t* __restrict__ pglob, int nsub,
+                                         const int64_t* __restrict__ pglob, int d, int nsub,
                                          double* __restrict__ normT2p) {
   for (int64_t i = threadIdx.x; i < I0; i += blockDim.x) {
     double acc = 0.0;
@@ -41,16 +42,22 @@ __global__ void slice_norms_final_kernel(const double* __restrict__ part, int nb
     double tot = 0.0;
     for (int64_t i = 0; i < I0; ++i) tot += s[i];
     *normT2 = tot;
-    for (int q = 0; q < nsub; ++q) normT2p[q] = tot - s[pglob[q]];
+    for (int q = 0; q < nsub; ++q) {
+      const int64_t p0 = pglob[q], p1 = (p0 + d < I0) ? p0 + d : I0;
+      double rm = 0.0;
+      for (int64_t i = p0; i < p1; ++i) rm += s[i];
+      normT2p[q] = tot - rm;
+    }
   }
 }
 
 // (a0) warm start: block k of the mode-n multi-factor = P_n (host col-major I x R staged on
-// the device); the mode-0 block k gets row p_k zeroed (Alg. 3 alg:cals_jk:multifactor0).
-// Columns [C, ldu) are zero (padding read by the KRP tiles).
+// the device); the mode-0 block k gets rows [p_k, p_k + d) zeroed (Alg. 3 alg:cals_jk:multifactor0;
+// delete-d). Columns [C, ldu) are zero (padding read by the KRP tiles).
 __global__ void broadcast_init_kernel(const double* __restrict__ P, int I, int R, int K, int64_t ldu,
                                       double* __restrict__ U, int zero_rows,
-                                      const int* __restrict__ blk2sub, const int64_t* __restrict__ pglob) {
+                                      const int* __restrict__ blk2sub, const int64_t* __restrict__ pglob,
+                                      int d) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)I * ldu) return;
   const int i = (int)(e / ldu);
@@ -59,22 +66,22 @@ __global__ void broadcast_init_kernel(const double* __restrict__ P, int I, int R
   if (c < K * R) {
     const int k = c / R, r = c % R;
     v = P[i + (int64_t)I * r];
-    if (zero_rows && i == pglob[blk2sub[k]]) v = 0.0;
+    if (zero_rows && i >= pglob[blk2sub[k]] && i < pglob[blk2sub[k]] + d) v = 0.0;
   }
   U[e] = v;
 }
 
 // one submodel's block from a host-provided col-major matrix (set_init_submodel): mode 0
-// arrives without row p, which is re-inserted as zeros.
+// arrives without its group's rows [pdrop, pdrop + cnt), which are re-inserted as zeros.
 __global__ void set_block_kernel(const double* __restrict__ src, int I, int R, int64_t ldu, int blk,
-                                 int64_t pdrop, double* __restrict__ U) {
+                                 int64_t pdrop, int cnt, double* __restrict__ U) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= I * R) return;
   const int i = e / R, r = e % R;
   double v;
   if (pdrop >= 0) {
-    const int rows = I - 1;
-    v = (i == pdrop) ? 0.0 : src[(i < pdrop ? i : i - 1) + (int64_t)rows * r];
+    const int rows = I - cnt;
+    v = (i >= pdrop && i < pdrop + cnt) ? 0.0 : src[(i < pdrop ? i : i - cnt) + (int64_t)rows * r];
   } else {
     v = src[i + (int64_t)I * r];
   }
@@ -121,30 +128,31 @@ __global__ void reset_state_kernel(int nsub, double* fit, double* fit_prev, doub
 }
 
 // (a9) extract a row-major (stride ld) I x R block into a column-major output, dropping
-// row `drop` (the left-out sample's zero row in mode 0) when drop >= 0.
+// rows [drop, drop + cnt) (the left-out group's zero rows in mode 0) when drop >= 0.
 __global__ void extract_kernel(const double* __restrict__ src, int64_t ld, int I, int R, int64_t drop,
-                               double* __restrict__ out) {
+                               int cnt, double* __restrict__ out) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  const int rows = drop >= 0 ? I - 1 : I;
+  const int rows = drop >= 0 ? I - cnt : I;
   if (e >= rows * R) return;
   const int r = e / rows, io = e % rows;
-  const int i = (drop >= 0 && io >= drop) ? io + 1 : io;
+  const int i = (drop >= 0 && io >= drop) ? io + cnt : io;
   out[e] = src[(int64_t)i * ld + r];
 }
 
 // (a9) every submodel's mode block at once: out[q] = column-major rows x R block of submodel q
-// (mode 0: the left-out row p_q dropped), q in submodel order.
+// (mode 0: the left-out rows [p_q, p_q + d) dropped), q in submodel order. For delete-d the caller
+// passes groups of equal size d (a ragged last group is extracted on its own).
 __global__ void extract_all_kernel(const double* __restrict__ base, const int64_t* __restrict__ src_off,
                                    const int64_t* __restrict__ src_ld, int nsub, int I, int R, int drop,
-                                   const int64_t* __restrict__ pglob, double* __restrict__ out) {
-  const int rows = drop ? I - 1 : I;
+                                   const int64_t* __restrict__ pglob, int d, double* __restrict__ out) {
+  const int rows = drop ? I - d : I;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)nsub * rows * R) return;
   const int q = (int)(e / ((int64_t)rows * R));
   const int rem = (int)(e % ((int64_t)rows * R));
   const int r = rem / rows, io = rem % rows;
   const int64_t p = drop ? pglob[q] : -1;
-  const int i = (drop && io >= p) ? io + 1 : io;
+  const int i = (drop && io >= p) ? io + d : io;
   out[e] = base[src_off[q] + (int64_t)i * src_ld[q] + r];
 }
 

@@ -29,7 +29,8 @@ struct EpiArgs {
   int nsub;                      // submodels of the handle (state arrays are indexed by sub)
   double* U;                     // multi-factor of mode n (row-major In x ldu)
   const int* blk2sub;            // live block -> submodel
-  const int64_t* pglob;          // submodel -> global left-out index p
+  const int64_t* pglob;          // submodel -> first global left-out row p0 (group g: p0 = g d)
+  int d;                         // delete-d group size: rows [p0, min(p0 + d, I_0)) are padded
   const double* parts;           // partial pieces of the fused MTTKRP
   const TileInfo* tinfo;
   int BM, BN, nMt;
@@ -131,7 +132,8 @@ __global__ void __launch_bounds__(kEpiThreads) als_epilogue_rows_kernel(EpiArgs 
   if (!a.active[sub]) return;  // frozen (converged or failed)
   const int R = a.R, n = a.n, N = a.N, tid = threadIdx.x;
   const bool last = (n == N - 1);
-  const int64_t pzero = (n == 0) ? a.pglob[sub] : -1;
+  const int64_t pz0 = (n == 0) ? a.pglob[sub] : -1;   // padded rows [pz0, pz1)
+  const int64_t pz1 = (n == 0) ? pz0 + a.d : -1;
   const int cb = k * R;
 
   __shared__ double H[RMAX * RMAX];
@@ -192,7 +194,7 @@ __global__ void __launch_bounds__(kEpiThreads) als_epilogue_rows_kernel(EpiArgs 
         m[r] = s;
       }
     }
-    if (i == pzero) {
+    if (i >= pz0 && i < pz1) {
 #pragma unroll
       for (int r = 0; r < RMAX; ++r) v[r] = 0.0;
     } else if (!pinv) {
@@ -433,7 +435,8 @@ __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int NW = kEpi2Threads / 32;
   const bool last = (n == N - 1);
-  const int64_t pzero = (n == 0) ? a.pglob[sub] : -1;
+  const int64_t pz0 = (n == 0) ? a.pglob[sub] : -1;   // padded rows [pz0, pz1)
+  const int64_t pz1 = (n == 0) ? pz0 + a.d : -1;
   const int cb = k * R;
 
   __shared__ double H[RMAX * RMAX];
@@ -512,7 +515,7 @@ __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
     double m[RMAX], v[RMAX];
 #pragma unroll
     for (int r = 0; r < RMAX; ++r) m[r] = (r < R) ? Ms[i * R + r] : 0.0;
-    if (i == pzero) {
+    if (i >= pz0 && i < pz1) {
 #pragma unroll
       for (int r = 0; r < RMAX; ++r) v[r] = 0.0;
     } else if (!pinv) {

@@ -458,7 +458,8 @@ struct jkcals_s {
   int N = 0;
   int64_t dims[kMaxModes] = {0};
   int R = 0;
-  int64_t sub_begin = 0, sub_end = 0;
+  int64_t sub_begin = 0, sub_end = 0;  // group indices g; group g leaves out rows [g d, min(g d + d, I_0))
+  int64_t d = 1;                       // delete-d group size (1 = leave-one-out)
   int nsub = 0, K = 0, C = 0;
   int64_t ldu = 0, P = 0, I0p = 0;
   int hist_cap = 1;
@@ -681,6 +682,7 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
   a.U = Uall[n];
   a.blk2sub = h->ptr<int>(h->off.blk2sub);
   a.pglob = h->ptr<int64_t>(h->off.pglob);
+  a.d = (int)h->d;
   a.parts = parts;
   a.tinfo = ti;
   a.BM = kBM;
@@ -829,13 +831,25 @@ size_t jkcals_workspace_bytes(int ndims, const int64_t* dims, int rank, int64_t 
   return o.total;
 }
 
+// rows of mode 0 left out by group g (the last group may be smaller)
+static int64_t group_rows(const jkcals_s* h, int64_t g) { return std::min(h->d, h->dims[0] - g * h->d); }
+
 jkcals_status jkcals_create(jkcals_t* out, int ndims, const int64_t* dims, int rank, int64_t sub_begin,
                             int64_t sub_end, const double* tensor, int tensor_is_device, jkcals_precision prec,
                             int device, void* cuda_stream, void* workspace, size_t workspace_bytes, int hist_cap) {
+  return jkcals_create_d(out, ndims, dims, rank, 1, sub_begin, sub_end, tensor, tensor_is_device, prec, device,
+                         cuda_stream, workspace, workspace_bytes, hist_cap);
+}
+
+jkcals_status jkcals_create_d(jkcals_t* out, int ndims, const int64_t* dims, int rank, int64_t d, int64_t sub_begin,
+                              int64_t sub_end, const double* tensor, int tensor_is_device, jkcals_precision prec,
+                              int device, void* cuda_stream, void* workspace, size_t workspace_bytes, int hist_cap) {
   if (!out) return JKCALS_E_ARG;
   *out = nullptr;
   if (!valid_dims(ndims, dims, rank) || !tensor || !workspace) return JKCALS_E_ARG;
-  if (sub_begin < 0 || sub_end > dims[0] || sub_end <= sub_begin || hist_cap < 1) return JKCALS_E_ARG;
+  if (d < 1 || (d > 1 && 2 * d > dims[0])) return JKCALS_E_ARG;  // d <= I_0 / 2
+  const int64_t ngroups = (dims[0] + d - 1) / d;
+  if (sub_begin < 0 || sub_end > ngroups || sub_end <= sub_begin || hist_cap < 1) return JKCALS_E_ARG;
   if (prec != JKCALS_FP64 && prec != JKCALS_FP32) return JKCALS_E_ARG;
   DeviceGuard dg(device);
   std::string kerr;
@@ -847,6 +861,7 @@ jkcals_status jkcals_create(jkcals_t* out, int ndims, const int64_t* dims, int r
   h->R = rank;
   h->sub_begin = sub_begin;
   h->sub_end = sub_end;
+  h->d = d;
   h->nsub = (int)(sub_end - sub_begin);
   h->K = h->nsub;
   h->C = h->K * rank;
@@ -884,7 +899,7 @@ jkcals_status jkcals_create(jkcals_t* out, int ndims, const int64_t* dims, int r
   std::vector<int64_t> pg(h->nsub);
   std::vector<int> b2s(h->nsub);
   for (int q = 0; q < h->nsub; ++q) {
-    pg[q] = sub_begin + q;
+    pg[q] = (sub_begin + q) * d;  // first left-out row of the group
     b2s[q] = q;
   }
   h->h_blk2sub = b2s;
@@ -904,7 +919,7 @@ jkcals_status jkcals_create(jkcals_t* out, int ndims, const int64_t* dims, int r
   slice_norms_final_kernel<<<1, 256, 0, h->stream>>>(h->ptr<double>(h->off.slice_part), nb_eff, I0,
                                                      h->ptr<double>(h->off.slice),
                                                      reinterpret_cast<double*>(h->ws + h->off.misc),
-                                                     h->ptr<int64_t>(h->off.pglob), h->nsub,
+                                                     h->ptr<int64_t>(h->off.pglob), (int)d, h->nsub,
                                                      h->ptr<double>(h->off.normT2p));
   CKH(h, cudaGetLastError());
   double nt2 = 0;
@@ -957,7 +972,7 @@ jkcals_status jkcals_set_init(jkcals_t h, const double* const* P) {
     int64_t tot = (int64_t)I * h->ldu;
     broadcast_init_kernel<<<(int)cdiv(tot, 256), 256, 0, h->stream>>>(stage, I, h->R, h->K, h->ldu, h->U(n),
                                                                       n == 0 ? 1 : 0, h->ptr<int>(h->off.blk2sub),
-                                                                      h->ptr<int64_t>(h->off.pglob));
+                                                                      h->ptr<int64_t>(h->off.pglob), (int)h->d);
     CKH(h, cudaGetLastError());
     CKH(h, cudaStreamSynchronize(h->stream));  // stage is reused by the next mode
   }
@@ -988,13 +1003,15 @@ jkcals_status jkcals_set_init_submodel(jkcals_t h, int64_t p, int mode, const do
     if (h->h_blk2sub[k] == sub) blk = k;
   if (blk < 0) return fail(h, JKCALS_E_STATE, "submodel %lld was compacted out", (long long)p);
   const int I = (int)h->dims[mode];
-  const int rows = mode == 0 ? I - 1 : I;
+  const int cnt = mode == 0 ? (int)group_rows(h, p) : 0;
+  const int rows = I - cnt;
   for (int64_t e = 0; e < (int64_t)rows * h->R; ++e)
     if (!std::isfinite(U[e])) return fail(h, JKCALS_E_NONFINITE, "non-finite init");
   double* stage = h->ptr<double>(h->off.stage);
   CKH(h, cudaMemcpyAsync(stage, U, sizeof(double) * rows * h->R, cudaMemcpyHostToDevice, h->stream));
   set_block_kernel<<<(int)cdiv((int64_t)I * h->R, 256), 256, 0, h->stream>>>(stage, I, h->R, h->ldu, blk,
-                                                                            mode == 0 ? p : -1, h->U(mode));
+                                                                            mode == 0 ? p * h->d : -1, cnt,
+                                                                            h->U(mode));
   CKH(h, cudaGetLastError());
   jkcals_status st = compute_grams(h);
   if (st != JKCALS_OK) return st;
@@ -1076,10 +1093,11 @@ jkcals_status jkcals_get_factors(jkcals_t h, int64_t p, int mode, double* U, dou
   jkcals_status st = locate(h, p, mode, &src, &ld, &sub);
   if (st != JKCALS_OK) return st;
   const int I = (int)h->dims[mode];
-  const int rows = mode == 0 ? I - 1 : I;
+  const int cnt = mode == 0 ? (int)group_rows(h, p) : 0;
+  const int rows = I - cnt;
   double* stage = h->ptr<double>(h->off.stage);
-  extract_kernel<<<(int)cdiv((int64_t)rows * h->R, 256), 256, 0, h->stream>>>(src, ld, I, h->R, mode == 0 ? p : -1,
-                                                                              stage);
+  extract_kernel<<<(int)cdiv((int64_t)rows * h->R, 256), 256, 0, h->stream>>>(
+      src, ld, I, h->R, mode == 0 ? p * h->d : -1, cnt, stage);
   CKH(h, cudaGetLastError());
   CKH(h, cudaMemcpyAsync(U, stage, sizeof(double) * rows * h->R, cudaMemcpyDeviceToHost, h->stream));
   if (lambda)
@@ -1098,14 +1116,34 @@ jkcals_status jkcals_get_all_factors(jkcals_t h, int mode, double* U, double* la
   jkcals_status st = build_src_table(h, mode);
   if (st != JKCALS_OK) return st;
   const int I = (int)h->dims[mode];
-  const int rows = mode == 0 ? I - 1 : I;
-  const int64_t tot = (int64_t)h->nsub * rows * h->R;
+  const int dd = mode == 0 ? (int)h->d : 0;
+  const int rows = I - dd;
+  // groups of the full size d go in one launch; a ragged last group (d does not divide I_0) is
+  // appended by its own extract (blocks are packed in submodel order either way)
+  const bool ragged = mode == 0 && group_rows(h, h->sub_end - 1) != h->d;
+  const int nfull = h->nsub - (ragged ? 1 : 0);
+  const int64_t tot = (int64_t)nfull * rows * h->R;
   double* stage = h->ptr<double>(h->off.stage);
-  extract_all_kernel<<<(int)cdiv(tot, 256), 256, 0, h->stream>>>(
-      reinterpret_cast<const double*>(h->ws), h->ptr<int64_t>(h->off.srcoff), h->ptr<int64_t>(h->off.srcld), h->nsub, I,
-      h->R, mode == 0 ? 1 : 0, h->ptr<int64_t>(h->off.pglob), stage);
-  CKH(h, cudaGetLastError());
-  CKH(h, cudaMemcpyAsync(U, stage, sizeof(double) * tot, cudaMemcpyDeviceToHost, h->stream));
+  if (tot > 0) {
+    extract_all_kernel<<<(int)cdiv(tot, 256), 256, 0, h->stream>>>(
+        reinterpret_cast<const double*>(h->ws), h->ptr<int64_t>(h->off.srcoff), h->ptr<int64_t>(h->off.srcld), nfull,
+        I, h->R, mode == 0 ? 1 : 0, h->ptr<int64_t>(h->off.pglob), dd, stage);
+    CKH(h, cudaGetLastError());
+  }
+  int64_t total = tot;
+  if (ragged) {
+    const double* src;
+    int64_t ld;
+    int sub;
+    jkcals_status st2 = locate(h, h->sub_end - 1, mode, &src, &ld, &sub);
+    if (st2 != JKCALS_OK) return st2;
+    const int cnt = (int)group_rows(h, h->sub_end - 1);
+    extract_kernel<<<(int)cdiv((int64_t)(I - cnt) * h->R, 256), 256, 0, h->stream>>>(
+        src, ld, I, h->R, (h->sub_end - 1) * h->d, cnt, stage + tot);
+    CKH(h, cudaGetLastError());
+    total += (int64_t)(I - cnt) * h->R;
+  }
+  CKH(h, cudaMemcpyAsync(U, stage, sizeof(double) * total, cudaMemcpyDeviceToHost, h->stream));
   if (lambda)
     CKH(h, cudaMemcpyAsync(lambda, h->ptr<double>(h->off.lambda), sizeof(double) * h->nsub * h->R,
                            cudaMemcpyDeviceToHost, h->stream));
@@ -1124,7 +1162,7 @@ jkcals_status jkcals_get_block(jkcals_t h, int64_t p, int mode, double* U) {
   if (st != JKCALS_OK) return st;
   const int I = (int)h->dims[mode];
   double* stage = h->ptr<double>(h->off.stage);
-  extract_kernel<<<(int)cdiv((int64_t)I * h->R, 256), 256, 0, h->stream>>>(src, ld, I, h->R, -1, stage);
+  extract_kernel<<<(int)cdiv((int64_t)I * h->R, 256), 256, 0, h->stream>>>(src, ld, I, h->R, -1, 0, stage);
   CKH(h, cudaGetLastError());
   CKH(h, cudaMemcpyAsync(U, stage, sizeof(double) * I * h->R, cudaMemcpyDeviceToHost, h->stream));
   CKH(h, cudaStreamSynchronize(h->stream));

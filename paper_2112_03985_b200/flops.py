@@ -16,17 +16,23 @@ def mttkrp_flops(dims, width):
     return 2 * int(width) * prod(int(d) for d in dims)
 
 
+def _groups(I, d):
+    """Sizes of the ceil(I/d) contiguous delete-d groups (last smaller)."""
+    return [min(d, I - g * d) for g in range(-(-I // d))]
+
+
 def jk_cals_mttkrp_flops(dims, R, d=1, mode=0):
-    """Fused JK-CALS MTTKRP flops of one mode, d | I_mode assumed."""
+    """Fused JK-CALS MTTKRP flops of one mode; I/d -> ceil(I/d) groups."""
     I = int(dims[mode])
-    return 2 * (I // d) * R * prod(int(x) for x in dims)
+    return 2 * len(_groups(I, d)) * R * prod(int(x) for x in dims)
 
 
 def jk_als_mttkrp_flops(dims, R, d=1, mode=0):
-    """JK-ALS MTTKRP flops of one mode over all submodels."""
+    """JK-ALS MTTKRP flops of one mode over all submodels: group g's submodel
+    works on I - |g| slices."""
     I = int(dims[mode])
     rest = prod(int(x) for k, x in enumerate(dims) if k != mode)
-    return (I // d) * 2 * R * (I - d) * rest
+    return sum(2 * R * (I - sz) * rest for sz in _groups(I, d))
 
 
 def overhead_ratio(dims, R, d=1, mode=0):

@@ -45,6 +45,7 @@ def lib():
         sigs = {
             "jkcals_workspace_bytes": (SZ, [I, P, I, I64, I, I, I]),
             "jkcals_create": (I, [P, I, P, I, I64, I64, P, I, I, I, P, P, SZ, I]),
+            "jkcals_create_d": (I, [P, I, P, I, I64, I64, I64, P, I, I, I, P, P, SZ, I]),
             "jkcals_set_init": (I, [P, P]),
             "jkcals_set_init_submodel": (I, [P, I64, I, P]),
             "jkcals_iterate": (I, [P, I, D, P]),
@@ -74,7 +75,7 @@ def lib():
 
 
 EXPORTED = [
-    "jkcals_workspace_bytes", "jkcals_create", "jkcals_set_init", "jkcals_set_init_submodel", "jkcals_iterate",
+    "jkcals_workspace_bytes", "jkcals_create", "jkcals_create_d", "jkcals_set_init", "jkcals_set_init_submodel", "jkcals_iterate",
     "jkcals_get_factors", "jkcals_get_all_factors", "jkcals_get_block", "jkcals_get_status", "jkcals_get_history", "jkcals_get_jackknife_stats",
     "jkcals_get_local_moments", "jkcals_set_instrument", "jkcals_get_kernel_times", "jkcals_sweep_flops",
     "jkcals_launches_per_sweep", "jkcals_last_error", "jkcals_destroy", "jkcals_mttkrp_scratch_bytes",
@@ -113,10 +114,14 @@ def column_major_flat(T):
 
 
 class JKCals:
-    """One shard [sub_begin, sub_end) of the I_1 leave-one-out submodels on one GPU."""
+    """One shard [sub_begin, sub_end) of the I_1 leave-one-out submodels on one GPU.
+
+    d > 1 selects delete-d jackknife: submodel p is then GROUP p, leaving
+    out mode-0 rows [p d, min(p d + d, I_0)); sub_range indexes groups (default all
+    ceil(I_0/d) of them)."""
 
     def __init__(self, T, rank, sub_range=None, device=None, stream=None, hist_cap=None,
-                 precision=FP64, dims=None):
+                 precision=FP64, dims=None, d=1):
         torch = _torch()
         self._torch = torch
         flat, tdims, is_dev = column_major_flat(T)
@@ -127,7 +132,9 @@ class JKCals:
         if device is None:
             device = flat.device.index if is_dev else torch.cuda.current_device()
         self.device = int(device)
-        self.sub_begin, self.sub_end = (0, self.dims[0]) if sub_range is None else map(int, sub_range)
+        self.d = int(d)
+        self.ngroups = -(-self.dims[0] // self.d) if self.d >= 1 else 0
+        self.sub_begin, self.sub_end = (0, self.ngroups) if sub_range is None else map(int, sub_range)
         self.nsub = self.sub_end - self.sub_begin
         self.hist_cap = int(hist_cap or DEFAULT_MAX_ITERS)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -140,7 +147,7 @@ class JKCals:
         self._keep = flat
         tptr = flat.data_ptr() if is_dev else flat.ctypes.data
         h = ctypes.c_void_p()
-        st = L.jkcals_create(ctypes.byref(h), self.N, _p(d), self.R, self.sub_begin, self.sub_end,
+        st = L.jkcals_create_d(ctypes.byref(h), self.N, _p(d), self.R, self.d, self.sub_begin, self.sub_end,
                              ctypes.c_void_p(tptr), 1 if is_dev else 0, precision, self.device,
                              ctypes.c_void_p(self.stream.cuda_stream), ctypes.c_void_p(self.workspace.data_ptr()),
                              nbytes, self.hist_cap)
@@ -186,24 +193,39 @@ class JKCals:
         self._check(lib().jkcals_iterate(self._h, int(max_iters), float(tol), ctypes.byref(done)))
         return done.value
 
+    def group_rows(self, p):
+        """Mode-0 rows left out by submodel (group) p."""
+        return min(self.d, self.dims[0] - p * self.d)
+
     def factors(self, p):
-        """Submodel p: ([U_0 ((I_0-1) x R, row p dropped), U_1, ...], lambda)."""
+        """Submodel p: ([U_0 ((I_0-|group|) x R, the group's rows dropped), U_1, ...], lambda)."""
         out, lam = [], np.zeros(self.R)
         for n in range(self.N):
-            rows = self.dims[n] - 1 if n == 0 else self.dims[n]
+            rows = self.dims[n] - self.group_rows(p) if n == 0 else self.dims[n]
             U = np.zeros((rows, self.R), order="F")
             self._check(lib().jkcals_get_factors(self._h, int(p), n, _p(U), _p(lam) if n == self.N - 1 else None))
             out.append(U)
         return out, lam
 
     def all_factors(self, mode):
-        """Every submodel's mode-`mode` factor at once: array (n_sub, rows, R) (row p dropped in
-        mode 0) and lambda (n_sub, R)."""
-        rows = self.dims[mode] - 1 if mode == 0 else self.dims[mode]
-        U = np.zeros((self.nsub, self.R, rows))  # C order: per submodel a column-major rows x R
+        """Every submodel's mode-`mode` factor at once: array (n_sub, rows, R) (the group's rows
+        dropped in mode 0) and lambda (n_sub, R). With delete-d and a ragged last group the
+        mode-0 factors come back as a list of (rows_q, R) arrays instead."""
         lam = np.zeros((self.nsub, self.R))
-        self._check(lib().jkcals_get_all_factors(self._h, int(mode), _p(U), _p(lam)))
-        return np.ascontiguousarray(U.transpose(0, 2, 1)), lam
+        if mode == 0:
+            rows_q = [self.dims[0] - self.group_rows(p) for p in range(self.sub_begin, self.sub_end)]
+        else:
+            rows_q = [self.dims[mode]] * self.nsub
+        flat = np.zeros(sum(rows_q) * self.R)
+        self._check(lib().jkcals_get_all_factors(self._h, int(mode), _p(flat), _p(lam)))
+        if len(set(rows_q)) == 1:
+            U = flat.reshape(self.nsub, self.R, rows_q[0])  # per submodel a column-major rows x R
+            return np.ascontiguousarray(U.transpose(0, 2, 1)), lam
+        out, off = [], 0
+        for r_ in rows_q:
+            out.append(flat[off:off + r_ * self.R].reshape((r_, self.R), order="F"))
+            off += r_ * self.R
+        return out, lam
 
     def block(self, p, mode):
         """Submodel p's full fused block of mode `mode` (mode 0 keeps the zero row p)."""

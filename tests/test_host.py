@@ -81,6 +81,11 @@ def test_flop_model_matches_paper():
     assert r10 == 50 / 40 and r10 <= 2
     assert jk_cals_mttkrp_flops((50, 200, 200), 5) == 50 * mttkrp_flops((50, 200, 200), 5)
     assert jk_als_mttkrp_flops((50, 200, 200), 5) == 50 * mttkrp_flops((49, 200, 200), 5)
+    # delete-d: d = I/2 is the worst case, ratio exactly 2
+    assert overhead_ratio((50, 30, 30), 5, d=25) == 2
+    # d does not divide I: ceil(I/d) groups, the last one smaller
+    assert jk_cals_mttkrp_flops((10, 8, 6), 2, d=3) == 4 * mttkrp_flops((10, 8, 6), 2)
+    assert jk_als_mttkrp_flops((10, 8, 6), 2, d=3) == 3 * mttkrp_flops((7, 8, 6), 2) + mttkrp_flops((9, 8, 6), 2)
 
 
 def test_shard_partition():
