@@ -106,10 +106,29 @@ jkcals_status jkcals_create_d(jkcals_t *out, int ndims, const int64_t *dims, int
                               void *cuda_stream, void *workspace, size_t workspace_bytes,
                               int hist_cap);
 
+/* Multi-model pool (the paper's "All" experiment, PAPER.md:501-504 and Fig. 5 PAPER.md:590-596:
+ * several fitted models of ranks R_m, e.g. {3,5,7,9} or {4,5,6}, jackknifed "simultaneously"):
+ * the submodels of every model share ONE fused multi-factor per mode whose column blocks have
+ * per-model widths R_m (CALS's sum_i R_i, §3.3), so one fused
+ * MTTKRP per mode serves all of them. Submodel ids s in [0, nmodels * ceil(I_0/d)) enumerate
+ * model m = s / ceil(I_0/d) and its group g = s % ceil(I_0/d) (d as in jkcals_create_d);
+ * [sub_begin, sub_end) selects a shard of ids. Every `p` argument of the calls below is such an
+ * id; factors of submodel s are rows x R_m. ranks[m] in [1, 16]. jkcals_create_d is the pool
+ * with nmodels = 1. Errors as jkcals_create_d. */
+size_t jkcals_pool_workspace_bytes(int ndims, const int64_t *dims, int nmodels, const int *ranks,
+                                   int64_t d, int64_t sub_begin, int64_t sub_end,
+                                   jkcals_precision prec, int hist_cap, int device);
+jkcals_status jkcals_create_pool(jkcals_t *out, int ndims, const int64_t *dims, int nmodels,
+                                 const int *ranks, int64_t d, int64_t sub_begin, int64_t sub_end,
+                                 const double *tensor, int tensor_is_device, jkcals_precision prec,
+                                 int device, void *cuda_stream, void *workspace,
+                                 size_t workspace_bytes, int hist_cap);
+
 /* Warm start every submodel from the overall model P (Alg. 2 alg:jk:model_subsample,
  * PAPER.md:331; Alg. 3 alg:start-jk-1..alg:stop-jk-1): P[n] is a host
  * column-major dims[n] x rank array; block k of the mode-0 multi-factor gets row p_k
- * zeroed. Resets fits, histories, flags and iteration counts. Errors: E_ARG, E_NONFINITE. */
+ * zeroed (its group's rows for delete-d). A pool takes nmodels * ndims arrays:
+ * P[m * ndims + n] is model m's dims[n] x ranks[m] factor. Resets fits, histories, flags and iteration counts. Errors: E_ARG, E_NONFINITE. */
 jkcals_status jkcals_set_init(jkcals_t h, const double *const *P);
 
 /* Optional per-submodel (re)initialisation, e.g. to resume: U is host column-major in the
@@ -155,6 +174,13 @@ jkcals_status jkcals_get_jackknife_stats(jkcals_t h, int mode, double *mean, dou
 /* Local moments for cross-shard merging (Chan et al.): per element of U_mode the count,
  * mean and sum of squared deviations M2 over this handle's submodels. mode >= 1. */
 jkcals_status jkcals_get_local_moments(jkcals_t h, int mode, double *count, double *mean,
+                                       double *m2);
+
+/* The same two calls for model `model` of a pool (over this handle's submodels of that model;
+ * g = their count; dims[mode] x ranks[model]). The single-model calls above are model 0 and
+ * return E_ARG on a handle with nmodels > 1. */
+jkcals_status jkcals_get_model_stats(jkcals_t h, int model, int mode, double *mean, double *std);
+jkcals_status jkcals_get_model_moments(jkcals_t h, int model, int mode, double *count, double *mean,
                                        double *m2);
 
 /* Instrumentation: when on, iterate() launches kernels eagerly (no CUDA graph) bracketed

@@ -51,29 +51,30 @@ __global__ void slice_norms_final_kernel(const double* __restrict__ part, int nb
   }
 }
 
-// (a0) warm start: block k of the mode-n multi-factor = P_n (host col-major I x R staged on
-// the device); the mode-0 block k gets rows [p_k, p_k + d) zeroed (Alg. 3 alg:cals_jk:multifactor0;
-// delete-d). Columns [C, ldu) are zero (padding read by the KRP tiles).
-__global__ void broadcast_init_kernel(const double* __restrict__ P, int I, int R, int K, int64_t ldu,
-                                      double* __restrict__ U, int zero_rows,
-                                      const int* __restrict__ blk2sub, const int64_t* __restrict__ pglob,
-                                      int d) {
+// (a0) warm start: block k of the mode-n multi-factor = P_n of its submodel's model. `P` is the
+// column concatenation [P_n(model 0) | P_n(model 1) | ...] (host col-major I x sum_m R_m staged on
+// the device); block k (columns [blkcol[k], blkcol[k] + R_k)) takes columns [subRc, subRc + R_k)
+// of it. The mode-0 block k gets its group's rows [p_k, p_k + d) zeroed (Alg. 3
+// alg:cals_jk:multifactor0; delete-d PAPER.md:416-417). The caller zeroes U first (padding).
+__global__ void init_blocks_kernel(const double* __restrict__ P, int I, int Rs, int K, int64_t ldu,
+                                   double* __restrict__ U, int zero_rows, const int* __restrict__ blk2sub,
+                                   const int* __restrict__ blkcol, const int* __restrict__ subR,
+                                   const int* __restrict__ subRc, const int64_t* __restrict__ pglob, int d) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)I * ldu) return;
-  const int i = (int)(e / ldu);
-  const int c = (int)(e % ldu);
-  double v = 0.0;
-  if (c < K * R) {
-    const int k = c / R, r = c % R;
-    v = P[i + (int64_t)I * r];
-    if (zero_rows && i >= pglob[blk2sub[k]] && i < pglob[blk2sub[k]] + d) v = 0.0;
-  }
-  U[e] = v;
+  if (e >= (int64_t)I * K * Rs) return;
+  const int r = (int)(e % Rs);
+  const int k = (int)((e / Rs) % K);
+  const int i = (int)(e / ((int64_t)Rs * K));
+  const int sub = blk2sub[k];
+  if (r >= subR[sub]) return;
+  double v = P[i + (int64_t)I * (subRc[sub] + r)];
+  if (zero_rows && i >= pglob[sub] && i < pglob[sub] + d) v = 0.0;
+  U[(int64_t)i * ldu + blkcol[k] + r] = v;
 }
 
 // one submodel's block from a host-provided col-major matrix (set_init_submodel): mode 0
 // arrives without its group's rows [pdrop, pdrop + cnt), which are re-inserted as zeros.
-__global__ void set_block_kernel(const double* __restrict__ src, int I, int R, int64_t ldu, int blk,
+__global__ void set_block_kernel(const double* __restrict__ src, int I, int R, int64_t ldu, int col,
                                  int64_t pdrop, int cnt, double* __restrict__ U) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= I * R) return;
@@ -85,21 +86,24 @@ __global__ void set_block_kernel(const double* __restrict__ src, int I, int R, i
   } else {
     v = src[i + (int64_t)I * r];
   }
-  U[(int64_t)i * ldu + (int64_t)blk * R + r] = v;
+  U[(int64_t)i * ldu + col + r] = v;
 }
 
 // Gramian of one block (one CTA per live block): Gram_n^(sub) = U_blk^T U_blk.
+// Block k spans columns [blkcol[k], blkcol[k] + R_k); gram is [N][nsub][Rs*Rs] (R_k x R_k used).
 template <int RMAX>
 __global__ void __launch_bounds__(kEpiThreads) gram_kernel(const double* __restrict__ U, int I, int64_t ldu,
-                                                           int R, const int* __restrict__ blk2sub, int nsub,
-                                                           int n, double* __restrict__ gram) {
-  const int k = blockIdx.x, sub = blk2sub[k];
+                                                           int Rs, const int* __restrict__ blk2sub,
+                                                           const int* __restrict__ blkcol,
+                                                           const int* __restrict__ subR, int nsub, int n,
+                                                           double* __restrict__ gram) {
+  const int k = blockIdx.x, sub = blk2sub[k], R = subR[sub];
   __shared__ double red[(kEpiThreads / 32 + 1) * (RMAX * RMAX + RMAX + 1)];
   double g[RMAX * RMAX];
 #pragma unroll
   for (int e = 0; e < RMAX * RMAX; ++e) g[e] = 0.0;
   for (int i = threadIdx.x; i < I; i += kEpiThreads) {
-    const double* row = U + (int64_t)i * ldu + (int64_t)k * R;
+    const double* row = U + (int64_t)i * ldu + blkcol[k];
     double u[RMAX];
 #pragma unroll
     for (int r = 0; r < RMAX; ++r) u[r] = r < R ? row[r] : 0.0;
@@ -111,7 +115,7 @@ __global__ void __launch_bounds__(kEpiThreads) gram_kernel(const double* __restr
   block_sum<RMAX>(g, RMAX * RMAX, red);
   const double* gt = red + (kEpiThreads / 32) * RMAX * RMAX;
   for (int e = threadIdx.x; e < R * R; e += kEpiThreads)
-    gram[((int64_t)n * nsub + sub) * R * R + e] = gt[(e / R) * RMAX + (e % R)];
+    gram[((int64_t)n * nsub + sub) * Rs * Rs + e] = gt[(e / R) * RMAX + (e % R)];
 }
 
 // reset per-submodel state at set_init
@@ -139,21 +143,24 @@ __global__ void extract_kernel(const double* __restrict__ src, int64_t ld, int I
   out[e] = src[(int64_t)i * ld + r];
 }
 
-// (a9) every submodel's mode block at once: out[q] = column-major rows x R block of submodel q
-// (mode 0: the left-out rows [p_q, p_q + d) dropped), q in submodel order. For delete-d the caller
-// passes groups of equal size d (a ragged last group is extracted on its own).
+// (a9) every submodel's mode block at once: submodel q's column-major rows_q x R_q block goes to
+// out + dstoff[q] (mode 0: its group's rows [p_q, p_q + |group|) dropped, |group| = min(d, I - p_q)).
+// grid.y strides over submodels.
 __global__ void extract_all_kernel(const double* __restrict__ base, const int64_t* __restrict__ src_off,
-                                   const int64_t* __restrict__ src_ld, int nsub, int I, int R, int drop,
+                                   const int64_t* __restrict__ src_ld, const int* __restrict__ subR,
+                                   const int64_t* __restrict__ dstoff, int nsub, int I, int drop,
                                    const int64_t* __restrict__ pglob, int d, double* __restrict__ out) {
-  const int rows = drop ? I - d : I;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)nsub * rows * R) return;
-  const int q = (int)(e / ((int64_t)rows * R));
-  const int rem = (int)(e % ((int64_t)rows * R));
-  const int r = rem / rows, io = rem % rows;
-  const int64_t p = drop ? pglob[q] : -1;
-  const int i = (drop && io >= p) ? io + d : io;
-  out[e] = base[src_off[q] + (int64_t)i * src_ld[q] + r];
+  for (int q = blockIdx.y; q < nsub; q += gridDim.y) {
+    const int R = subR[q];
+    const int64_t p = drop ? pglob[q] : -1;
+    const int cnt = drop ? (int)((p + d < I) ? d : I - p) : 0;
+    const int rows = I - cnt;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * R; e += gridDim.x * blockDim.x) {
+      const int r = e / rows, io = e % rows;
+      const int i = (drop && io >= p) ? io + cnt : io;
+      out[dstoff[q] + e] = base[src_off[q] + (int64_t)i * src_ld[q] + r];
+    }
+  }
 }
 
 // (a9) per-element moments over the handle's submodels, fixed order (two-pass):
@@ -177,28 +184,23 @@ __global__ void moments_kernel(const double* __restrict__ base, const int64_t* _
   m2[e] = ss;
 }
 
-// (a8) store a converged block into the result store (row-major I x R per submodel).
-__global__ void store_block_kernel(const double* __restrict__ U, int I, int64_t ldu, int R, int blk,
+// (a8) store a converged block (columns [col, col + R)) into the result store (row-major I x R).
+__global__ void store_block_kernel(const double* __restrict__ U, int I, int64_t ldu, int R, int col,
                                    double* __restrict__ dst) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= I * R) return;
   const int i = e / R, r = e % R;
-  dst[e] = U[(int64_t)i * ldu + (int64_t)blk * R + r];
+  dst[e] = U[(int64_t)i * ldu + col + r];
 }
 
-// (a8) masked compaction: gather the surviving blocks (old index map[k]) to the front of
-// the other multi-factor buffer; columns >= K_new*R become zero padding.
+// (a8) masked compaction: gather the surviving blocks' columns (new column c <- old column
+// colmap[c]) to the front of the other multi-factor buffer; columns >= C_new become zero padding.
 __global__ void gather_blocks_kernel(const double* __restrict__ Uold, double* __restrict__ Unew, int I,
-                                     int64_t ldu, int R, const int* __restrict__ map, int Knew) {
+                                     int64_t ldu, const int* __restrict__ colmap, int Cnew) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)I * ldu) return;
   const int i = (int)(e / ldu), c = (int)(e % ldu);
-  double v = 0.0;
-  if (c < Knew * R) {
-    const int k = c / R, r = c % R;
-    v = Uold[(int64_t)i * ldu + (int64_t)map[k] * R + r];
-  }
-  Unew[e] = v;
+  Unew[e] = (c < Cnew) ? Uold[(int64_t)i * ldu + colmap[c]] : 0.0;
 }
 
 }  // namespace jk

@@ -23,7 +23,9 @@ namespace jk {
 enum { F_CONVERGED = 1, F_PINV = 2, F_NONFINITE = 4, F_BREAKDOWN = 8 };
 
 struct EpiArgs {
-  int N, n, R;
+  int N, n, R;                   // R: the handle's largest rank Rs (strides of gram / lambda)
+  const int* subR;               // mixed-rank pool: submodel -> rank R_k (nullptr: every block has R)
+  const int* blkcol;             // mixed-rank pool: live block -> first column (nullptr: k R)
   int In;
   int64_t ldu;
   int nsub;                      // submodels of the handle (state arrays are indexed by sub)
@@ -130,11 +132,11 @@ __global__ void __launch_bounds__(kEpiThreads) als_epilogue_rows_kernel(EpiArgs 
   if (a.n == 0 && k == 0 && threadIdx.x == 0) *a.active_count = 0;  // per-sweep counter reset
   const int sub = a.blk2sub[k];
   if (!a.active[sub]) return;  // frozen (converged or failed)
-  const int R = a.R, n = a.n, N = a.N, tid = threadIdx.x;
+  const int R = a.subR ? a.subR[sub] : a.R, Rs = a.R, n = a.n, N = a.N, tid = threadIdx.x;
   const bool last = (n == N - 1);
   const int64_t pz0 = (n == 0) ? a.pglob[sub] : -1;   // padded rows [pz0, pz1)
   const int64_t pz1 = (n == 0) ? pz0 + a.d : -1;
-  const int cb = k * R;
+  const int cb = a.blkcol ? a.blkcol[k] : k * R;
 
   __shared__ double H[RMAX * RMAX];
   __shared__ double Lf[RMAX * RMAX];       // Cholesky factor (row-major lower) or H^+
@@ -145,7 +147,7 @@ __global__ void __launch_bounds__(kEpiThreads) als_epilogue_rows_kernel(EpiArgs 
   for (int e = tid; e < R * R; e += kEpiThreads) {
     double h = 1.0;
     for (int m = 0; m < N; ++m)
-      if (m != n) h *= a.gram[((int64_t)m * a.nsub + sub) * R * R + e];
+      if (m != n) h *= a.gram[((int64_t)m * a.nsub + sub) * Rs * Rs + e];
     H[e] = h;
   }
   __syncthreads();
@@ -294,9 +296,9 @@ __global__ void __launch_bounds__(kEpiThreads) als_epilogue_rows_kernel(EpiArgs 
   const double* gt = red + NW * RMAX * RMAX;
   for (int e = tid; e < R * R; e += kEpiThreads) {
     int r = e / R, q = e % R;
-    a.gram[((int64_t)n * a.nsub + sub) * R * R + e] = gt[r * RMAX + q];
+    a.gram[((int64_t)n * a.nsub + sub) * Rs * Rs + e] = gt[r * RMAX + q];
   }
-  if (tid < R) a.lambda[(int64_t)sub * R + tid] = lam[tid];
+  if (tid < R) a.lambda[(int64_t)sub * Rs + tid] = lam[tid];
 
   if (last && tid == 0) {  // (a7) error, fit, history, convergence mask
     const double nt2 = a.normT2p[sub];
@@ -431,13 +433,13 @@ __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
   if (a.n == 0 && k == 0 && threadIdx.x == 0) *a.active_count = 0;  // per-sweep counter reset
   const int sub = a.blk2sub[k];
   if (!a.active[sub]) return;  // frozen (converged or failed)
-  const int R = a.R, n = a.n, N = a.N, tid = threadIdx.x, In = a.In;
+  const int R = a.subR ? a.subR[sub] : a.R, Rs = a.R, n = a.n, N = a.N, tid = threadIdx.x, In = a.In;
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int NW = kEpi2Threads / 32;
   const bool last = (n == N - 1);
   const int64_t pz0 = (n == 0) ? a.pglob[sub] : -1;   // padded rows [pz0, pz1)
   const int64_t pz1 = (n == 0) ? pz0 + a.d : -1;
-  const int cb = k * R;
+  const int cb = a.blkcol ? a.blkcol[k] : k * R;
 
   __shared__ double H[RMAX * RMAX];
   __shared__ double Lf[RMAX * RMAX];   // Cholesky factor (row-major lower) or H^+
@@ -454,7 +456,7 @@ __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
   if (tid < R * R) {
     double h = 1.0;
     for (int m = 0; m < N; ++m)
-      if (m != n) h *= a.gram[((int64_t)m * a.nsub + sub) * R * R + tid];
+      if (m != n) h *= a.gram[((int64_t)m * a.nsub + sub) * Rs * Rs + tid];
     H[tid] = h;
   }
   // (a2) fixed-order sum of the partial pieces of this submodel's R columns: J elements per
@@ -585,7 +587,7 @@ __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
   if (tid < R) {
     const double lm = sqrt(vtv(tid, tid));
     ilam_s[tid] = lm > 0.0 ? 1.0 / lm : 1.0;
-    a.lambda[(int64_t)sub * R + tid] = lm;
+    a.lambda[(int64_t)sub * Rs + tid] = lm;
   }
   __syncthreads();
   for (int e = tid; e < In * R; e += blockDim.x) {
@@ -594,7 +596,7 @@ __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
   }
   if (tid < R * R) {
     const int r = tid / R, c = tid % R;
-    a.gram[((int64_t)n * a.nsub + sub) * R * R + tid] = vtv(r, c) * ilam_s[r] * ilam_s[c];
+    a.gram[((int64_t)n * a.nsub + sub) * Rs * Rs + tid] = vtv(r, c) * ilam_s[r] * ilam_s[c];
   }
   EPI_PROBE(6);
   if (last && tid == 0) {  // (a7) error, fit, history, convergence mask

@@ -371,7 +371,8 @@ struct Layout {
 
 struct Offsets {
   size_t T, T32hi, T32lo, T1hi, T1lo, U[2][kMaxModes], Ures, parts, tinfo[kMaxModes], gram, lambda, normT2p, fit, fit_prev, err, hist,
-      slice, slice_part, stage, iters, flags, active, blk2sub, map, pglob, misc, srcoff, srcld;
+      slice, slice_part, stage, iters, flags, active, blk2sub, map, pglob, misc, srcoff, srcld, subR, subRc, blkcol,
+      dstoff;
   int64_t parts_cap;
   int tiles_cap;
   int slice_nb;
@@ -379,8 +380,9 @@ struct Offsets {
   size_t total;
 };
 
+// R: the largest rank in the handle (Rs); sumRm: sum of the pool's model ranks (staging of P)
 bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_cap, const KernelInfo& ki,
-                     Offsets* o, bool tf32 = false) {
+                     Offsets* o, bool tf32 = false, int64_t sumRm = 0) {
   int64_t P = 1, sumI = 0, maxI = 0;
   for (int k = 0; k < N; ++k) {
     P *= dims[k];
@@ -423,15 +425,20 @@ bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_c
   o->slice_nb = (int)std::min<int64_t>(J0, 2 * (int64_t)ki.nsm);
   o->slice_part = L.take((int64_t)o->slice_nb * dims[0] * 8);
   o->stage_cap = std::max<int64_t>(std::max<int64_t>(3 * maxI * R, nsub * maxI * R), 64);
+  o->stage_cap = std::max<int64_t>(o->stage_cap, maxI * sumRm);
   o->stage = L.take(o->stage_cap * 8);
   o->iters = L.take(nsub * 4);
   o->flags = L.take(nsub * 4);
   o->active = L.take(nsub * 4);
   o->blk2sub = L.take(nsub * 4);
-  o->map = L.take(nsub * 4);
+  o->map = L.take(ldu * 4);  // compaction column map
   o->pglob = L.take(nsub * 8);
   o->srcoff = L.take(nsub * 8);
   o->srcld = L.take(nsub * 8);
+  o->subR = L.take(nsub * 4);
+  o->subRc = L.take(nsub * 4);
+  o->blkcol = L.take(nsub * 4);
+  o->dstoff = L.take(nsub * 8);
   o->misc = L.take(256);  // [0] normT2 (double), [8] tol (double), [16] active_count (int)
   o->total = L.off + kAlign;  // slack for re-alignment of the caller's pointer
   return true;
@@ -460,6 +467,13 @@ struct jkcals_s {
   int R = 0;
   int64_t sub_begin = 0, sub_end = 0;  // group indices g; group g leaves out rows [g d, min(g d + d, I_0))
   int64_t d = 1;                       // delete-d group size (1 = leave-one-out)
+  int64_t ngroups = 0;                 // ceil(I_0 / d); submodel s = model * ngroups + group
+  int nmodels = 1;
+  std::vector<int> ranks;              // rank of each pooled model
+  bool mixed = false;                  // blocks of different widths (per-block rank / column tables)
+  std::vector<int> h_subR, h_subRc, h_model;  // per local submodel: rank, rank prefix of its model, model
+  std::vector<int64_t> h_group;        // per local submodel: group index g
+  std::vector<int> h_blkcol;           // per live block: first column
   int nsub = 0, K = 0, C = 0;
   int64_t ldu = 0, P = 0, I0p = 0;
   int hist_cap = 1;
@@ -676,6 +690,8 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
   a.N = h->N;
   a.n = n;
   a.R = h->R;
+  a.subR = h->mixed ? h->ptr<int>(h->off.subR) : nullptr;
+  a.blkcol = h->mixed ? h->ptr<int>(h->off.blkcol) : nullptr;
   a.In = (int)h->dims[n];
   a.ldu = h->ldu;
   a.nsub = h->nsub;
@@ -746,7 +762,8 @@ jkcals_status ensure_graph(jkcals_t h) {
 template <int RMAX>
 void launch_gram(jkcals_t h, int n) {
   gram_kernel<RMAX><<<h->K, kEpiThreads, 0, h->stream>>>(h->U(n), (int)h->dims[n], h->ldu, h->R,
-                                                          h->ptr<int>(h->off.blk2sub), h->nsub, n,
+                                                          h->ptr<int>(h->off.blk2sub), h->ptr<int>(h->off.blkcol),
+                                                          h->ptr<int>(h->off.subR), h->nsub, n,
                                                           h->ptr<double>(h->off.gram));
 }
 
@@ -760,56 +777,74 @@ jkcals_status compute_grams(jkcals_t h) {
   return JKCALS_OK;
 }
 
+// upload the live-block column table (prefix sums of the live blocks' ranks) and set C
+jkcals_status set_blocks(jkcals_t h, const std::vector<int>& b2s) {
+  h->h_blk2sub = b2s;
+  h->K = (int)b2s.size();
+  h->h_blkcol.assign(h->K, 0);
+  int c = 0;
+  for (int k = 0; k < h->K; ++k) {
+    h->h_blkcol[k] = c;
+    c += h->h_subR[b2s[k]];
+  }
+  h->C = c;
+  if (h->K > 0) {
+    CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.blk2sub), b2s.data(), sizeof(int) * h->K, cudaMemcpyHostToDevice,
+                           h->stream));
+    CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.blkcol), h->h_blkcol.data(), sizeof(int) * h->K,
+                           cudaMemcpyHostToDevice, h->stream));
+  }
+  CKH(h, cudaStreamSynchronize(h->stream));  // host vectors are the copy sources
+  return JKCALS_OK;
+}
+
+int64_t sum_dims(jkcals_t h) {
+  int64_t sumI = 0;
+  for (int n = 0; n < h->N; ++n) sumI += h->dims[n];
+  return sumI;
+}
+
 // (a8) compact: store converged live blocks, gather the active ones to the front.
 jkcals_status compact(jkcals_t h) {
   std::vector<int> act(h->nsub);
   CKH(h, cudaMemcpyAsync(act.data(), h->ptr<int>(h->off.active), sizeof(int) * h->nsub, cudaMemcpyDeviceToHost,
                          h->stream));
   CKH(h, cudaStreamSynchronize(h->stream));
-  int64_t sumI = 0;
-  for (int n = 0; n < h->N; ++n) sumI += h->dims[n];
-  std::vector<int> map;
+  const int64_t sumI = sum_dims(h);
+  std::vector<int> keep, colmap;
   for (int k = 0; k < h->K; ++k) {
-    int sub = h->h_blk2sub[k];
+    const int sub = h->h_blk2sub[k], R = h->h_subR[sub], col = h->h_blkcol[k];
     if (act[sub]) {
-      map.push_back(k);
+      keep.push_back(sub);
+      for (int r = 0; r < R; ++r) colmap.push_back(col + r);
     } else if (!h->h_stored[sub]) {
       int64_t o = 0;
       for (int n = 0; n < h->N; ++n) {
         int I = (int)h->dims[n];
         double* dst = h->ptr<double>(h->off.Ures) + (int64_t)sub * sumI * h->R + o;
-        store_block_kernel<<<(int)cdiv((int64_t)I * h->R, 256), 256, 0, h->stream>>>(h->U(n), I, h->ldu, h->R, k,
-                                                                                     dst);
+        store_block_kernel<<<(int)cdiv((int64_t)I * R, 256), 256, 0, h->stream>>>(h->U(n), I, h->ldu, R, col, dst);
         CKH(h, cudaGetLastError());
-        o += (int64_t)I * h->R;
+        o += (int64_t)I * R;
       }
       h->h_stored[sub] = 1;
     }
   }
-  const int Knew = (int)map.size();
+  const int Knew = (int)keep.size();
   if (Knew == h->K) return JKCALS_OK;
-  std::vector<int> nb2s(std::max(Knew, 1));
-  for (int k = 0; k < Knew; ++k) nb2s[k] = h->h_blk2sub[map[k]];
-  if (Knew > 0) {
-    CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.map), map.data(), sizeof(int) * Knew, cudaMemcpyHostToDevice,
+  const int Cnew = (int)colmap.size();
+  if (Cnew > 0)
+    CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.map), colmap.data(), sizeof(int) * Cnew, cudaMemcpyHostToDevice,
                            h->stream));
-  }
   const int other = h->cur ^ 1;
   for (int n = 0; n < h->N; ++n) {
     int64_t tot = h->dims[n] * h->ldu;
     gather_blocks_kernel<<<(int)cdiv(tot, 256), 256, 0, h->stream>>>(
-        h->U(n), h->ptr<double>(h->off.U[other][n]), (int)h->dims[n], h->ldu, h->R, h->ptr<int>(h->off.map), Knew);
+        h->U(n), h->ptr<double>(h->off.U[other][n]), (int)h->dims[n], h->ldu, h->ptr<int>(h->off.map), Cnew);
     CKH(h, cudaGetLastError());
   }
-  if (Knew > 0) {
-    CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.blk2sub), nb2s.data(), sizeof(int) * Knew, cudaMemcpyHostToDevice,
-                           h->stream));
-  }
-  CKH(h, cudaStreamSynchronize(h->stream));
+  jkcals_status st = set_blocks(h, keep);  // synchronises (colmap is a host temporary)
+  if (st != JKCALS_OK) return st;
   h->cur = other;
-  h->h_blk2sub.assign(nb2s.begin(), nb2s.begin() + Knew);
-  h->K = Knew;
-  h->C = Knew * h->R;
   if (Knew > 0) return replan(h);
   return JKCALS_OK;
 }
@@ -819,16 +854,51 @@ jkcals_status compact(jkcals_t h) {
 // ====================================================================== C ABI
 extern "C" {
 
-size_t jkcals_workspace_bytes(int ndims, const int64_t* dims, int rank, int64_t n_sub, jkcals_precision prec,
-                              int hist_cap, int device) {
-  if (!valid_dims(ndims, dims, rank) || n_sub < 1 || n_sub > dims[0] || hist_cap < 1) return 0;
+// pool geometry shared by jkcals_pool_workspace_bytes and jkcals_create_pool
+struct PoolGeo {
+  int Rs = 0;          // largest rank among the handle's submodels
+  int64_t sumRm = 0;   // sum of all model ranks
+  int64_t ngroups = 0;
+  int64_t C = 0;       // total fused width of the handle
+};
+
+static bool pool_geo(int ndims, const int64_t* dims, int nmodels, const int* ranks, int64_t d, int64_t sub_begin,
+                     int64_t sub_end, PoolGeo* g) {
+  if (nmodels < 1 || !ranks || !dims || ndims < 3 || ndims > JKCALS_MAX_MODES) return false;
+  if (dims[0] < 2 || d < 1 || (d > 1 && 2 * d > dims[0])) return false;  // d <= I_0 / 2
+  for (int m = 0; m < nmodels; ++m)
+    if (ranks[m] < 1 || ranks[m] > 16) return false;
+  g->ngroups = (dims[0] + d - 1) / d;
+  if (sub_begin < 0 || sub_end <= sub_begin || sub_end > (int64_t)nmodels * g->ngroups) return false;
+  g->Rs = 0;
+  g->C = 0;
+  g->sumRm = 0;
+  for (int m = 0; m < nmodels; ++m) g->sumRm += ranks[m];
+  for (int64_t s = sub_begin; s < sub_end; ++s) {
+    const int R = ranks[s / g->ngroups];
+    g->Rs = std::max(g->Rs, R);
+    g->C += R;
+  }
+  return valid_dims(ndims, dims, g->Rs) && g->C <= (1 << 24);
+}
+
+size_t jkcals_pool_workspace_bytes(int ndims, const int64_t* dims, int nmodels, const int* ranks, int64_t d,
+                                   int64_t sub_begin, int64_t sub_end, jkcals_precision prec, int hist_cap,
+                                   int device) {
+  PoolGeo g;
+  if (!pool_geo(ndims, dims, nmodels, ranks, d, sub_begin, sub_end, &g) || hist_cap < 1) return 0;
   if (prec != JKCALS_FP64 && prec != JKCALS_FP32) return 0;
-  if (n_sub * rank > (1 << 24)) return 0;
   KernelInfo* ki = kernel_info(device, nullptr);
   if (!ki) return 0;
   Offsets o;
-  compute_offsets(ndims, dims, rank, n_sub, hist_cap, *ki, &o, prec == JKCALS_FP32);
+  compute_offsets(ndims, dims, g.Rs, sub_end - sub_begin, hist_cap, *ki, &o, prec == JKCALS_FP32, g.sumRm);
   return o.total;
+}
+
+size_t jkcals_workspace_bytes(int ndims, const int64_t* dims, int rank, int64_t n_sub, jkcals_precision prec,
+                              int hist_cap, int device) {
+  if (!dims || ndims < 3 || n_sub < 1 || n_sub > dims[0]) return 0;
+  return jkcals_pool_workspace_bytes(ndims, dims, 1, &rank, 1, 0, n_sub, prec, hist_cap, device);
 }
 
 // rows of mode 0 left out by group g (the last group may be smaller)
@@ -837,19 +907,27 @@ static int64_t group_rows(const jkcals_s* h, int64_t g) { return std::min(h->d, 
 jkcals_status jkcals_create(jkcals_t* out, int ndims, const int64_t* dims, int rank, int64_t sub_begin,
                             int64_t sub_end, const double* tensor, int tensor_is_device, jkcals_precision prec,
                             int device, void* cuda_stream, void* workspace, size_t workspace_bytes, int hist_cap) {
-  return jkcals_create_d(out, ndims, dims, rank, 1, sub_begin, sub_end, tensor, tensor_is_device, prec, device,
-                         cuda_stream, workspace, workspace_bytes, hist_cap);
+  return jkcals_create_pool(out, ndims, dims, 1, &rank, 1, sub_begin, sub_end, tensor, tensor_is_device, prec,
+                            device, cuda_stream, workspace, workspace_bytes, hist_cap);
 }
 
 jkcals_status jkcals_create_d(jkcals_t* out, int ndims, const int64_t* dims, int rank, int64_t d, int64_t sub_begin,
                               int64_t sub_end, const double* tensor, int tensor_is_device, jkcals_precision prec,
                               int device, void* cuda_stream, void* workspace, size_t workspace_bytes, int hist_cap) {
+  return jkcals_create_pool(out, ndims, dims, 1, &rank, d, sub_begin, sub_end, tensor, tensor_is_device, prec,
+                            device, cuda_stream, workspace, workspace_bytes, hist_cap);
+}
+
+jkcals_status jkcals_create_pool(jkcals_t* out, int ndims, const int64_t* dims, int nmodels, const int* ranks,
+                                 int64_t d, int64_t sub_begin, int64_t sub_end, const double* tensor,
+                                 int tensor_is_device, jkcals_precision prec, int device, void* cuda_stream,
+                                 void* workspace, size_t workspace_bytes, int hist_cap) {
   if (!out) return JKCALS_E_ARG;
   *out = nullptr;
-  if (!valid_dims(ndims, dims, rank) || !tensor || !workspace) return JKCALS_E_ARG;
-  if (d < 1 || (d > 1 && 2 * d > dims[0])) return JKCALS_E_ARG;  // d <= I_0 / 2
-  const int64_t ngroups = (dims[0] + d - 1) / d;
-  if (sub_begin < 0 || sub_end > ngroups || sub_end <= sub_begin || hist_cap < 1) return JKCALS_E_ARG;
+  PoolGeo pg0;
+  if (!pool_geo(ndims, dims, nmodels, ranks, d, sub_begin, sub_end, &pg0) || !tensor || !workspace ||
+      hist_cap < 1)
+    return JKCALS_E_ARG;
   if (prec != JKCALS_FP64 && prec != JKCALS_FP32) return JKCALS_E_ARG;
   DeviceGuard dg(device);
   std::string kerr;
@@ -858,13 +936,27 @@ jkcals_status jkcals_create_d(jkcals_t* out, int ndims, const int64_t* dims, int
   jkcals_t h = new jkcals_s();
   h->N = ndims;
   for (int k = 0; k < ndims; ++k) h->dims[k] = dims[k];
-  h->R = rank;
+  h->R = pg0.Rs;
   h->sub_begin = sub_begin;
   h->sub_end = sub_end;
   h->d = d;
+  h->ngroups = pg0.ngroups;
+  h->nmodels = nmodels;
+  h->ranks.assign(ranks, ranks + nmodels);
   h->nsub = (int)(sub_end - sub_begin);
+  std::vector<int> rc(nmodels, 0);
+  for (int m = 1; m < nmodels; ++m) rc[m] = rc[m - 1] + ranks[m - 1];
+  for (int q = 0; q < h->nsub; ++q) {
+    const int64_t s = sub_begin + q;
+    const int m = (int)(s / h->ngroups);
+    h->h_model.push_back(m);
+    h->h_group.push_back(s % h->ngroups);
+    h->h_subR.push_back(ranks[m]);
+    h->h_subRc.push_back(rc[m]);
+    if (ranks[m] != h->R) h->mixed = true;
+  }
   h->K = h->nsub;
-  h->C = h->K * rank;
+  h->C = (int)pg0.C;
   h->ldu = rup(std::max<int64_t>(h->C, 1), 128);
   h->P = 1;
   for (int k = 0; k < ndims; ++k) h->P *= dims[k];
@@ -875,7 +967,7 @@ jkcals_status jkcals_create_d(jkcals_t* out, int ndims, const int64_t* dims, int
   h->es = h->stream;
   h->ki = ki;
   h->tf32 = (prec == JKCALS_FP32) ? 1 : 0;
-  compute_offsets(ndims, dims, rank, h->nsub, hist_cap, *ki, &h->off, h->tf32 != 0);
+  compute_offsets(ndims, dims, h->R, h->nsub, hist_cap, *ki, &h->off, h->tf32 != 0, pg0.sumRm);
   // align the caller's pointer
   uintptr_t base = reinterpret_cast<uintptr_t>(workspace);
   uintptr_t aligned = (base + kAlign - 1) & ~(uintptr_t)(kAlign - 1);
@@ -899,15 +991,20 @@ jkcals_status jkcals_create_d(jkcals_t* out, int ndims, const int64_t* dims, int
   std::vector<int64_t> pg(h->nsub);
   std::vector<int> b2s(h->nsub);
   for (int q = 0; q < h->nsub; ++q) {
-    pg[q] = (sub_begin + q) * d;  // first left-out row of the group
+    pg[q] = h->h_group[q] * d;  // first left-out row of the group
     b2s[q] = q;
   }
-  h->h_blk2sub = b2s;
   h->h_stored.assign(h->nsub, 0);
   CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.pglob), pg.data(), sizeof(int64_t) * h->nsub,
                          cudaMemcpyHostToDevice, h->stream));
-  CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.blk2sub), b2s.data(), sizeof(int) * h->nsub, cudaMemcpyHostToDevice,
+  CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.subR), h->h_subR.data(), sizeof(int) * h->nsub, cudaMemcpyHostToDevice,
                          h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.subRc), h->h_subRc.data(), sizeof(int) * h->nsub,
+                         cudaMemcpyHostToDevice, h->stream));
+  {
+    jkcals_status st0 = set_blocks(h, b2s);
+    if (st0 != JKCALS_OK) return st0;
+  }
   // (a0) slice norms, ||T||^2, ||T_-p||^2
   const int64_t I0 = dims[0], J0 = h->P / I0;
   const int nb = h->off.slice_nb;
@@ -946,37 +1043,51 @@ jkcals_status jkcals_create_d(jkcals_t* out, int ndims, const int64_t* dims, int
   return JKCALS_OK;
 }
 
+// the live block of local submodel `sub`, or -1
+static int block_of(jkcals_t h, int sub) {
+  for (int k = 0; k < h->K; ++k)
+    if (h->h_blk2sub[k] == sub) return k;
+  return -1;
+}
+
 jkcals_status jkcals_set_init(jkcals_t h, const double* const* P) {
   if (!h || !P) return JKCALS_E_ARG;
   DeviceGuard dg(h->device);
-  for (int n = 0; n < h->N; ++n) {
-    if (!P[n]) return fail(h, JKCALS_E_ARG, "P[%d] is NULL", n);
-    for (int64_t e = 0; e < h->dims[n] * h->R; ++e)
-      if (!std::isfinite(P[n][e])) return fail(h, JKCALS_E_NONFINITE, "P[%d] has a non-finite entry", n);
-  }
+  for (int m = 0; m < h->nmodels; ++m)
+    for (int n = 0; n < h->N; ++n) {
+      const double* Pm = P[m * h->N + n];
+      if (!Pm) return fail(h, JKCALS_E_ARG, "P[%d] is NULL", m * h->N + n);
+      for (int64_t e = 0; e < h->dims[n] * h->ranks[m]; ++e)
+        if (!std::isfinite(Pm[e])) return fail(h, JKCALS_E_NONFINITE, "P[%d] has a non-finite entry", m * h->N + n);
+    }
   // full reset of the fused layout (undo any compaction)
   bool relayout = (h->K != h->nsub) || (h->cur != 0);
   h->cur = 0;
-  h->K = h->nsub;
-  h->C = h->K * h->R;
   std::vector<int> b2s(h->nsub);
   for (int q = 0; q < h->nsub; ++q) b2s[q] = q;
-  h->h_blk2sub = b2s;
+  jkcals_status st = set_blocks(h, b2s);
+  if (st != JKCALS_OK) return st;
   h->h_stored.assign(h->nsub, 0);
-  CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.blk2sub), b2s.data(), sizeof(int) * h->nsub, cudaMemcpyHostToDevice,
-                         h->stream));
   double* stage = h->ptr<double>(h->off.stage);
   for (int n = 0; n < h->N; ++n) {
     const int I = (int)h->dims[n];
-    CKH(h, cudaMemcpyAsync(stage, P[n], sizeof(double) * I * h->R, cudaMemcpyHostToDevice, h->stream));
-    int64_t tot = (int64_t)I * h->ldu;
-    broadcast_init_kernel<<<(int)cdiv(tot, 256), 256, 0, h->stream>>>(stage, I, h->R, h->K, h->ldu, h->U(n),
-                                                                      n == 0 ? 1 : 0, h->ptr<int>(h->off.blk2sub),
-                                                                      h->ptr<int64_t>(h->off.pglob), (int)h->d);
+    // stage = [P_n(model 0) | P_n(model 1) | ...], column-major I x sum_m R_m
+    int64_t c0 = 0;
+    for (int m = 0; m < h->nmodels; ++m) {
+      CKH(h, cudaMemcpyAsync(stage + (int64_t)I * c0, P[m * h->N + n], sizeof(double) * I * h->ranks[m],
+                             cudaMemcpyHostToDevice, h->stream));
+      c0 += h->ranks[m];
+    }
+    CKH(h, cudaMemsetAsync(h->U(n), 0, sizeof(double) * I * h->ldu, h->stream));
+    const int64_t tot = (int64_t)I * h->K * h->R;
+    init_blocks_kernel<<<(int)cdiv(tot, 256), 256, 0, h->stream>>>(
+        stage, I, h->R, h->K, h->ldu, h->U(n), n == 0 ? 1 : 0, h->ptr<int>(h->off.blk2sub),
+        h->ptr<int>(h->off.blkcol), h->ptr<int>(h->off.subR), h->ptr<int>(h->off.subRc),
+        h->ptr<int64_t>(h->off.pglob), (int)h->d);
     CKH(h, cudaGetLastError());
     CKH(h, cudaStreamSynchronize(h->stream));  // stage is reused by the next mode
   }
-  jkcals_status st = compute_grams(h);
+  st = compute_grams(h);
   if (st != JKCALS_OK) return st;
   reset_state_kernel<<<(int)cdiv(h->nsub, 256), 256, 0, h->stream>>>(
       h->nsub, h->ptr<double>(h->off.fit), h->ptr<double>(h->off.fit_prev), h->ptr<double>(h->off.err),
@@ -998,20 +1109,19 @@ jkcals_status jkcals_set_init_submodel(jkcals_t h, int64_t p, int mode, const do
   if (!h->inited) return fail(h, JKCALS_E_STATE, "set_init must come first");
   DeviceGuard dg(h->device);
   const int sub = (int)(p - h->sub_begin);
-  int blk = -1;
-  for (int k = 0; k < h->K; ++k)
-    if (h->h_blk2sub[k] == sub) blk = k;
+  const int blk = block_of(h, sub);
   if (blk < 0) return fail(h, JKCALS_E_STATE, "submodel %lld was compacted out", (long long)p);
   const int I = (int)h->dims[mode];
-  const int cnt = mode == 0 ? (int)group_rows(h, p) : 0;
+  const int R = h->h_subR[sub];
+  const int64_t g = h->h_group[sub];
+  const int cnt = mode == 0 ? (int)group_rows(h, g) : 0;
   const int rows = I - cnt;
-  for (int64_t e = 0; e < (int64_t)rows * h->R; ++e)
+  for (int64_t e = 0; e < (int64_t)rows * R; ++e)
     if (!std::isfinite(U[e])) return fail(h, JKCALS_E_NONFINITE, "non-finite init");
   double* stage = h->ptr<double>(h->off.stage);
-  CKH(h, cudaMemcpyAsync(stage, U, sizeof(double) * rows * h->R, cudaMemcpyHostToDevice, h->stream));
-  set_block_kernel<<<(int)cdiv((int64_t)I * h->R, 256), 256, 0, h->stream>>>(stage, I, h->R, h->ldu, blk,
-                                                                            mode == 0 ? p * h->d : -1, cnt,
-                                                                            h->U(mode));
+  CKH(h, cudaMemcpyAsync(stage, U, sizeof(double) * rows * R, cudaMemcpyHostToDevice, h->stream));
+  set_block_kernel<<<(int)cdiv((int64_t)I * R, 256), 256, 0, h->stream>>>(stage, I, R, h->ldu, h->h_blkcol[blk],
+                                                                         mode == 0 ? g * h->d : -1, cnt, h->U(mode));
   CKH(h, cudaGetLastError());
   jkcals_status st = compute_grams(h);
   if (st != JKCALS_OK) return st;
@@ -1066,21 +1176,19 @@ jkcals_status jkcals_iterate(jkcals_t h, int max_iters, double tol, int* sweeps_
 static jkcals_status locate(jkcals_t h, int64_t p, int mode, const double** src, int64_t* ld, int* sub_out) {
   const int sub = (int)(p - h->sub_begin);
   *sub_out = sub;
+  const int R = h->h_subR[sub];
   if (h->h_stored[sub]) {
-    int64_t sumI = 0, o = 0;
-    for (int n = 0; n < h->N; ++n) sumI += h->dims[n];
-    for (int n = 0; n < mode; ++n) o += h->dims[n] * h->R;
-    *src = h->ptr<double>(h->off.Ures) + (int64_t)sub * sumI * h->R + o;
-    *ld = h->R;
+    int64_t o = 0;
+    for (int n = 0; n < mode; ++n) o += h->dims[n] * R;
+    *src = h->ptr<double>(h->off.Ures) + (int64_t)sub * sum_dims(h) * h->R + o;
+    *ld = R;
     return JKCALS_OK;
   }
-  for (int k = 0; k < h->K; ++k)
-    if (h->h_blk2sub[k] == sub) {
-      *src = h->U(mode) + (int64_t)k * h->R;
-      *ld = h->ldu;
-      return JKCALS_OK;
-    }
-  return fail(h, JKCALS_E_STATE, "submodel %lld not found", (long long)p);
+  const int k = block_of(h, sub);
+  if (k < 0) return fail(h, JKCALS_E_STATE, "submodel %lld not found", (long long)p);
+  *src = h->U(mode) + h->h_blkcol[k];
+  *ld = h->ldu;
+  return JKCALS_OK;
 }
 
 jkcals_status jkcals_get_factors(jkcals_t h, int64_t p, int mode, double* U, double* lambda) {
@@ -1093,60 +1201,58 @@ jkcals_status jkcals_get_factors(jkcals_t h, int64_t p, int mode, double* U, dou
   jkcals_status st = locate(h, p, mode, &src, &ld, &sub);
   if (st != JKCALS_OK) return st;
   const int I = (int)h->dims[mode];
-  const int cnt = mode == 0 ? (int)group_rows(h, p) : 0;
+  const int R = h->h_subR[sub];
+  const int cnt = mode == 0 ? (int)group_rows(h, h->h_group[sub]) : 0;
   const int rows = I - cnt;
   double* stage = h->ptr<double>(h->off.stage);
-  extract_kernel<<<(int)cdiv((int64_t)rows * h->R, 256), 256, 0, h->stream>>>(
-      src, ld, I, h->R, mode == 0 ? p * h->d : -1, cnt, stage);
+  extract_kernel<<<(int)cdiv((int64_t)rows * R, 256), 256, 0, h->stream>>>(
+      src, ld, I, R, mode == 0 ? h->h_group[sub] * h->d : -1, cnt, stage);
   CKH(h, cudaGetLastError());
-  CKH(h, cudaMemcpyAsync(U, stage, sizeof(double) * rows * h->R, cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaMemcpyAsync(U, stage, sizeof(double) * rows * R, cudaMemcpyDeviceToHost, h->stream));
   if (lambda)
-    CKH(h, cudaMemcpyAsync(lambda, h->ptr<double>(h->off.lambda) + (int64_t)sub * h->R, sizeof(double) * h->R,
+    CKH(h, cudaMemcpyAsync(lambda, h->ptr<double>(h->off.lambda) + (int64_t)sub * h->R, sizeof(double) * R,
                            cudaMemcpyDeviceToHost, h->stream));
   CKH(h, cudaStreamSynchronize(h->stream));
   return JKCALS_OK;
 }
 
-static jkcals_status build_src_table(jkcals_t h, int mode);
+static jkcals_status build_src_table(jkcals_t h, int mode, const std::vector<int>& subs);
 
 jkcals_status jkcals_get_all_factors(jkcals_t h, int mode, double* U, double* lambda) {
   if (!h || !U || mode < 0 || mode >= h->N) return JKCALS_E_ARG;
   if (!h->inited) return fail(h, JKCALS_E_STATE, "no model yet");
   DeviceGuard dg(h->device);
-  jkcals_status st = build_src_table(h, mode);
+  std::vector<int> subs(h->nsub);
+  for (int q = 0; q < h->nsub; ++q) subs[q] = q;
+  jkcals_status st = build_src_table(h, mode, subs);
   if (st != JKCALS_OK) return st;
   const int I = (int)h->dims[mode];
-  const int dd = mode == 0 ? (int)h->d : 0;
-  const int rows = I - dd;
-  // groups of the full size d go in one launch; a ragged last group (d does not divide I_0) is
-  // appended by its own extract (blocks are packed in submodel order either way)
-  const bool ragged = mode == 0 && group_rows(h, h->sub_end - 1) != h->d;
-  const int nfull = h->nsub - (ragged ? 1 : 0);
-  const int64_t tot = (int64_t)nfull * rows * h->R;
+  // packed output: submodel q's rows_q x R_q block at dstoff[q]
+  std::vector<int64_t> dst(h->nsub);
+  int64_t total = 0;
+  for (int q = 0; q < h->nsub; ++q) {
+    dst[q] = total;
+    const int rows = I - (mode == 0 ? (int)group_rows(h, h->h_group[q]) : 0);
+    total += (int64_t)rows * h->h_subR[q];
+  }
+  CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.dstoff), dst.data(), 8 * h->nsub, cudaMemcpyHostToDevice, h->stream));
   double* stage = h->ptr<double>(h->off.stage);
-  if (tot > 0) {
-    extract_all_kernel<<<(int)cdiv(tot, 256), 256, 0, h->stream>>>(
-        reinterpret_cast<const double*>(h->ws), h->ptr<int64_t>(h->off.srcoff), h->ptr<int64_t>(h->off.srcld), nfull,
-        I, h->R, mode == 0 ? 1 : 0, h->ptr<int64_t>(h->off.pglob), dd, stage);
-    CKH(h, cudaGetLastError());
-  }
-  int64_t total = tot;
-  if (ragged) {
-    const double* src;
-    int64_t ld;
-    int sub;
-    jkcals_status st2 = locate(h, h->sub_end - 1, mode, &src, &ld, &sub);
-    if (st2 != JKCALS_OK) return st2;
-    const int cnt = (int)group_rows(h, h->sub_end - 1);
-    extract_kernel<<<(int)cdiv((int64_t)(I - cnt) * h->R, 256), 256, 0, h->stream>>>(
-        src, ld, I, h->R, (h->sub_end - 1) * h->d, cnt, stage + tot);
-    CKH(h, cudaGetLastError());
-    total += (int64_t)(I - cnt) * h->R;
-  }
+  const int per = (int)std::min<int64_t>(cdiv((int64_t)I * h->R, 256), 64);
+  extract_all_kernel<<<dim3(per, (unsigned)std::min(h->nsub, 65535)), 256, 0, h->stream>>>(
+      reinterpret_cast<const double*>(h->ws), h->ptr<int64_t>(h->off.srcoff), h->ptr<int64_t>(h->off.srcld),
+      h->ptr<int>(h->off.subR), h->ptr<int64_t>(h->off.dstoff), h->nsub, I, mode == 0 ? 1 : 0,
+      h->ptr<int64_t>(h->off.pglob), (int)h->d, stage);
+  CKH(h, cudaGetLastError());
   CKH(h, cudaMemcpyAsync(U, stage, sizeof(double) * total, cudaMemcpyDeviceToHost, h->stream));
-  if (lambda)
-    CKH(h, cudaMemcpyAsync(lambda, h->ptr<double>(h->off.lambda), sizeof(double) * h->nsub * h->R,
+  if (lambda) {  // packed the same way: R_q values per submodel
+    std::vector<double> lam((size_t)h->nsub * h->R);
+    CKH(h, cudaMemcpyAsync(lam.data(), h->ptr<double>(h->off.lambda), sizeof(double) * lam.size(),
                            cudaMemcpyDeviceToHost, h->stream));
+    CKH(h, cudaStreamSynchronize(h->stream));
+    int64_t o = 0;
+    for (int q = 0; q < h->nsub; ++q)
+      for (int r = 0; r < h->h_subR[q]; ++r) lambda[o++] = lam[(size_t)q * h->R + r];
+  }
   CKH(h, cudaStreamSynchronize(h->stream));
   return JKCALS_OK;
 }
@@ -1161,10 +1267,11 @@ jkcals_status jkcals_get_block(jkcals_t h, int64_t p, int mode, double* U) {
   jkcals_status st = locate(h, p, mode, &src, &ld, &sub);
   if (st != JKCALS_OK) return st;
   const int I = (int)h->dims[mode];
+  const int R = h->h_subR[sub];
   double* stage = h->ptr<double>(h->off.stage);
-  extract_kernel<<<(int)cdiv((int64_t)I * h->R, 256), 256, 0, h->stream>>>(src, ld, I, h->R, -1, 0, stage);
+  extract_kernel<<<(int)cdiv((int64_t)I * R, 256), 256, 0, h->stream>>>(src, ld, I, R, -1, 0, stage);
   CKH(h, cudaGetLastError());
-  CKH(h, cudaMemcpyAsync(U, stage, sizeof(double) * I * h->R, cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaMemcpyAsync(U, stage, sizeof(double) * I * R, cudaMemcpyDeviceToHost, h->stream));
   CKH(h, cudaStreamSynchronize(h->stream));
   return JKCALS_OK;
 }
@@ -1202,62 +1309,85 @@ jkcals_status jkcals_get_history(jkcals_t h, int64_t p, double* err, int cap, in
   return JKCALS_OK;
 }
 
-// device table locating every submodel's mode-`mode` block (live multi-factor or result store)
-static jkcals_status build_src_table(jkcals_t h, int mode) {
-  std::vector<int64_t> off(h->nsub), ld(h->nsub);
-  for (int q = 0; q < h->nsub; ++q) {
+// device table locating the mode-`mode` blocks of the listed local submodels (live
+// multi-factor or result store), in list order
+static jkcals_status build_src_table(jkcals_t h, int mode, const std::vector<int>& subs) {
+  const int ns = (int)subs.size();
+  std::vector<int64_t> off(ns), ld(ns);
+  for (int q = 0; q < ns; ++q) {
     const double* src;
     int64_t l;
     int sub;
-    jkcals_status st = locate(h, h->sub_begin + q, mode, &src, &l, &sub);
+    jkcals_status st = locate(h, h->sub_begin + subs[q], mode, &src, &l, &sub);
     if (st != JKCALS_OK) return st;
     off[q] = src - reinterpret_cast<const double*>(h->ws);
     ld[q] = l;
   }
-  CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.srcoff), off.data(), 8 * h->nsub, cudaMemcpyHostToDevice, h->stream));
-  CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.srcld), ld.data(), 8 * h->nsub, cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.srcoff), off.data(), 8 * ns, cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.srcld), ld.data(), 8 * ns, cudaMemcpyHostToDevice, h->stream));
   CKH(h, cudaStreamSynchronize(h->stream));  // off/ld are host temporaries
   return JKCALS_OK;
 }
 
-static jkcals_status moments(jkcals_t h, int mode, double* mean_d, double* m2_d) {
-  jkcals_status st = build_src_table(h, mode);
+// per-element moments of model `model`'s local submodels; returns their count in *g
+static jkcals_status moments(jkcals_t h, int model, int mode, double* mean_d, double* m2_d, int* g) {
+  std::vector<int> subs;
+  for (int q = 0; q < h->nsub; ++q)
+    if (h->h_model[q] == model) subs.push_back(q);
+  *g = (int)subs.size();
+  if (subs.empty()) return JKCALS_OK;
+  jkcals_status st = build_src_table(h, mode, subs);
   if (st != JKCALS_OK) return st;
-  const int I = (int)h->dims[mode];
-  moments_kernel<<<(int)cdiv((int64_t)I * h->R, 128), 128, 0, h->stream>>>(
+  const int I = (int)h->dims[mode], R = h->ranks[model];
+  moments_kernel<<<(int)cdiv((int64_t)I * R, 128), 128, 0, h->stream>>>(
       reinterpret_cast<const double*>(h->ws), h->ptr<int64_t>(h->off.srcoff), h->ptr<int64_t>(h->off.srcld),
-      h->nsub, I, h->R, mean_d, m2_d);
+      (int)subs.size(), I, R, mean_d, m2_d);
   CKH(h, cudaGetLastError());
-  CKH(h, cudaStreamSynchronize(h->stream));  // off/ld host vectors go out of scope
+  CKH(h, cudaStreamSynchronize(h->stream));
+  return JKCALS_OK;
+}
+
+jkcals_status jkcals_get_model_moments(jkcals_t h, int model, int mode, double* count, double* mean, double* m2) {
+  if (!h || !mean || !m2 || mode < 1 || mode >= h->N || model < 0 || model >= h->nmodels) return JKCALS_E_ARG;
+  if (!h->inited) return fail(h, JKCALS_E_STATE, "no model yet");
+  DeviceGuard dg(h->device);
+  const int64_t IR = h->dims[mode] * h->ranks[model];
+  double* stage = h->ptr<double>(h->off.stage);
+  int g = 0;
+  jkcals_status st = moments(h, model, mode, stage, stage + IR, &g);
+  if (st != JKCALS_OK) return st;
+  if (g == 0) {
+    for (int64_t e = 0; e < IR; ++e) mean[e] = m2[e] = 0.0;
+  } else {
+    CKH(h, cudaMemcpyAsync(mean, stage, 8 * IR, cudaMemcpyDeviceToHost, h->stream));
+    CKH(h, cudaMemcpyAsync(m2, stage + IR, 8 * IR, cudaMemcpyDeviceToHost, h->stream));
+    CKH(h, cudaStreamSynchronize(h->stream));
+  }
+  if (count)
+    for (int64_t e = 0; e < IR; ++e) count[e] = (double)g;
+  return JKCALS_OK;
+}
+
+jkcals_status jkcals_get_model_stats(jkcals_t h, int model, int mode, double* mean, double* std_out) {
+  if (!h || !mean || !std_out || mode < 1 || mode >= h->N || model < 0 || model >= h->nmodels) return JKCALS_E_ARG;
+  const int64_t IR = h->dims[mode] * h->ranks[model];
+  std::vector<double> m2(IR), cnt(IR);
+  jkcals_status st = jkcals_get_model_moments(h, model, mode, cnt.data(), mean, m2.data());
+  if (st != JKCALS_OK) return st;
+  const double g = IR > 0 ? cnt[0] : 0.0;
+  if (g < 2) return fail(h, JKCALS_E_ARG, "jackknife statistics need >= 2 submodels of the model");
+  for (int64_t e = 0; e < IR; ++e) std_out[e] = std::sqrt(((g - 1.0) / g) * m2[e]);
   return JKCALS_OK;
 }
 
 jkcals_status jkcals_get_local_moments(jkcals_t h, int mode, double* count, double* mean, double* m2) {
-  if (!h || !mean || !m2 || mode < 1 || mode >= h->N) return JKCALS_E_ARG;
-  if (!h->inited) return fail(h, JKCALS_E_STATE, "no model yet");
-  DeviceGuard dg(h->device);
-  const int64_t IR = h->dims[mode] * h->R;
-  double* stage = h->ptr<double>(h->off.stage);
-  jkcals_status st = moments(h, mode, stage, stage + IR);
-  if (st != JKCALS_OK) return st;
-  CKH(h, cudaMemcpyAsync(mean, stage, 8 * IR, cudaMemcpyDeviceToHost, h->stream));
-  CKH(h, cudaMemcpyAsync(m2, stage + IR, 8 * IR, cudaMemcpyDeviceToHost, h->stream));
-  CKH(h, cudaStreamSynchronize(h->stream));
-  if (count)
-    for (int64_t e = 0; e < IR; ++e) count[e] = (double)h->nsub;
-  return JKCALS_OK;
+  if (h && h->nmodels != 1) return fail(h, JKCALS_E_ARG, "pooled handle: use jkcals_get_model_moments");
+  return jkcals_get_model_moments(h, 0, mode, count, mean, m2);
 }
 
 jkcals_status jkcals_get_jackknife_stats(jkcals_t h, int mode, double* mean, double* std_out) {
-  if (!h || !mean || !std_out || mode < 1 || mode >= h->N) return JKCALS_E_ARG;
-  if (h->nsub < 2) return fail(h, JKCALS_E_ARG, "jackknife statistics need >= 2 submodels");
-  const int64_t IR = h->dims[mode] * h->R;
-  std::vector<double> m2(IR);
-  jkcals_status st = jkcals_get_local_moments(h, mode, nullptr, mean, m2.data());
-  if (st != JKCALS_OK) return st;
-  const double g = (double)h->nsub;
-  for (int64_t e = 0; e < IR; ++e) std_out[e] = std::sqrt(((g - 1.0) / g) * m2[e]);
-  return JKCALS_OK;
+  if (h && h->nmodels != 1) return fail(h, JKCALS_E_ARG, "pooled handle: use jkcals_get_model_stats");
+  return jkcals_get_model_stats(h, 0, mode, mean, std_out);
 }
 
 jkcals_status jkcals_set_instrument(jkcals_t h, int on) {

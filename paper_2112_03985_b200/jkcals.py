@@ -46,6 +46,10 @@ def lib():
             "jkcals_workspace_bytes": (SZ, [I, P, I, I64, I, I, I]),
             "jkcals_create": (I, [P, I, P, I, I64, I64, P, I, I, I, P, P, SZ, I]),
             "jkcals_create_d": (I, [P, I, P, I, I64, I64, I64, P, I, I, I, P, P, SZ, I]),
+            "jkcals_pool_workspace_bytes": (SZ, [I, P, I, P, I64, I64, I64, I, I, I]),
+            "jkcals_create_pool": (I, [P, I, P, I, P, I64, I64, I64, P, I, I, I, P, P, SZ, I]),
+            "jkcals_get_model_stats": (I, [P, I, I, P, P]),
+            "jkcals_get_model_moments": (I, [P, I, I, P, P, P]),
             "jkcals_set_init": (I, [P, P]),
             "jkcals_set_init_submodel": (I, [P, I64, I, P]),
             "jkcals_iterate": (I, [P, I, D, P]),
@@ -75,7 +79,8 @@ def lib():
 
 
 EXPORTED = [
-    "jkcals_workspace_bytes", "jkcals_create", "jkcals_create_d", "jkcals_set_init", "jkcals_set_init_submodel", "jkcals_iterate",
+    "jkcals_workspace_bytes", "jkcals_create", "jkcals_create_d", "jkcals_pool_workspace_bytes",
+    "jkcals_create_pool", "jkcals_get_model_stats", "jkcals_get_model_moments", "jkcals_set_init", "jkcals_set_init_submodel", "jkcals_iterate",
     "jkcals_get_factors", "jkcals_get_all_factors", "jkcals_get_block", "jkcals_get_status", "jkcals_get_history", "jkcals_get_jackknife_stats",
     "jkcals_get_local_moments", "jkcals_set_instrument", "jkcals_get_kernel_times", "jkcals_sweep_flops",
     "jkcals_launches_per_sweep", "jkcals_last_error", "jkcals_destroy", "jkcals_mttkrp_scratch_bytes",
@@ -118,7 +123,11 @@ class JKCals:
 
     d > 1 selects delete-d jackknife: submodel p is then GROUP p, leaving
     out mode-0 rows [p d, min(p d + d, I_0)); sub_range indexes groups (default all
-    ceil(I_0/d) of them)."""
+    ceil(I_0/d) of them).
+
+    rank may be a sequence of ranks (R_0, R_1, ...): a multi-model pool (the paper's "All"
+    experiment): submodel id s = m * ceil(I_0/d) + g is model m's group g,
+    all fused into one multi-factor per mode; set_init then takes one factor list per model."""
 
     def __init__(self, T, rank, sub_range=None, device=None, stream=None, hist_cap=None,
                  precision=FP64, dims=None, d=1):
@@ -128,29 +137,35 @@ class JKCals:
         if dims is not None:
             tdims = tuple(int(d) for d in dims)
         self.dims = tuple(int(d) for d in tdims)
-        self.N, self.R = len(self.dims), int(rank)
+        self.pool = not np.isscalar(rank)
+        self.ranks = [int(r) for r in rank] if self.pool else [int(rank)]
+        self.N, self.R = len(self.dims), max(self.ranks)
+        self.nmodels = len(self.ranks)
         if device is None:
             device = flat.device.index if is_dev else torch.cuda.current_device()
         self.device = int(device)
         self.d = int(d)
         self.ngroups = -(-self.dims[0] // self.d) if self.d >= 1 else 0
-        self.sub_begin, self.sub_end = (0, self.ngroups) if sub_range is None else map(int, sub_range)
+        nall = self.nmodels * self.ngroups
+        self.sub_begin, self.sub_end = (0, nall) if sub_range is None else map(int, sub_range)
         self.nsub = self.sub_end - self.sub_begin
         self.hist_cap = int(hist_cap or DEFAULT_MAX_ITERS)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         L = lib()
         d = _i64(self.dims)
-        nbytes = L.jkcals_workspace_bytes(self.N, _p(d), self.R, self.nsub, precision, self.hist_cap, self.device)
+        rk = np.ascontiguousarray(self.ranks, dtype=np.int32)
+        nbytes = L.jkcals_pool_workspace_bytes(self.N, _p(d), self.nmodels, _p(rk), self.d, self.sub_begin,
+                                               self.sub_end, precision, self.hist_cap, self.device)
         if nbytes == 0:
             raise JKCalsError(-1, f"unsupported arguments dims={self.dims} rank={self.R} nsub={self.nsub}")
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{self.device}")
         self._keep = flat
         tptr = flat.data_ptr() if is_dev else flat.ctypes.data
         h = ctypes.c_void_p()
-        st = L.jkcals_create_d(ctypes.byref(h), self.N, _p(d), self.R, self.d, self.sub_begin, self.sub_end,
-                             ctypes.c_void_p(tptr), 1 if is_dev else 0, precision, self.device,
-                             ctypes.c_void_p(self.stream.cuda_stream), ctypes.c_void_p(self.workspace.data_ptr()),
-                             nbytes, self.hist_cap)
+        st = L.jkcals_create_pool(ctypes.byref(h), self.N, _p(d), self.nmodels, _p(rk), self.d, self.sub_begin,
+                                  self.sub_end, ctypes.c_void_p(tptr), 1 if is_dev else 0, precision, self.device,
+                                  ctypes.c_void_p(self.stream.cuda_stream),
+                                  ctypes.c_void_p(self.workspace.data_ptr()), nbytes, self.hist_cap)
         self._h = h
         if st != 0:
             msg = L.jkcals_last_error(h).decode() if h.value else ""
@@ -176,12 +191,21 @@ class JKCals:
 
     # ------------------------------------------------------------------ ABI
     def set_init(self, P):
-        """Warm start from the overall model P = [U_1..U_N] (Alg. 2 alg:jk:model_subsample)."""
-        mats = [np.asfortranarray(np.asarray(p, dtype=np.float64)) for p in P]
-        for n, m in enumerate(mats):
-            if m.shape != (self.dims[n], self.R):
-                raise JKCalsError(-1, f"P[{n}] has shape {m.shape}, expected {(self.dims[n], self.R)}")
-        arr = (ctypes.c_void_p * self.N)(*[m.ctypes.data for m in mats])
+        """Warm start from the overall model P = [U_1..U_N] (Alg. 2 alg:jk:model_subsample); a
+        pool takes [P_model0, P_model1, ...]."""
+        models = P if self.pool else [P]
+        if len(models) != self.nmodels:
+            raise JKCalsError(-1, f"expected {self.nmodels} models, got {len(models)}")
+        mats = []
+        for mi, Pm in enumerate(models):
+            for n, p in enumerate(Pm):
+                m = np.asfortranarray(np.asarray(p, dtype=np.float64))
+                if m.shape != (self.dims[n], self.ranks[mi]):
+                    raise JKCalsError(-1, f"P[{mi}][{n}] has shape {m.shape}, expected "
+                                          f"{(self.dims[n], self.ranks[mi])}")
+                mats.append(m)
+        self._init_keep = mats
+        arr = (ctypes.c_void_p * len(mats))(*[m.ctypes.data for m in mats])
         self._check(lib().jkcals_set_init(self._h, arr))
 
     def set_init_submodel(self, p, mode, U):
@@ -193,16 +217,27 @@ class JKCals:
         self._check(lib().jkcals_iterate(self._h, int(max_iters), float(tol), ctypes.byref(done)))
         return done.value
 
+    def group_of(self, p):
+        return p % self.ngroups
+
+    def model_of(self, p):
+        return p // self.ngroups
+
+    def rank_of(self, p):
+        return self.ranks[p // self.ngroups]
+
     def group_rows(self, p):
-        """Mode-0 rows left out by submodel (group) p."""
-        return min(self.d, self.dims[0] - p * self.d)
+        """Mode-0 rows left out by submodel p (its group g = p mod ceil(I_0/d))."""
+        g = p % self.ngroups
+        return min(self.d, self.dims[0] - g * self.d)
 
     def factors(self, p):
         """Submodel p: ([U_0 ((I_0-|group|) x R, the group's rows dropped), U_1, ...], lambda)."""
-        out, lam = [], np.zeros(self.R)
+        R = self.rank_of(p)
+        out, lam = [], np.zeros(R)
         for n in range(self.N):
             rows = self.dims[n] - self.group_rows(p) if n == 0 else self.dims[n]
-            U = np.zeros((rows, self.R), order="F")
+            U = np.zeros((rows, R), order="F")
             self._check(lib().jkcals_get_factors(self._h, int(p), n, _p(U), _p(lam) if n == self.N - 1 else None))
             out.append(U)
         return out, lam
@@ -211,25 +246,30 @@ class JKCals:
         """Every submodel's mode-`mode` factor at once: array (n_sub, rows, R) (the group's rows
         dropped in mode 0) and lambda (n_sub, R). With delete-d and a ragged last group the
         mode-0 factors come back as a list of (rows_q, R) arrays instead."""
-        lam = np.zeros((self.nsub, self.R))
+        subs = range(self.sub_begin, self.sub_end)
+        R_q = [self.rank_of(p) for p in subs]
         if mode == 0:
-            rows_q = [self.dims[0] - self.group_rows(p) for p in range(self.sub_begin, self.sub_end)]
+            rows_q = [self.dims[0] - self.group_rows(p) for p in subs]
         else:
             rows_q = [self.dims[mode]] * self.nsub
-        flat = np.zeros(sum(rows_q) * self.R)
-        self._check(lib().jkcals_get_all_factors(self._h, int(mode), _p(flat), _p(lam)))
-        if len(set(rows_q)) == 1:
-            U = flat.reshape(self.nsub, self.R, rows_q[0])  # per submodel a column-major rows x R
-            return np.ascontiguousarray(U.transpose(0, 2, 1)), lam
-        out, off = [], 0
-        for r_ in rows_q:
-            out.append(flat[off:off + r_ * self.R].reshape((r_, self.R), order="F"))
-            off += r_ * self.R
+        flat = np.zeros(sum(r * c for r, c in zip(rows_q, R_q)))
+        lamf = np.zeros(sum(R_q))
+        self._check(lib().jkcals_get_all_factors(self._h, int(mode), _p(flat), _p(lamf)))
+        if len(set(rows_q)) == 1 and len(set(R_q)) == 1:
+            R = R_q[0]
+            U = flat.reshape(self.nsub, R, rows_q[0])  # per submodel a column-major rows x R
+            return np.ascontiguousarray(U.transpose(0, 2, 1)), lamf.reshape(self.nsub, R)
+        out, lam, off, lo = [], [], 0, 0
+        for r_, R in zip(rows_q, R_q):
+            out.append(flat[off:off + r_ * R].reshape((r_, R), order="F"))
+            lam.append(lamf[lo:lo + R])
+            off += r_ * R
+            lo += R
         return out, lam
 
     def block(self, p, mode):
         """Submodel p's full fused block of mode `mode` (mode 0 keeps the zero row p)."""
-        U = np.zeros((self.dims[mode], self.R), order="F")
+        U = np.zeros((self.dims[mode], self.rank_of(p)), order="F")
         self._check(lib().jkcals_get_block(self._h, int(p), int(mode), _p(U)))
         return U
 
@@ -245,16 +285,16 @@ class JKCals:
         self._check(lib().jkcals_get_history(self._h, int(p), _p(buf), cap, ctypes.byref(cnt)))
         return buf[: cnt.value]
 
-    def jackknife_stats(self, mode):
-        mean = np.zeros((self.dims[mode], self.R), order="F")
-        std = np.zeros((self.dims[mode], self.R), order="F")
-        self._check(lib().jkcals_get_jackknife_stats(self._h, int(mode), _p(mean), _p(std)))
+    def jackknife_stats(self, mode, model=0):
+        shp = (self.dims[mode], self.ranks[model])
+        mean, std = np.zeros(shp, order="F"), np.zeros(shp, order="F")
+        self._check(lib().jkcals_get_model_stats(self._h, int(model), int(mode), _p(mean), _p(std)))
         return mean, std
 
-    def local_moments(self, mode):
-        shp = (self.dims[mode], self.R)
+    def local_moments(self, mode, model=0):
+        shp = (self.dims[mode], self.ranks[model])
         cnt, mean, m2 = (np.zeros(shp, order="F") for _ in range(3))
-        self._check(lib().jkcals_get_local_moments(self._h, int(mode), _p(cnt), _p(mean), _p(m2)))
+        self._check(lib().jkcals_get_model_moments(self._h, int(model), int(mode), _p(cnt), _p(mean), _p(m2)))
         return cnt, mean, m2
 
     def set_instrument(self, on=True):

@@ -5,4 +5,5 @@ Gramians, no solves): it only draws random planted factors, composes the
 planted tensor T = [[A_1..A_N]] + noise (the input recipe of SURVEY §8d /
 SPEC.md:426) and a warm-start model P. See DESIGN.md "Input recipe".
 """
-from .workloads import CONFIGS, Workload, make_workload, make_tensor, make_warm_start  # noqa: F401
+from .workloads import (CONFIGS, POOLS, PoolWorkload, Workload, make_pool, make_tensor,  # noqa: F401
+                        make_warm_start, make_workload)

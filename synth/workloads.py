@@ -109,3 +109,36 @@ def make_workload(name_or_spec, seed=0, sweeps=None) -> Workload:
     T, A = make_tensor(dims, R_true, eta, kind, seed)
     P = make_warm_start(A, R, seed)
     return Workload(name, tuple(dims), R, sweeps if sweeps is not None else sw, T, P, A)
+
+
+# Multi-model pools (the paper's "All" experiment; Fig. 5's {4,5,6} models,
+# PAPER.md:590-593): name -> (dims, ranks, R_true, eta, kind, sweeps). Every model is warm-started
+# from the planted factors of the SAME tensor (make_warm_start per rank).
+POOLS = {
+    "all_small": ((50, 100, 100), (3, 5, 7, 9), 5, 0.01, "syn", 100),
+    "all_medium": ((50, 200, 200), (3, 5, 7, 9), 5, 0.01, "syn", 100),
+    "eem_all": ((268, 201, 61), (4, 5, 6), 5, 0.02, "eem", 100),
+}
+
+
+@dataclass
+class PoolWorkload:
+    name: str
+    dims: tuple
+    ranks: tuple
+    sweeps: int
+    T: np.ndarray
+    Ps: list               # one warm start (list of (I_n, R_m) arrays) per model
+    A: list
+
+
+def make_pool(name_or_spec, seed=0, sweeps=None) -> PoolWorkload:
+    if isinstance(name_or_spec, str):
+        dims, ranks, R_true, eta, kind, sw = POOLS[name_or_spec]
+        name = name_or_spec
+    else:
+        dims, ranks, R_true, eta, kind, sw = name_or_spec
+        name = "custom"
+    T, A = make_tensor(dims, R_true, eta, kind, seed)
+    Ps = [make_warm_start(A, R, seed) for R in ranks]
+    return PoolWorkload(name, tuple(dims), tuple(ranks), sweeps if sweeps is not None else sw, T, Ps, A)
