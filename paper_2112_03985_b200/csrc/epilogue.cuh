@@ -419,21 +419,14 @@ __device__ __forceinline__ void warp_reduce_all(int nq, int In, double* out, F f
   }
 }
 
+// Body of the fast epilogue for one live block k (submodel `sub`, rank R <= RMAX).
 template <int RMAX>
-__global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
+__device__ __forceinline__ void epi_smem_body(const EpiArgs& a, const int k, const int sub, const int R) {
   constexpr int NQ = RMAX * (RMAX + 1) / 2;  // upper triangle of V^T V
-  const int k = blockIdx.x;
 #ifdef JK_EPI_PROF
   __shared__ unsigned long long epi_ts_[16];
 #endif
-  EPI_PROBE(0);
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the MTTKRP grid has completed
-  asm volatile("griddepcontrol.launch_dependents;\n" :::);
-  EPI_PROBE(1);
-  if (a.n == 0 && k == 0 && threadIdx.x == 0) *a.active_count = 0;  // per-sweep counter reset
-  const int sub = a.blk2sub[k];
-  if (!a.active[sub]) return;  // frozen (converged or failed)
-  const int R = a.subR ? a.subR[sub] : a.R, Rs = a.R, n = a.n, N = a.N, tid = threadIdx.x, In = a.In;
+  const int Rs = a.R, n = a.n, N = a.N, tid = threadIdx.x, In = a.In;
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int NW = kEpi2Threads / 32;
   const bool last = (n == N - 1);
@@ -632,6 +625,39 @@ __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
   }
   EPI_PROBE(7);
   EPI_PROBE_DUMP();
+}
+
+template <int RMAX>
+__global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
+  const int k = blockIdx.x;
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the MTTKRP grid has completed
+  asm volatile("griddepcontrol.launch_dependents;\n" :::);
+  if (a.n == 0 && k == 0 && threadIdx.x == 0) *a.active_count = 0;  // per-sweep counter reset
+  const int sub = a.blk2sub[k];
+  if (!a.active[sub]) return;  // frozen (converged or failed)
+  epi_smem_body<RMAX>(a, k, sub, a.subR ? a.subR[sub] : a.R);
+}
+
+// Mixed-rank pool: one launch for every block; each block runs the body instantiated for the
+// smallest rank class that holds its own rank (so an R = 3 block does not pay for R = 9).
+// RMAXC, the class of the pool's largest rank, bounds the branches compiled in (and so the
+// kernel's register count: classes <= 8 keep two 256-thread CTAs per SM).
+template <int RMAXC>
+__global__ void __launch_bounds__(kEpi2Threads) als_epilogue_mixed_kernel(EpiArgs a) {
+  const int k = blockIdx.x;
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" :::);
+  if (a.n == 0 && k == 0 && threadIdx.x == 0) *a.active_count = 0;
+  const int sub = a.blk2sub[k];
+  if (!a.active[sub]) return;
+  const int R = a.subR[sub];
+  if (R <= 2) epi_smem_body<2>(a, k, sub, R);
+  else if (RMAXC >= 4 && R <= 4) epi_smem_body<(RMAXC >= 4 ? 4 : 2)>(a, k, sub, R);
+  else if (RMAXC >= 6 && R <= 6) epi_smem_body<(RMAXC >= 6 ? 6 : 2)>(a, k, sub, R);
+  else if (RMAXC >= 8 && R <= 8) epi_smem_body<(RMAXC >= 8 ? 8 : 2)>(a, k, sub, R);
+  else if (RMAXC >= 10 && R <= 10) epi_smem_body<(RMAXC >= 10 ? 10 : 2)>(a, k, sub, R);
+  else if (RMAXC >= 12 && R <= 12) epi_smem_body<(RMAXC >= 12 ? 12 : 2)>(a, k, sub, R);
+  else if (RMAXC >= 16) epi_smem_body<(RMAXC >= 16 ? 16 : 2)>(a, k, sub, R);
 }
 
 }  // namespace jk

@@ -607,7 +607,17 @@ void launch_epi(jkcals_t h, const EpiArgs& a, bool pdl) {
   cfg.stream = h->es;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (dyn <= kMaxDyn) {
+  if (dyn <= kMaxDyn && h->mixed) {
+    static unsigned mixed_mask = 0;
+    if (!(mixed_mask & (1u << (h->device & 31)))) {
+      cudaFuncSetAttribute(als_epilogue_mixed_kernel<RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)kMaxDyn);
+      mixed_mask |= 1u << (h->device & 31);
+    }
+    cfg.blockDim = dim3(kEpi2Threads);
+    cfg.dynamicSmemBytes = dyn;
+    cudaLaunchKernelEx(&cfg, als_epilogue_mixed_kernel<RMAX>, a);
+  } else if (dyn <= kMaxDyn) {
     cfg.blockDim = dim3(kEpi2Threads);
     cfg.dynamicSmemBytes = dyn;
     cudaLaunchKernelEx(&cfg, als_epilogue_kernel<RMAX>, a);
@@ -722,6 +732,8 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
   else if (h->R <= 4) launch_epi<4>(h, a, pdl);
   else if (h->R <= 6) launch_epi<6>(h, a, pdl);
   else if (h->R <= 8) launch_epi<8>(h, a, pdl);
+  else if (h->R <= 10) launch_epi<10>(h, a, pdl);
+  else if (h->R <= 12) launch_epi<12>(h, a, pdl);
   else launch_epi<16>(h, a, pdl);
   CKH(h, cudaGetLastError());
   if (timed) CKH(h, cudaEventRecord(h->ev[4 * n + 2], h->es));
