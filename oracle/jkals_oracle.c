@@ -486,3 +486,89 @@ int orc_jackknife_stats(int64_t g, int64_t len, const double *X, double *mean, d
   }
   return 0;
 }
+
+/* ------------------------------------------------------------------ alignment (Alg. 2 line 6)
+ * "permutation and scale adjustment of P_hat_{-p}"; the paper defers the scheme
+ * to its citation, so this follows the reading in DESIGN.md:
+ *   cos_n(r,s) = <Uh_n(:,r), P_n(:,s)> / (||Uh_n(:,r)|| ||P_n(:,s)||)   (0 if a norm is 0), n >= 1
+ *   C(r,s)     = prod_{n>=1} |cos_n(r,s)|
+ *   sigma      = the permutation maximising sum_r C(r, sigma(r)); exhaustive search in
+ *                lexicographic order, the first strict maximum wins (lowest-index tie-break)
+ *   sign_n(r)  = -1 if cos_n(r, sigma(r)) < 0 else +1 (n >= 1); sign_0(r) = prod_{n>=1} sign_n(r)
+ *   out_n(:, sigma(r)) = sign_n(r) Uh_n(:,r) / ||Uh_n(:,r)||                        (n >= 1)
+ *   out_0(:, sigma(r)) = sign_0(r) lam_r prod_{n>=1} ||Uh_n(:,r)|| Uh_0(:,r)
+ * so the model's tensor is unchanged and every non-sampled column has unit norm. */
+static double col_dot(const double *a, const double *b, int64_t I) {
+  double s = 0.0;
+  for (int64_t i = 0; i < I; ++i) s += a[i] * b[i];
+  return s;
+}
+
+static int next_perm(int *a, int n) { /* lexicographic successor; 0 when a is the last */
+  int i = n - 2;
+  while (i >= 0 && a[i] >= a[i + 1]) --i;
+  if (i < 0) return 0;
+  int j = n - 1;
+  while (a[j] <= a[i]) --j;
+  int t = a[i]; a[i] = a[j]; a[j] = t;
+  for (int l = i + 1, r = n - 1; l < r; ++l, --r) { t = a[l]; a[l] = a[r]; a[r] = t; }
+  return 1;
+}
+
+int orc_align(int N, const int64_t *rows, int R, const double *const *Uh, const double *lam,
+              const double *const *P, double *const *out, int *perm, int *sign, double *cong) {
+  if (N < 2 || R < 1 || R > 10) return -1;
+  double *cosv = malloc(sizeof(double) * (size_t)(N * R * R));
+  double *C = malloc(sizeof(double) * (size_t)(R * R));
+  double *nu = malloc(sizeof(double) * (size_t)(N * R));
+  for (int n = 1; n < N; ++n)
+    for (int r = 0; r < R; ++r) {
+      const double *u = Uh[n] + rows[n] * r;
+      nu[n * R + r] = sqrt(col_dot(u, u, rows[n]));
+      for (int s = 0; s < R; ++s) {
+        const double *p = P[n] + rows[n] * s;
+        double np = sqrt(col_dot(p, p, rows[n]));
+        double den = nu[n * R + r] * np;
+        cosv[(n * R + r) * R + s] = den > 0.0 ? col_dot(u, p, rows[n]) / den : 0.0;
+      }
+    }
+  for (int r = 0; r < R; ++r)
+    for (int s = 0; s < R; ++s) {
+      double c = 1.0;
+      for (int n = 1; n < N; ++n) c *= fabs(cosv[(n * R + r) * R + s]);
+      C[r * R + s] = c;
+    }
+  int a[16], best[16];
+  for (int r = 0; r < R; ++r) a[r] = best[r] = r;
+  double bestv = -1.0;
+  do {
+    double v = 0.0;
+    for (int r = 0; r < R; ++r) v += C[r * R + a[r]];
+    if (v > bestv) {
+      bestv = v;
+      memcpy(best, a, sizeof(int) * (size_t)R);
+    }
+  } while (next_perm(a, R));
+  for (int r = 0; r < R; ++r) {
+    const int s = best[r];
+    perm[r] = s;
+    cong[s] = C[r * R + s];
+    int s0 = 1;
+    double scale = lam ? lam[r] : 1.0;
+    for (int n = 1; n < N; ++n) {
+      int sg = cosv[(n * R + r) * R + s] < 0.0 ? -1 : 1;
+      sign[n * R + r] = sg;
+      s0 *= sg;
+      double nr = nu[n * R + r];
+      scale *= nr;
+      for (int64_t i = 0; i < rows[n]; ++i)
+        out[n][i + rows[n] * s] = nr > 0.0 ? sg * Uh[n][i + rows[n] * r] / nr : Uh[n][i + rows[n] * r];
+    }
+    sign[r] = s0;
+    for (int64_t i = 0; i < rows[0]; ++i) out[0][i + rows[0] * s] = s0 * scale * Uh[0][i + rows[0] * r];
+  }
+  free(cosv);
+  free(C);
+  free(nu);
+  return 0;
+}

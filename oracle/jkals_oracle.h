@@ -94,6 +94,18 @@ int orc_jk_als_d(int N, const int64_t *dims, const double *T, int R, const doubl
 void orc_remove_slices(int N, const int64_t *dims, const double *T, int mode, int64_t p0, int64_t p1,
                        double *out);
 
+/* Alignment of one fitted submodel to the reference model (Alg. 2 alg:jk:perm_scale, PAPER.md:333;
+ * scheme: DESIGN.md reading A12): congruence C(r,s) = prod_{n>=1} |cos_n(r,s)|,
+ * sigma maximising sum_r C(r, sigma(r)) by exhaustive lexicographic search (R <= 10), signs so
+ * that every cos_n(r, sigma(r)) >= 0 (n >= 1) with the compensating flip in mode 0, unit
+ * columns in modes >= 1 and lam_r (and the removed norms) absorbed into mode 0.
+ * rows[n]: rows of Uh[n] / out[n] (P[n] has rows[n] rows for n >= 1; P[0] unused);
+ * lam may be NULL (ones). Outputs: out[n] column-major rows[n] x R, perm[r] = sigma(r),
+ * sign[n*R + r] (n = 0 the compensating sign), cong[sigma(r)] = C(r, sigma(r)).
+ * Returns -1 on bad arguments. */
+int orc_align(int N, const int64_t *rows, int R, const double *const *Uh, const double *lam,
+              const double *const *P, double *const *out, int *perm, int *sign, double *cong);
+
 /* Jackknife mean and standard error over g submodels (alg:jk:std;
  * estimator reading SURVEY §8c A11): X is g blocks of len doubles;
  * std = sqrt(((g-1)/g) * sum_p (X_p - mean)^2). Returns -1 if g < 2. */

@@ -59,6 +59,7 @@ def lib():
             "orc_jk_als": (I, [I, P, P, I, P, P, I64, I, D, I, P, P, P, P, P]),
             "orc_jk_als_d": (I, [I, P, P, I, P, I64, P, I64, I, D, I, P, P, P, P, P]),
             "orc_remove_slices": (None, [I, P, P, I, I64, I64, P]),
+            "orc_align": (I, [I, P, I, P, P, P, P, P, P, P]),
             "orc_jackknife_stats": (I, [I64, I64, P, P, P]),
         }
         for name, (res, args) in sig.items():
@@ -303,3 +304,60 @@ def jackknife_stats(X):
     if rc != 0:
         raise ValueError("jackknife stats need g >= 2")
     return mean.reshape(X.shape[1:]), std.reshape(X.shape[1:])
+
+
+def align(Uh, lam, P):
+    """Alg. 2 alg:jk:perm_scale with DESIGN.md reading A12: returns
+    (aligned factors, perm (R,), sign (N, R), congruence (R,))."""
+    Uh = [_f64(u) for u in Uh]
+    P = [_f64(p) for p in P]
+    N, R = len(Uh), Uh[0].shape[1]
+    rows = np.ascontiguousarray([u.shape[0] for u in Uh], dtype=np.int64)
+    out = [np.zeros(u.shape, order="F") for u in Uh]
+    perm = np.zeros(R, dtype=np.int32)
+    sign = np.zeros((N, R), dtype=np.int32)
+    cong = np.zeros(R)
+    lp = None
+    if lam is not None:
+        lam = np.ascontiguousarray(lam, dtype=np.float64)
+        lp = _p(lam)
+    rc = lib().orc_align(N, _p(rows), R, _ptr_array(Uh), lp, _ptr_array(P), _ptr_array(out), _p(perm),
+                         _p(sign), _p(cong))
+    if rc != 0:
+        raise ValueError("orc_align rejected its arguments")
+    return out, perm, sign, cong
+
+
+def mode0_full(U0, group, I0):
+    """A submodel's mode-0 factor ((I0 - |group|) x R) re-indexed to the I0 global rows, the
+    group's rows NaN (absent)."""
+    R = U0.shape[1]
+    out = np.full((I0, R), np.nan)
+    keep = [i for i in range(I0) if i not in set(group)]
+    out[keep] = U0
+    return out
+
+
+def present_stats(X):
+    """Jackknife mean and SE per element over the submodels in which the element is present
+    (X: (g, ...) with NaN = absent; reading A20 for the sampled mode):
+    g_e = present count, std = sqrt(((g_e - 1)/g_e) sum (x - mean)^2); elements with g_e < 2
+    get std = 0 (and mean = the value, or 0 if absent everywhere)."""
+    X = np.asarray(X, dtype=np.float64)
+    g = X.shape[0]
+    flat = X.reshape(g, -1)
+    mean = np.zeros(flat.shape[1])
+    std = np.zeros(flat.shape[1])
+    cnt = np.zeros(flat.shape[1])
+    for e in range(flat.shape[1]):
+        vals = [flat[q, e] for q in range(g) if not np.isnan(flat[q, e])]
+        cnt[e] = len(vals)
+        if not vals:
+            continue
+        mu = sum(vals) / len(vals)
+        mean[e] = mu
+        if len(vals) >= 2:
+            ss = sum((v - mu) * (v - mu) for v in vals)
+            std[e] = np.sqrt(((len(vals) - 1) / len(vals)) * ss)
+    shp = X.shape[1:]
+    return mean.reshape(shp), std.reshape(shp), cnt.reshape(shp)

@@ -415,3 +415,102 @@ def test_delete_d_jk_cals_equals_jk_als(d):
         for n in (1, 2):
             assert np.allclose(U[q][n], a[n], rtol=1e-10, atol=1e-12)
         assert np.allclose(errs[q], res.history(q), rtol=1e-9)
+
+
+# ---------------------------------------------------------------- alignment (Alg. 2 line 6)
+def _recon(U, lam=None):
+    return compose([u * (lam if (lam is not None and k == 0) else 1.0) for k, u in enumerate(U)])
+
+
+def _unit(U):
+    return [u / np.linalg.norm(u, axis=0) for u in U]
+
+
+def test_align_recovers_column_permutation():
+    # SPEC.md:361 self-alignment: P_hat = P with columns permuted -> permutation recovered exactly
+    g = rng(31)
+    P = [g.uniform(0, 1, (I, 4)) for I in (7, 6, 5)]
+    pi = np.array([2, 0, 3, 1])              # P_hat column r = P column pi[r]
+    Uh = _unit([p[:, pi] for p in P])
+    lam = np.array([1.5, 2.0, 0.5, 3.0])
+    out, perm, sign, cong = O.align(Uh, lam, P)
+    assert np.array_equal(perm, pi) and np.all(sign == 1)
+    assert np.allclose(cong, 1.0, rtol=0, atol=1e-14)
+    Pu = _unit(P)
+    for n in (1, 2):
+        assert np.allclose(out[n], Pu[n], rtol=0, atol=1e-15)
+    # mode 0 absorbs lambda: column pi[r] of out_0 = lam_r * Uh_0(:, r)
+    for r in range(4):
+        assert np.allclose(out[0][:, pi[r]], lam[r] * Uh[0][:, r], rtol=1e-15)
+
+
+def test_align_sign_flips_restored_model_unchanged():
+    # one column negated in two non-sampled modes -> flips undone, tensor unchanged
+    g = rng(32)
+    P = _unit([g.uniform(0, 1, (I, 3)) for I in (6, 5, 4, 3)])
+    Uh = [p.copy() for p in P]
+    Uh[1][:, 2] *= -1
+    Uh[3][:, 2] *= -1
+    out, perm, sign, cong = O.align(Uh, None, P)
+    assert np.array_equal(perm, [0, 1, 2])
+    assert sign[1, 2] == -1 and sign[3, 2] == -1 and sign[0, 2] == 1 and sign[2, 2] == 1
+    for n in range(4):
+        assert np.allclose(out[n], P[n], rtol=0, atol=1e-15)
+    # an odd number of flips is compensated in mode 0
+    Uh = [p.copy() for p in P]
+    Uh[2][:, 0] *= -1
+    out, _, sign, _ = O.align(Uh, None, P)
+    assert sign[0, 0] == -1 and sign[2, 0] == -1
+    assert np.allclose(out[0][:, 0], -Uh[0][:, 0]) and np.allclose(out[2][:, 0], P[2][:, 0])
+
+
+def test_align_reconstruction_invariant_and_congruent():
+    # alignment never changes the model's tensor (<= 1e-12 relative); afterwards
+    # every non-sampled column has unit norm and non-negative cosine with its reference column
+    g = rng(33)
+    for R in (1, 2, 5, 7):
+        P = [g.uniform(0, 1, (I, R)) for I in (8, 7, 6)]
+        pi = g.permutation(R)
+        Uh = [p[:, pi] + 0.2 * g.standard_normal((p.shape[0], R)) for p in P]
+        Uh[1][:, 0] *= -1
+        lam = g.uniform(0.5, 2, R)
+        out, perm, sign, cong = O.align(Uh, lam, P)
+        T0 = _recon(Uh, lam)
+        assert np.linalg.norm(_recon(out) - T0) <= 1e-12 * np.linalg.norm(T0)
+        for n in (1, 2):
+            assert np.allclose(np.linalg.norm(out[n], axis=0), 1.0, atol=1e-14)
+            assert np.all(np.sum(out[n] * P[n], axis=0) >= 0)
+        assert sorted(perm.tolist()) == list(range(R))
+
+
+def test_align_assignment_matches_scipy():
+    # the exhaustive lexicographic search finds the same optimum as scipy's linear_sum_assignment
+    # (a library routine) on the congruence matrix
+    from scipy.optimize import linear_sum_assignment
+    g = rng(34)
+    for trial in range(10):
+        R = int(g.integers(2, 9))
+        P = [g.standard_normal((I, R)) for I in (5, 9, 8)]
+        Uh = [g.standard_normal((I, R)) for I in (5, 9, 8)]
+        _, perm, _, cong = O.align(Uh, None, P)
+        C = np.ones((R, R))
+        for n in (1, 2):
+            a = Uh[n] / np.linalg.norm(Uh[n], axis=0)
+            b = P[n] / np.linalg.norm(P[n], axis=0)
+            C *= np.abs(a.T @ b)
+        r_, c_ = linear_sum_assignment(C, maximize=True)
+        assert np.isclose(C[r_, c_].sum(), sum(C[r, perm[r]] for r in range(R)), rtol=1e-13)
+        assert np.array_equal(perm, c_[np.argsort(r_)])
+
+
+def test_present_stats():
+    # sampled-mode stats over the submodels in which a row is present (A20):
+    # a row missing from one of g submodels has g-1 contributions; two-point case -> delta
+    X = np.array([[[1.0], [np.nan]], [[3.0], [5.0]], [[np.nan], [7.0]]])
+    m, s, c = O.present_stats(X)
+    assert np.array_equal(c[:, 0], [2, 2])
+    assert np.allclose(m[:, 0], [2.0, 6.0]) and np.allclose(s[:, 0], [1.0, 1.0])
+    Y = rng(35).standard_normal((6, 4, 2))
+    m2, s2, c2 = O.present_stats(Y)
+    mj, sj = O.jackknife_stats(Y)
+    assert np.allclose(m2, mj, rtol=1e-14) and np.allclose(s2, sj, rtol=1e-13) and np.all(c2 == 6)
