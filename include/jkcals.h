@@ -183,6 +183,38 @@ jkcals_status jkcals_get_model_stats(jkcals_t h, int model, int mode, double *me
 jkcals_status jkcals_get_model_moments(jkcals_t h, int model, int mode, double *count, double *mean,
                                        double *m2);
 
+/* Submodel alignment (Alg. 2 alg:jk:perm_scale, "permutation and scale
+ * adjustment"; the scheme is DESIGN.md reading A12 since the paper defers it to its citation):
+ * every local submodel is aligned to its model's reference, the warm start P given to
+ * jkcals_set_init. With cos_n(r,s) the cosine between submodel column r and reference column s
+ * of mode n >= 1, C(r,s) = prod_{n>=1} |cos_n(r,s)|; the permutation sigma maximises
+ * sum_r C(r, sigma(r)) (exhaustive search, lowest lexicographic rank among equal maxima);
+ * column r moves to sigma(r); modes n >= 1 get unit columns with sign(cos_n(r, sigma(r))),
+ * mode 0 the compensating sign times lambda_r (so the model's tensor is unchanged). The result
+ * goes to a separate aligned store (the fitted state is untouched) and stays valid until the
+ * next iterate / set_init / set_init_submodel. Needs every rank <= 10 (E_SHAPE otherwise);
+ * E_STATE before set_init. */
+jkcals_status jkcals_align(jkcals_t h);
+
+/* Alignment of submodel p: perm[r] = sigma(r) (rank values), sign[n*rank + r] the sign applied to
+ * column r of mode n (n = 0: the compensating sign), congruence[sigma(r)] = C(r, sigma(r)).
+ * Any output may be NULL. E_STATE if jkcals_align has not run on the current factors. */
+jkcals_status jkcals_get_alignment(jkcals_t h, int64_t p, int *perm, int *sign, double *congruence);
+
+/* Aligned factors of submodel p in the get_factors layout (mode 0 without its group's rows and
+ * with lambda absorbed; modes >= 1 unit columns). E_STATE as above. */
+jkcals_status jkcals_get_aligned_factors(jkcals_t h, int64_t p, int mode, double *U);
+
+/* Full jackknife statistics of model `model`'s aligned submodels on this handle, any mode
+ * (Alg. 2 alg:jk:std): per element of U_mode (column-major dims[mode] x rank)
+ * count g_e, mean and M2 = sum (x - mean)^2 over the submodels in which the element exists --
+ * all of them for modes >= 1; for the sampled mode 0 those whose left-out group does not
+ * contain the row (reading A20) -- and std = sqrt(((g_e-1)/g_e) M2) (0 if g_e < 2).
+ * The moments merge across shards with Chan's formula. E_STATE as above. */
+jkcals_status jkcals_get_aligned_moments(jkcals_t h, int model, int mode, double *count, double *mean,
+                                         double *m2);
+jkcals_status jkcals_get_aligned_stats(jkcals_t h, int model, int mode, double *mean, double *std);
+
 /* Instrumentation: when on, iterate() launches kernels eagerly (no CUDA graph) bracketed
  * by CUDA events on the handle's stream and accumulates per-mode kernel times. */
 jkcals_status jkcals_set_instrument(jkcals_t h, int on);

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "../../include/jkcals.h"
+#include "align.cuh"
 #include "aux_kernels.cuh"
 #include "epilogue.cuh"
 #include "mttkrp.cuh"
@@ -372,7 +373,7 @@ struct Layout {
 struct Offsets {
   size_t T, T32hi, T32lo, T1hi, T1lo, U[2][kMaxModes], Ures, parts, tinfo[kMaxModes], gram, lambda, normT2p, fit, fit_prev, err, hist,
       slice, slice_part, stage, iters, flags, active, blk2sub, map, pglob, misc, srcoff, srcld, subR, subRc, blkcol,
-      dstoff;
+      dstoff, pref[kMaxModes], aln, aperm, asign, acong, asrc, asld, srcpg;
   int64_t parts_cap;
   int tiles_cap;
   int slice_nb;
@@ -439,6 +440,15 @@ bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_c
   o->subRc = L.take(nsub * 4);
   o->blkcol = L.take(nsub * 4);
   o->dstoff = L.take(nsub * 8);
+  // the pool's reference models (warm starts): mode n is col-major I_n x sumRm
+  for (int k = 0; k < N; ++k) o->pref[k] = L.take(dims[k] * std::max<int64_t>(sumRm, R) * 8);
+  o->aln = L.take(nsub * sumI * R * 8);  // aligned factors (NEXT #3), slot layout as Ures
+  o->aperm = L.take(nsub * R * 4);
+  o->asign = L.take(nsub * N * R * 4);
+  o->acong = L.take(nsub * R * 8);
+  o->asrc = L.take(nsub * N * 8);
+  o->asld = L.take(nsub * N * 8);
+  o->srcpg = L.take(nsub * 8);
   o->misc = L.take(256);  // [0] normT2 (double), [8] tol (double), [16] active_count (int)
   o->total = L.off + kAlign;  // slack for re-alignment of the caller's pointer
   return true;
@@ -474,6 +484,8 @@ struct jkcals_s {
   std::vector<int> h_subR, h_subRc, h_model;  // per local submodel: rank, rank prefix of its model, model
   std::vector<int64_t> h_group;        // per local submodel: group index g
   std::vector<int> h_blkcol;           // per live block: first column
+  int64_t sumRm = 0;                   // sum of the pool's model ranks (reference store width)
+  bool aligned = false;                // the aligned store holds jkcals_align's result
   int nsub = 0, K = 0, C = 0;
   int64_t ldu = 0, P = 0, I0p = 0;
   int hist_cap = 1;
@@ -955,6 +967,7 @@ jkcals_status jkcals_create_pool(jkcals_t* out, int ndims, const int64_t* dims, 
   h->ngroups = pg0.ngroups;
   h->nmodels = nmodels;
   h->ranks.assign(ranks, ranks + nmodels);
+  h->sumRm = pg0.sumRm;
   h->nsub = (int)(sub_end - sub_begin);
   std::vector<int> rc(nmodels, 0);
   for (int m = 1; m < nmodels; ++m) rc[m] = rc[m - 1] + ranks[m - 1];
@@ -1080,10 +1093,11 @@ jkcals_status jkcals_set_init(jkcals_t h, const double* const* P) {
   jkcals_status st = set_blocks(h, b2s);
   if (st != JKCALS_OK) return st;
   h->h_stored.assign(h->nsub, 0);
-  double* stage = h->ptr<double>(h->off.stage);
   for (int n = 0; n < h->N; ++n) {
     const int I = (int)h->dims[n];
-    // stage = [P_n(model 0) | P_n(model 1) | ...], column-major I x sum_m R_m
+    // reference store = [P_n(model 0) | P_n(model 1) | ...], column-major I x sum_m R_m; kept for
+    // the alignment (Alg. 2 aligns every submodel to P)
+    double* stage = h->ptr<double>(h->off.pref[n]);
     int64_t c0 = 0;
     for (int m = 0; m < h->nmodels; ++m) {
       CKH(h, cudaMemcpyAsync(stage + (int64_t)I * c0, P[m * h->N + n], sizeof(double) * I * h->ranks[m],
@@ -1097,7 +1111,6 @@ jkcals_status jkcals_set_init(jkcals_t h, const double* const* P) {
         h->ptr<int>(h->off.blkcol), h->ptr<int>(h->off.subR), h->ptr<int>(h->off.subRc),
         h->ptr<int64_t>(h->off.pglob), (int)h->d);
     CKH(h, cudaGetLastError());
-    CKH(h, cudaStreamSynchronize(h->stream));  // stage is reused by the next mode
   }
   st = compute_grams(h);
   if (st != JKCALS_OK) return st;
@@ -1110,9 +1123,10 @@ jkcals_status jkcals_set_init(jkcals_t h, const double* const* P) {
     st = replan(h);
     if (st != JKCALS_OK) return st;
   }
-  CKH(h, cudaStreamSynchronize(h->stream));
+  CKH(h, cudaStreamSynchronize(h->stream));  // the host P arrays are the copy sources
   h->inited = true;
   h->ran = false;
+  h->aligned = false;
   return JKCALS_OK;
 }
 
@@ -1123,6 +1137,7 @@ jkcals_status jkcals_set_init_submodel(jkcals_t h, int64_t p, int mode, const do
   const int sub = (int)(p - h->sub_begin);
   const int blk = block_of(h, sub);
   if (blk < 0) return fail(h, JKCALS_E_STATE, "submodel %lld was compacted out", (long long)p);
+  h->aligned = false;
   const int I = (int)h->dims[mode];
   const int R = h->h_subR[sub];
   const int64_t g = h->h_group[sub];
@@ -1146,6 +1161,7 @@ jkcals_status jkcals_iterate(jkcals_t h, int max_iters, double tol, int* sweeps_
   if (sweeps_done) *sweeps_done = 0;
   if (!h->inited) return fail(h, JKCALS_E_STATE, "iterate before set_init");
   DeviceGuard dg(h->device);
+  h->aligned = false;
   h->tol_host = tol;
   CKH(h, cudaMemcpyAsync(h->ws + h->off.misc + 8, &h->tol_host, sizeof(double), cudaMemcpyHostToDevice, h->stream));
   int it = 0;
@@ -1389,6 +1405,142 @@ jkcals_status jkcals_get_model_stats(jkcals_t h, int model, int mode, double* me
   const double g = IR > 0 ? cnt[0] : 0.0;
   if (g < 2) return fail(h, JKCALS_E_ARG, "jackknife statistics need >= 2 submodels of the model");
   for (int64_t e = 0; e < IR; ++e) std_out[e] = std::sqrt(((g - 1.0) / g) * m2[e]);
+  return JKCALS_OK;
+}
+
+// ---------------------------------------------------------------- alignment (NEXT #3)
+jkcals_status jkcals_align(jkcals_t h) {
+  if (!h) return JKCALS_E_ARG;
+  if (!h->inited) return fail(h, JKCALS_E_STATE, "no model yet");
+  for (int m = 0; m < h->nmodels; ++m)
+    if (h->ranks[m] > kAlignRMax) return fail(h, JKCALS_E_SHAPE, "alignment supports rank <= %d", kAlignRMax);
+  DeviceGuard dg(h->device);
+  std::vector<int64_t> off((size_t)h->nsub * h->N), ld((size_t)h->nsub * h->N);
+  for (int q = 0; q < h->nsub; ++q)
+    for (int n = 0; n < h->N; ++n) {
+      const double* src;
+      int64_t l;
+      int sub;
+      jkcals_status st = locate(h, h->sub_begin + q, n, &src, &l, &sub);
+      if (st != JKCALS_OK) return st;
+      off[(size_t)q * h->N + n] = src - reinterpret_cast<const double*>(h->ws);
+      ld[(size_t)q * h->N + n] = l;
+    }
+  CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.asrc), off.data(), 8 * off.size(), cudaMemcpyHostToDevice,
+                         h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.asld), ld.data(), 8 * ld.size(), cudaMemcpyHostToDevice, h->stream));
+  AlignArgs a = {};
+  a.base = reinterpret_cast<const double*>(h->ws);
+  a.asrc = h->ptr<int64_t>(h->off.asrc);
+  a.asld = h->ptr<int64_t>(h->off.asld);
+  a.lambda = h->ptr<double>(h->off.lambda);
+  a.subR = h->ptr<int>(h->off.subR);
+  a.subRc = h->ptr<int>(h->off.subRc);
+  for (int n = 0; n < h->N; ++n) {
+    a.pref[n] = h->ptr<double>(h->off.pref[n]);
+    a.dims[n] = h->dims[n];
+  }
+  a.N = h->N;
+  a.Rs = h->R;
+  a.sumI = sum_dims(h);
+  a.aln = h->ptr<double>(h->off.aln);
+  a.perm = h->ptr<int>(h->off.aperm);
+  a.sign = h->ptr<int>(h->off.asign);
+  a.cong = h->ptr<double>(h->off.acong);
+  align_kernel<<<h->nsub, kAlignThreads, 0, h->stream>>>(a);
+  CKH(h, cudaGetLastError());
+  CKH(h, cudaStreamSynchronize(h->stream));  // off/ld are host temporaries
+  h->aligned = true;
+  return JKCALS_OK;
+}
+
+jkcals_status jkcals_get_alignment(jkcals_t h, int64_t p, int* perm, int* sign, double* congruence) {
+  if (!h || p < h->sub_begin || p >= h->sub_end) return JKCALS_E_ARG;
+  if (!h->aligned) return fail(h, JKCALS_E_STATE, "jkcals_align has not run on the current factors");
+  DeviceGuard dg(h->device);
+  const int sub = (int)(p - h->sub_begin), R = h->h_subR[sub];
+  if (perm)
+    CKH(h, cudaMemcpyAsync(perm, h->ptr<int>(h->off.aperm) + (int64_t)sub * h->R, 4 * R, cudaMemcpyDeviceToHost,
+                           h->stream));
+  if (congruence)
+    CKH(h, cudaMemcpyAsync(congruence, h->ptr<double>(h->off.acong) + (int64_t)sub * h->R, 8 * R,
+                           cudaMemcpyDeviceToHost, h->stream));
+  if (sign)
+    for (int n = 0; n < h->N; ++n)
+      CKH(h, cudaMemcpyAsync(sign + (int64_t)n * R, h->ptr<int>(h->off.asign) + ((int64_t)sub * h->N + n) * h->R,
+                             4 * R, cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaStreamSynchronize(h->stream));
+  return JKCALS_OK;
+}
+
+// aligned block of local submodel `sub`, mode n: row-major I_n x R_sub
+static const double* aligned_block(jkcals_t h, int sub, int mode) {
+  int64_t o = 0;
+  for (int n = 0; n < mode; ++n) o += h->dims[n] * h->h_subR[sub];
+  return h->ptr<double>(h->off.aln) + (int64_t)sub * sum_dims(h) * h->R + o;
+}
+
+jkcals_status jkcals_get_aligned_factors(jkcals_t h, int64_t p, int mode, double* U) {
+  if (!h || !U || mode < 0 || mode >= h->N || p < h->sub_begin || p >= h->sub_end) return JKCALS_E_ARG;
+  if (!h->aligned) return fail(h, JKCALS_E_STATE, "jkcals_align has not run on the current factors");
+  DeviceGuard dg(h->device);
+  const int sub = (int)(p - h->sub_begin), R = h->h_subR[sub];
+  const int I = (int)h->dims[mode];
+  const int cnt = mode == 0 ? (int)group_rows(h, h->h_group[sub]) : 0;
+  double* stage = h->ptr<double>(h->off.stage);
+  extract_kernel<<<(int)cdiv((int64_t)(I - cnt) * R, 256), 256, 0, h->stream>>>(
+      aligned_block(h, sub, mode), R, I, R, mode == 0 ? h->h_group[sub] * h->d : -1, cnt, stage);
+  CKH(h, cudaGetLastError());
+  CKH(h, cudaMemcpyAsync(U, stage, sizeof(double) * (I - cnt) * R, cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaStreamSynchronize(h->stream));
+  return JKCALS_OK;
+}
+
+jkcals_status jkcals_get_aligned_moments(jkcals_t h, int model, int mode, double* count, double* mean, double* m2) {
+  if (!h || !count || !mean || !m2 || mode < 0 || mode >= h->N || model < 0 || model >= h->nmodels)
+    return JKCALS_E_ARG;
+  if (!h->aligned) return fail(h, JKCALS_E_STATE, "jkcals_align has not run on the current factors");
+  DeviceGuard dg(h->device);
+  std::vector<int64_t> off, ld, pg;
+  for (int q = 0; q < h->nsub; ++q)
+    if (h->h_model[q] == model) {
+      off.push_back(aligned_block(h, q, mode) - reinterpret_cast<const double*>(h->ws));
+      ld.push_back(h->h_subR[q]);
+      pg.push_back(h->h_group[q] * h->d);
+    }
+  const int I = (int)h->dims[mode], R = h->ranks[model];
+  const int64_t IR = (int64_t)I * R;
+  const int ns = (int)off.size();
+  if (ns == 0) {
+    for (int64_t e = 0; e < IR; ++e) count[e] = mean[e] = m2[e] = 0.0;
+    return JKCALS_OK;
+  }
+  CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.srcoff), off.data(), 8 * ns, cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.srcld), ld.data(), 8 * ns, cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.srcpg), pg.data(), 8 * ns, cudaMemcpyHostToDevice, h->stream));
+  double* stage = h->ptr<double>(h->off.stage);
+  moments_present_kernel<<<(int)cdiv(IR, 128), 128, 0, h->stream>>>(
+      reinterpret_cast<const double*>(h->ws), h->ptr<int64_t>(h->off.srcoff), h->ptr<int64_t>(h->off.srcld),
+      h->ptr<int64_t>(h->off.srcpg), mode == 0 ? 1 : 0, (int)h->d, ns, I, R, stage, stage + IR, stage + 2 * IR);
+  CKH(h, cudaGetLastError());
+  CKH(h, cudaMemcpyAsync(count, stage, 8 * IR, cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaMemcpyAsync(mean, stage + IR, 8 * IR, cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaMemcpyAsync(m2, stage + 2 * IR, 8 * IR, cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaStreamSynchronize(h->stream));
+  return JKCALS_OK;
+}
+
+jkcals_status jkcals_get_aligned_stats(jkcals_t h, int model, int mode, double* mean, double* std_out) {
+  if (!h || !mean || !std_out || mode < 0 || mode >= h->N || model < 0 || model >= h->nmodels)
+    return JKCALS_E_ARG;
+  const int64_t IR = h->dims[mode] * h->ranks[model];
+  std::vector<double> cnt(IR), m2(IR);
+  jkcals_status st = jkcals_get_aligned_moments(h, model, mode, cnt.data(), mean, m2.data());
+  if (st != JKCALS_OK) return st;
+  for (int64_t e = 0; e < IR; ++e) {
+    const double g = cnt[e];
+    std_out[e] = g >= 2.0 ? std::sqrt(((g - 1.0) / g) * m2[e]) : 0.0;
+  }
   return JKCALS_OK;
 }
 

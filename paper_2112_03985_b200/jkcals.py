@@ -50,6 +50,11 @@ def lib():
             "jkcals_create_pool": (I, [P, I, P, I, P, I64, I64, I64, P, I, I, I, P, P, SZ, I]),
             "jkcals_get_model_stats": (I, [P, I, I, P, P]),
             "jkcals_get_model_moments": (I, [P, I, I, P, P, P]),
+            "jkcals_align": (I, [P]),
+            "jkcals_get_alignment": (I, [P, I64, P, P, P]),
+            "jkcals_get_aligned_factors": (I, [P, I64, I, P]),
+            "jkcals_get_aligned_moments": (I, [P, I, I, P, P, P]),
+            "jkcals_get_aligned_stats": (I, [P, I, I, P, P]),
             "jkcals_set_init": (I, [P, P]),
             "jkcals_set_init_submodel": (I, [P, I64, I, P]),
             "jkcals_iterate": (I, [P, I, D, P]),
@@ -80,7 +85,9 @@ def lib():
 
 EXPORTED = [
     "jkcals_workspace_bytes", "jkcals_create", "jkcals_create_d", "jkcals_pool_workspace_bytes",
-    "jkcals_create_pool", "jkcals_get_model_stats", "jkcals_get_model_moments", "jkcals_set_init", "jkcals_set_init_submodel", "jkcals_iterate",
+    "jkcals_create_pool", "jkcals_get_model_stats", "jkcals_get_model_moments", "jkcals_align",
+    "jkcals_get_alignment", "jkcals_get_aligned_factors", "jkcals_get_aligned_moments", "jkcals_get_aligned_stats",
+    "jkcals_set_init", "jkcals_set_init_submodel", "jkcals_iterate",
     "jkcals_get_factors", "jkcals_get_all_factors", "jkcals_get_block", "jkcals_get_status", "jkcals_get_history", "jkcals_get_jackknife_stats",
     "jkcals_get_local_moments", "jkcals_set_instrument", "jkcals_get_kernel_times", "jkcals_sweep_flops",
     "jkcals_launches_per_sweep", "jkcals_last_error", "jkcals_destroy", "jkcals_mttkrp_scratch_bytes",
@@ -296,6 +303,39 @@ class JKCals:
         cnt, mean, m2 = (np.zeros(shp, order="F") for _ in range(3))
         self._check(lib().jkcals_get_model_moments(self._h, int(model), int(mode), _p(cnt), _p(mean), _p(m2)))
         return cnt, mean, m2
+
+    # ------------------------------------------------------------------ alignment (NEXT #3)
+    def align(self):
+        """Align every submodel to its model's warm start (Alg. 2 alg:jk:perm_scale)."""
+        self._check(lib().jkcals_align(self._h))
+
+    def alignment(self, p):
+        R = self.rank_of(p)
+        perm, sign, cong = np.zeros(R, dtype=np.int32), np.zeros((self.N, R), dtype=np.int32), np.zeros(R)
+        self._check(lib().jkcals_get_alignment(self._h, int(p), _p(perm), _p(sign), _p(cong)))
+        return perm, sign, cong
+
+    def aligned_factors(self, p):
+        R = self.rank_of(p)
+        out = []
+        for n in range(self.N):
+            rows = self.dims[n] - self.group_rows(p) if n == 0 else self.dims[n]
+            U = np.zeros((rows, R), order="F")
+            self._check(lib().jkcals_get_aligned_factors(self._h, int(p), n, _p(U)))
+            out.append(U)
+        return out
+
+    def aligned_moments(self, mode, model=0):
+        shp = (self.dims[mode], self.ranks[model])
+        cnt, mean, m2 = (np.zeros(shp, order="F") for _ in range(3))
+        self._check(lib().jkcals_get_aligned_moments(self._h, int(model), int(mode), _p(cnt), _p(mean), _p(m2)))
+        return cnt, mean, m2
+
+    def aligned_stats(self, mode, model=0):
+        shp = (self.dims[mode], self.ranks[model])
+        mean, std = np.zeros(shp, order="F"), np.zeros(shp, order="F")
+        self._check(lib().jkcals_get_aligned_stats(self._h, int(model), int(mode), _p(mean), _p(std)))
+        return mean, std
 
     def set_instrument(self, on=True):
         self._check(lib().jkcals_set_instrument(self._h, 1 if on else 0))
