@@ -114,7 +114,11 @@ jkcals_status jkcals_create_d(jkcals_t *out, int ndims, const int64_t *dims, int
  * model m = s / ceil(I_0/d) and its group g = s % ceil(I_0/d) (d as in jkcals_create_d);
  * [sub_begin, sub_end) selects a shard of ids. Every `p` argument of the calls below is such an
  * id; factors of submodel s are rows x R_m. ranks[m] in [1, 16]. jkcals_create_d is the pool
- * with nmodels = 1. Errors as jkcals_create_d. */
+ * with nmodels = 1. Errors as jkcals_create_d.
+ * d = 0 selects plain CALS (§3.3): nothing is left out, each
+ * id s in [0, nmodels) is one model fitted to the full tensor from its own initial model (e.g.
+ * K random starts of one rank, or models of ranks R_m), with error ||T||^2 + ... and
+ * convergence per model; the same fused sweep (a single padded-free multi-factor) serves all. */
 size_t jkcals_pool_workspace_bytes(int ndims, const int64_t *dims, int nmodels, const int *ranks,
                                    int64_t d, int64_t sub_begin, int64_t sub_end,
                                    jkcals_precision prec, int hist_cap, int device);

@@ -6,5 +6,5 @@ arguments (jkcals.py), plans shards and merges statistics across ranks (dist.py)
 counts the paper's flops (flops.py).
 """
 from .flops import jk_als_mttkrp_flops, jk_cals_mttkrp_flops, mttkrp_flops  # noqa: F401
-from .jkcals import (DEFAULT_MAX_ITERS, DEFAULT_TOL, JKCals, JKCalsError, krp, lib,  # noqa: F401
+from .jkcals import (DEFAULT_MAX_ITERS, DEFAULT_TOL, JKCals, JKCalsError, cals, krp, lib,  # noqa: F401
                      mttkrp)

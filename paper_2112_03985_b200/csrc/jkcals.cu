@@ -889,10 +889,11 @@ struct PoolGeo {
 static bool pool_geo(int ndims, const int64_t* dims, int nmodels, const int* ranks, int64_t d, int64_t sub_begin,
                      int64_t sub_end, PoolGeo* g) {
   if (nmodels < 1 || !ranks || !dims || ndims < 3 || ndims > JKCALS_MAX_MODES) return false;
-  if (dims[0] < 2 || d < 1 || (d > 1 && 2 * d > dims[0])) return false;  // d <= I_0 / 2
+  if (dims[0] < 2 || d < 0 || (d > 1 && 2 * d > dims[0])) return false;  // d <= I_0 / 2
   for (int m = 0; m < nmodels; ++m)
     if (ranks[m] < 1 || ranks[m] > 16) return false;
-  g->ngroups = (dims[0] + d - 1) / d;
+  // d = 0: plain CALS (§3.3): one model per id, nothing left out
+  g->ngroups = d == 0 ? 1 : (dims[0] + d - 1) / d;
   if (sub_begin < 0 || sub_end <= sub_begin || sub_end > (int64_t)nmodels * g->ngroups) return false;
   g->Rs = 0;
   g->C = 0;
@@ -938,6 +939,7 @@ jkcals_status jkcals_create(jkcals_t* out, int ndims, const int64_t* dims, int r
 jkcals_status jkcals_create_d(jkcals_t* out, int ndims, const int64_t* dims, int rank, int64_t d, int64_t sub_begin,
                               int64_t sub_end, const double* tensor, int tensor_is_device, jkcals_precision prec,
                               int device, void* cuda_stream, void* workspace, size_t workspace_bytes, int hist_cap) {
+  if (d < 1) return JKCALS_E_ARG;
   return jkcals_create_pool(out, ndims, dims, 1, &rank, d, sub_begin, sub_end, tensor, tensor_is_device, prec,
                             device, cuda_stream, workspace, workspace_bytes, hist_cap);
 }

@@ -152,7 +152,8 @@ class JKCals:
             device = flat.device.index if is_dev else torch.cuda.current_device()
         self.device = int(device)
         self.d = int(d)
-        self.ngroups = -(-self.dims[0] // self.d) if self.d >= 1 else 0
+        # d = 0: plain CALS (one model per id, nothing left out); d < 0 is rejected by the ABI
+        self.ngroups = -(-self.dims[0] // self.d) if self.d >= 1 else (1 if self.d == 0 else 0)
         nall = self.nmodels * self.ngroups
         self.sub_begin, self.sub_end = (0, nall) if sub_range is None else map(int, sub_range)
         self.nsub = self.sub_end - self.sub_begin
@@ -234,7 +235,7 @@ class JKCals:
         return self.ranks[p // self.ngroups]
 
     def group_rows(self, p):
-        """Mode-0 rows left out by submodel p (its group g = p mod ceil(I_0/d))."""
+        """Mode-0 rows left out by submodel p (its group g = p mod ceil(I_0/d)); 0 for CALS."""
         g = p % self.ngroups
         return min(self.d, self.dims[0] - g * self.d)
 
@@ -350,6 +351,16 @@ class JKCals:
 
     def launches_per_sweep(self):
         return lib().jkcals_launches_per_sweep(self._h)
+
+
+def cals(T, ranks, inits=None, **kw):
+    """Plain CALS (§3.3): len(ranks) CP models of T fitted concurrently in one
+    fused sweep, each from its own initial model (nothing is left out: d = 0). Call
+    set_init(inits) with one factor list per model (or pass inits here)."""
+    h = JKCals(T, list(ranks), d=0, **kw)
+    if inits is not None:
+        h.set_init(inits)
+    return h
 
 
 # ---------------------------------------------------------------------- stand-alone ops
