@@ -128,6 +128,30 @@ jkcals_status jkcals_create_pool(jkcals_t *out, int ndims, const int64_t *dims, 
                                  int device, void *cuda_stream, void *workspace,
                                  size_t workspace_bytes, int hist_cap);
 
+/* Full configuration (all of the above plus spare slots). `spare` extra slots let the handle
+ * later adopt submodels exported by another handle of the same problem (jkcals_import_submodel,
+ * tol-mode load rebalancing across GPUs); with spare > 0 every slot can
+ * hold the largest model rank. A handle has n_slots = (sub_end - sub_begin) + spare slots; the
+ * per-submodel arrays of jkcals_get_status are per SLOT (n_slots long, slot q holds the id
+ * jkcals_get_ids reports, -1 = free; without spare slots and migration slot q holds
+ * sub_begin + q). */
+typedef struct jkcals_config {
+  int ndims;
+  const int64_t *dims;
+  int nmodels;          /* >= 1 */
+  const int *ranks;     /* nmodels ranks in [1, 16] */
+  int64_t d;            /* 0 = plain CALS, 1 = leave-one-out, > 1 = delete-d */
+  int64_t sub_begin, sub_end;
+  int spare;            /* >= 0 */
+  jkcals_precision prec;
+  int hist_cap;         /* >= 1 */
+  int device;
+} jkcals_config;
+size_t jkcals_config_workspace_bytes(const jkcals_config *cfg);
+jkcals_status jkcals_create_config(jkcals_t *out, const jkcals_config *cfg, const double *tensor,
+                                   int tensor_is_device, void *cuda_stream, void *workspace,
+                                   size_t workspace_bytes);
+
 /* Warm start every submodel from the overall model P (Alg. 2 alg:jk:model_subsample,
  * PAPER.md:331; Alg. 3 alg:start-jk-1..alg:stop-jk-1): P[n] is a host
  * column-major dims[n] x rank array; block k of the mode-0 multi-factor gets row p_k
@@ -164,7 +188,8 @@ jkcals_status jkcals_get_all_factors(jkcals_t h, int mode, double *U, double *la
  * row, which must be exactly +0.0/-0.0 after every sweep (alg:cals_jk:multifactor). */
 jkcals_status jkcals_get_block(jkcals_t h, int64_t p, int mode, double *U);
 
-/* Per-submodel status, arrays of n_sub entries in submodel order (any may be NULL). */
+/* Per-submodel status, arrays of n_slots entries in slot order (= n_sub in submodel order for a
+ * handle without spare slots; any may be NULL). */
 jkcals_status jkcals_get_status(jkcals_t h, double *fit, double *err, int *iters, int *flags);
 
 /* Error history of submodel p (oldest first): up to `cap` values; *count = number written. */
@@ -218,6 +243,22 @@ jkcals_status jkcals_get_aligned_factors(jkcals_t h, int64_t p, int mode, double
 jkcals_status jkcals_get_aligned_moments(jkcals_t h, int model, int mode, double *count, double *mean,
                                          double *m2);
 jkcals_status jkcals_get_aligned_stats(jkcals_t h, int model, int mode, double *mean, double *std);
+
+/* Slots and migration (tol-mode load rebalancing across GPUs). A live
+ * (not yet converged-and-stored) submodel's whole ALS state -- its factor blocks (mode 0 with its
+ * zero rows), lambda, cached Gramians, fit / error / iteration count / flags / activity and
+ * error history -- is serialised into a host buffer of jkcals_state_bytes(h, p) bytes by
+ * jkcals_export_submodel, which also removes it from h (its slot becomes free). Importing the
+ * buffer into another handle of the same problem (same tensor, pool, d and hist_cap) with a free
+ * slot continues the fit where it stopped: the sweeps that follow are those the exporting
+ * handle would have run, up to the floating-point summation order of the new fused layout's
+ * split-K partition (rounding-level differences). Errors: E_ARG (unknown id, foreign state, small buffer),
+ * E_STATE (not live / before set_init), E_OOM (no free slot or column room). */
+int jkcals_num_slots(jkcals_t h);
+jkcals_status jkcals_get_ids(jkcals_t h, int64_t *ids);
+size_t jkcals_state_bytes(jkcals_t h, int64_t p);
+jkcals_status jkcals_export_submodel(jkcals_t h, int64_t p, void *buf, size_t bytes);
+jkcals_status jkcals_import_submodel(jkcals_t h, const void *buf, size_t bytes);
 
 /* Instrumentation: when on, iterate() launches kernels eagerly (no CUDA graph) bracketed
  * by CUDA events on the handle's stream and accumulates per-mode kernel times. */

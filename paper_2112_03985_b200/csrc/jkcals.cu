@@ -485,6 +485,10 @@ struct jkcals_s {
   std::vector<int64_t> h_group;        // per local submodel: group index g
   std::vector<int> h_blkcol;           // per live block: first column
   int64_t sumRm = 0;                   // sum of the pool's model ranks (reference store width)
+  // slots: nsub = owned-at-create + spare; h_id[q] = global submodel id held by slot q (-1 free).
+  // Submodels migrate between handles (tol-mode rebalancing) through export / import.
+  std::vector<int64_t> h_id;
+  int spare = 0;
   bool aligned = false;                // the aligned store holds jkcals_align's result
   int nsub = 0, K = 0, C = 0;
   int64_t ldu = 0, P = 0, I0p = 0;
@@ -828,33 +832,17 @@ int64_t sum_dims(jkcals_t h) {
   return sumI;
 }
 
-// (a8) compact: store converged live blocks, gather the active ones to the front.
-jkcals_status compact(jkcals_t h) {
-  std::vector<int> act(h->nsub);
-  CKH(h, cudaMemcpyAsync(act.data(), h->ptr<int>(h->off.active), sizeof(int) * h->nsub, cudaMemcpyDeviceToHost,
-                         h->stream));
-  CKH(h, cudaStreamSynchronize(h->stream));
-  const int64_t sumI = sum_dims(h);
-  std::vector<int> keep, colmap;
-  for (int k = 0; k < h->K; ++k) {
-    const int sub = h->h_blk2sub[k], R = h->h_subR[sub], col = h->h_blkcol[k];
-    if (act[sub]) {
-      keep.push_back(sub);
-      for (int r = 0; r < R; ++r) colmap.push_back(col + r);
-    } else if (!h->h_stored[sub]) {
-      int64_t o = 0;
-      for (int n = 0; n < h->N; ++n) {
-        int I = (int)h->dims[n];
-        double* dst = h->ptr<double>(h->off.Ures) + (int64_t)sub * sumI * h->R + o;
-        store_block_kernel<<<(int)cdiv((int64_t)I * R, 256), 256, 0, h->stream>>>(h->U(n), I, h->ldu, R, col, dst);
-        CKH(h, cudaGetLastError());
-        o += (int64_t)I * R;
-      }
-      h->h_stored[sub] = 1;
-    }
+// gather the blocks of `keep` (in that order, all currently live) to the front of the other
+// multi-factor buffer set and re-plan
+jkcals_status relayout(jkcals_t h, const std::vector<int>& keep) {
+  std::vector<int> colmap;
+  for (int sub : keep) {
+    int k = -1;
+    for (int j = 0; j < h->K; ++j)
+      if (h->h_blk2sub[j] == sub) k = j;
+    if (k < 0) return fail(h, JKCALS_E_STATE, "internal: slot %d is not live", sub);
+    for (int r = 0; r < h->h_subR[sub]; ++r) colmap.push_back(h->h_blkcol[k] + r);
   }
-  const int Knew = (int)keep.size();
-  if (Knew == h->K) return JKCALS_OK;
   const int Cnew = (int)colmap.size();
   if (Cnew > 0)
     CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.map), colmap.data(), sizeof(int) * Cnew, cudaMemcpyHostToDevice,
@@ -869,8 +857,45 @@ jkcals_status compact(jkcals_t h) {
   jkcals_status st = set_blocks(h, keep);  // synchronises (colmap is a host temporary)
   if (st != JKCALS_OK) return st;
   h->cur = other;
-  if (Knew > 0) return replan(h);
+  if (!keep.empty()) return replan(h);
   return JKCALS_OK;
+}
+
+// (a8) compact: store converged live blocks, gather the active ones to the front.
+jkcals_status compact(jkcals_t h) {
+  std::vector<int> act(h->nsub);
+  CKH(h, cudaMemcpyAsync(act.data(), h->ptr<int>(h->off.active), sizeof(int) * h->nsub, cudaMemcpyDeviceToHost,
+                         h->stream));
+  CKH(h, cudaStreamSynchronize(h->stream));
+  const int64_t sumI = sum_dims(h);
+  std::vector<int> keep;
+  for (int k = 0; k < h->K; ++k) {
+    const int sub = h->h_blk2sub[k], R = h->h_subR[sub], col = h->h_blkcol[k];
+    if (act[sub]) {
+      keep.push_back(sub);
+    } else if (!h->h_stored[sub]) {
+      int64_t o = 0;
+      for (int n = 0; n < h->N; ++n) {
+        int I = (int)h->dims[n];
+        double* dst = h->ptr<double>(h->off.Ures) + (int64_t)sub * sumI * h->R + o;
+        store_block_kernel<<<(int)cdiv((int64_t)I * R, 256), 256, 0, h->stream>>>(h->U(n), I, h->ldu, R, col, dst);
+        CKH(h, cudaGetLastError());
+        o += (int64_t)I * R;
+      }
+      h->h_stored[sub] = 1;
+    }
+  }
+  if ((int)keep.size() == h->K) return JKCALS_OK;
+  return relayout(h, keep);
+}
+
+// slot holding global submodel id p, or -1
+int slot_of(const jkcals_s* h, int64_t p) {
+  if (p >= h->sub_begin && p < h->sub_end && p - h->sub_begin < h->nsub && h->h_id[p - h->sub_begin] == p)
+    return (int)(p - h->sub_begin);
+  for (int q = 0; q < h->nsub; ++q)
+    if (h->h_id[q] == p && p >= 0) return q;
+  return -1;
 }
 
 }  // namespace
@@ -878,46 +903,76 @@ jkcals_status compact(jkcals_t h) {
 // ====================================================================== C ABI
 extern "C" {
 
-// pool geometry shared by jkcals_pool_workspace_bytes and jkcals_create_pool
+// pool geometry shared by the workspace-size query and creation
 struct PoolGeo {
-  int Rs = 0;          // largest rank among the handle's submodels
+  int Rs = 0;          // largest rank a slot may hold (all models' max when there are spare slots)
   int64_t sumRm = 0;   // sum of all model ranks
   int64_t ngroups = 0;
-  int64_t C = 0;       // total fused width of the handle
+  int64_t C = 0;       // fused width of the owned submodels
+  int64_t nslot = 0;   // owned + spare
 };
 
-static bool pool_geo(int ndims, const int64_t* dims, int nmodels, const int* ranks, int64_t d, int64_t sub_begin,
-                     int64_t sub_end, PoolGeo* g) {
-  if (nmodels < 1 || !ranks || !dims || ndims < 3 || ndims > JKCALS_MAX_MODES) return false;
-  if (dims[0] < 2 || d < 0 || (d > 1 && 2 * d > dims[0])) return false;  // d <= I_0 / 2
-  for (int m = 0; m < nmodels; ++m)
-    if (ranks[m] < 1 || ranks[m] > 16) return false;
+static bool pool_geo(const jkcals_config* c, PoolGeo* g) {
+  if (!c || c->nmodels < 1 || !c->ranks || !c->dims || c->ndims < 3 || c->ndims > JKCALS_MAX_MODES) return false;
+  const int64_t* dims = c->dims;
+  const int64_t d = c->d;
+  if (dims[0] < 2 || d < 0 || (d > 1 && 2 * d > dims[0]) || c->spare < 0 || c->hist_cap < 1) return false;
+  if (c->prec != JKCALS_FP64 && c->prec != JKCALS_FP32) return false;
+  for (int m = 0; m < c->nmodels; ++m)
+    if (c->ranks[m] < 1 || c->ranks[m] > 16) return false;
   // d = 0: plain CALS (§3.3): one model per id, nothing left out
   g->ngroups = d == 0 ? 1 : (dims[0] + d - 1) / d;
-  if (sub_begin < 0 || sub_end <= sub_begin || sub_end > (int64_t)nmodels * g->ngroups) return false;
+  if (c->sub_begin < 0 || c->sub_end <= c->sub_begin || c->sub_end > (int64_t)c->nmodels * g->ngroups) return false;
   g->Rs = 0;
   g->C = 0;
   g->sumRm = 0;
-  for (int m = 0; m < nmodels; ++m) g->sumRm += ranks[m];
-  for (int64_t s = sub_begin; s < sub_end; ++s) {
-    const int R = ranks[s / g->ngroups];
+  int rmax = 0;
+  for (int m = 0; m < c->nmodels; ++m) {
+    g->sumRm += c->ranks[m];
+    rmax = std::max(rmax, c->ranks[m]);
+  }
+  for (int64_t s = c->sub_begin; s < c->sub_end; ++s) {
+    const int R = c->ranks[s / g->ngroups];
     g->Rs = std::max(g->Rs, R);
     g->C += R;
   }
-  return valid_dims(ndims, dims, g->Rs) && g->C <= (1 << 24);
+  if (c->spare > 0) g->Rs = rmax;
+  g->nslot = c->sub_end - c->sub_begin + c->spare;
+  return valid_dims(c->ndims, dims, g->Rs) && g->nslot * g->Rs <= (1 << 24);
+}
+
+size_t jkcals_config_workspace_bytes(const jkcals_config* c) {
+  PoolGeo g;
+  if (!pool_geo(c, &g)) return 0;
+  KernelInfo* ki = kernel_info(c->device, nullptr);
+  if (!ki) return 0;
+  Offsets o;
+  compute_offsets(c->ndims, c->dims, g.Rs, g.nslot, c->hist_cap, *ki, &o, c->prec == JKCALS_FP32, g.sumRm);
+  return o.total;
+}
+
+static jkcals_config make_cfg(int ndims, const int64_t* dims, int nmodels, const int* ranks, int64_t d,
+                              int64_t sub_begin, int64_t sub_end, jkcals_precision prec, int hist_cap, int device) {
+  jkcals_config c = {};
+  c.ndims = ndims;
+  c.dims = dims;
+  c.nmodels = nmodels;
+  c.ranks = ranks;
+  c.d = d;
+  c.sub_begin = sub_begin;
+  c.sub_end = sub_end;
+  c.spare = 0;
+  c.prec = prec;
+  c.hist_cap = hist_cap;
+  c.device = device;
+  return c;
 }
 
 size_t jkcals_pool_workspace_bytes(int ndims, const int64_t* dims, int nmodels, const int* ranks, int64_t d,
                                    int64_t sub_begin, int64_t sub_end, jkcals_precision prec, int hist_cap,
                                    int device) {
-  PoolGeo g;
-  if (!pool_geo(ndims, dims, nmodels, ranks, d, sub_begin, sub_end, &g) || hist_cap < 1) return 0;
-  if (prec != JKCALS_FP64 && prec != JKCALS_FP32) return 0;
-  KernelInfo* ki = kernel_info(device, nullptr);
-  if (!ki) return 0;
-  Offsets o;
-  compute_offsets(ndims, dims, g.Rs, sub_end - sub_begin, hist_cap, *ki, &o, prec == JKCALS_FP32, g.sumRm);
-  return o.total;
+  jkcals_config c = make_cfg(ndims, dims, nmodels, ranks, d, sub_begin, sub_end, prec, hist_cap, device);
+  return jkcals_config_workspace_bytes(&c);
 }
 
 size_t jkcals_workspace_bytes(int ndims, const int64_t* dims, int rank, int64_t n_sub, jkcals_precision prec,
@@ -948,13 +1003,22 @@ jkcals_status jkcals_create_pool(jkcals_t* out, int ndims, const int64_t* dims, 
                                  int64_t d, int64_t sub_begin, int64_t sub_end, const double* tensor,
                                  int tensor_is_device, jkcals_precision prec, int device, void* cuda_stream,
                                  void* workspace, size_t workspace_bytes, int hist_cap) {
+  jkcals_config c = make_cfg(ndims, dims, nmodels, ranks, d, sub_begin, sub_end, prec, hist_cap, device);
+  return jkcals_create_config(out, &c, tensor, tensor_is_device, cuda_stream, workspace, workspace_bytes);
+}
+
+jkcals_status jkcals_create_config(jkcals_t* out, const jkcals_config* cfg, const double* tensor,
+                                   int tensor_is_device, void* cuda_stream, void* workspace,
+                                   size_t workspace_bytes) {
   if (!out) return JKCALS_E_ARG;
   *out = nullptr;
   PoolGeo pg0;
-  if (!pool_geo(ndims, dims, nmodels, ranks, d, sub_begin, sub_end, &pg0) || !tensor || !workspace ||
-      hist_cap < 1)
-    return JKCALS_E_ARG;
-  if (prec != JKCALS_FP64 && prec != JKCALS_FP32) return JKCALS_E_ARG;
+  if (!pool_geo(cfg, &pg0) || !tensor || !workspace) return JKCALS_E_ARG;
+  const int ndims = cfg->ndims, nmodels = cfg->nmodels, hist_cap = cfg->hist_cap, device = cfg->device;
+  const int64_t* dims = cfg->dims;
+  const int* ranks = cfg->ranks;
+  const int64_t d = cfg->d, sub_begin = cfg->sub_begin, sub_end = cfg->sub_end;
+  const jkcals_precision prec = cfg->prec;
   DeviceGuard dg(device);
   std::string kerr;
   KernelInfo* ki = kernel_info(device, &kerr);
@@ -970,21 +1034,35 @@ jkcals_status jkcals_create_pool(jkcals_t* out, int ndims, const int64_t* dims, 
   h->nmodels = nmodels;
   h->ranks.assign(ranks, ranks + nmodels);
   h->sumRm = pg0.sumRm;
-  h->nsub = (int)(sub_end - sub_begin);
+  h->spare = cfg->spare;
+  h->nsub = (int)pg0.nslot;
+  const int nown = (int)(sub_end - sub_begin);
   std::vector<int> rc(nmodels, 0);
   for (int m = 1; m < nmodels; ++m) rc[m] = rc[m - 1] + ranks[m - 1];
   for (int q = 0; q < h->nsub; ++q) {
-    const int64_t s = sub_begin + q;
-    const int m = (int)(s / h->ngroups);
-    h->h_model.push_back(m);
-    h->h_group.push_back(s % h->ngroups);
-    h->h_subR.push_back(ranks[m]);
-    h->h_subRc.push_back(rc[m]);
-    if (ranks[m] != h->R) h->mixed = true;
+    if (q < nown) {
+      const int64_t s = sub_begin + q;
+      const int m = (int)(s / h->ngroups);
+      h->h_id.push_back(s);
+      h->h_model.push_back(m);
+      h->h_group.push_back(s % h->ngroups);
+      h->h_subR.push_back(ranks[m]);
+      h->h_subRc.push_back(rc[m]);
+      if (ranks[m] != h->R) h->mixed = true;
+    } else {  // spare slot
+      h->h_id.push_back(-1);
+      h->h_model.push_back(-1);
+      h->h_group.push_back(0);
+      h->h_subR.push_back(0);
+      h->h_subRc.push_back(0);
+    }
   }
-  h->K = h->nsub;
+  if (h->spare > 0)
+    for (int m = 0; m < nmodels; ++m)
+      if (ranks[m] != h->R) h->mixed = true;
+  h->K = nown;
   h->C = (int)pg0.C;
-  h->ldu = rup(std::max<int64_t>(h->C, 1), 128);
+  h->ldu = rup(std::max<int64_t>(pg0.C + (int64_t)h->spare * h->R, 1), 128);  // room for imports
   h->P = 1;
   for (int k = 0; k < ndims; ++k) h->P *= dims[k];
   h->I0p = rup(dims[0], 2);
@@ -1016,11 +1094,9 @@ jkcals_status jkcals_create_pool(jkcals_t* out, int ndims, const int64_t* dims, 
                            sizeof(double) * dims[0], h->P / dims[0],
                            tensor_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
   std::vector<int64_t> pg(h->nsub);
-  std::vector<int> b2s(h->nsub);
-  for (int q = 0; q < h->nsub; ++q) {
-    pg[q] = h->h_group[q] * d;  // first left-out row of the group
-    b2s[q] = q;
-  }
+  std::vector<int> b2s(nown);
+  for (int q = 0; q < h->nsub; ++q) pg[q] = h->h_group[q] * d;  // first left-out row of the group
+  for (int q = 0; q < nown; ++q) b2s[q] = q;
   h->h_stored.assign(h->nsub, 0);
   CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.pglob), pg.data(), sizeof(int64_t) * h->nsub,
                          cudaMemcpyHostToDevice, h->stream));
@@ -1087,11 +1163,12 @@ jkcals_status jkcals_set_init(jkcals_t h, const double* const* P) {
       for (int64_t e = 0; e < h->dims[n] * h->ranks[m]; ++e)
         if (!std::isfinite(Pm[e])) return fail(h, JKCALS_E_NONFINITE, "P[%d] has a non-finite entry", m * h->N + n);
     }
-  // full reset of the fused layout (undo any compaction)
-  bool relayout = (h->K != h->nsub) || (h->cur != 0);
+  // full reset of the fused layout (undo any compaction): one block per owned slot
+  std::vector<int> b2s;
+  for (int q = 0; q < h->nsub; ++q)
+    if (h->h_id[q] >= 0) b2s.push_back(q);
+  bool relayout = (b2s != h->h_blk2sub) || (h->cur != 0);
   h->cur = 0;
-  std::vector<int> b2s(h->nsub);
-  for (int q = 0; q < h->nsub; ++q) b2s[q] = q;
   jkcals_status st = set_blocks(h, b2s);
   if (st != JKCALS_OK) return st;
   h->h_stored.assign(h->nsub, 0);
@@ -1120,6 +1197,8 @@ jkcals_status jkcals_set_init(jkcals_t h, const double* const* P) {
       h->nsub, h->ptr<double>(h->off.fit), h->ptr<double>(h->off.fit_prev), h->ptr<double>(h->off.err),
       h->ptr<int>(h->off.iters), h->ptr<int>(h->off.flags), h->ptr<int>(h->off.active));
   CKH(h, cudaGetLastError());
+  for (int q = 0; q < h->nsub; ++q)  // free slots never run
+    if (h->h_id[q] < 0) CKH(h, cudaMemsetAsync(h->ptr<int>(h->off.active) + q, 0, sizeof(int), h->stream));
   CKH(h, cudaMemsetAsync(h->ptr<double>(h->off.hist), 0, sizeof(double) * h->nsub * (size_t)h->hist_cap, h->stream));
   if (relayout) {
     st = replan(h);
@@ -1133,10 +1212,10 @@ jkcals_status jkcals_set_init(jkcals_t h, const double* const* P) {
 }
 
 jkcals_status jkcals_set_init_submodel(jkcals_t h, int64_t p, int mode, const double* U) {
-  if (!h || !U || mode < 0 || mode >= h->N || p < h->sub_begin || p >= h->sub_end) return JKCALS_E_ARG;
+  if (!h || !U || mode < 0 || mode >= h->N || slot_of(h, p) < 0) return JKCALS_E_ARG;
   if (!h->inited) return fail(h, JKCALS_E_STATE, "set_init must come first");
   DeviceGuard dg(h->device);
-  const int sub = (int)(p - h->sub_begin);
+  const int sub = slot_of(h, p);
   const int blk = block_of(h, sub);
   if (blk < 0) return fail(h, JKCALS_E_STATE, "submodel %lld was compacted out", (long long)p);
   h->aligned = false;
@@ -1203,9 +1282,7 @@ jkcals_status jkcals_iterate(jkcals_t h, int max_iters, double tol, int* sweeps_
   return JKCALS_OK;
 }
 
-static jkcals_status locate(jkcals_t h, int64_t p, int mode, const double** src, int64_t* ld, int* sub_out) {
-  const int sub = (int)(p - h->sub_begin);
-  *sub_out = sub;
+static jkcals_status locate_slot(jkcals_t h, int sub, int mode, const double** src, int64_t* ld) {
   const int R = h->h_subR[sub];
   if (h->h_stored[sub]) {
     int64_t o = 0;
@@ -1215,14 +1292,21 @@ static jkcals_status locate(jkcals_t h, int64_t p, int mode, const double** src,
     return JKCALS_OK;
   }
   const int k = block_of(h, sub);
-  if (k < 0) return fail(h, JKCALS_E_STATE, "submodel %lld not found", (long long)p);
+  if (k < 0) return fail(h, JKCALS_E_STATE, "slot %d holds no submodel", sub);
   *src = h->U(mode) + h->h_blkcol[k];
   *ld = h->ldu;
   return JKCALS_OK;
 }
 
+static jkcals_status locate(jkcals_t h, int64_t p, int mode, const double** src, int64_t* ld, int* sub_out) {
+  const int sub = slot_of(h, p);
+  *sub_out = sub;
+  if (sub < 0) return fail(h, JKCALS_E_ARG, "submodel %lld is not on this handle", (long long)p);
+  return locate_slot(h, sub, mode, src, ld);
+}
+
 jkcals_status jkcals_get_factors(jkcals_t h, int64_t p, int mode, double* U, double* lambda) {
-  if (!h || !U || mode < 0 || mode >= h->N || p < h->sub_begin || p >= h->sub_end) return JKCALS_E_ARG;
+  if (!h || !U || mode < 0 || mode >= h->N || slot_of(h, p) < 0) return JKCALS_E_ARG;
   if (!h->inited) return fail(h, JKCALS_E_STATE, "no model yet");
   DeviceGuard dg(h->device);
   const double* src;
@@ -1252,26 +1336,35 @@ jkcals_status jkcals_get_all_factors(jkcals_t h, int mode, double* U, double* la
   if (!h || !U || mode < 0 || mode >= h->N) return JKCALS_E_ARG;
   if (!h->inited) return fail(h, JKCALS_E_STATE, "no model yet");
   DeviceGuard dg(h->device);
-  std::vector<int> subs(h->nsub);
-  for (int q = 0; q < h->nsub; ++q) subs[q] = q;
+  std::vector<int> subs;  // owned slots, in slot order
+  for (int q = 0; q < h->nsub; ++q)
+    if (h->h_id[q] >= 0) subs.push_back(q);
+  const int ns = (int)subs.size();
+  if (ns == 0) return JKCALS_OK;
   jkcals_status st = build_src_table(h, mode, subs);
   if (st != JKCALS_OK) return st;
   const int I = (int)h->dims[mode];
-  // packed output: submodel q's rows_q x R_q block at dstoff[q]
-  std::vector<int64_t> dst(h->nsub);
+  // packed output: the j-th owned slot's rows x R block at dstoff[j]; per-listed rank / row start
+  std::vector<int64_t> dst(ns), pg(ns);
+  std::vector<int> rk(ns);
   int64_t total = 0;
-  for (int q = 0; q < h->nsub; ++q) {
-    dst[q] = total;
+  for (int j = 0; j < ns; ++j) {
+    const int q = subs[j];
+    dst[j] = total;
+    rk[j] = h->h_subR[q];
+    pg[j] = h->h_group[q] * h->d;
     const int rows = I - (mode == 0 ? (int)group_rows(h, h->h_group[q]) : 0);
     total += (int64_t)rows * h->h_subR[q];
   }
-  CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.dstoff), dst.data(), 8 * h->nsub, cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.dstoff), dst.data(), 8 * ns, cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.srcpg), pg.data(), 8 * ns, cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.map), rk.data(), 4 * ns, cudaMemcpyHostToDevice, h->stream));
   double* stage = h->ptr<double>(h->off.stage);
   const int per = (int)std::min<int64_t>(cdiv((int64_t)I * h->R, 256), 64);
-  extract_all_kernel<<<dim3(per, (unsigned)std::min(h->nsub, 65535)), 256, 0, h->stream>>>(
+  extract_all_kernel<<<dim3(per, (unsigned)std::min(ns, 65535)), 256, 0, h->stream>>>(
       reinterpret_cast<const double*>(h->ws), h->ptr<int64_t>(h->off.srcoff), h->ptr<int64_t>(h->off.srcld),
-      h->ptr<int>(h->off.subR), h->ptr<int64_t>(h->off.dstoff), h->nsub, I, mode == 0 ? 1 : 0,
-      h->ptr<int64_t>(h->off.pglob), (int)h->d, stage);
+      h->ptr<int>(h->off.map), h->ptr<int64_t>(h->off.dstoff), ns, I, mode == 0 ? 1 : 0,
+      h->ptr<int64_t>(h->off.srcpg), (int)h->d, stage);
   CKH(h, cudaGetLastError());
   CKH(h, cudaMemcpyAsync(U, stage, sizeof(double) * total, cudaMemcpyDeviceToHost, h->stream));
   if (lambda) {  // packed the same way: R_q values per submodel
@@ -1280,7 +1373,7 @@ jkcals_status jkcals_get_all_factors(jkcals_t h, int mode, double* U, double* la
                            cudaMemcpyDeviceToHost, h->stream));
     CKH(h, cudaStreamSynchronize(h->stream));
     int64_t o = 0;
-    for (int q = 0; q < h->nsub; ++q)
+    for (int q : subs)
       for (int r = 0; r < h->h_subR[q]; ++r) lambda[o++] = lam[(size_t)q * h->R + r];
   }
   CKH(h, cudaStreamSynchronize(h->stream));
@@ -1288,7 +1381,7 @@ jkcals_status jkcals_get_all_factors(jkcals_t h, int mode, double* U, double* la
 }
 
 jkcals_status jkcals_get_block(jkcals_t h, int64_t p, int mode, double* U) {
-  if (!h || !U || mode < 0 || mode >= h->N || p < h->sub_begin || p >= h->sub_end) return JKCALS_E_ARG;
+  if (!h || !U || mode < 0 || mode >= h->N || slot_of(h, p) < 0) return JKCALS_E_ARG;
   if (!h->inited) return fail(h, JKCALS_E_STATE, "no model yet");
   DeviceGuard dg(h->device);
   const double* src;
@@ -1319,9 +1412,9 @@ jkcals_status jkcals_get_status(jkcals_t h, double* fit, double* err, int* iters
 }
 
 jkcals_status jkcals_get_history(jkcals_t h, int64_t p, double* err, int cap, int* count) {
-  if (!h || !err || cap < 0 || p < h->sub_begin || p >= h->sub_end) return JKCALS_E_ARG;
+  if (!h || !err || cap < 0 || slot_of(h, p) < 0) return JKCALS_E_ARG;
   DeviceGuard dg(h->device);
-  const int sub = (int)(p - h->sub_begin);
+  const int sub = slot_of(h, p);
   int it = 0;
   CKH(h, cudaMemcpyAsync(&it, h->ptr<int>(h->off.iters) + sub, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   std::vector<double> ring(h->hist_cap);
@@ -1348,7 +1441,8 @@ static jkcals_status build_src_table(jkcals_t h, int mode, const std::vector<int
     const double* src;
     int64_t l;
     int sub;
-    jkcals_status st = locate(h, h->sub_begin + subs[q], mode, &src, &l, &sub);
+    (void)sub;
+    jkcals_status st = locate_slot(h, subs[q], mode, &src, &l);
     if (st != JKCALS_OK) return st;
     off[q] = src - reinterpret_cast<const double*>(h->ws);
     ld[q] = l;
@@ -1423,7 +1517,13 @@ jkcals_status jkcals_align(jkcals_t h) {
       const double* src;
       int64_t l;
       int sub;
-      jkcals_status st = locate(h, h->sub_begin + q, n, &src, &l, &sub);
+      (void)sub;
+      if (h->h_id[q] < 0) {  // free slot: nothing to align (R = 0 there)
+        off[(size_t)q * h->N + n] = 0;
+        ld[(size_t)q * h->N + n] = 0;
+        continue;
+      }
+      jkcals_status st = locate_slot(h, q, n, &src, &l);
       if (st != JKCALS_OK) return st;
       off[(size_t)q * h->N + n] = src - reinterpret_cast<const double*>(h->ws);
       ld[(size_t)q * h->N + n] = l;
@@ -1457,10 +1557,10 @@ jkcals_status jkcals_align(jkcals_t h) {
 }
 
 jkcals_status jkcals_get_alignment(jkcals_t h, int64_t p, int* perm, int* sign, double* congruence) {
-  if (!h || p < h->sub_begin || p >= h->sub_end) return JKCALS_E_ARG;
+  if (!h || slot_of(h, p) < 0) return JKCALS_E_ARG;
   if (!h->aligned) return fail(h, JKCALS_E_STATE, "jkcals_align has not run on the current factors");
   DeviceGuard dg(h->device);
-  const int sub = (int)(p - h->sub_begin), R = h->h_subR[sub];
+  const int sub = slot_of(h, p), R = h->h_subR[sub];
   if (perm)
     CKH(h, cudaMemcpyAsync(perm, h->ptr<int>(h->off.aperm) + (int64_t)sub * h->R, 4 * R, cudaMemcpyDeviceToHost,
                            h->stream));
@@ -1483,10 +1583,10 @@ static const double* aligned_block(jkcals_t h, int sub, int mode) {
 }
 
 jkcals_status jkcals_get_aligned_factors(jkcals_t h, int64_t p, int mode, double* U) {
-  if (!h || !U || mode < 0 || mode >= h->N || p < h->sub_begin || p >= h->sub_end) return JKCALS_E_ARG;
+  if (!h || !U || mode < 0 || mode >= h->N || slot_of(h, p) < 0) return JKCALS_E_ARG;
   if (!h->aligned) return fail(h, JKCALS_E_STATE, "jkcals_align has not run on the current factors");
   DeviceGuard dg(h->device);
-  const int sub = (int)(p - h->sub_begin), R = h->h_subR[sub];
+  const int sub = slot_of(h, p), R = h->h_subR[sub];
   const int I = (int)h->dims[mode];
   const int cnt = mode == 0 ? (int)group_rows(h, h->h_group[sub]) : 0;
   double* stage = h->ptr<double>(h->off.stage);
@@ -1554,6 +1654,161 @@ jkcals_status jkcals_get_local_moments(jkcals_t h, int mode, double* count, doub
 jkcals_status jkcals_get_jackknife_stats(jkcals_t h, int mode, double* mean, double* std_out) {
   if (h && h->nmodels != 1) return fail(h, JKCALS_E_ARG, "pooled handle: use jkcals_get_model_stats");
   return jkcals_get_model_stats(h, 0, mode, mean, std_out);
+}
+
+// ---------------------------------------------------------------- slots and migration (NEXT #4)
+int jkcals_num_slots(jkcals_t h) { return h ? h->nsub : 0; }
+
+jkcals_status jkcals_get_ids(jkcals_t h, int64_t* ids) {
+  if (!h || !ids) return JKCALS_E_ARG;
+  for (int q = 0; q < h->nsub; ++q) ids[q] = h->h_id[q];
+  return JKCALS_OK;
+}
+
+enum { kStHdr = 16 };
+static const double kStMagic = 1245397825.0;  // "JKCA"
+
+static size_t state_doubles(const jkcals_s* h, int R) {
+  return kStHdr + (size_t)R + (size_t)h->N * R * R + (size_t)h->hist_cap + (size_t)sum_dims(const_cast<jkcals_s*>(h)) * R;
+}
+
+size_t jkcals_state_bytes(jkcals_t h, int64_t p) {
+  if (!h) return 0;
+  const int sub = slot_of(h, p);
+  if (sub < 0) return 0;
+  return 8 * state_doubles(h, h->h_subR[sub]);
+}
+
+jkcals_status jkcals_export_submodel(jkcals_t h, int64_t p, void* buf, size_t bytes) {
+  if (!h || !buf) return JKCALS_E_ARG;
+  const int sub = slot_of(h, p);
+  if (sub < 0) return JKCALS_E_ARG;
+  if (!h->inited) return fail(h, JKCALS_E_STATE, "no model yet");
+  const int R = h->h_subR[sub], N = h->N;
+  if (bytes < 8 * state_doubles(h, R)) return fail(h, JKCALS_E_ARG, "state buffer too small");
+  const int blk = block_of(h, sub);
+  if (blk < 0) return fail(h, JKCALS_E_STATE, "submodel %lld is not live (converged and stored)", (long long)p);
+  DeviceGuard dg(h->device);
+  double* b = static_cast<double*>(buf);
+  int it = 0, fl = 0, ac = 0;
+  double fit = 0, fitp = 0, err = 0, nt2 = 0;
+  CKH(h, cudaMemcpyAsync(&it, h->ptr<int>(h->off.iters) + sub, 4, cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaMemcpyAsync(&fl, h->ptr<int>(h->off.flags) + sub, 4, cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaMemcpyAsync(&ac, h->ptr<int>(h->off.active) + sub, 4, cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaMemcpyAsync(&fit, h->ptr<double>(h->off.fit) + sub, 8, cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaMemcpyAsync(&fitp, h->ptr<double>(h->off.fit_prev) + sub, 8, cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaMemcpyAsync(&err, h->ptr<double>(h->off.err) + sub, 8, cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaMemcpyAsync(&nt2, h->ptr<double>(h->off.normT2p) + sub, 8, cudaMemcpyDeviceToHost, h->stream));
+  double* o = b + kStHdr;
+  CKH(h, cudaMemcpyAsync(o, h->ptr<double>(h->off.lambda) + (int64_t)sub * h->R, 8 * R, cudaMemcpyDeviceToHost,
+                         h->stream));
+  o += R;
+  for (int n = 0; n < N; ++n, o += R * R)
+    CKH(h, cudaMemcpyAsync(o, h->ptr<double>(h->off.gram) + ((int64_t)n * h->nsub + sub) * h->R * h->R, 8 * R * R,
+                           cudaMemcpyDeviceToHost, h->stream));
+  CKH(h, cudaMemcpyAsync(o, h->ptr<double>(h->off.hist) + (int64_t)sub * h->hist_cap, 8 * h->hist_cap,
+                         cudaMemcpyDeviceToHost, h->stream));
+  o += h->hist_cap;
+  double* stage = h->ptr<double>(h->off.stage);
+  for (int n = 0; n < N; ++n) {  // full blocks (mode 0 keeps its zero rows), column-major
+    const int I = (int)h->dims[n];
+    extract_kernel<<<(int)cdiv((int64_t)I * R, 256), 256, 0, h->stream>>>(h->U(n) + h->h_blkcol[blk], h->ldu, I, R,
+                                                                         -1, 0, stage);
+    CKH(h, cudaGetLastError());
+    CKH(h, cudaMemcpyAsync(o, stage, 8 * (size_t)I * R, cudaMemcpyDeviceToHost, h->stream));
+    CKH(h, cudaStreamSynchronize(h->stream));  // stage is reused by the next mode
+    o += (int64_t)I * R;
+  }
+  CKH(h, cudaStreamSynchronize(h->stream));
+  const double hdr[kStHdr] = {kStMagic, (double)p, (double)R, (double)h->h_model[sub], (double)h->h_group[sub],
+                              (double)it, (double)fl, (double)ac, fit, fitp, err, nt2, (double)h->hist_cap,
+                              (double)N, 0.0, 0.0};
+  std::memcpy(b, hdr, sizeof hdr);
+  // the submodel leaves this handle: drop its block and free the slot
+  std::vector<int> keep;
+  for (int k = 0; k < h->K; ++k)
+    if (h->h_blk2sub[k] != sub) keep.push_back(h->h_blk2sub[k]);
+  jkcals_status st = relayout(h, keep);
+  if (st != JKCALS_OK) return st;
+  h->h_id[sub] = -1;
+  h->h_model[sub] = -1;
+  h->h_subR[sub] = 0;
+  const int zero = 0;
+  CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.subR) + sub, &zero, 4, cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.active) + sub, &zero, 4, cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaStreamSynchronize(h->stream));
+  h->aligned = false;
+  return JKCALS_OK;
+}
+
+jkcals_status jkcals_import_submodel(jkcals_t h, const void* buf, size_t bytes) {
+  if (!h || !buf || bytes < 8 * kStHdr) return JKCALS_E_ARG;
+  if (!h->inited) return fail(h, JKCALS_E_STATE, "set_init must come first");
+  const double* b = static_cast<const double*>(buf);
+  if (b[0] != kStMagic) return fail(h, JKCALS_E_ARG, "not a submodel state");
+  const int64_t id = (int64_t)b[1];
+  const int R = (int)b[2], model = (int)b[3];
+  const int64_t group = (int64_t)b[4];
+  if ((int)b[12] != h->hist_cap || (int)b[13] != h->N) return fail(h, JKCALS_E_ARG, "state from another problem");
+  if (model < 0 || model >= h->nmodels || h->ranks[model] != R || group < 0 || group >= h->ngroups ||
+      id != model * h->ngroups + group)
+    return fail(h, JKCALS_E_ARG, "state does not match this pool");
+  if (bytes < 8 * state_doubles(h, R)) return fail(h, JKCALS_E_ARG, "state buffer truncated");
+  if (slot_of(h, id) >= 0) return fail(h, JKCALS_E_ARG, "submodel %lld is already here", (long long)id);
+  if (R > h->R || h->C + R > h->ldu) return fail(h, JKCALS_E_OOM, "no column room for the submodel");
+  int sub = -1;
+  for (int q = 0; q < h->nsub && sub < 0; ++q)
+    if (h->h_id[q] < 0) sub = q;
+  if (sub < 0) return fail(h, JKCALS_E_OOM, "no free slot (create with spare slots)");
+  DeviceGuard dg(h->device);
+  int rc = 0;
+  for (int m = 0; m < model; ++m) rc += h->ranks[m];
+  h->h_id[sub] = id;
+  h->h_model[sub] = model;
+  h->h_group[sub] = group;
+  h->h_subR[sub] = R;
+  h->h_subRc[sub] = rc;
+  h->h_stored[sub] = 0;
+  const int64_t pg = group * h->d;
+  const int it = (int)b[5], fl = (int)b[6], ac = (int)b[7];
+  CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.subR) + sub, &h->h_subR[sub], 4, cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.subRc) + sub, &h->h_subRc[sub], 4, cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<int64_t>(h->off.pglob) + sub, &pg, 8, cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.iters) + sub, &it, 4, cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.flags) + sub, &fl, 4, cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<int>(h->off.active) + sub, &ac, 4, cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<double>(h->off.fit) + sub, b + 8, 8, cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<double>(h->off.fit_prev) + sub, b + 9, 8, cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<double>(h->off.err) + sub, b + 10, 8, cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<double>(h->off.normT2p) + sub, b + 11, 8, cudaMemcpyHostToDevice, h->stream));
+  const double* o = b + kStHdr;
+  CKH(h, cudaMemcpyAsync(h->ptr<double>(h->off.lambda) + (int64_t)sub * h->R, o, 8 * R, cudaMemcpyHostToDevice,
+                         h->stream));
+  o += R;
+  for (int n = 0; n < h->N; ++n, o += R * R)
+    CKH(h, cudaMemcpyAsync(h->ptr<double>(h->off.gram) + ((int64_t)n * h->nsub + sub) * h->R * h->R, o, 8 * R * R,
+                           cudaMemcpyHostToDevice, h->stream));
+  CKH(h, cudaMemcpyAsync(h->ptr<double>(h->off.hist) + (int64_t)sub * h->hist_cap, o, 8 * h->hist_cap,
+                         cudaMemcpyHostToDevice, h->stream));
+  o += h->hist_cap;
+  // append its block at the end of the live layout
+  std::vector<int> b2s = h->h_blk2sub;
+  b2s.push_back(sub);
+  jkcals_status st = set_blocks(h, b2s);
+  if (st != JKCALS_OK) return st;
+  const int col = h->h_blkcol[h->K - 1];
+  double* stage = h->ptr<double>(h->off.stage);
+  for (int n = 0; n < h->N; ++n) {
+    const int I = (int)h->dims[n];
+    CKH(h, cudaMemcpyAsync(stage, o, 8 * (size_t)I * R, cudaMemcpyHostToDevice, h->stream));
+    set_block_kernel<<<(int)cdiv((int64_t)I * R, 256), 256, 0, h->stream>>>(stage, I, R, h->ldu, col, -1, 0,
+                                                                           h->U(n));
+    CKH(h, cudaGetLastError());
+    CKH(h, cudaStreamSynchronize(h->stream));  // stage is reused by the next mode
+    o += (int64_t)I * R;
+  }
+  h->aligned = false;
+  return replan(h);
 }
 
 jkcals_status jkcals_set_instrument(jkcals_t h, int on) {

@@ -51,6 +51,13 @@ def lib():
             "jkcals_get_model_stats": (I, [P, I, I, P, P]),
             "jkcals_get_model_moments": (I, [P, I, I, P, P, P]),
             "jkcals_align": (I, [P]),
+            "jkcals_config_workspace_bytes": (SZ, [P]),
+            "jkcals_create_config": (I, [P, P, P, I, P, P, SZ]),
+            "jkcals_num_slots": (I, [P]),
+            "jkcals_get_ids": (I, [P, P]),
+            "jkcals_state_bytes": (SZ, [P, I64]),
+            "jkcals_export_submodel": (I, [P, I64, P, SZ]),
+            "jkcals_import_submodel": (I, [P, P, SZ]),
             "jkcals_get_alignment": (I, [P, I64, P, P, P]),
             "jkcals_get_aligned_factors": (I, [P, I64, I, P]),
             "jkcals_get_aligned_moments": (I, [P, I, I, P, P, P]),
@@ -86,6 +93,8 @@ def lib():
 EXPORTED = [
     "jkcals_workspace_bytes", "jkcals_create", "jkcals_create_d", "jkcals_pool_workspace_bytes",
     "jkcals_create_pool", "jkcals_get_model_stats", "jkcals_get_model_moments", "jkcals_align",
+    "jkcals_config_workspace_bytes", "jkcals_create_config", "jkcals_num_slots", "jkcals_get_ids",
+    "jkcals_state_bytes", "jkcals_export_submodel", "jkcals_import_submodel",
     "jkcals_get_alignment", "jkcals_get_aligned_factors", "jkcals_get_aligned_moments", "jkcals_get_aligned_stats",
     "jkcals_set_init", "jkcals_set_init_submodel", "jkcals_iterate",
     "jkcals_get_factors", "jkcals_get_all_factors", "jkcals_get_block", "jkcals_get_status", "jkcals_get_history", "jkcals_get_jackknife_stats",
@@ -125,6 +134,14 @@ def column_major_flat(T):
     return np.ravel(a, order="F"), dims, False
 
 
+class _Config(ctypes.Structure):
+    """struct jkcals_config (include/jkcals.h)."""
+    _fields_ = [("ndims", ctypes.c_int), ("dims", ctypes.c_void_p), ("nmodels", ctypes.c_int),
+                ("ranks", ctypes.c_void_p), ("d", ctypes.c_int64), ("sub_begin", ctypes.c_int64),
+                ("sub_end", ctypes.c_int64), ("spare", ctypes.c_int), ("prec", ctypes.c_int),
+                ("hist_cap", ctypes.c_int), ("device", ctypes.c_int)]
+
+
 class JKCals:
     """One shard [sub_begin, sub_end) of the I_1 leave-one-out submodels on one GPU.
 
@@ -137,7 +154,7 @@ class JKCals:
     all fused into one multi-factor per mode; set_init then takes one factor list per model."""
 
     def __init__(self, T, rank, sub_range=None, device=None, stream=None, hist_cap=None,
-                 precision=FP64, dims=None, d=1):
+                 precision=FP64, dims=None, d=1, spare=0):
         torch = _torch()
         self._torch = torch
         flat, tdims, is_dev = column_major_flat(T)
@@ -162,24 +179,26 @@ class JKCals:
         L = lib()
         d = _i64(self.dims)
         rk = np.ascontiguousarray(self.ranks, dtype=np.int32)
-        nbytes = L.jkcals_pool_workspace_bytes(self.N, _p(d), self.nmodels, _p(rk), self.d, self.sub_begin,
-                                               self.sub_end, precision, self.hist_cap, self.device)
+        self._cfg_keep = (d, rk)
+        cfg = _Config(self.N, d.ctypes.data, self.nmodels, rk.ctypes.data, self.d, self.sub_begin, self.sub_end,
+                      int(spare), int(precision), self.hist_cap, self.device)
+        nbytes = L.jkcals_config_workspace_bytes(ctypes.byref(cfg))
         if nbytes == 0:
             raise JKCalsError(-1, f"unsupported arguments dims={self.dims} rank={self.R} nsub={self.nsub}")
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{self.device}")
         self._keep = flat
         tptr = flat.data_ptr() if is_dev else flat.ctypes.data
         h = ctypes.c_void_p()
-        st = L.jkcals_create_pool(ctypes.byref(h), self.N, _p(d), self.nmodels, _p(rk), self.d, self.sub_begin,
-                                  self.sub_end, ctypes.c_void_p(tptr), 1 if is_dev else 0, precision, self.device,
-                                  ctypes.c_void_p(self.stream.cuda_stream),
-                                  ctypes.c_void_p(self.workspace.data_ptr()), nbytes, self.hist_cap)
+        st = L.jkcals_create_config(ctypes.byref(h), ctypes.byref(cfg), ctypes.c_void_p(tptr), 1 if is_dev else 0,
+                                    ctypes.c_void_p(self.stream.cuda_stream),
+                                    ctypes.c_void_p(self.workspace.data_ptr()), nbytes)
         self._h = h
         if st != 0:
             msg = L.jkcals_last_error(h).decode() if h.value else ""
             self.close()
             raise JKCalsError(st, msg)
         self._keep = None  # the tensor now lives in the workspace
+        self.nslots = L.jkcals_num_slots(h)
 
     # ------------------------------------------------------------------ helpers
     def _check(self, st):
@@ -254,19 +273,19 @@ class JKCals:
         """Every submodel's mode-`mode` factor at once: array (n_sub, rows, R) (the group's rows
         dropped in mode 0) and lambda (n_sub, R). With delete-d and a ragged last group the
         mode-0 factors come back as a list of (rows_q, R) arrays instead."""
-        subs = range(self.sub_begin, self.sub_end)
+        subs = [int(p) for p in self.ids() if p >= 0]   # owned submodels in slot order
         R_q = [self.rank_of(p) for p in subs]
         if mode == 0:
             rows_q = [self.dims[0] - self.group_rows(p) for p in subs]
         else:
-            rows_q = [self.dims[mode]] * self.nsub
+            rows_q = [self.dims[mode]] * len(subs)
         flat = np.zeros(sum(r * c for r, c in zip(rows_q, R_q)))
         lamf = np.zeros(sum(R_q))
         self._check(lib().jkcals_get_all_factors(self._h, int(mode), _p(flat), _p(lamf)))
         if len(set(rows_q)) == 1 and len(set(R_q)) == 1:
             R = R_q[0]
-            U = flat.reshape(self.nsub, R, rows_q[0])  # per submodel a column-major rows x R
-            return np.ascontiguousarray(U.transpose(0, 2, 1)), lamf.reshape(self.nsub, R)
+            U = flat.reshape(len(subs), R, rows_q[0])  # per submodel a column-major rows x R
+            return np.ascontiguousarray(U.transpose(0, 2, 1)), lamf.reshape(len(subs), R)
         out, lam, off, lo = [], [], 0, 0
         for r_, R in zip(rows_q, R_q):
             out.append(flat[off:off + r_ * R].reshape((r_, R), order="F"))
@@ -282,8 +301,9 @@ class JKCals:
         return U
 
     def status(self):
-        fit, err = np.zeros(self.nsub), np.zeros(self.nsub)
-        it, fl = np.zeros(self.nsub, dtype=np.int32), np.zeros(self.nsub, dtype=np.int32)
+        n = self.nslots   # per slot (slot q holds ids()[q])
+        fit, err = np.zeros(n), np.zeros(n)
+        it, fl = np.zeros(n, dtype=np.int32), np.zeros(n, dtype=np.int32)
         self._check(lib().jkcals_get_status(self._h, _p(fit), _p(err), _p(it), _p(fl)))
         return {"fit": fit, "err": err, "iters": it, "flags": fl}
 
@@ -304,6 +324,32 @@ class JKCals:
         cnt, mean, m2 = (np.zeros(shp, order="F") for _ in range(3))
         self._check(lib().jkcals_get_model_moments(self._h, int(model), int(mode), _p(cnt), _p(mean), _p(m2)))
         return cnt, mean, m2
+
+    # ------------------------------------------------------------------ slots / migration (NEXT #4)
+    def ids(self):
+        """Global submodel id held by each slot (-1 = free)."""
+        out = np.zeros(self.nslots, dtype=np.int64)
+        self._check(lib().jkcals_get_ids(self._h, _p(out)))
+        return out
+
+    def active_ids(self):
+        """Ids of the owned submodels that still iterate (not converged, not failed)."""
+        ids, fl = self.ids(), self.status()["flags"]
+        return [int(p) for p, f in zip(ids, fl) if p >= 0 and not (f & 5)]
+
+    def export_submodel(self, p):
+        """Serialise submodel p's live ALS state (bytes) and remove it from this handle."""
+        nb = lib().jkcals_state_bytes(self._h, int(p))
+        if nb == 0:
+            raise JKCalsError(-1, f"submodel {p} is not on this handle")
+        buf = np.zeros(nb // 8)
+        self._check(lib().jkcals_export_submodel(self._h, int(p), _p(buf), nb))
+        return buf.tobytes()
+
+    def import_submodel(self, state):
+        """Adopt a submodel exported by another handle of the same problem (a free slot needed)."""
+        buf = np.frombuffer(bytes(state), dtype=np.float64).copy()
+        self._check(lib().jkcals_import_submodel(self._h, _p(buf), buf.nbytes))
 
     # ------------------------------------------------------------------ alignment (NEXT #3)
     def align(self):

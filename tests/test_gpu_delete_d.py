@@ -152,6 +152,6 @@ def test_delete_d_set_init_submodel_roundtrip():
 def test_delete_d_rejects_bad_d():
     from paper_2112_03985_b200 import JKCals, JKCalsError
     w = make_workload("tiny")
-    for d, rng_ in [(0, None), (6, None), (3, (0, 5))]:
+    for d, rng_ in [(-1, None), (6, None), (3, (0, 5))]:   # (d = 0 is plain CALS)
         with pytest.raises(JKCalsError):
             JKCals(w.T, w.R, d=d, sub_range=rng_)

@@ -157,3 +157,72 @@ def test_gloo_world2_gathers(tmp_path):
     for p, (o, e) in zip(procs, outs):
         assert p.returncode == 0, e
         assert o.startswith("ok")
+
+
+def test_plan_moves_balances_within_free_slots():
+    from paper_2112_03985_b200.dist import plan_moves
+    assert plan_moves([10, 2], [0, 6]) == [(0, 1, 4)]
+    assert plan_moves([5, 5, 5], [2, 2, 2]) == []
+    # capacity-bound: the destination only has 1 free slot
+    assert plan_moves([9, 0], [0, 1]) == [(0, 1, 1)]
+    # 4 ranks, one loaded: balanced to max - min <= 1 (free slots permitting)
+    act, free = [12, 0, 0, 0], [0, 8, 8, 8]
+    moves = plan_moves(act, free)
+    for s, d, n in moves:
+        act[s] -= n
+        act[d] += n
+    assert max(act) - min(act) <= 1 and sum(act) == 12
+    assert plan_moves([3], [5]) == []
+
+
+_GLOO_REBALANCE = r"""
+import sys, numpy as np, torch.distributed as dist
+sys.path.insert(0, sys.argv[1])
+from paper_2112_03985_b200.dist import rebalance
+
+class FakeHandle:
+    # stands in for JKCals on CPU: slots with ids, an active set, opaque per-submodel states
+    def __init__(self, ids, active, spare):
+        self.slots = list(ids) + [-1] * spare
+        self.act = set(active)
+    def ids(self):
+        return np.array(self.slots, dtype=np.int64)
+    def active_ids(self):
+        return sorted(p for p in self.slots if p >= 0 and p in self.act)
+    def export_submodel(self, p):
+        self.slots[self.slots.index(p)] = -1
+        self.act.discard(p)
+        return np.array([p, 7 * p], dtype=np.float64).tobytes()
+    def import_submodel(self, b):
+        p, chk = np.frombuffer(b, dtype=np.float64)
+        assert chk == 7 * p
+        self.slots[self.slots.index(-1)] = int(p)
+        self.act.add(int(p))
+
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:" + sys.argv[2], rank=int(sys.argv[3]), world_size=2)
+r = dist.get_rank()
+# rank 0: 10 active of its 12; rank 1: 1 active of its 12 (the rest converged); 6 spare slots each
+h = FakeHandle(range(12 * r, 12 * r + 12), range(12 * r, 12 * r + (10 if r == 0 else 1)), 6)
+moves = rebalance(h)
+assert moves == [(0, 1, 4)], moves
+n = len(h.active_ids())
+assert n == (6 if r == 0 else 5), (r, n, h.active_ids())
+if r == 1:
+    assert h.active_ids() == [6, 7, 8, 9, 12], h.active_ids()
+dist.barrier()
+dist.destroy_process_group()
+print("ok", r)
+"""
+
+
+def test_gloo_world2_rebalance(tmp_path):
+    script = tmp_path / "rb.py"
+    script.write_text(_GLOO_REBALANCE)
+    port = str(_free_port())
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    procs = [subprocess.Popen([sys.executable, str(script), ROOT, port, str(r)], stdout=subprocess.PIPE,
+                              stderr=subprocess.PIPE, text=True, env=env) for r in range(2)]
+    outs = [p.communicate(timeout=180) for p in procs]
+    for p, (o, e) in zip(procs, outs):
+        assert p.returncode == 0, e
+        assert o.startswith("ok")
