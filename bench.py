@@ -153,6 +153,7 @@ def main():
     ap.add_argument("--ref-sweeps", type=int, default=30, help="sweeps per oracle sample step (~10 s on 16 cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the supplementary FP32-path measurement")
+    ap.add_argument("--no-supp", action="store_true", help="skip the supplementary pool / delete-d lines")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -292,6 +293,47 @@ def main():
                              "peak_source": "measured bf16 cuBLAS 1678 TF/s x nominal tf32/bf16 ratio 1.1/2.25"},
                 "parity_bar": "1e-4 relative Frobenius vs the FP64 oracle"}
         h32.close()
+    # --- supplementary (N = 1 only): the paper's "All" pool (50 x 200 x 200, R in {3,5,7,9}, the
+    # P:496-504 medium tensor) and delete-d on the bench workload, 100 fixed sweeps each, FP64
+    supp = None
+    if world == 1 and not args.no_supp:
+        from synth import make_pool
+
+        def timed(hh, init, sweeps, reps=2):
+            hh.set_init(init)
+            hh.iterate(sweeps, 0.0)
+            tot = 0.0
+            for _ in range(reps):
+                flush.random_(0, 255)
+                torch.cuda.synchronize()
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record(hh.stream)
+                hh.set_init(init)
+                hh.iterate(sweeps, 0.0)
+                e.record(hh.stream)
+                e.synchronize()
+                tot += s.elapsed_time(e)
+            return tot / reps / 1e3
+
+        pw = make_pool("all_medium")
+        hp = JKCals(pw.T, list(pw.ranks), hist_cap=pw.sweeps)
+        tp = timed(hp, pw.Ps, pw.sweeps)
+        fl_p = hp.sweep_flops() * pw.sweeps
+        hp.close()
+        dd = 10
+        hd = JKCals(Td, w.R, hist_cap=w.sweeps, dims=w.dims, d=dd)
+        td = timed(hd, w.P, w.sweeps)
+        fl_d = hd.sweep_flops() * w.sweeps
+        hd.close()
+        supp = {
+            "all_pool": {"workload": "all_medium: 50x200x200, models R in {3,5,7,9} jackknifed together "
+                                     "(200 submodels, C = 1200), 100 sweeps", "value": round(tp, 5), "unit": "s",
+                         "mttkrp_flop_rate_tflops": round(fl_p / tp / 1e12, 2)},
+            "delete_d": {"workload": f"{args.config} delete-{dd} jackknife ({-(-w.dims[0] // dd)} groups), "
+                                     f"{w.sweeps} sweeps", "value": round(td, 5), "unit": "s",
+                         "mttkrp_flop_rate_tflops": round(fl_d / td / 1e12, 2)},
+        }
+
     line = None
     if rank == 0:
         cpu = None
@@ -320,6 +362,7 @@ def main():
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches_per_step * args.steps),
             "fp32_path": fp32,
+            "supplementary": supp,
             "clocks": {"sm_mhz": csum["sm_mhz"], "sm_max_mhz": csum["sm_max_mhz"], "reasons": csum["reasons"]},
         }
         print(json.dumps(line), flush=True)
