@@ -231,6 +231,12 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
         double* st = stage0 + (size_t)slot * stage_sz;
         uint64_t* bar = &full[slot];
         const bool new_slab = (ld_b0 != loaded_b0);
+        // the slab buffer (b0 & 1) was last read by the tiles of block b0 - 2; the slot WAR wait
+        // above covers them only when a block spans >= STAGES - 1 tiles, so for very short
+        // blocks (tiny tensors) drain every issued tile first
+        if (new_slab && loaded_b0 >= 0 && v.Jp < STAGES - 1)
+          for (unsigned q = (ld_git >= (unsigned)STAGES ? ld_git - STAGES + 1 : 0); q < ld_git; ++q)
+            mbar_wait(&empty[q % STAGES], (q / STAGES) & 1u);
         {
           mbar_expect_tx(bar, Cfg::kTBytes + s_bytes + (new_slab ? (unsigned)(kBK * kBMP * 8) : 0u));
           // U_q0 rows [b0*BK, b0*BK+BK) x columns [c0, c0+BMP): OOB rows are zero
