@@ -141,10 +141,36 @@ struct ModePlan {
 // CTA b processes units [cta_u[b], cta_u[b+1]) of the (tile, k-tile) space, split uniformly.
 // (r01 measurement: weighting units by their DMMA count made the CTAs on ragged tiles the
 // stragglers -- the per-k-tile time is dominated by its fixed part -- so the split is uniform.)
-void finish_plan(ModePlan& p, const ModeGeo& mg) {
-  (void)mg;
+// Stream-K split of the (tile, k-tile) units over G CTAs. A unit of a ragged tile (the last
+// M tile when C is not a multiple of 128, the last N tile) costs less than a full one: cost =
+// alpha + (1 - alpha) * (live DMMA fraction of the tile), alpha the per-k-tile fixed share
+// (barriers, fragment loads, KRP scaling). alpha = 1 is the uniform split.
+void finish_plan(ModePlan& p, const ModeGeo& mg, int64_t C = 0, double alpha = 1.0) {
   p.cta_u.assign(p.G + 1, 0);
-  for (int b = 0; b <= p.G; ++b) p.cta_u[b] = (int)((int64_t)b * p.units / p.G);
+  if (alpha >= 1.0 || C <= 0) {
+    for (int b = 0; b <= p.G; ++b) p.cta_u[b] = (int)((int64_t)b * p.units / p.G);
+  } else {
+    std::vector<double> w(p.ntiles), cum(p.ntiles + 1, 0.0);
+    for (int t = 0; t < p.ntiles; ++t) {
+      const int tm = t % p.nMt, tn = t / p.nMt;
+      const int64_t lc = std::min<int64_t>(kBM, C - (int64_t)tm * kBM);
+      const int64_t lr = std::min<int64_t>(p.BN, mg.In - (int64_t)tn * p.BN);
+      const double f = (double)rup(lc, 16) / kBM * (double)rup(lr, 8) / p.BN;
+      w[t] = alpha + (1.0 - alpha) * f;
+      cum[t + 1] = cum[t] + w[t] * p.KT;
+    }
+    int t = 0;
+    for (int b = 0; b <= p.G; ++b) {
+      const double target = cum[p.ntiles] * b / p.G;
+      while (t < p.ntiles - 1 && cum[t + 1] < target) ++t;
+      int64_t u = (int64_t)t * p.KT + (int64_t)std::llround((target - cum[t]) / w[t]);
+      u = std::min<int64_t>(std::max<int64_t>(u, 0), p.units);
+      p.cta_u[b] = (int)u;
+    }
+    p.cta_u[0] = 0;
+    p.cta_u[p.G] = (int)p.units;
+    for (int b = 1; b <= p.G; ++b) p.cta_u[b] = std::max(p.cta_u[b], p.cta_u[b - 1]);
+  }
   // drop empty ranges so that the CTAs touching a tile are consecutive and the piece index of
   // CTA b in tile t is b - first_cta[t]
   p.cta_u.erase(std::unique(p.cta_u.begin(), p.cta_u.end()), p.cta_u.end());
@@ -227,7 +253,13 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
   constexpr int64_t kMaxPieces = 48;
   gmax = std::min<int64_t>(gmax, kMaxPieces * p.ntiles);
   p.G = (int)std::min<int64_t>(p.units, gmax);
-  finish_plan(p, mg);
+  // cost-weighted split only when a tile is mostly idle (e.g. 4-way C = 400: the last M tile
+  // has 16 of 128 columns): r01 measured alpha = 0.7 +6 % there, while nearly-full ragged tiles
+  // (syn200: 104 of 128) are best with the uniform split. JKCALS_SK_ALPHA overrides (tuning).
+  static double env_alpha = [] { const char* e = getenv("JKCALS_SK_ALPHA"); return e ? atof(e) : -1.0; }();
+  const double live_m = (double)rup(C - (int64_t)(p.nMt - 1) * kBM, 16) / kBM;
+  const double alpha = env_alpha >= 0.0 ? env_alpha : (live_m < 0.5 ? 0.7 : 1.0);
+  finish_plan(p, mg, C, alpha);
   return p;
 }
 
