@@ -1,0 +1,112 @@
+"""GPU robustness tests from SURVEY §4 / §5 (SPEC acceptance items): fusion transparency,
+the padded-row invariant after EVERY sweep, monotone error histories, per-submodel fault
+isolation, and checkpoint / resume through get_factors + set_init_submodel."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from synth import make_workload
+
+pytestmark = pytest.mark.gpu
+NCPU = os.cpu_count() or 1
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def test_fusion_transparency_block_equals_solo():
+    # a submodel fitted inside the fused batch equals the same submodel
+    # fitted alone (only the split-K summation order differs: rounding level)
+    from paper_2112_03985_b200 import JKCals
+    w = make_workload("syn50_r3")
+    full = JKCals(w.T, w.R, hist_cap=100)
+    full.set_init(w.P)
+    full.iterate(100, 0.0)
+    for p in (0, 17, 49):
+        solo = JKCals(w.T, w.R, sub_range=(p, p + 1), hist_cap=100)
+        solo.set_init(w.P)
+        solo.iterate(100, 0.0)
+        fa, la = full.factors(p)
+        fb, lb = solo.factors(p)
+        for a, b in zip(fa, fb):
+            assert rel(a, b) <= 1e-12, (p, rel(a, b))
+        assert np.allclose(full.history(p), solo.history(p), rtol=1e-12)
+
+
+@pytest.mark.parametrize("d", [1, 3])
+def test_padded_rows_zero_after_every_sweep(d):
+    # the group's rows are bitwise zero in the fused mode-0 factor after
+    # every sweep (checked sweep by sweep, graph replay path)
+    from paper_2112_03985_b200 import JKCals
+    w = make_workload("tiny")
+    h = JKCals(w.T, w.R, hist_cap=20, d=d)
+    h.set_init(w.P)
+    G = -(-10 // d)
+    for sweep in range(20):
+        h.iterate(1, 0.0)
+        for g in range(G):
+            rows = list(range(g * d, min(g * d + d, 10)))
+            assert np.all(h.block(g, 0)[rows] == 0.0), (sweep, g)
+
+
+def test_error_history_monotone():
+    # ALS never increases the error (slack 1e-12 ||T||^2) -- on the GPU histories
+    from paper_2112_03985_b200 import JKCals
+    w = make_workload("syn50_r4")
+    h = JKCals(w.T, w.R, hist_cap=100)
+    h.set_init(w.P)
+    h.iterate(100, 0.0)
+    slack = 1e-12 * O.norm_sq(w.T)
+    for p in range(50):
+        e = h.history(p)
+        assert np.all(np.diff(e) <= slack), (p, np.diff(e).max())
+
+
+def test_fault_isolated_to_one_submodel():
+    # SURVEY §5 fault injection: a submodel driven to overflow (factor scaled by 1e300) is
+    # flagged non-finite and frozen; every other submodel is untouched (bitwise vs a clean run)
+    from paper_2112_03985_b200 import JKCals
+    w = make_workload("syn50_r2")
+    clean = JKCals(w.T, w.R, hist_cap=30)
+    clean.set_init(w.P)
+    clean.iterate(30, 0.0)
+    h = JKCals(w.T, w.R, hist_cap=30)
+    h.set_init(w.P)
+    bad = w.P[2] * 1e300
+    h.set_init_submodel(7, 2, bad)
+    h.set_init_submodel(7, 1, w.P[1] * 1e300)
+    h.iterate(30, 0.0)
+    st = h.status()
+    assert st["flags"][7] & 4, st["flags"][7]            # F_NONFINITE
+    assert st["iters"][7] < 30                             # frozen
+    for p in range(50):
+        if p == 7:
+            continue
+        assert not (st["flags"][p] & 4)
+        for a, b in zip(h.factors(p)[0], clean.factors(p)[0]):
+            assert rel(a, b) <= 1e-12
+
+
+def test_checkpoint_resume():
+    # get_factors + set_init_submodel resume. 20 sweeps, checkpoint every submodel,
+    # resume in a fresh handle for 20 more == 40 sweeps straight (oracle at 1e-10)
+    from paper_2112_03985_b200 import JKCals
+    w = make_workload("tiny")
+    a = JKCals(w.T, w.R, hist_cap=40)
+    a.set_init(w.P)
+    a.iterate(20, 0.0)
+    ck = {p: a.factors(p)[0] for p in range(10)}
+    b = JKCals(w.T, w.R, hist_cap=40)
+    b.set_init(w.P)
+    for p, fac in ck.items():
+        for n, U in enumerate(fac):
+            b.set_init_submodel(p, n, U)
+    b.iterate(20, 0.0)
+    res = O.jk_als(w.T, w.P, max_iters=40, nthreads=NCPU)
+    for p in range(10):
+        for x, y in zip(b.factors(p)[0], res.factors[p]):
+            assert rel(x, y) <= 1e-10, (p, rel(x, y))

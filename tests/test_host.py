@@ -226,3 +226,9 @@ def test_gloo_world2_rebalance(tmp_path):
     for p, (o, e) in zip(procs, outs):
         assert p.returncode == 0, e
         assert o.startswith("ok")
+
+
+def test_binding_defaults_follow_the_paper():
+    # tol 1e-6 and max_iters 1000
+    from paper_2112_03985_b200 import DEFAULT_MAX_ITERS, DEFAULT_TOL
+    assert DEFAULT_TOL == 1e-6 and DEFAULT_MAX_ITERS == 1000
