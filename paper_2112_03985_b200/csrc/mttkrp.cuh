@@ -402,6 +402,9 @@ __global__ void __launch_bounds__(256) krp_gen_kernel(ModeView v, int C, int64_t
   for (int q = 0; q < kMaxModes - 1; ++q)
     if (q < v.nrest) { idx[q] = rem % v.rdim[q]; rem /= v.rdim[q]; }
   const bool full4 = (c + 4 <= C) && ((ldu & 3) == 0) && ((ldk & 3) == 0);
+  // unrolled so that the factor-row loads of several rows are in flight at once (the loop is
+  // otherwise one L2 round trip per 32-byte store); streaming (.cs) stores: K is not re-read here
+#pragma unroll 4
   for (int j = j0; j < j1; ++j) {
     double r0 = 1.0, r1 = 1.0, r2 = 1.0, r3 = 1.0;
 #pragma unroll
@@ -421,7 +424,7 @@ __global__ void __launch_bounds__(256) krp_gen_kernel(ModeView v, int C, int64_t
     }
     double* dst = K + (int64_t)j * ldk + c;
     if (full4) {
-      asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(dst), "d"(r0), "d"(r1), "d"(r2), "d"(r3)
+      asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(dst), "d"(r0), "d"(r1), "d"(r2), "d"(r3)
                    : "memory");
     } else {
       dst[0] = r0;
