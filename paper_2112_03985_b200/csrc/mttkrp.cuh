@@ -388,7 +388,7 @@ __global__ void reduce_parts_kernel(const double* __restrict__ parts, const Tile
 // Materialised Khatri-Rao generation (a1 in SURVEY §8a): K(j, c) = prod_{m != n} U_m(i_m(j), c),
 // row-major J x ldk. Each thread owns 4 consecutive columns and a run of kKrpRows consecutive j,
 // advancing the mixed-radix index incrementally; stores are 32-byte vectors (st.global.v4.f64).
-constexpr int kKrpRows = 64;
+constexpr int kKrpRows = 16;  // r01 sweep: 4-8-16-64-256 rows per CTA -> 16 best (4.0-4.5 TB/s)
 __global__ void __launch_bounds__(256) krp_gen_kernel(ModeView v, int C, int64_t ldu, double* __restrict__ K,
                                                       int64_t ldk) {
   const int c = (blockIdx.y * blockDim.x + threadIdx.x) * 4;
