@@ -53,6 +53,36 @@ struct EpiArgs {
 
 constexpr int kEpiThreads = 128;
 
+// Pre-reduction of the stream-K partial pieces for tiles split over many CTAs (a small-C shard
+// fills the GPU with up to 64 CTAs per tile; one epilogue CTA per submodel would otherwise sum
+// them alone). Element e of tile t: red[t][e] = ((0 + p_0) + p_1) + ... in piece order -- the
+// very sum the epilogue forms itself, so results are bitwise those of the direct path. The
+// epilogue then reads one piece per tile.
+__global__ void __launch_bounds__(256) reduce_pieces_kernel(const double* __restrict__ parts,
+                                                            const TileInfo* __restrict__ tinfo, int ntiles,
+                                                            int tile_elems, double* __restrict__ red) {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the MTTKRP grid has completed
+  asm volatile("griddepcontrol.launch_dependents;\n" :::);
+  const int64_t total = (int64_t)ntiles * tile_elems;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(e / tile_elems);
+    const int64_t o = e - (int64_t)t * tile_elems;
+    const TileInfo ti = tinfo[t];
+    const double* p = parts + (int64_t)ti.piece_base * tile_elems + o;
+    double s = 0.0;
+    int pc = 0;
+    for (; pc + 8 <= ti.npieces; pc += 8) {
+      double x[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) x[q] = __ldcg(p + (int64_t)(pc + q) * tile_elems);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s += x[q];
+    }
+    for (; pc < ti.npieces; ++pc) s += __ldcg(p + (int64_t)pc * tile_elems);
+    red[e] = s;
+  }
+}
+
 template <int RMAX>
 __device__ __forceinline__ void block_sum(double* vals, int cnt, double* red) {
   // vals: per-thread array of cnt (<= RMAX*RMAX + RMAX + 1) values -> summed into red[0..cnt)

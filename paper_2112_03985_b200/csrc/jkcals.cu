@@ -250,8 +250,10 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
   int64_t gmax = (int64_t)ki.nsm * ki.occ[p.KM][p.ST4][p.NT - 1][mg.nslow];
   // at most kMaxPieces partial pieces per output tile: small problems (few tiles) would
   // otherwise write and re-read a BN x BM piece per CTA for ~1 k-tile of work each
+  // (only for < 4 tiles: a single 128-column M tile x 5 N tiles -- a syn200 shard at 8 GPUs --
+  // must still fill both CTA slots of every SM, r01 +20 %; such tiles are pre-reduced, kRedPieces)
   constexpr int64_t kMaxPieces = 48;
-  gmax = std::min<int64_t>(gmax, kMaxPieces * p.ntiles);
+  if (p.ntiles < 4) gmax = std::min<int64_t>(gmax, kMaxPieces * p.ntiles);
   p.G = (int)std::min<int64_t>(p.units, gmax);
   // cost-weighted split only when a tile is mostly idle (e.g. 4-way C = 400: the last M tile
   // has 16 of 128 columns): r01 measured alpha = 0.7 +6 % there, while nearly-full ragged tiles
@@ -262,6 +264,8 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
   finish_plan(p, mg, C, alpha);
   return p;
 }
+
+constexpr int kRedPieces = 16;  // pre-reduce when a tile has more partial pieces than this
 
 int64_t plan_parts_doubles(const ModePlan& p) { return (int64_t)p.npieces * p.BN * kBM; }
 
@@ -278,7 +282,8 @@ std::vector<char> pack_plan(const ModePlan& p) {
 void plan_bounds(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, int64_t* parts, int* tiles,
                  bool tf32 = false) {
   ModePlan p = make_plan(mg, n, C, ki, tf32);
-  *parts = (int64_t)(p.G + p.ntiles) * p.BN * kBM;
+  // any later (compacted, smaller-C) plan has G <= 8 nsm CTAs and <= ntiles tiles
+  *parts = (int64_t)(std::max<int64_t>(p.G, 8 * (int64_t)ki.nsm) + p.ntiles) * p.BN * kBM;
   *tiles = p.ntiles;
 }
 
@@ -403,7 +408,8 @@ struct Layout {
 };
 
 struct Offsets {
-  size_t T, T32hi, T32lo, T1hi, T1lo, U[2][kMaxModes], Ures, parts, tinfo[kMaxModes], gram, lambda, normT2p, fit, fit_prev, err, hist,
+  size_t T, T32hi, T32lo, T1hi, T1lo, U[2][kMaxModes], Ures, parts, tinfo[kMaxModes], tinfo1[kMaxModes], red, gram,
+      lambda, normT2p, fit, fit_prev, err, hist,
       slice, slice_part, stage, iters, flags, active, blk2sub, map, pglob, misc, srcoff, srcld, subR, subRc, blkcol,
       dstoff, pref[kMaxModes], aln, aperm, asign, acong, asrc, asld, srcpg;
   int64_t parts_cap;
@@ -446,6 +452,14 @@ bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_c
   }
   o->parts = L.take(o->parts_cap * 8);
   for (int n = 0; n < N; ++n) o->tinfo[n] = L.take(plan_table_bytes(o->tiles_cap, ki.nsm * 8));
+  // pre-reduced pieces (one per tile) for tiles split over many CTAs, and their 1-piece tables
+  int64_t red_cap = 0;
+  for (int n = 0; n < N; ++n) {
+    const ModePlan q = make_plan(mode_geo(N, dims, n), n, C, ki, tf32);
+    red_cap = std::max<int64_t>(red_cap, (int64_t)q.ntiles * q.BN * kBM);
+  }
+  o->red = L.take(red_cap * 8);
+  for (int n = 0; n < N; ++n) o->tinfo1[n] = L.take(o->tiles_cap * sizeof(TileInfo));
   o->gram = L.take((size_t)N * nsub * R * R * 8);
   o->lambda = L.take(nsub * R * 8);
   o->normT2p = L.take(nsub * 8);
@@ -538,6 +552,8 @@ struct jkcals_s {
   CUtensorMap tmT[kMaxModes];
   CUtensorMap tmU[2][kMaxModes];
   std::vector<char> table[kMaxModes];  // host copy of each mode's device plan table
+  bool red_on[kMaxModes] = {false};    // pieces of this mode pre-reduced before the epilogue
+  std::vector<TileInfo> table1[kMaxModes];
   int tf32 = 0;                        // precision JKCALS_FP32: 3xTF32 tcgen05 MTTKRP
   CUtensorMap tmThi[kMaxModes], tmTlo[kMaxModes];
   cudaGraphExec_t gexec = nullptr;
@@ -599,6 +615,22 @@ jkcals_status replan(jkcals_t h) {
       return fail(h, JKCALS_E_OOM, "internal: plan exceeds workspace bounds");
     h->table[n] = pack_plan(p);
     CKH(h, cudaMemcpyAsync(h->ptr<TileInfo>(h->off.tinfo[n]), h->table[n].data(), h->table[n].size(),
+                           cudaMemcpyHostToDevice, h->stream));
+    // many pieces per tile: pre-reduce them with the whole GPU (kRedPieces, r01: G = 8 shard)
+    int maxp = 0;
+    for (const TileInfo& ti : p.tinfo) maxp = std::max(maxp, ti.npieces);
+    static int red_thr = [] { const char* e = getenv("JKCALS_RED_PIECES"); return e ? atoi(e) : kRedPieces; }();
+    // ... and only when each epilogue CTA would sum many pieces over many rows (r01: a syn200 shard
+    // at G = 8, I_n x pieces = 200 x 59, gains 14 %; syn50, 50 x 48, loses 20 % to the extra launch)
+    h->red_on[n] = red_thr > 0 && maxp > red_thr && h->dims[n] * maxp > 8192;
+    h->table1[n].assign(p.ntiles, TileInfo{});
+    for (int t = 0; t < p.ntiles; ++t) {
+      h->table1[n][t].first_cta = 0;
+      h->table1[n][t].npieces = 1;
+      h->table1[n][t].piece_base = t;
+      h->table1[n][t].pad_ = 0;
+    }
+    CKH(h, cudaMemcpyAsync(h->ptr<TileInfo>(h->off.tinfo1[n]), h->table1[n].data(), p.ntiles * sizeof(TileInfo),
                            cudaMemcpyHostToDevice, h->stream));
     // TMA descriptors: the tensor view of mode n and the U_q0 slab source of both U buffer sets
     if (!make_tmap_T(&h->tmT[n], h->ptr<double>(h->off.T), h->N, h->dims, h->I0p, n, p.BN, bnp_of(p.NT)))
@@ -744,6 +776,25 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
   }
   CKH(h, cudaGetLastError());
   if (timed) CKH(h, cudaEventRecord(h->ev[4 * n + 1], h->es));
+  const double* epi_parts = parts;
+  const TileInfo* epi_ti = ti;
+  if (h->red_on[n]) {  // pre-reduce the pieces across the whole GPU (PDL-chained)
+    const int tile_elems = p.BN * kBM;
+    const int64_t tot = (int64_t)p.ntiles * tile_elems;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = (h->pdl && !timed) ? 1 : 0;
+    cfg.gridDim = dim3((unsigned)std::min<int64_t>(cdiv(tot, 256), 4 * (int64_t)h->ki->nsm));
+    cfg.blockDim = dim3(256);
+    cfg.stream = h->es;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    double* red = h->ptr<double>(h->off.red);
+    CKH(h, cudaLaunchKernelEx(&cfg, reduce_pieces_kernel, (const double*)parts, ti, p.ntiles, tile_elems, red));
+    epi_parts = red;
+    epi_ti = h->ptr<TileInfo>(h->off.tinfo1[n]);
+  }
   EpiArgs a;
   a.N = h->N;
   a.n = n;
@@ -757,8 +808,8 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
   a.blk2sub = h->ptr<int>(h->off.blk2sub);
   a.pglob = h->ptr<int64_t>(h->off.pglob);
   a.d = (int)h->d;
-  a.parts = parts;
-  a.tinfo = ti;
+  a.parts = epi_parts;
+  a.tinfo = epi_ti;
   a.BM = kBM;
   a.BN = p.BN;
   a.nMt = p.nMt;
@@ -1866,7 +1917,12 @@ double jkcals_sweep_flops(jkcals_t h) {
   return 2.0 * (double)h->C * (double)h->P * (double)h->N;
 }
 
-int jkcals_launches_per_sweep(jkcals_t h) { return h ? 2 * h->N : 0; }
+int jkcals_launches_per_sweep(jkcals_t h) {
+  if (!h) return 0;
+  int n_red = 0;
+  for (int n = 0; n < h->N; ++n) n_red += h->red_on[n] ? 1 : 0;
+  return 2 * h->N + n_red;
+}
 
 const char* jkcals_last_error(jkcals_t h) { return h ? h->err.c_str() : "null handle"; }
 
