@@ -456,6 +456,8 @@ __device__ __forceinline__ void epi_smem_body(const EpiArgs& a, const int k, con
 #ifdef JK_EPI_PROF
   __shared__ unsigned long long epi_ts_[16];
 #endif
+  EPI_PROBE(0);  // (stamps are relative to the body's start, after griddepcontrol.wait)
+  EPI_PROBE(1);
   const int Rs = a.R, n = a.n, N = a.N, tid = threadIdx.x, In = a.In;
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int NW = kEpi2Threads / 32;

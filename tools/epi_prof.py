@@ -12,7 +12,8 @@ import torch
 from paper_2112_03985_b200 import JKCals
 from synth import make_workload
 w = make_workload(sys.argv[1] if len(sys.argv) > 1 else "syn200")
-h = JKCals(w.T, w.R, hist_cap=10)
+nsub = int(sys.argv[2]) if len(sys.argv) > 2 else w.dims[0]
+h = JKCals(w.T, w.R, hist_cap=10, sub_range=(0, nsub))
 h.set_init(w.P)
 h.iterate(2, 0.0)
 torch.cuda.synchronize()
