@@ -909,7 +909,7 @@ jkcals_status set_blocks(jkcals_t h, const std::vector<int>& b2s) {
   return JKCALS_OK;
 }
 
-int64_t sum_dims(jkcals_t h) {
+int64_t sum_dims(const jkcals_s* h) {
   int64_t sumI = 0;
   for (int n = 0; n < h->N; ++n) sumI += h->dims[n];
   return sumI;
@@ -1392,7 +1392,7 @@ jkcals_status jkcals_get_factors(jkcals_t h, int64_t p, int mode, double* U, dou
   if (!h || !U || mode < 0 || mode >= h->N || slot_of(h, p) < 0) return JKCALS_E_ARG;
   if (!h->inited) return fail(h, JKCALS_E_STATE, "no model yet");
   DeviceGuard dg(h->device);
-  const double* src;
+  const double* src = nullptr;
   int64_t ld;
   int sub;
   jkcals_status st = locate(h, p, mode, &src, &ld, &sub);
@@ -1467,7 +1467,7 @@ jkcals_status jkcals_get_block(jkcals_t h, int64_t p, int mode, double* U) {
   if (!h || !U || mode < 0 || mode >= h->N || slot_of(h, p) < 0) return JKCALS_E_ARG;
   if (!h->inited) return fail(h, JKCALS_E_STATE, "no model yet");
   DeviceGuard dg(h->device);
-  const double* src;
+  const double* src = nullptr;
   int64_t ld;
   int sub;
   jkcals_status st = locate(h, p, mode, &src, &ld, &sub);
@@ -1521,10 +1521,8 @@ static jkcals_status build_src_table(jkcals_t h, int mode, const std::vector<int
   const int ns = (int)subs.size();
   std::vector<int64_t> off(ns), ld(ns);
   for (int q = 0; q < ns; ++q) {
-    const double* src;
-    int64_t l;
-    int sub;
-    (void)sub;
+    const double* src = nullptr;
+    int64_t l = 0;
     jkcals_status st = locate_slot(h, subs[q], mode, &src, &l);
     if (st != JKCALS_OK) return st;
     off[q] = src - reinterpret_cast<const double*>(h->ws);
@@ -1597,10 +1595,8 @@ jkcals_status jkcals_align(jkcals_t h) {
   std::vector<int64_t> off((size_t)h->nsub * h->N), ld((size_t)h->nsub * h->N);
   for (int q = 0; q < h->nsub; ++q)
     for (int n = 0; n < h->N; ++n) {
-      const double* src;
-      int64_t l;
-      int sub;
-      (void)sub;
+      const double* src = nullptr;
+      int64_t l = 0;
       if (h->h_id[q] < 0) {  // free slot: nothing to align (R = 0 there)
         off[(size_t)q * h->N + n] = 0;
         ld[(size_t)q * h->N + n] = 0;
@@ -1752,7 +1748,7 @@ enum { kStHdr = 16 };
 static const double kStMagic = 1245397825.0;  // "JKCA"
 
 static size_t state_doubles(const jkcals_s* h, int R) {
-  return kStHdr + (size_t)R + (size_t)h->N * R * R + (size_t)h->hist_cap + (size_t)sum_dims(const_cast<jkcals_s*>(h)) * R;
+  return kStHdr + (size_t)R + (size_t)h->N * R * R + (size_t)h->hist_cap + (size_t)sum_dims(h) * R;
 }
 
 size_t jkcals_state_bytes(jkcals_t h, int64_t p) {
