@@ -239,6 +239,19 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
       p.nNt = (int)ntiles_n;
     }
   }
+  // JKCALS_FORCE_NT=<mode>:<NT>[,<mode>:<NT>...] overrides the model (tuning experiments only)
+  if (const char* e = getenv("JKCALS_FORCE_NT")) {
+    for (const char* q = e; *q;) {
+      int mm = -1, nt = 0, used = 0;
+      if (sscanf(q, "%d:%d%n", &mm, &nt, &used) != 2) break;
+      if (mm == n && nt >= 1 && nt <= kMaxNT) {
+        p.NT = nt;
+        p.nNt = (int)cdiv(nI8, nt);
+      }
+      q += used;
+      if (*q == ',') ++q;
+    }
+  }
   p.BN = p.NT * 8;
   p.KM = (n != 0) ? 1 : 0;
   p.ST4 = (mg.Jp >= 3) ? 1 : 0;  // the U_q0 slab double buffer needs J' >= STAGES - 1
