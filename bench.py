@@ -365,6 +365,8 @@ def main():
                          "kernel": "mttkrp_dmma_kernel (FP64 DMMA)", "flops_per_launch": flops_launch,
                          "avg_launch_ms": round(avg_launch_ms, 4), "share_of_step": round(mttkrp_share, 4),
                          "frac_of_cublas_dgemm": round(achieved / FP64_DGEMM_TFLOPS, 4),
+                         # the JK-ALS-useful share of the padded work, (I_0 - 1) / I_0
+                         "useful_tflops": round(achieved * (w.dims[0] - 1) / w.dims[0], 3),
                          "peak_source": "measured FP64 DMMA pipe peak (profiles/r01_fp64_microbench.txt)"},
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e, 4), "unit": "s", "h2d_bytes_per_step": int(h2d),
