@@ -514,3 +514,10 @@ def test_present_stats():
     m2, s2, c2 = O.present_stats(Y)
     mj, sj = O.jackknife_stats(Y)
     assert np.allclose(m2, mj, rtol=1e-14) and np.allclose(s2, sj, rtol=1e-13) and np.all(c2 == 6)
+
+
+def test_mode0_full_reindexing():
+    # a submodel's mode-0 factor without its group's rows, put back on the I_0 global rows
+    U0 = np.arange(14.0).reshape(7, 2)
+    F = O.mode0_full(U0, [3, 4, 5], 10)
+    assert np.all(np.isnan(F[3:6])) and np.array_equal(F[:3], U0[:3]) and np.array_equal(F[6:], U0[3:])
