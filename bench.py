@@ -176,9 +176,17 @@ def main():
     stream = h.stream
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 
+    from paper_2112_03985_b200.dist import allgather_moments
+
     def step():
+        # one whole job: warm start, fixed sweeps, then the jackknife statistics of modes 1..N-1
+        # (per-shard moments, all-gathered and Chan-merged over NCCL when N > 1)
         h.set_init(w.P)
         h.iterate(w.sweeps, 0.0)
+        for m in range(1, len(w.dims)):
+            mom = h.local_moments(m)
+            if world > 1:
+                allgather_moments(mom)
 
     def barrier():
         if world > 1:
@@ -268,7 +276,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = float(t.item())
 
-    launches_per_step = (2 * len(w.dims) + 1) + h.launches_per_sweep() * w.sweeps
+    # set_init: N init_blocks + N gram + 1 reset; the sweeps; N - 1 moments kernels
+    launches_per_step = (2 * len(w.dims) + 1) + h.launches_per_sweep() * w.sweeps + (len(w.dims) - 1)
 
     # --- supplementary: the optional FP32 path (3xTF32 on tcgen05, FP64 epilogue), same workload
     fp32 = None
