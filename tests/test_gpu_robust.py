@@ -110,3 +110,43 @@ def test_checkpoint_resume():
     for p in range(10):
         for x, y in zip(b.factors(p)[0], res.factors[p]):
             assert rel(x, y) <= 1e-10, (p, rel(x, y))
+
+
+def test_c_abi_from_plain_c(tmp_path):
+    # the boundary is a C ABI: a plain C99 program (tests/c_abi_demo.c, gcc, no Python) drives
+    # create / set_init / iterate / get_factors and must produce exactly the binding's results
+    import subprocess
+    from paper_2112_03985_b200 import JKCals, _build
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.dirname(_build.LIB)
+    exe = tmp_path / "c_abi_demo"
+    subprocess.check_call(["gcc", "-std=c99", "-O2", os.path.join(root, "tests", "c_abi_demo.c"),
+                           "-I", os.path.join(root, "include"), "-I", "/usr/local/cuda/include",
+                           "-L", libdir, "-ljkcals", "-L", "/usr/local/cuda/lib64", "-lcudart",
+                           "-Wl,-rpath," + libdir, "-o", str(exe)])
+    w = make_workload("tiny")
+    sweeps = 20
+    with open(tmp_path / "in.bin", "wb") as f:
+        np.array([len(w.dims), *w.dims, w.R], dtype=np.int64).tofile(f)
+        np.ravel(w.T, order="F").tofile(f)
+        for p in w.P:
+            np.ravel(p, order="F").tofile(f)
+    out = subprocess.run([str(exe), str(tmp_path / "in.bin"), str(tmp_path / "out.bin"), str(sweeps)],
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    got = np.fromfile(tmp_path / "out.bin")
+    h = JKCals(w.T, w.R, hist_cap=sweeps)
+    h.set_init(w.P)
+    h.iterate(sweeps, 0.0)
+    res = O.jk_als(w.T, w.P, max_iters=sweeps, nthreads=NCPU)
+    off = 0
+    for p in range(10):
+        fac, lam = h.factors(p)
+        for n, U in enumerate(fac):
+            blk = got[off:off + U.size].reshape(U.shape, order="F")
+            off += U.size
+            assert np.array_equal(blk, U), (p, n)          # same library, same results, bitwise
+            assert rel(blk, res.factors[p][n]) <= 1e-10
+        assert np.array_equal(got[off:off + w.R], lam)
+        off += w.R
+    assert off == got.size

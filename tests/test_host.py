@@ -232,3 +232,16 @@ def test_binding_defaults_follow_the_paper():
     # tol 1e-6 and max_iters 1000
     from paper_2112_03985_b200 import DEFAULT_MAX_ITERS, DEFAULT_TOL
     assert DEFAULT_TOL == 1e-6 and DEFAULT_MAX_ITERS == 1000
+
+
+def test_header_is_plain_c99_and_links(tmp_path):
+    # include/jkcals.h compiles as C99 and a C program links against libjkcals.so (no GPU needed
+    # to build; tests/test_gpu_robust.py runs the same program on a B200)
+    import subprocess
+    from paper_2112_03985_b200 import _build
+    lib = _build.build()
+    subprocess.check_call(["gcc", "-std=c99", "-Wall", "-Wextra", "-Werror", "-O2",
+                           os.path.join(ROOT, "tests", "c_abi_demo.c"), "-I", os.path.join(ROOT, "include"),
+                           "-I", "/usr/local/cuda/include", "-L", os.path.dirname(lib), "-ljkcals",
+                           "-L", "/usr/local/cuda/lib64", "-lcudart", "-o", str(tmp_path / "demo")])
+    assert (tmp_path / "demo").exists()
