@@ -164,6 +164,11 @@ jkcals_status jkcals_set_init(jkcals_t h, const double *const *P);
  * delete-d: (dims[0]-|group p|) x rank for mode 0, the group's rows absent). */
 jkcals_status jkcals_set_init_submodel(jkcals_t h, int64_t p, int mode, const double *U);
 
+/* The same for every submodel on the handle at once (SURVEY §8b set_init_submodels; resume from
+ * a checkpoint written with jkcals_get_all_factors): U is that call's packed layout for `mode`.
+ * Errors: E_STATE (before set_init, or a submodel was compacted out), E_NONFINITE, E_ARG. */
+jkcals_status jkcals_set_init_all(jkcals_t h, int mode, const double *U);
+
 /* Run up to max_iters ALS sweeps of all active submodels (Alg. 3 repeat loop,
  * PAPER.md:432-445). tol <= 0: exactly max_iters sweeps (the §5.1 protocol);
  * tol > 0: submodels freeze as they converge and converged submodels are compacted out of

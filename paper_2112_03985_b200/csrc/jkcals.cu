@@ -1333,6 +1333,41 @@ jkcals_status jkcals_set_init_submodel(jkcals_t h, int64_t p, int mode, const do
   return JKCALS_OK;
 }
 
+jkcals_status jkcals_set_init_all(jkcals_t h, int mode, const double* U) {
+  if (!h || !U || mode < 0 || mode >= h->N) return JKCALS_E_ARG;
+  if (!h->inited) return fail(h, JKCALS_E_STATE, "set_init must come first");
+  DeviceGuard dg(h->device);
+  // packed like jkcals_get_all_factors: the owned slots in slot order, each rows_q x R_q
+  const int I = (int)h->dims[mode];
+  std::vector<int> subs;
+  int64_t total = 0;
+  for (int q = 0; q < h->nsub; ++q)
+    if (h->h_id[q] >= 0) {
+      if (block_of(h, q) < 0) return fail(h, JKCALS_E_STATE, "submodel %lld was compacted out", (long long)h->h_id[q]);
+      subs.push_back(q);
+      total += (int64_t)(I - (mode == 0 ? group_rows(h, h->h_group[q]) : 0)) * h->h_subR[q];
+    }
+  for (int64_t e = 0; e < total; ++e)
+    if (!std::isfinite(U[e])) return fail(h, JKCALS_E_NONFINITE, "non-finite init");
+  if (total > h->off.stage_cap) return fail(h, JKCALS_E_OOM, "internal: staging buffer too small");
+  h->aligned = false;
+  double* stage = h->ptr<double>(h->off.stage);
+  CKH(h, cudaMemcpyAsync(stage, U, sizeof(double) * total, cudaMemcpyHostToDevice, h->stream));
+  int64_t o = 0;
+  for (int q : subs) {
+    const int R = h->h_subR[q];
+    const int cnt = mode == 0 ? (int)group_rows(h, h->h_group[q]) : 0;
+    set_block_kernel<<<(int)cdiv((int64_t)I * R, 256), 256, 0, h->stream>>>(
+        stage + o, I, R, h->ldu, h->h_blkcol[block_of(h, q)], mode == 0 ? h->h_group[q] * h->d : -1, cnt, h->U(mode));
+    CKH(h, cudaGetLastError());
+    o += (int64_t)(I - cnt) * R;
+  }
+  jkcals_status st = compute_grams(h);
+  if (st != JKCALS_OK) return st;
+  CKH(h, cudaStreamSynchronize(h->stream));  // U is the copy source
+  return JKCALS_OK;
+}
+
 jkcals_status jkcals_iterate(jkcals_t h, int max_iters, double tol, int* sweeps_done) {
   if (!h || max_iters < 0) return JKCALS_E_ARG;
   if (sweeps_done) *sweeps_done = 0;

@@ -64,6 +64,7 @@ def lib():
             "jkcals_get_aligned_stats": (I, [P, I, I, P, P]),
             "jkcals_set_init": (I, [P, P]),
             "jkcals_set_init_submodel": (I, [P, I64, I, P]),
+            "jkcals_set_init_all": (I, [P, I, P]),
             "jkcals_iterate": (I, [P, I, D, P]),
             "jkcals_get_factors": (I, [P, I64, I, P, P]),
             "jkcals_get_block": (I, [P, I64, I, P]),
@@ -93,7 +94,7 @@ def lib():
 EXPORTED = [
     "jkcals_workspace_bytes", "jkcals_create", "jkcals_create_d", "jkcals_pool_workspace_bytes",
     "jkcals_create_pool", "jkcals_get_model_stats", "jkcals_get_model_moments", "jkcals_align",
-    "jkcals_config_workspace_bytes", "jkcals_create_config", "jkcals_num_slots", "jkcals_get_ids",
+    "jkcals_set_init_all", "jkcals_config_workspace_bytes", "jkcals_create_config", "jkcals_num_slots", "jkcals_get_ids",
     "jkcals_state_bytes", "jkcals_export_submodel", "jkcals_import_submodel",
     "jkcals_get_alignment", "jkcals_get_aligned_factors", "jkcals_get_aligned_moments", "jkcals_get_aligned_stats",
     "jkcals_set_init", "jkcals_set_init_submodel", "jkcals_iterate",
@@ -238,6 +239,12 @@ class JKCals:
     def set_init_submodel(self, p, mode, U):
         m = np.asfortranarray(np.asarray(U, dtype=np.float64))
         self._check(lib().jkcals_set_init_submodel(self._h, int(p), int(mode), _p(m)))
+
+    def set_init_all(self, mode, U_all):
+        """Every submodel's mode-`mode` block at once, in the all_factors layout (array or list)."""
+        parts = list(U_all) if not isinstance(U_all, np.ndarray) or U_all.ndim == 3 else [U_all]
+        flat = np.concatenate([np.ravel(np.asarray(u, dtype=np.float64), order="F") for u in parts])
+        self._check(lib().jkcals_set_init_all(self._h, int(mode), _p(flat)))
 
     def iterate(self, max_iters=DEFAULT_MAX_ITERS, tol=DEFAULT_TOL):
         done = ctypes.c_int()

@@ -150,3 +150,29 @@ def test_c_abi_from_plain_c(tmp_path):
         assert np.array_equal(got[off:off + w.R], lam)
         off += w.R
     assert off == got.size
+
+
+def test_checkpoint_resume_all_factors_pool():
+    # batched resume: all_factors per mode -> set_init_all on a fresh handle (a mixed-rank pool
+    # with a ragged delete-d group), then the continued fit equals one straight run
+    from paper_2112_03985_b200 import JKCals
+    from synth import make_pool
+    w = make_pool(((11, 7, 6), (2, 3), 3, 0.01, "syn", 20), seed=3)
+    a = JKCals(w.T, list(w.ranks), hist_cap=30, d=3)
+    a.set_init(w.Ps)
+    a.iterate(12, 0.0)
+    ck = [a.all_factors(n)[0] for n in range(3)]
+    b = JKCals(w.T, list(w.ranks), hist_cap=30, d=3)
+    b.set_init(w.Ps)
+    for n in range(3):
+        b.set_init_all(n, ck[n])
+    for n in range(3):
+        got = b.all_factors(n)[0]
+        for x, y in zip(got, ck[n]):
+            assert np.array_equal(x, y)
+    b.iterate(18, 0.0)
+    for m, P in enumerate(w.Ps):
+        res = O.jk_als_d(w.T, P, 3, max_iters=30, nthreads=NCPU)
+        for g in range(4):
+            for x, y in zip(b.factors(m * 4 + g)[0], res.factors[g]):
+                assert rel(x, y) <= 1e-10
