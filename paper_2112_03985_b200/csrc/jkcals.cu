@@ -16,6 +16,8 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: host ranges for nsys timelines
 #include <vector>
 
 #include "../../include/jkcals.h"
@@ -590,6 +592,12 @@ struct jkcals_s {
 
 namespace {
 
+// RAII NVTX range around the host API calls (iterate, compaction, re-plan, create)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 jkcals_status fail(jkcals_t h, jkcals_status st, const char* fmt, ...) {
   if (h) {
     char buf[512];
@@ -621,6 +629,7 @@ struct DeviceGuard {
 };
 
 jkcals_status replan(jkcals_t h) {
+  NvtxRange nv("jkcals replan");
   for (int n = 0; n < h->N; ++n) {
     h->plan[n] = make_plan(mode_geo(h->N, h->dims, n), n, h->C, *h->ki, h->tf32 != 0);
     const ModePlan& p = h->plan[n];
@@ -959,6 +968,7 @@ jkcals_status relayout(jkcals_t h, const std::vector<int>& keep) {
 
 // (a8) compact: store converged live blocks, gather the active ones to the front.
 jkcals_status compact(jkcals_t h) {
+  NvtxRange nv("jkcals compact");
   std::vector<int> act(h->nsub);
   CKH(h, cudaMemcpyAsync(act.data(), h->ptr<int>(h->off.active), sizeof(int) * h->nsub, cudaMemcpyDeviceToHost,
                          h->stream));
@@ -1108,6 +1118,7 @@ jkcals_status jkcals_create_config(jkcals_t* out, const jkcals_config* cfg, cons
                                    size_t workspace_bytes) {
   if (!out) return JKCALS_E_ARG;
   *out = nullptr;
+  NvtxRange nv("jkcals_create");
   PoolGeo pg0;
   if (!pool_geo(cfg, &pg0) || !tensor || !workspace) return JKCALS_E_ARG;
   const int ndims = cfg->ndims, nmodels = cfg->nmodels, hist_cap = cfg->hist_cap, device = cfg->device;
@@ -1369,6 +1380,7 @@ jkcals_status jkcals_set_init_all(jkcals_t h, int mode, const double* U) {
 }
 
 jkcals_status jkcals_iterate(jkcals_t h, int max_iters, double tol, int* sweeps_done) {
+  NvtxRange nv("jkcals_iterate");
   if (!h || max_iters < 0) return JKCALS_E_ARG;
   if (sweeps_done) *sweeps_done = 0;
   if (!h->inited) return fail(h, JKCALS_E_STATE, "iterate before set_init");
