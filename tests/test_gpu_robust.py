@@ -176,3 +176,17 @@ def test_checkpoint_resume_all_factors_pool():
         for g in range(4):
             for x, y in zip(b.factors(m * 4 + g)[0], res.factors[g]):
                 assert rel(x, y) <= 1e-10
+
+
+@pytest.mark.parametrize("R", [7, 10, 12, 16])
+def test_large_ranks_epilogue_classes(R):
+    # the R > 8 rank classes (RMAX 10 / 12 / 16 epilogues, 16 = the ABI maximum) vs the oracle
+    from paper_2112_03985_b200 import JKCals
+    w = make_workload(((12, 30, 28), R, 16, 0.01, "syn", 15), seed=R)
+    h = JKCals(w.T, w.R, hist_cap=15)
+    h.set_init(w.P)
+    h.iterate(15, 0.0)
+    res = O.jk_als(w.T, w.P, max_iters=15, nthreads=NCPU)
+    for p in (0, 5, 11):
+        for a, b in zip(h.factors(p)[0], res.factors[p]):
+            assert rel(a, b) <= 1e-10, (R, p, rel(a, b))
