@@ -72,7 +72,7 @@ enum {
 #define JKCALS_MAX_MODES 8
 
 /* Bytes of device workspace needed by jkcals_create for these arguments on `device`.
- * ndims in [3, 8]; dims[k] >= 1, dims[0] >= 2; rank >= 1; n_sub = sub_end - sub_begin >= 1;
+ * ndims in [3, 8]; dims[k] >= 1, dims[0] >= 2; 1 <= rank <= 32 (ranks above 16 use the streaming large-rank epilogue); n_sub = sub_end - sub_begin >= 1;
  * hist_cap >= 1 is the per-submodel error-history ring length. Returns 0 on bad arguments. */
 size_t jkcals_workspace_bytes(int ndims, const int64_t *dims, int rank, int64_t n_sub,
                               jkcals_precision prec, int hist_cap, int device);
@@ -113,7 +113,7 @@ jkcals_status jkcals_create_d(jkcals_t *out, int ndims, const int64_t *dims, int
  * MTTKRP per mode serves all of them. Submodel ids s in [0, nmodels * ceil(I_0/d)) enumerate
  * model m = s / ceil(I_0/d) and its group g = s % ceil(I_0/d) (d as in jkcals_create_d);
  * [sub_begin, sub_end) selects a shard of ids. Every `p` argument of the calls below is such an
- * id; factors of submodel s are rows x R_m. ranks[m] in [1, 16]. jkcals_create_d is the pool
+ * id; factors of submodel s are rows x R_m. ranks[m] in [1, 32]. jkcals_create_d is the pool
  * with nmodels = 1. Errors as jkcals_create_d.
  * d = 0 selects plain CALS (§3.3): nothing is left out, each
  * id s in [0, nmodels) is one model fitted to the full tensor from its own initial model (e.g.
@@ -139,7 +139,7 @@ typedef struct jkcals_config {
   int ndims;
   const int64_t *dims;
   int nmodels;          /* >= 1 */
-  const int *ranks;     /* nmodels ranks in [1, 16] */
+  const int *ranks;     /* nmodels ranks in [1, 32] */
   int64_t d;            /* 0 = plain CALS, 1 = leave-one-out, > 1 = delete-d */
   int64_t sub_begin, sub_end;
   int spare;            /* >= 0 */

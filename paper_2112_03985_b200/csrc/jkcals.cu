@@ -24,6 +24,7 @@
 #include "align.cuh"
 #include "aux_kernels.cuh"
 #include "epilogue.cuh"
+#include "epilogue_large.cuh"
 #include "mttkrp.cuh"
 #include "mttkrp_tf32.cuh"
 
@@ -516,7 +517,7 @@ bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_c
 }
 
 bool valid_dims(int N, const int64_t* dims, int R) {
-  if (N < 3 || N > JKCALS_MAX_MODES || !dims || R < 1 || R > 16) return false;
+  if (N < 3 || N > JKCALS_MAX_MODES || !dims || R < 1 || R > kLgRMax) return false;
   int64_t P = 1;
   for (int k = 0; k < N; ++k) {
     if (dims[k] < 1) return false;
@@ -849,7 +850,27 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
   a.tol = reinterpret_cast<const double*>(h->ws + h->off.misc + 8);
   a.active_count = reinterpret_cast<int*>(h->ws + h->off.misc + 16);
   const bool pdl = h->pdl && !timed;
-  if (h->R <= 2) launch_epi<2>(h, a, pdl);
+  if (h->R > 16) {  // ranks 17..32: the streaming large-rank epilogue (any I_n, mixed pools too)
+    static unsigned lg_mask = 0;
+    if (!(lg_mask & (1u << (h->device & 31)))) {
+      cudaFuncSetAttribute(als_epilogue_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)epi_large_smem_bytes());
+      lg_mask |= 1u << (h->device & 31);
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.gridDim = dim3(h->K);
+    cfg.blockDim = dim3(kLgThreads);
+    cfg.dynamicSmemBytes = epi_large_smem_bytes();
+    cfg.stream = h->es;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (!a.subR) a.subR = h->ptr<int>(h->off.subR);  // the large kernel reads per-block ranks
+    if (!a.blkcol) a.blkcol = h->ptr<int>(h->off.blkcol);
+    cudaLaunchKernelEx(&cfg, als_epilogue_large_kernel, a);
+  } else if (h->R <= 2) launch_epi<2>(h, a, pdl);
   else if (h->R <= 4) launch_epi<4>(h, a, pdl);
   else if (h->R <= 6) launch_epi<6>(h, a, pdl);
   else if (h->R <= 8) launch_epi<8>(h, a, pdl);
@@ -904,7 +925,12 @@ jkcals_status compute_grams(jkcals_t h) {
   for (int n = 0; n < h->N; ++n) {
     if (h->R <= 4) launch_gram<4>(h, n);
     else if (h->R <= 8) launch_gram<8>(h, n);
-    else launch_gram<16>(h, n);
+    else if (h->R <= 16) launch_gram<16>(h, n);
+    else
+      gram_large_kernel<<<h->K, kLgThreads, 0, h->stream>>>(h->U(n), (int)h->dims[n], h->ldu, h->R,
+                                                            h->ptr<int>(h->off.blk2sub), h->ptr<int>(h->off.blkcol),
+                                                            h->ptr<int>(h->off.subR), h->nsub, n,
+                                                            h->ptr<double>(h->off.gram));
     CKH(h, cudaGetLastError());
   }
   return JKCALS_OK;
@@ -1025,7 +1051,7 @@ static bool pool_geo(const jkcals_config* c, PoolGeo* g) {
   if (dims[0] < 2 || d < 0 || (d > 1 && 2 * d > dims[0]) || c->spare < 0 || c->hist_cap < 1) return false;
   if (c->prec != JKCALS_FP64 && c->prec != JKCALS_FP32) return false;
   for (int m = 0; m < c->nmodels; ++m)
-    if (c->ranks[m] < 1 || c->ranks[m] > 16) return false;
+    if (c->ranks[m] < 1 || c->ranks[m] > kLgRMax) return false;
   // d = 0: plain CALS (§3.3): one model per id, nothing left out
   g->ngroups = d == 0 ? 1 : (dims[0] + d - 1) / d;
   if (c->sub_begin < 0 || c->sub_end <= c->sub_begin || c->sub_end > (int64_t)c->nmodels * g->ngroups) return false;

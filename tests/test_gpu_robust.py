@@ -190,3 +190,57 @@ def test_large_ranks_epilogue_classes(R):
     for p in (0, 5, 11):
         for a, b in zip(h.factors(p)[0], res.factors[p]):
             assert rel(a, b) <= 1e-10, (R, p, rel(a, b))
+
+
+@pytest.mark.parametrize("R", [17, 20, 32])
+def test_ranks_above_16_streaming_epilogue(R):
+    # ranks 17..32 run the streaming large-rank epilogue (epilogue_large.cuh); I_1 = 300 > one
+    # 128-row chunk, I_0 = 9 submodels
+    from paper_2112_03985_b200 import JKCals
+    w = make_workload(((9, 300, 40), R, 32, 0.01, "syn", 12), seed=R)
+    h = JKCals(w.T, w.R, hist_cap=12)
+    h.set_init(w.P)
+    h.iterate(12, 0.0)
+    res = O.jk_als(w.T, w.P, max_iters=12, nthreads=NCPU)
+    for p in range(9):
+        fac, lam = h.factors(p)
+        for a, b in zip(fac, res.factors[p]):
+            assert rel(a, b) <= 1e-10, (R, p, rel(a, b))
+        assert rel(lam, res.lam[p]) <= 1e-10
+        assert np.allclose(h.history(p), res.history(p), rtol=1e-9, atol=1e-13 * O.norm_sq(w.T))
+
+
+def test_paper_application_pool_ranks_19_20_21():
+    # the paper's second application jackknifes three models of ranks {19, 20, 21} together
+    # (PAPER.md:590-596); here on a small 44 x 120 x 30 tensor with delete-2 groups
+    from paper_2112_03985_b200 import JKCals
+    from synth import make_pool
+    w = make_pool(((44, 120, 30), (19, 20, 21), 20, 0.01, "syn", 8), seed=5)
+    h = JKCals(w.T, list(w.ranks), hist_cap=8, d=2)
+    h.set_init(w.Ps)
+    h.iterate(8, 0.0)
+    for m, P in enumerate(w.Ps):
+        res = O.jk_als_d(w.T, P, 2, g_list=[0, 21], max_iters=8, nthreads=NCPU)
+        for q, g in enumerate([0, 21]):
+            fac, _ = h.factors(m * 22 + g)
+            for a, b in zip(fac, res.factors[q]):
+                assert rel(a, b) <= 1e-10, (m, g, rel(a, b))
+
+
+def test_large_rank_pinv_fallback():
+    # the large-rank epilogue's Jacobi pseudoinverse (shared-memory scratch): a zero column in
+    # one submodel's mode-1 init makes its H singular; it matches the oracle's pinv path
+    from paper_2112_03985_b200 import JKCals
+    w = make_workload(((8, 60, 40), 18, 32, 0.01, "syn", 10), seed=18)
+    h = JKCals(w.T, w.R, hist_cap=10)
+    h.set_init(w.P)
+    bad = w.P[1].copy()
+    bad[:, 4] = 0.0
+    h.set_init_submodel(3, 1, bad)
+    h.iterate(10, 0.0)
+    st = h.status()
+    assert st["flags"][3] & 2 and not np.any(np.delete(st["flags"], 3) & 2)
+    res3 = O.jk_als(w.T, [w.P[0], bad, w.P[2]], p_list=[3], max_iters=10, nthreads=NCPU)
+    assert res3.flags[0] & 2
+    for a, b in zip(h.factors(3)[0], res3.factors[0]):
+        assert rel(a, b) <= 1e-9, rel(a, b)
