@@ -72,7 +72,8 @@ enum {
 #define JKCALS_MAX_MODES 8
 
 /* Bytes of device workspace needed by jkcals_create for these arguments on `device`.
- * ndims in [3, 8]; dims[k] >= 1, dims[0] >= 2; 1 <= rank <= 32 (ranks above 16 use the streaming large-rank epilogue); n_sub = sub_end - sub_begin >= 1;
+ * ndims in [3, 8]; dims[k] >= 1, dims[0] >= 2; 1 <= rank <= 32 (ranks above 16 use the
+ * streaming large-rank epilogue); n_sub = sub_end - sub_begin >= 1;
  * hist_cap >= 1 is the per-submodel error-history ring length. Returns 0 on bad arguments. */
 size_t jkcals_workspace_bytes(int ndims, const int64_t *dims, int rank, int64_t n_sub,
                               jkcals_precision prec, int hist_cap, int device);
