@@ -70,9 +70,10 @@ __device__ __noinline__ void jacobi_pinv_ptr(const double* H, int R, double* A, 
   }
 }
 constexpr int kLgRMax = 32;
-constexpr int kLgRows = 128;  // rows per chunk: Ms + Vs = 2 x 128 x 32 x 8 = 64 KB of shared memory
-
-inline size_t epi_large_smem_bytes() { return (size_t)2 * kLgRows * kLgRMax * sizeof(double); }
+constexpr int kLgRows = 256;           // rows per chunk: one row per thread
+constexpr int kLgLd = kLgRMax + 1;     // odd row stride: thread-per-row accesses hit distinct banks
+// Ms + Vs = 2 x 256 x 33 x 8 = 132 KB of dynamic shared memory (opt-in; one CTA per SM)
+inline size_t epi_large_smem_bytes() { return (size_t)2 * kLgRows * kLgLd * sizeof(double); }
 
 __global__ void __launch_bounds__(kLgThreads) als_epilogue_large_kernel(EpiArgs a) {
   const int k = blockIdx.x;
@@ -95,8 +96,8 @@ __global__ void __launch_bounds__(kLgThreads) als_epilogue_large_kernel(EpiArgs 
   __shared__ double ilam_s[kLgRMax];
   __shared__ int use_pinv;
   extern __shared__ double dyn[];
-  double* Ms = dyn;                      // [kLgRows][R]
-  double* Vs = dyn + kLgRows * kLgRMax;  // [kLgRows][R]
+  double* Ms = dyn;                    // [kLgRows][kLgLd]
+  double* Vs = dyn + kLgRows * kLgLd;  // [kLgRows][kLgLd]
 
   // (a3) Hadamard of the cached Gramians of every other mode
   for (int e = tid; e < R * R; e += kLgThreads) {
@@ -175,14 +176,14 @@ __global__ void __launch_bounds__(kLgThreads) als_epilogue_large_kernel(EpiArgs 
       const double* p = a.parts + (int64_t)ti.piece_base * piece + (int64_t)(i - tn * a.BN) * a.BM + (c - tm * a.BM);
       double s = 0.0;
       for (int pc = 0; pc < ti.npieces; ++pc) s += __ldcg(p + (int64_t)pc * piece);
-      Ms[il * kLgRMax + r] = s;
+      Ms[il * kLgLd + r] = s;
     }
     __syncthreads();
     // (a4/a5) row solves V(i,:) = M(i,:) H^{-1}, one row per thread, in shared memory
     for (int il = tid; il < rows; il += kLgThreads) {
       const int64_t i = i0 + il;
-      const double* m = Ms + il * kLgRMax;
-      double* v = Vs + il * kLgRMax;
+      const double* m = Ms + il * kLgLd;
+      double* v = Vs + il * kLgLd;
       if (i >= pz0 && i < pz1) {
         for (int r = 0; r < R; ++r) v[r] = 0.0;
       } else if (!pinv) {
@@ -209,12 +210,12 @@ __global__ void __launch_bounds__(kLgThreads) als_epilogue_large_kernel(EpiArgs 
 #pragma unroll
     for (int o = 0; o < kOwn; ++o)
       if (own_r[o] >= 0)
-        for (int il = 0; il < rows; ++il) own_acc[o] += Vs[il * kLgRMax + own_r[o]] * Vs[il * kLgRMax + own_c[o]];
+        for (int il = 0; il < rows; ++il) own_acc[o] += Vs[il * kLgLd + own_r[o]] * Vs[il * kLgLd + own_c[o]];
     if (tid < R)
-      for (int il = 0; il < rows; ++il) cross += Vs[il * kLgRMax + tid] * Ms[il * kLgRMax + tid];
+      for (int il = 0; il < rows; ++il) cross += Vs[il * kLgLd + tid] * Ms[il * kLgLd + tid];
     for (int e = tid; e < rows * R; e += kLgThreads) {
       const int il = e / R, r = e % R;
-      a.U[(int64_t)(i0 + il) * a.ldu + cb + r] = Vs[il * kLgRMax + r];
+      a.U[(int64_t)(i0 + il) * a.ldu + cb + r] = Vs[il * kLgLd + r];
     }
     __syncthreads();
   }
