@@ -395,7 +395,7 @@ __device__ __forceinline__ double warp_sum(double x) {
 
 
 template <int J, int Q>
-__device__ __forceinline__ void sum_pieces(const EpiArgs& a, int cb, int R, int In, double* Ms) {
+__device__ __forceinline__ void sum_pieces(const EpiArgs& a, int cb, int R, int In, double* Ms, int ldm) {
   const int64_t piece = (int64_t)a.BN * a.BM;
   const int T = blockDim.x;
   for (int e0 = threadIdx.x; e0 < In * R; e0 += J * T) {
@@ -432,7 +432,7 @@ __device__ __forceinline__ void sum_pieces(const EpiArgs& a, int cb, int R, int 
     }
 #pragma unroll
     for (int j = 0; j < J; ++j)
-      if (e0 + j * T < In * R) Ms[e0 + j * T] = s[j];
+      if (e0 + j * T < In * R) Ms[((e0 + j * T) / R) * ldm + (e0 + j * T) % R] = s[j];
   }
 }
 
@@ -474,8 +474,11 @@ __device__ __forceinline__ void epi_smem_body(const EpiArgs& a, const int k, con
   __shared__ double ilam_s[RMAX];
   __shared__ int use_pinv;
   extern __shared__ double dyn[];
-  double* Ms = dyn;             // [In][R]
-  double* Vs = dyn + In * R;    // [In][R]
+  double* Ms = dyn;             // [In][ldm]
+  // rows padded to an odd stride: the thread-per-row solve then reads / writes distinct banks
+  // (an even R such as the 4-way config's 4 would otherwise conflict R-ways)
+  const int ldm = R | 1;
+  double* Vs = dyn + In * ldm;  // [In][ldm]
 
   // (a3) Hadamard of the cached Gramians of every other mode
   if (tid < R * R) {
@@ -486,8 +489,8 @@ __device__ __forceinline__ void epi_smem_body(const EpiArgs& a, const int k, con
   }
   // (a2) fixed-order sum of the partial pieces of this submodel's R columns: J elements per
   // thread x Q pieces = 16 independent loads in flight; the adds of each element stay in order
-  if (In * R <= kEpi2Threads) sum_pieces<1, 16>(a, cb, R, In, Ms);
-  else sum_pieces<4, 4>(a, cb, R, In, Ms);
+  if (In * R <= kEpi2Threads) sum_pieces<1, 16>(a, cb, R, In, Ms, ldm);
+  else sum_pieces<4, 4>(a, cb, R, In, Ms, ldm);
   __syncthreads();
   EPI_PROBE(2);
   // (a4) Cholesky H = L L^T (textbook, no pivoting) in registers of thread 0; pinv fallback
@@ -541,7 +544,7 @@ __device__ __forceinline__ void epi_smem_body(const EpiArgs& a, const int k, con
   for (int i = tid; i < In; i += blockDim.x) {
     double m[RMAX], v[RMAX];
 #pragma unroll
-    for (int r = 0; r < RMAX; ++r) m[r] = (r < R) ? Ms[i * R + r] : 0.0;
+    for (int r = 0; r < RMAX; ++r) m[r] = (r < R) ? Ms[i * ldm + r] : 0.0;
     if (i >= pz0 && i < pz1) {
 #pragma unroll
       for (int r = 0; r < RMAX; ++r) v[r] = 0.0;
@@ -581,7 +584,7 @@ __device__ __forceinline__ void epi_smem_body(const EpiArgs& a, const int k, con
     int q = 0;
 #pragma unroll
     for (int r = 0; r < RMAX; ++r) {
-      if (r < R) Vs[i * R + r] = v[r];
+      if (r < R) Vs[i * ldm + r] = v[r];
 #pragma unroll
       for (int c = r; c < RMAX; ++c, ++q) acc[q] += v[r] * v[c];
     }
@@ -617,7 +620,7 @@ __device__ __forceinline__ void epi_smem_body(const EpiArgs& a, const int k, con
   __syncthreads();
   for (int e = tid; e < In * R; e += blockDim.x) {
     const int i = e / R, r = e % R;
-    a.U[(int64_t)i * a.ldu + cb + r] = Vs[e] * ilam_s[r];
+    a.U[(int64_t)i * a.ldu + cb + r] = Vs[i * ldm + r] * ilam_s[r];
   }
   if (tid < R * R) {
     const int r = tid / R, c = tid % R;

@@ -695,7 +695,7 @@ jkcals_status replan(jkcals_t h) {
 
 template <int RMAX>
 void launch_epi(jkcals_t h, const EpiArgs& a, bool pdl) {
-  const size_t dyn = (size_t)2 * a.In * a.R * sizeof(double);
+  const size_t dyn = (size_t)2 * a.In * (a.R | 1) * sizeof(double);  // odd row stride (epilogue.cuh)
   constexpr size_t kMaxDyn = 96 * 1024;
   static unsigned attr_mask = 0;  // per RMAX instantiation and device
   if (!(attr_mask & (1u << (h->device & 31)))) {
