@@ -244,3 +244,30 @@ def test_large_rank_pinv_fallback():
     assert res3.flags[0] & 2
     for a, b in zip(h.factors(3)[0], res3.factors[0]):
         assert rel(a, b) <= 1e-9, rel(a, b)
+
+
+def test_stress_eight_modes_and_unit_dims():
+    # N = 8 (JKCALS_MAX_MODES) with unit-length modes in the middle and a short sampled mode
+    from paper_2112_03985_b200 import JKCals
+    w = make_workload(((5, 3, 1, 4, 2, 1, 3, 2), 2, 2, 0.01, "syn", 15), seed=8)
+    h = JKCals(w.T, w.R, hist_cap=15)
+    h.set_init(w.P)
+    h.iterate(15, 0.0)
+    res = O.jk_als(w.T, w.P, max_iters=15, nthreads=NCPU)
+    for p in range(5):
+        for a, b in zip(h.factors(p)[0], res.factors[p]):
+            assert rel(a, b) <= 1e-10, (p, rel(a, b))
+
+
+def test_stress_wide_fused_width():
+    # a wide fused multi-factor: 268 submodels x R = 20 = 5360 columns (42 M tiles), EEM shape
+    from paper_2112_03985_b200 import JKCals
+    w = make_workload(((268, 40, 30), 20, 20, 0.02, "eem", 6), seed=2)
+    h = JKCals(w.T, w.R, hist_cap=6)
+    h.set_init(w.P)
+    h.iterate(6, 0.0)
+    ps = [0, 133, 267]
+    res = O.jk_als(w.T, w.P, p_list=ps, max_iters=6, nthreads=NCPU)
+    for q, p in enumerate(ps):
+        for a, b in zip(h.factors(p)[0], res.factors[q]):
+            assert rel(a, b) <= 1e-10, (p, rel(a, b))
