@@ -207,6 +207,7 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
     // FP32 (3xTF32 tcgen05) path: UMMA M = 128 fused columns, N = whole I_n up to 256 per tile
     p.tf32 = 1;
     p.nNt = (int)cdiv(mg.In, kTfMaxN);
+    if (const char* e = getenv("JKCALS_TF32_MIN_NNT")) p.nNt = std::max<int>(p.nNt, atoi(e));  // tuning only
     p.BN = (int)rup(cdiv(mg.In, p.nNt), 16);
     p.NT = p.BN / 8;
     p.KM = 1;
