@@ -165,25 +165,33 @@ __global__ void extract_all_kernel(const double* __restrict__ base, const int64_
   }
 }
 
-// (a9) per-element moments over the handle's submodels, fixed order (two-pass):
-// mean = sum/g, M2 = sum (x - mean)^2. src_off[q] / src_ld[q] locate submodel q's block
-// (row-major) relative to `base`. Output column-major I x R.
+// (a9) per-element moments over the handle's submodels (two-pass: mean = sum/g, M2 = sum
+// (x - mean)^2). One warp per element: lanes stride over the submodels, then a shuffle tree --
+// a fixed order, so the result is deterministic. src_off[q] / src_ld[q] locate submodel q's
+// block (row-major) relative to `base`. Output column-major I x R.
 __global__ void moments_kernel(const double* __restrict__ base, const int64_t* __restrict__ src_off,
                                const int64_t* __restrict__ src_ld, int nsub, int I, int R,
                                double* __restrict__ mean, double* __restrict__ m2) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= I * R) return;
+  const int lane = threadIdx.x & 31;
+  const int e = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (e >= I * R) return;  // (warp-uniform)
   const int r = e / I, i = e % I;
   double s = 0.0;
-  for (int q = 0; q < nsub; ++q) s += base[src_off[q] + (int64_t)i * src_ld[q] + r];
+  for (int q = lane; q < nsub; q += 32) s += base[src_off[q] + (int64_t)i * src_ld[q] + r];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   const double mu = s / (double)nsub;
   double ss = 0.0;
-  for (int q = 0; q < nsub; ++q) {
+  for (int q = lane; q < nsub; q += 32) {
     const double d = base[src_off[q] + (int64_t)i * src_ld[q] + r] - mu;
     ss += d * d;
   }
-  mean[e] = mu;
-  m2[e] = ss;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if (lane == 0) {
+    mean[e] = mu;
+    m2[e] = ss;
+  }
 }
 
 // (a8) store a converged block (columns [col, col + R)) into the result store (row-major I x R).

@@ -1631,7 +1631,7 @@ static jkcals_status moments(jkcals_t h, int model, int mode, double* mean_d, do
   jkcals_status st = build_src_table(h, mode, subs);
   if (st != JKCALS_OK) return st;
   const int I = (int)h->dims[mode], R = h->ranks[model];
-  moments_kernel<<<(int)cdiv((int64_t)I * R, 128), 128, 0, h->stream>>>(
+  moments_kernel<<<(int)cdiv((int64_t)I * R * 32, 256), 256, 0, h->stream>>>(
       reinterpret_cast<const double*>(h->ws), h->ptr<int64_t>(h->off.srcoff), h->ptr<int64_t>(h->off.srcld),
       (int)subs.size(), I, R, mean_d, m2_d);
   CKH(h, cudaGetLastError());
