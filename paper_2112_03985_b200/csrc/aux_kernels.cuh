@@ -36,7 +36,8 @@ __global__ void slice_norms_final_kernel(const double* __restrict__ part, int nb
                                          double* __restrict__ normT2p) {
   for (int64_t i = threadIdx.x; i < I0; i += blockDim.x) {
     double acc = 0.0;
-    for (int b = 0; b < nb; ++b) acc += part[(int64_t)b * I0 + i];
+#pragma unroll 8
+    for (int b = 0; b < nb; ++b) acc += part[(int64_t)b * I0 + i];  // (8 loads in flight, adds in order)
     s[i] = acc;
   }
   __syncthreads();
