@@ -183,15 +183,15 @@ jkcals_status jkcals_iterate(jkcals_t h, int max_iters, double tol, int *sweeps_
  * NULL) holds the column norms of the LAST updated mode (mode ndims-1 after a sweep). */
 jkcals_status jkcals_get_factors(jkcals_t h, int64_t p, int mode, double *U, double *lambda);
 
-/* Factors of ALL this handle's submodels for one mode in one call: U receives n_sub blocks in
- * submodel order, each in the get_factors layout ((dims[0]-1) x rank for mode 0 with row p
- * dropped; dims[mode] x rank otherwise), column-major, packed back to back (delete-d with a
- * ragged last group: that block has dims[0]-|group| rows); lambda (n_sub x rank, may be NULL). */
+/* Factors of ALL the submodels this handle holds, for one mode, in one call: U receives one block
+ * per held submodel in slot order (= submodel order without migration), each in the get_factors
+ * layout ((dims[0]-|group|) x R_p for mode 0, dims[mode] x R_p otherwise), column-major, packed
+ * back to back; lambda (may be NULL) receives R_p values per submodel, packed the same way. */
 jkcals_status jkcals_get_all_factors(jkcals_t h, int mode, double *U, double *lambda);
 
 /* Debug/invariant view: submodel p's FULL block of the mode-`mode` multi-factor as it sits
- * in the fused layout, dims[mode] x rank column-major. For mode 0 row p is the padded zero
- * row, which must be exactly +0.0/-0.0 after every sweep (alg:cals_jk:multifactor). */
+ * in the fused layout, dims[mode] x R_p column-major. For mode 0 the rows of p's left-out group
+ * are the padded zero rows, exactly +0.0/-0.0 after every sweep (alg:cals_jk:multifactor). */
 jkcals_status jkcals_get_block(jkcals_t h, int64_t p, int mode, double *U);
 
 /* Per-submodel status, arrays of n_slots entries in slot order (= n_sub in submodel order for a
@@ -258,8 +258,8 @@ jkcals_status jkcals_get_aligned_stats(jkcals_t h, int model, int mode, double *
  * buffer into another handle of the same problem (same tensor, pool, d and hist_cap) with a free
  * slot continues the fit where it stopped: the sweeps that follow are those the exporting
  * handle would have run, up to the floating-point summation order of the new fused layout's
- * split-K partition (rounding-level differences). Errors: E_ARG (unknown id, foreign state, small buffer),
- * E_STATE (not live / before set_init), E_OOM (no free slot or column room). */
+ * split-K partition (rounding-level differences). Errors: E_ARG (unknown id, foreign state,
+ * small buffer), E_STATE (not live / before set_init), E_OOM (no free slot or column room). */
 int jkcals_num_slots(jkcals_t h);
 jkcals_status jkcals_get_ids(jkcals_t h, int64_t *ids);
 size_t jkcals_state_bytes(jkcals_t h, int64_t p);
