@@ -157,7 +157,8 @@ jkcals_status jkcals_create_config(jkcals_t *out, const jkcals_config *cfg, cons
  * PAPER.md:331; Alg. 3 alg:start-jk-1..alg:stop-jk-1): P[n] is a host
  * column-major dims[n] x rank array; block k of the mode-0 multi-factor gets row p_k
  * zeroed (its group's rows for delete-d). A pool takes nmodels * ndims arrays:
- * P[m * ndims + n] is model m's dims[n] x ranks[m] factor. Resets fits, histories, flags and iteration counts. Errors: E_ARG, E_NONFINITE. */
+ * P[m * ndims + n] is model m's dims[n] x ranks[m] factor. Resets fits, histories, flags and
+ * iteration counts. Errors: E_ARG, E_NONFINITE. */
 jkcals_status jkcals_set_init(jkcals_t h, const double *const *P);
 
 /* Optional per-submodel (re)initialisation, e.g. to resume: U is host column-major in the
@@ -246,8 +247,8 @@ jkcals_status jkcals_get_aligned_factors(jkcals_t h, int64_t p, int mode, double
  * all of them for modes >= 1; for the sampled mode 0 those whose left-out group does not
  * contain the row (reading A20) -- and std = sqrt(((g_e-1)/g_e) M2) (0 if g_e < 2).
  * The moments merge across shards with Chan's formula. E_STATE as above. */
-jkcals_status jkcals_get_aligned_moments(jkcals_t h, int model, int mode, double *count, double *mean,
-                                         double *m2);
+jkcals_status jkcals_get_aligned_moments(jkcals_t h, int model, int mode, double *count,
+                                         double *mean, double *m2);
 jkcals_status jkcals_get_aligned_stats(jkcals_t h, int model, int mode, double *mean, double *std);
 
 /* Slots and migration (tol-mode load rebalancing across GPUs). A live
