@@ -295,6 +295,17 @@ jkcals_status jkcals_mttkrp(int ndims, const int64_t *dims, int n, const double 
                             const double *const *U, int64_t C, int64_t ldu, double *M, int64_t ldm,
                             void *scratch, size_t scratch_bytes, void *stream);
 
+/* EXPERIMENTAL: the same MTTKRP, FP64-accurate from INT8 tcgen05 MMAs -- both
+ * operands of the per-j' inner products (T per mode-n row, U_q0 per column) split into 7 balanced
+ * base-128 digits with power-of-two scales, digit products accumulated exactly in int32 TMEM
+ * accumulators per significance, the slow-mode row product S(j', c) applied in FP64. Same
+ * arguments as jkcals_mttkrp (ldu >= C); scratch from jkcals_mttkrp_i8_scratch_bytes. Not yet on
+ * the JK-CALS path. */
+size_t jkcals_mttkrp_i8_scratch_bytes(int ndims, const int64_t *dims, int n, int64_t C, int device);
+jkcals_status jkcals_mttkrp_i8(int ndims, const int64_t *dims, int n, const double *T,
+                               const double *const *U, int64_t C, int64_t ldu, double *M, int64_t ldm,
+                               void *scratch, size_t scratch_bytes, void *stream);
+
 /* Khatri-Rao generation (descending order of Eq. 1), materialised:
  *   K(j, c) = prod_{m != n} U_m(i_m(j), c),  j in [0, prod_{m!=n} dims[m]) by Eq. 3, c < C,
  * U[m] device row-major dims[m] x ldu; K device row-major J x ldk. HBM-write-bound. */

@@ -27,6 +27,7 @@
 #include "epilogue_large.cuh"
 #include "mttkrp.cuh"
 #include "mttkrp_tf32.cuh"
+#include "mttkrp_i8.cuh"
 
 using namespace jk;
 
@@ -2096,6 +2097,171 @@ jkcals_status jkcals_mttkrp(int ndims, const int64_t* dims, int n, const double*
   reduce_parts_kernel<<<(int)cdiv(tot, 256), 256, 0, s>>>(parts, ti, (int)dims[n], (int)C, p.BN, p.nMt, M, ldm);
   if (cudaGetLastError() != cudaSuccess) return JKCALS_E_CUDA;
   // tinfo staging is pageable-host -> device: make sure the copy has consumed it
+  if (cudaStreamSynchronize(s) != cudaSuccess) return JKCALS_E_CUDA;
+  return JKCALS_OK;
+}
+
+// ---------------------------------------------------------------- EXPERIMENTAL: INT8-sliced MTTKRP
+namespace {
+struct I8Plan {
+  int64_t In, Iq0, Jp, InP, KP, CP;
+  int nMt, nNt;
+  ModePlan p;
+};
+I8Plan make_i8_plan(int ndims, const int64_t* dims, int n, int64_t C, const KernelInfo& ki) {
+  I8Plan q;
+  const ModeGeo mg = mode_geo(ndims, dims, n);
+  q.In = mg.In;
+  q.Iq0 = mg.Iq0;
+  q.Jp = mg.Jp;
+  q.InP = rup(q.In, kI8N);
+  q.KP = rup(q.Iq0, kI8K);
+  q.CP = rup(C, 128);
+  q.nMt = (int)(q.CP / 128);
+  q.nNt = (int)(q.InP / kI8N);
+  ModePlan& p = q.p;
+  p.nMt = q.nMt;
+  p.nNt = q.nNt;
+  p.BN = kI8N;
+  p.KT = (int)q.Jp;
+  p.ntiles = p.nMt * p.nNt;
+  p.units = (int64_t)p.ntiles * p.KT;
+  p.G = (int)std::min<int64_t>(p.units, (int64_t)ki.nsm);
+  finish_plan(p, mg);
+  return q;
+}
+struct I8Scratch {
+  TileInfo* ti;
+  double* parts;
+  int8_t *A, *B;
+  int *eT, *eU, *dims_d;
+  int64_t* st_d;
+  double* Up[kMaxModes];
+  size_t total;
+};
+I8Scratch i8_layout(uintptr_t base0, int ndims, const int64_t* dims, const I8Plan& q) {
+  I8Scratch x;
+  uintptr_t base = (base0 + kAlign - 1) & ~(uintptr_t)(kAlign - 1);
+  const uintptr_t start = base;
+  auto take = [&](size_t bytes) {
+    uintptr_t o = base;
+    base += rup((int64_t)bytes, kAlign);
+    return o;
+  };
+  x.ti = reinterpret_cast<TileInfo*>(take(plan_table_bytes(q.p.ntiles, q.p.G)));
+  x.parts = reinterpret_cast<double*>(take((size_t)(q.p.G + q.p.ntiles) * kI8N * 128 * 8));
+  x.A = reinterpret_cast<int8_t*>(take((size_t)kI8S * q.CP * q.KP));
+  x.B = reinterpret_cast<int8_t*>(take((size_t)kI8S * q.Jp * q.InP * q.KP));
+  x.eT = reinterpret_cast<int*>(take((size_t)q.InP * 4));
+  x.eU = reinterpret_cast<int*>(take((size_t)q.CP * 4));
+  x.dims_d = reinterpret_cast<int*>(take(kMaxModes * 4));
+  x.st_d = reinterpret_cast<int64_t*>(take(kMaxModes * 8));
+  for (int m = 0; m < ndims; ++m) x.Up[m] = reinterpret_cast<double*>(take((size_t)dims[m] * q.CP * 8));
+  x.total = (size_t)(base - start) + kAlign;
+  return x;
+}
+bool make_tmap_i8(CUtensorMap* tm, const int8_t* base, int64_t kp, int64_t rows, int box_rows) {
+  auto enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t gdim[3] = {(cuuint64_t)kp, (cuuint64_t)rows, (cuuint64_t)kI8S};
+  cuuint64_t gstr[2] = {(cuuint64_t)kp, (cuuint64_t)(kp * rows)};
+  cuuint32_t box[3] = {(cuuint32_t)kI8K, (cuuint32_t)box_rows, (cuuint32_t)kI8S}, est[3] = {1, 1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), gdim, gstr, box, est,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+}  // namespace
+
+size_t jkcals_mttkrp_i8_scratch_bytes(int ndims, const int64_t* dims, int n, int64_t C, int device) {
+  if (!valid_dims(ndims, dims, 1) || n < 0 || n >= ndims || C < 1) return 0;
+  KernelInfo* ki = kernel_info(device, nullptr);
+  if (!ki) return 0;
+  const I8Plan q = make_i8_plan(ndims, dims, n, C, *ki);
+  return i8_layout(0, ndims, dims, q).total;
+}
+
+jkcals_status jkcals_mttkrp_i8(int ndims, const int64_t* dims, int n, const double* T, const double* const* U,
+                               int64_t C, int64_t ldu, double* M, int64_t ldm, void* scratch, size_t scratch_bytes,
+                               void* stream) {
+  if (!valid_dims(ndims, dims, 1) || n < 0 || n >= ndims || !T || !U || !M || C < 1 || ldu < C || ldm < C)
+    return JKCALS_E_ARG;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  KernelInfo* ki = kernel_info(dev, nullptr);
+  if (!ki) return JKCALS_E_CUDA;
+  if (scratch_bytes < jkcals_mttkrp_i8_scratch_bytes(ndims, dims, n, C, dev)) return JKCALS_E_OOM;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(mttkrp_i8_kernel<kI8Stages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kI8Smem) != cudaSuccess)
+      return JKCALS_E_CUDA;
+    attr = true;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const I8Plan q = make_i8_plan(ndims, dims, n, C, *ki);
+  I8Scratch x = i8_layout(reinterpret_cast<uintptr_t>(scratch), ndims, dims, q);
+  const int q0 = (n == 0) ? 1 : 0;
+  int64_t st[kMaxModes];
+  int dd[kMaxModes];
+  int64_t P = 1;
+  for (int m = 0; m < ndims; ++m) {
+    st[m] = P;
+    dd[m] = (int)dims[m];
+    P *= dims[m];
+  }
+  if (cudaMemcpyAsync(x.st_d, st, 8 * ndims, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(x.dims_d, dd, 4 * ndims, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return JKCALS_E_CUDA;
+  for (int m = 0; m < ndims; ++m) {
+    if (m == n) continue;
+    if (cudaMemsetAsync(x.Up[m], 0, dims[m] * q.CP * 8, s) != cudaSuccess ||
+        cudaMemcpy2DAsync(x.Up[m], q.CP * 8, U[m], ldu * 8, C * 8, dims[m], cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      return JKCALS_E_CUDA;
+  }
+  // operands: T digits per mode-n row scale, U_q0 digits per column scale
+  if (cudaMemsetAsync(x.eT, 0, q.InP * 4, s) != cudaSuccess) return JKCALS_E_CUDA;
+  row_exp_t_kernel<<<(int)q.In, 256, 0, s>>>(T, ndims, x.st_d, x.dims_d, n, P / dims[n], x.eT);
+  slice_t_i8_kernel<<<(int)cdiv(q.Jp * q.InP * q.KP, 256), 256, 0, s>>>(T, ndims, x.st_d, x.dims_d, n, q0, (int)q.In,
+                                                                        (int)q.InP, (int)q.Iq0, (int)q.KP, q.Jp,
+                                                                        x.eT, x.B);
+  col_exp_u_kernel<<<(int)cdiv(q.CP, 128), 128, 0, s>>>(x.Up[q0], q.CP, (int)q.Iq0, (int)C, (int)q.CP, x.eU);
+  slice_u_i8_kernel<<<(int)cdiv(q.CP * q.KP, 256), 256, 0, s>>>(x.Up[q0], q.CP, (int)q.Iq0, (int)C, (int)q.CP,
+                                                                (int)q.KP, x.eU, x.A);
+  if (cudaGetLastError() != cudaSuccess) return JKCALS_E_CUDA;
+  std::vector<char> table = pack_plan(q.p);
+  if (cudaMemcpyAsync(x.ti, table.data(), table.size(), cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return JKCALS_E_CUDA;
+  CUtensorMap tmA, tmB;
+  if (!make_tmap_i8(&tmA, x.A, q.KP, q.CP, 128) || !make_tmap_i8(&tmB, x.B, q.KP, q.Jp * q.InP, kI8N))
+    return JKCALS_E_CUDA;
+  I8Geom g;
+  g.nMt = q.nMt;
+  g.nNt = q.nNt;
+  g.Jp = (int)q.Jp;
+  g.KS = (int)(q.KP / kI8K);
+  g.units = q.p.units;
+  g.InP = (int)q.InP;
+  g.nslow = ndims - 2;
+  int sl = 0;
+  for (int m = 0; m < ndims; ++m) {
+    if (m == n || m == q0) continue;
+    g.sdim[sl] = (int)dims[m];
+    g.Us[sl] = x.Up[m];
+    ++sl;
+  }
+  for (; sl < kMaxModes - 2; ++sl) {
+    g.sdim[sl] = 1;
+    g.Us[sl] = nullptr;
+  }
+  g.ldu = q.CP;
+  g.eT = x.eT;
+  g.eU = x.eU;
+  mttkrp_i8_kernel<kI8Stages><<<q.p.G, kI8Threads, kI8Smem, s>>>(tmA, tmB, g, x.ti, x.parts);
+  if (cudaGetLastError() != cudaSuccess) return JKCALS_E_CUDA;
+  const int64_t tot = q.In * C;
+  reduce_parts_kernel<<<(int)cdiv(tot, 256), 256, 0, s>>>(x.parts, x.ti, (int)q.In, (int)C, kI8N, q.nMt, M, ldm);
+  if (cudaGetLastError() != cudaSuccess) return JKCALS_E_CUDA;
   if (cudaStreamSynchronize(s) != cudaSuccess) return JKCALS_E_CUDA;
   return JKCALS_OK;
 }

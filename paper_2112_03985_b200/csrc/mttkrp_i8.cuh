@@ -1,0 +1,311 @@
+// mttkrp_i8.cuh — EXPERIMENTAL stand-alone FP64-accurate MTTKRP from INT8 tcgen05 MMAs
+// (not on the JK-CALS path yet).
+//
+//   M(i, c) = sum_j' S(j', c) * sum_iq0 T(i, iq0, j') U_q0(iq0, c)          (the KRP factorisation)
+//
+// Both operands of the inner product are split into 7 balanced base-128 digits with power-of-two
+// scales (T per mode-n row i, U_q0 per column c): x = 2^e sum_s d_s 2^(-7(s+1)), |d_s| <= 64.
+// Products of digits a, b with a + b = dg accumulate exactly (int32) in TMEM accumulator D_dg; per
+// j' the drain warps fold sum_dg D_dg 2^(-14-7 dg) times S(j', c) into FP64 registers, and the
+// scales 2^(e_T(i) + e_U(c)) are applied when the CTA's partial piece is written. One stream-K
+// unit = (output tile, j'); K = I_q0 padded to 32 per unit (7 K32 steps for I_q0 = 200).
+// Operands are precomputed by slice_t_i8_kernel / slice_u_i8_kernel into GEMM-friendly layouts:
+//   Bsl[s][j'][i (InP)][k (KP)]  and  Asl[s][c (CP)][k (KP)]   (int8, k contiguous)
+// and loaded per K32 step by 3-D TMA boxes (32 B, rows, 7 slices) with SWIZZLE_32B.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "mttkrp_tf32.cuh"
+
+namespace jk {
+
+constexpr int kI8S = 7;          // digits (slices) per operand
+constexpr int kI8N = 64;         // UMMA N = rows i of an output tile (7 accumulators x 64 <= 512)
+constexpr int kI8K = 32;         // K per step (32-byte SWIZZLE_32B rows)
+constexpr int kI8Stages = 4;
+constexpr int kI8Threads = 6 * 32;  // warp 0 TMA, warp 1 MMA, warps 2-5 drain (TMEM lane quadrants)
+constexpr size_t kI8ABytes = (size_t)kI8S * 128 * kI8K;    // 28 KB
+constexpr size_t kI8BBytes = (size_t)kI8S * kI8N * kI8K;   // 14 KB
+constexpr size_t kI8StageBytes = kI8ABytes + kI8BBytes;
+constexpr size_t kI8Smem = 1024 + kI8Stages * kI8StageBytes + 256;
+
+struct I8Geom {
+  int nMt, nNt;      // output tiles: C / 128, I_n / 64 (padded)
+  int Jp, KS;        // j' count, K32 steps per unit (KP / 32)
+  int64_t units;     // nMt * nNt * Jp
+  int InP;           // padded I_n (rows of a j' block of Bsl)
+  int nslow;
+  int sdim[kMaxModes - 2];
+  const double* Us[kMaxModes - 2];  // slow modes' U (row-major rows x ldu)
+  int64_t ldu;
+  const int* eT;     // [InP] row exponents of T
+  const int* eU;     // [CP] column exponents of U_q0
+};
+
+__device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1u << 16) | ((uint64_t)(256u >> 4) << 32) |
+         ((uint64_t)1u << 46) | ((uint64_t)6u << 61);
+}
+__device__ __forceinline__ uint32_t umma_idesc_i8(int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
+}
+__device__ __forceinline__ void umma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+               "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(a), "l"(b), "r"(idesc),
+               "r"(acc));
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// digits of x * 2^-e (|x 2^-e| <= 1/2): 7 balanced base-128 digits, most significant first
+__device__ __forceinline__ void i8_digits(double x, int e, int8_t* d) {
+  double r = ldexp(x, -e);
+#pragma unroll
+  for (int s = 0; s < kI8S; ++s) {
+    r *= 128.0;
+    const double q = rint(r);
+    d[s] = (int8_t)q;
+    r -= q;
+  }
+}
+__device__ __forceinline__ int i8_exponent(double m) {  // e with m * 2^-e <= 1/2
+  if (!(m > 0.0)) return 0;
+  int e;
+  frexp(m, &e);  // m = f 2^e, f in [0.5, 1)
+  return e + 1;
+}
+
+template <int kStages>
+__global__ void __launch_bounds__(kI8Threads, 1)
+    mttkrp_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, I8Geom g,
+                     const TileInfo* __restrict__ tinfo, double* __restrict__ parts) {
+  extern __shared__ __align__(1024) unsigned char ism[];
+  unsigned char* stages = ism;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kStages * kI8StageBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = full + kStages;
+  uint64_t* acc_full = empty + kStages;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int b = blockIdx.x;
+  const int* cta_u = reinterpret_cast<const int*>(tinfo + g.nMt * g.nNt);
+  const int64_t u0 = cta_u[b], u1 = cta_u[b + 1];
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const int KT = g.Jp;  // units per tile
+
+  if (warp == 0) {
+    // ---------------- TMA producer: per unit, KS steps of (A box, B box), each all 7 slices
+    unsigned it = 0;
+    for (int64_t u = u0; u < u1; ++u) {
+      const int t = (int)(u / KT), jp = (int)(u % KT);
+      const int tm = t % g.nMt, tn = t / g.nMt;
+      for (int ks = 0; ks < g.KS; ++ks, ++it) {
+        const int slot = (int)(it % kStages);
+        if (it >= (unsigned)kStages) mbar_wait_safe(&empty[slot], ((it / kStages) - 1) & 1u);
+        if (elect_one()) {
+          unsigned char* st = stages + slot * kI8StageBytes;
+          mbar_expect_tx(&full[slot], (unsigned)kI8StageBytes);
+          tma_load_3d(st, &tmA, ks * kI8K, tm * 128, 0, &full[slot]);
+          tma_load_3d(st + kI8ABytes, &tmB, ks * kI8K, jp * g.InP + tn * kI8N, 0, &full[slot]);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: 28 digit products per K32 step into the 7 diagonal accumulators
+    const uint32_t idesc = umma_idesc_i8(kI8N);
+    unsigned it = 0, un = 0;
+    for (int64_t u = u0; u < u1; ++u, ++un) {
+      if (un >= 1) mbar_wait_safe(acc_empty, (un - 1) & 1u);  // the drain has read the previous unit
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      for (int ks = 0; ks < g.KS; ++ks, ++it) {
+        const int slot = (int)(it % kStages);
+        mbar_wait_safe(&full[slot], (it / kStages) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t a0 = smem_u32(stages + slot * kI8StageBytes);
+        const uint32_t b0 = a0 + (uint32_t)kI8ABytes;
+        if (elect_one()) {
+#pragma unroll
+          for (int dg = 0; dg < kI8S; ++dg)
+#pragma unroll
+            for (int a = 0; a <= dg; ++a)
+              umma_i8(tmem + dg * kI8N, umma_desc_sw32(a0 + a * 128 * kI8K), umma_desc_sw32(b0 + (dg - a) * kI8N * kI8K),
+                      idesc, (ks > 0 || a > 0) ? 1u : 0u);
+          umma_commit(&empty[slot]);
+          if (ks == g.KS - 1) umma_commit(acc_full);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- drain warps: TMEM lane quadrant q <-> fused columns 32q..32q+31 of the tile
+    // (a warp may only read the TMEM lanes of its own quadrant, warp % 4)
+    const int q = warp & 3;
+    const int cl = q * 32 + lane;
+    double acc[kI8N];
+#pragma unroll
+    for (int i = 0; i < kI8N; ++i) acc[i] = 0.0;
+    unsigned un = 0;
+    int64_t seg_t = -1;
+    auto flush = [&](int64_t t) {  // write this CTA's piece of tile t, with the scales
+      const int tm = (int)(t % g.nMt), tn = (int)(t / g.nMt);
+      const TileInfo ti = tinfo[t];
+      double* P = parts + ((int64_t)ti.piece_base + (b - ti.first_cta)) * (int64_t)(kI8N * 128) + cl;
+      const int eu = g.eU[tm * 128 + cl];
+#pragma unroll
+      for (int il = 0; il < kI8N; ++il) {
+        P[(int64_t)il * 128] = ldexp(acc[il], eu + g.eT[tn * kI8N + il]);
+        acc[il] = 0.0;
+      }
+    };
+    for (int64_t u = u0; u < u1; ++u, ++un) {
+      const int64_t t = u / KT;
+      const int jp = (int)(u % KT);
+      if (seg_t >= 0 && t != seg_t) flush(seg_t);
+      seg_t = t;
+      const int c = (int)(t % g.nMt) * 128 + cl;
+      // S(j', c) = prod of the slow modes' rows (FP64, from L2)
+      double s = 1.0;
+      {
+        int rem = jp;
+        for (int m = 0; m < g.nslow; ++m) {
+          const int idx = rem % g.sdim[m];
+          rem /= g.sdim[m];
+          s *= g.Us[m][(int64_t)idx * g.ldu + c];
+        }
+      }
+      mbar_wait_safe(acc_full, un & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
+#pragma unroll
+      for (int cg = 0; cg < kI8N; cg += 16) {
+        double v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = 0.0;
+#pragma unroll 1
+        for (int dg = kI8S - 1; dg >= 0; --dg) {  // small terms first, fixed order
+          uint32_t r[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+              : "r"(lb + (uint32_t)(dg * kI8N + cg)));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+          const double w = ldexp(1.0, -14 - 7 * dg);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += (double)(int)r[i] * w;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[cg + i] += s * v[i];
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty);
+    }
+    if (seg_t >= 0) flush(seg_t);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+  }
+}
+
+// ---- operand preparation -----------------------------------------------------------------
+// row exponents of T_(n): e_T(i) with max_j |T(i, j)| 2^-e <= 1/2 (one block per row)
+__global__ void row_exp_t_kernel(const double* __restrict__ T, int N, const int64_t* __restrict__ st_dev,
+                                 const int* __restrict__ dims_dev, int n, int64_t J, int* __restrict__ eT) {
+  // st_dev: element strides of T per mode; the J other indices enumerated in Eq. 3 order
+  const int i = blockIdx.x;
+  double m = 0.0;
+  for (int64_t j = threadIdx.x; j < J; j += blockDim.x) {
+    int64_t rem = j, off = (int64_t)i * st_dev[n];
+    for (int k = 0; k < N; ++k) {
+      if (k == n) continue;
+      off += (rem % dims_dev[k]) * st_dev[k];
+      rem /= dims_dev[k];
+    }
+    m = fmax(m, fabs(T[off]));
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) eT[i] = i8_exponent(red[0]);
+}
+
+// Bsl[s][j'][i][k] = digit s of T(i_n = i, i_q0 = k, j') * 2^-e_T(i); zero padding outside
+__global__ void slice_t_i8_kernel(const double* __restrict__ T, int N, const int64_t* __restrict__ st_dev,
+                                  const int* __restrict__ dims_dev, int n, int q0, int In, int InP, int Iq0, int KP,
+                                  int64_t Jp, const int* __restrict__ eT, int8_t* __restrict__ B) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per = (int64_t)InP * KP;
+  if (e >= Jp * per) return;
+  const int64_t jp = e / per;
+  const int i = (int)((e % per) / KP), k = (int)(e % KP);
+  int8_t d[kI8S] = {0, 0, 0, 0, 0, 0, 0};
+  if (i < In && k < Iq0) {
+    int64_t rem = jp, off = (int64_t)i * st_dev[n] + (int64_t)k * st_dev[q0];
+    for (int m = 0; m < N; ++m) {
+      if (m == n || m == q0) continue;
+      off += (rem % dims_dev[m]) * st_dev[m];
+      rem /= dims_dev[m];
+    }
+    i8_digits(T[off], eT[i], d);
+  }
+  const int64_t slice = Jp * per;
+#pragma unroll
+  for (int s = 0; s < kI8S; ++s) B[(int64_t)s * slice + e] = d[s];
+}
+
+// column exponents of U_q0 and Asl[s][c][k] = digit s of U_q0(k, c) * 2^-e_U(c)
+__global__ void col_exp_u_kernel(const double* __restrict__ U, int64_t ldu, int rows, int C, int CP,
+                                 int* __restrict__ eU) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= CP) return;
+  double m = 0.0;
+  if (c < C)
+    for (int k = 0; k < rows; ++k) m = fmax(m, fabs(U[(int64_t)k * ldu + c]));
+  eU[c] = i8_exponent(m);
+}
+__global__ void slice_u_i8_kernel(const double* __restrict__ U, int64_t ldu, int rows, int C, int CP, int KP,
+                                  const int* __restrict__ eU, int8_t* __restrict__ A) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)CP * KP) return;
+  const int c = (int)(e / KP), k = (int)(e % KP);
+  int8_t d[kI8S] = {0, 0, 0, 0, 0, 0, 0};
+  if (c < C && k < rows) i8_digits(U[(int64_t)k * ldu + c], eU[c], d);
+  const int64_t slice = (int64_t)CP * KP;
+#pragma unroll
+  for (int s = 0; s < kI8S; ++s) A[(int64_t)s * slice + e] = d[s];
+}
+
+}  // namespace jk

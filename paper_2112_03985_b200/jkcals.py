@@ -81,6 +81,8 @@ def lib():
             "jkcals_destroy": (None, [P]),
             "jkcals_mttkrp_scratch_bytes": (SZ, [I, P, I, I64, I]),
             "jkcals_mttkrp": (I, [I, P, I, P, P, I64, I64, P, I64, P, SZ, P]),
+            "jkcals_mttkrp_i8_scratch_bytes": (SZ, [I, P, I, I64, I]),
+            "jkcals_mttkrp_i8": (I, [I, P, I, P, P, I64, I64, P, I64, P, SZ, P]),
             "jkcals_krp": (I, [I, P, I, P, I64, I64, P, I64, P]),
         }
         for name, (res, args) in sigs.items():
@@ -94,7 +96,7 @@ def lib():
 EXPORTED = [
     "jkcals_workspace_bytes", "jkcals_create", "jkcals_create_d", "jkcals_pool_workspace_bytes",
     "jkcals_create_pool", "jkcals_get_model_stats", "jkcals_get_model_moments", "jkcals_align",
-    "jkcals_set_init_all", "jkcals_config_workspace_bytes", "jkcals_create_config", "jkcals_num_slots", "jkcals_get_ids",
+    "jkcals_set_init_all", "jkcals_config_workspace_bytes", "jkcals_mttkrp_i8_scratch_bytes", "jkcals_mttkrp_i8", "jkcals_create_config", "jkcals_num_slots", "jkcals_get_ids",
     "jkcals_state_bytes", "jkcals_export_submodel", "jkcals_import_submodel",
     "jkcals_get_alignment", "jkcals_get_aligned_factors", "jkcals_get_aligned_moments", "jkcals_get_aligned_stats",
     "jkcals_set_init", "jkcals_set_init_submodel", "jkcals_iterate",
@@ -437,6 +439,27 @@ def mttkrp(T_flat, dims, n, U, C):
                          ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
     if st != 0:
         raise JKCalsError(st, "jkcals_mttkrp failed")
+    return M
+
+
+def mttkrp_i8(T_flat, dims, n, U, C):
+    """EXPERIMENTAL: the same MTTKRP, FP64-accurate from INT8 tcgen05 MMAs."""
+    torch = _torch()
+    L = lib()
+    d = _i64(dims)
+    ldu = U[(n + 1) % len(dims)].shape[1]
+    dev = T_flat.device.index
+    nb = L.jkcals_mttkrp_i8_scratch_bytes(len(dims), _p(d), n, C, dev)
+    if nb == 0:
+        raise JKCalsError(-1, "unsupported mttkrp_i8 arguments")
+    scratch = torch.empty(nb, dtype=torch.uint8, device=T_flat.device)
+    M = torch.empty((dims[n], C), dtype=torch.float64, device=T_flat.device)
+    ptrs = (ctypes.c_void_p * len(dims))(*[u.data_ptr() for u in U])
+    st = L.jkcals_mttkrp_i8(len(dims), _p(d), n, ctypes.c_void_p(T_flat.data_ptr()), ptrs, C, ldu,
+                            ctypes.c_void_p(M.data_ptr()), C, ctypes.c_void_p(scratch.data_ptr()), nb,
+                            ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+    if st != 0:
+        raise JKCalsError(st, "jkcals_mttkrp_i8 failed")
     return M
 
 

@@ -310,3 +310,22 @@ def test_fp32_path_vs_oracle(name, ps):
     p_list = list(range(w.dims[0])) if ps is None else ps
     res = O.jk_als(w.T, w.P, p_list=p_list, max_iters=sweeps, nthreads=NCPU)
     check32(h, res, p_list)
+
+
+@pytest.mark.parametrize("dims,C", [((10, 8, 6), 20), ((37, 23, 11), 129), ((13, 7, 5, 3), 70),
+                                    ((50, 50, 50), 250), ((5, 300, 4), 10)])
+def test_experimental_int8_sliced_mttkrp(dims, C):
+    # the FP64-accurate MTTKRP from INT8 tcgen05 MMAs (7-digit slicing, exact int32
+    # diagonal accumulators, S applied in FP64) matches the oracle like the DMMA kernel does
+    import torch
+    from paper_2112_03985_b200.jkcals import mttkrp_i8
+    g = np.random.default_rng(sum(dims) + C + 7)
+    T = np.asfortranarray(g.standard_normal(dims))
+    U = [g.standard_normal((I, C)) for I in dims]
+    ldu = ((C + 127) // 128) * 128
+    Ud = [torch.from_numpy(np.pad(u, ((0, 0), (0, ldu - C)))).cuda() for u in U]
+    Td = torch.from_numpy(np.ravel(T, order="F").copy()).cuda()
+    for n in range(len(dims)):
+        M = mttkrp_i8(Td, dims, n, Ud, C).cpu().numpy()
+        ref = O.mttkrp(T, U, n)
+        assert rel(M, ref) <= 1e-13, (dims, C, n, rel(M, ref))
