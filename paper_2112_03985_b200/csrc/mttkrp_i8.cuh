@@ -25,7 +25,8 @@ constexpr int kI8S = 7;          // digits (slices) per operand
 constexpr int kI8N = 64;         // UMMA N = rows i of an output tile (7 accumulators x 64 <= 512)
 constexpr int kI8K = 32;         // K per step (32-byte SWIZZLE_32B rows)
 constexpr int kI8Stages = 4;
-constexpr int kI8Threads = 6 * 32;  // warp 0 TMA, warp 1 MMA, warps 2-5 drain (TMEM lane quadrants)
+constexpr int kI8Threads = 10 * 32;  // warp 0 TMA, warp 1 MMA, warps 2-9 drain (lane quadrant x column half)
+constexpr int kI8DWarps = 8;
 constexpr size_t kI8ABytes = (size_t)kI8S * 128 * kI8K;    // 28 KB
 constexpr size_t kI8BBytes = (size_t)kI8S * kI8N * kI8K;   // 14 KB
 constexpr size_t kI8StageBytes = kI8ABytes + kI8BBytes;
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(acc_full, 1);
-    mbar_init(acc_empty, 4);
+    mbar_init(acc_empty, kI8DWarps);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 0) {
@@ -163,23 +164,25 @@ __global__ void __launch_bounds__(kI8Threads, 1)
     }
   } else {
     // ---------------- drain warps: TMEM lane quadrant q <-> fused columns 32q..32q+31 of the tile
-    // (a warp may only read the TMEM lanes of its own quadrant, warp % 4)
-    const int q = warp & 3;
+    // (a warp may only read the TMEM lanes of its own quadrant, warp % 4); each of the two warps of
+    // a quadrant folds one 32-column half of the N = 64 accumulator columns
+    const int q = warp & 3, h = (warp - 2) >> 2;
     const int cl = q * 32 + lane;
-    double acc[kI8N];
+    double acc[kI8N / 2];
 #pragma unroll
-    for (int i = 0; i < kI8N; ++i) acc[i] = 0.0;
+    for (int i = 0; i < kI8N / 2; ++i) acc[i] = 0.0;
     unsigned un = 0;
     int64_t seg_t = -1;
-    auto flush = [&](int64_t t) {  // write this CTA's piece of tile t, with the scales
+    auto flush = [&](int64_t t) {  // write this CTA's piece of tile t (its column half), with the scales
       const int tm = (int)(t % g.nMt), tn = (int)(t / g.nMt);
       const TileInfo ti = tinfo[t];
       double* P = parts + ((int64_t)ti.piece_base + (b - ti.first_cta)) * (int64_t)(kI8N * 128) + cl;
       const int eu = g.eU[tm * 128 + cl];
 #pragma unroll
-      for (int il = 0; il < kI8N; ++il) {
-        P[(int64_t)il * 128] = ldexp(acc[il], eu + g.eT[tn * kI8N + il]);
-        acc[il] = 0.0;
+      for (int i = 0; i < kI8N / 2; ++i) {
+        const int il = h * (kI8N / 2) + i;
+        P[(int64_t)il * 128] = ldexp(acc[i], eu + g.eT[tn * kI8N + il]);
+        acc[i] = 0.0;
       }
     };
     for (int64_t u = u0; u < u1; ++u, ++un) {
@@ -188,7 +191,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       if (seg_t >= 0 && t != seg_t) flush(seg_t);
       seg_t = t;
       const int c = (int)(t % g.nMt) * 128 + cl;
-      // S(j', c) = prod of the slow modes' rows (FP64, from L2)
+      // S(j', c) = prod of the slow modes' rows (FP64, from L2; overlaps this unit's MMAs)
       double s = 1.0;
       {
         int rem = jp;
@@ -200,27 +203,28 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       }
       mbar_wait_safe(acc_full, un & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
+      const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * (kI8N / 2));
 #pragma unroll
-      for (int cg = 0; cg < kI8N; cg += 16) {
-        double v[16];
+      for (int cg = 0; cg < kI8N / 2; cg += 16) {
+        // all 7 diagonals of these 16 columns in flight, one wait
+        uint32_t r[kI8S][16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = 0.0;
-#pragma unroll 1
-        for (int dg = kI8S - 1; dg >= 0; --dg) {  // small terms first, fixed order
-          uint32_t r[16];
+        for (int dg = 0; dg < kI8S; ++dg)
           asm volatile(
               "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+              : "=r"(r[dg][0]), "=r"(r[dg][1]), "=r"(r[dg][2]), "=r"(r[dg][3]), "=r"(r[dg][4]), "=r"(r[dg][5]),
+                "=r"(r[dg][6]), "=r"(r[dg][7]), "=r"(r[dg][8]), "=r"(r[dg][9]), "=r"(r[dg][10]), "=r"(r[dg][11]),
+                "=r"(r[dg][12]), "=r"(r[dg][13]), "=r"(r[dg][14]), "=r"(r[dg][15])
               : "r"(lb + (uint32_t)(dg * kI8N + cg)));
-          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-          const double w = ldexp(1.0, -14 - 7 * dg);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] += (double)(int)r[i] * w;
+        for (int i = 0; i < 16; ++i) {
+          double v = 0.0;
+#pragma unroll
+          for (int dg = kI8S - 1; dg >= 0; --dg)  // small terms first, fixed order
+            v += (double)(int)r[dg][i] * ldexp(1.0, -14 - 7 * dg);
+          acc[cg + i] += s * v;
         }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) acc[cg + i] += s * v[i];
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       __syncwarp();
