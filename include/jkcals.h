@@ -60,7 +60,9 @@ typedef enum {
   JKCALS_E_NONFINITE = -6  /* non-finite value in the tensor or the initial model */
 } jkcals_status;
 
-typedef enum { JKCALS_FP64 = 0, JKCALS_FP32 = 1 } jkcals_precision;
+/* JKCALS_FP64_I8 (experimental): FP64 factors and epilogue, the MTTKRP from INT8
+ * tcgen05 MMAs on 7-digit operand slices with exact integer accumulation (FP64-accurate). */
+typedef enum { JKCALS_FP64 = 0, JKCALS_FP32 = 1, JKCALS_FP64_I8 = 2 } jkcals_precision;
 
 enum {
   JKCALS_F_CONVERGED = 1,

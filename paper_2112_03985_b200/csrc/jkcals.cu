@@ -84,6 +84,8 @@ KernelInfo* kernel_info(int device, std::string* err) {
       e = cudaFuncSetAttribute(mttkrp_tf32_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTfSmemMax);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(mttkrp_tf32_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTfSmemMax);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(mttkrp_i8_kernel<kI8Stages>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8Smem);
     if (e != cudaSuccess) {
       if (err) *err = std::string("cudaFuncSetAttribute(tf32): ") + cudaGetErrorString(e);
       cudaSetDevice(prev);
@@ -415,6 +417,46 @@ int bnp_of(int NT) {
   return BN + ((4 - BN % 16) + 16) % 16;
 }
 
+// ---------------------------------------------------------------- INT8-sliced MTTKRP plans (§9b)
+struct I8Plan {
+  int64_t In, Iq0, Jp, InP, KP, CP;
+  int nMt, nNt;
+  ModePlan p;
+};
+I8Plan make_i8_plan(int ndims, const int64_t* dims, int n, int64_t C, const KernelInfo& ki) {
+  I8Plan q;
+  const ModeGeo mg = mode_geo(ndims, dims, n);
+  q.In = mg.In;
+  q.Iq0 = mg.Iq0;
+  q.Jp = mg.Jp;
+  q.InP = rup(q.In, kI8N);
+  q.KP = rup(q.Iq0, kI8K);
+  q.CP = rup(C, 128);
+  q.nMt = (int)(q.CP / 128);
+  q.nNt = (int)(q.InP / kI8N);
+  ModePlan& p = q.p;
+  p.nMt = q.nMt;
+  p.nNt = q.nNt;
+  p.BN = kI8N;
+  p.KT = (int)q.Jp;
+  p.ntiles = p.nMt * p.nNt;
+  p.units = (int64_t)p.ntiles * p.KT;
+  p.G = (int)std::min<int64_t>(p.units, (int64_t)ki.nsm);
+  finish_plan(p, mg);
+  return q;
+}
+bool make_tmap_i8(CUtensorMap* tm, const int8_t* base, int64_t kp, int64_t rows, int box_rows) {
+  auto enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t gdim[3] = {(cuuint64_t)kp, (cuuint64_t)rows, (cuuint64_t)kI8S};
+  cuuint64_t gstr[2] = {(cuuint64_t)kp, (cuuint64_t)(kp * rows)};
+  cuuint32_t box[3] = {(cuuint32_t)kI8K, (cuuint32_t)box_rows, (cuuint32_t)kI8S}, est[3] = {1, 1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), gdim, gstr, box, est,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // ---------------------------------------------------------------- workspace layout
 struct Layout {
   size_t off = 0;
@@ -430,6 +472,7 @@ struct Offsets {
       lambda, normT2p, fit, fit_prev, err, hist,
       slice, slice_part, stage, iters, flags, active, blk2sub, map, pglob, misc, srcoff, srcld, subR, subRc, blkcol,
       dstoff, pref[kMaxModes], aln, aperm, asign, acong, asrc, asld, srcpg;
+  size_t i8B[kMaxModes], i8eT[kMaxModes], i8A, i8eU, i8st, i8dims;  // INT8-sliced MTTKRP (§9b)
   int64_t parts_cap;
   int tiles_cap;
   int slice_nb;
@@ -439,7 +482,7 @@ struct Offsets {
 
 // R: the largest rank in the handle (Rs); sumRm: sum of the pool's model ranks (staging of P)
 bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_cap, const KernelInfo& ki,
-                     Offsets* o, bool tf32 = false, int64_t sumRm = 0) {
+                     Offsets* o, bool tf32 = false, int64_t sumRm = 0, bool i8 = false) {
   int64_t P = 1, sumI = 0, maxI = 0;
   for (int k = 0; k < N; ++k) {
     P *= dims[k];
@@ -464,7 +507,13 @@ bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_c
   for (int n = 0; n < N; ++n) {
     int64_t pc;
     int tc;
-    plan_bounds(mode_geo(N, dims, n), n, C, ki, &pc, &tc, tf32);
+    if (i8) {
+      const I8Plan q = make_i8_plan(N, dims, n, C, ki);
+      pc = (std::max<int64_t>(q.p.G, ki.nsm) + q.p.ntiles) * kI8N * kBM;
+      tc = q.p.ntiles;
+    } else {
+      plan_bounds(mode_geo(N, dims, n), n, C, ki, &pc, &tc, tf32);
+    }
     o->parts_cap = std::max(o->parts_cap, pc);
     o->tiles_cap = std::max(o->tiles_cap, tc);
   }
@@ -473,7 +522,7 @@ bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_c
   // pre-reduced pieces (one per tile) for tiles split over many CTAs, and their 1-piece tables
   int64_t red_cap = 0;
   for (int n = 0; n < N; ++n) {
-    const ModePlan q = make_plan(mode_geo(N, dims, n), n, C, ki, tf32);
+    const ModePlan q = i8 ? make_i8_plan(N, dims, n, C, ki).p : make_plan(mode_geo(N, dims, n), n, C, ki, tf32);
     red_cap = std::max<int64_t>(red_cap, (int64_t)q.ntiles * q.BN * kBM);
   }
   o->red = L.take(red_cap * 8);
@@ -504,6 +553,22 @@ bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_c
   o->subRc = L.take(nsub * 4);
   o->blkcol = L.take(nsub * 4);
   o->dstoff = L.take(nsub * 8);
+  for (int k = 0; k < kMaxModes; ++k) o->i8B[k] = o->i8eT[k] = 0;
+  o->i8A = o->i8eU = o->i8st = o->i8dims = 0;
+  if (i8) {  // per-mode T digits (fixed) + the U_q0 digits of the mode being updated
+    int64_t amax = 0, cpmax = 0;
+    for (int n = 0; n < N; ++n) {
+      const I8Plan q = make_i8_plan(N, dims, n, C, ki);
+      o->i8B[n] = L.take((size_t)kI8S * q.Jp * q.InP * q.KP);
+      o->i8eT[n] = L.take((size_t)q.InP * 4);
+      amax = std::max<int64_t>(amax, (int64_t)kI8S * q.CP * q.KP);
+      cpmax = std::max<int64_t>(cpmax, q.CP);
+    }
+    o->i8A = L.take(amax);
+    o->i8eU = L.take(cpmax * 4);
+    o->i8st = L.take(kMaxModes * 8);
+    o->i8dims = L.take(kMaxModes * 4);
+  }
   // the pool's reference models (warm starts): mode n is col-major I_n x sumRm
   for (int k = 0; k < N; ++k) o->pref[k] = L.take(dims[k] * std::max<int64_t>(sumRm, R) * 8);
   o->aln = L.take(nsub * sumI * R * 8);  // aligned factors (NEXT #3), slot layout as Ures
@@ -573,6 +638,9 @@ struct jkcals_s {
   bool red_on[kMaxModes] = {false};    // pieces of this mode pre-reduced before the epilogue
   std::vector<TileInfo> table1[kMaxModes];
   int tf32 = 0;                        // precision JKCALS_FP32: 3xTF32 tcgen05 MTTKRP
+  int i8 = 0;                          // precision JKCALS_FP64_I8: INT8-sliced FP64-accurate MTTKRP
+  I8Plan i8q[kMaxModes];
+  CUtensorMap tmA8[kMaxModes], tmB8[kMaxModes];
   CUtensorMap tmThi[kMaxModes], tmTlo[kMaxModes];
   cudaGraphExec_t gexec = nullptr;
   bool graph_ok = false;
@@ -634,7 +702,12 @@ struct DeviceGuard {
 jkcals_status replan(jkcals_t h) {
   NvtxRange nv("jkcals replan");
   for (int n = 0; n < h->N; ++n) {
-    h->plan[n] = make_plan(mode_geo(h->N, h->dims, n), n, h->C, *h->ki, h->tf32 != 0);
+    if (h->i8) {
+      h->i8q[n] = make_i8_plan(h->N, h->dims, n, h->C, *h->ki);
+      h->plan[n] = h->i8q[n].p;
+    } else {
+      h->plan[n] = make_plan(mode_geo(h->N, h->dims, n), n, h->C, *h->ki, h->tf32 != 0);
+    }
     const ModePlan& p = h->plan[n];
     if (plan_parts_doubles(p) > h->off.parts_cap || p.ntiles > h->off.tiles_cap)
       return fail(h, JKCALS_E_OOM, "internal: plan exceeds workspace bounds");
@@ -657,6 +730,13 @@ jkcals_status replan(jkcals_t h) {
     }
     CKH(h, cudaMemcpyAsync(h->ptr<TileInfo>(h->off.tinfo1[n]), h->table1[n].data(), p.ntiles * sizeof(TileInfo),
                            cudaMemcpyHostToDevice, h->stream));
+    if (h->i8) {  // 3-D boxes over the U_q0 digits (rebuilt each mode) and this mode's T digits
+      const I8Plan& q = h->i8q[n];
+      if (!make_tmap_i8(&h->tmA8[n], h->ptr<int8_t>(h->off.i8A), q.KP, q.CP, 128) ||
+          !make_tmap_i8(&h->tmB8[n], h->ptr<int8_t>(h->off.i8B[n]), q.KP, q.Jp * q.InP, kI8N))
+        return fail(h, JKCALS_E_CUDA, "cuTensorMapEncodeTiled failed for the int8 digits of mode %d", n);
+      continue;
+    }
     // TMA descriptors: the tensor view of mode n and the U_q0 slab source of both U buffer sets
     if (!make_tmap_T(&h->tmT[n], h->ptr<double>(h->off.T), h->N, h->dims, h->I0p, n, p.BN, bnp_of(p.NT)))
       return fail(h, JKCALS_E_CUDA, "cuTensorMapEncodeTiled failed for the tensor view of mode %d", n);
@@ -749,7 +829,41 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
   const TileInfo* ti = h->ptr<TileInfo>(h->off.tinfo[n]);
   double* parts = h->ptr<double>(h->off.parts);
   if (timed) CKH(h, cudaEventRecord(h->ev[4 * n + 0], h->es));
-  if (h->tf32) {
+  if (h->i8) {
+    // U_q0 digits of the just-updated factor, then the INT8 MMAs
+    const I8Plan& q = h->i8q[n];
+    const int q0 = (n == 0) ? 1 : 0;
+    int* eU = h->ptr<int>(h->off.i8eU);
+    int8_t* A = h->ptr<int8_t>(h->off.i8A);
+    col_exp_u_kernel<<<(int)cdiv(q.CP, 128), 128, 0, h->es>>>(Uall[q0], h->ldu, (int)q.Iq0, h->C, (int)q.CP, eU);
+    CKH(h, cudaGetLastError());
+    slice_u_i8_kernel<<<(int)cdiv(q.CP * q.KP, 256), 256, 0, h->es>>>(Uall[q0], h->ldu, (int)q.Iq0, h->C, (int)q.CP,
+                                                                     (int)q.KP, eU, A);
+    CKH(h, cudaGetLastError());
+    I8Geom ig;
+    ig.nMt = q.nMt;
+    ig.nNt = q.nNt;
+    ig.Jp = (int)q.Jp;
+    ig.KS = (int)(q.KP / kI8K);
+    ig.units = p.units;
+    ig.InP = (int)q.InP;
+    ig.nslow = h->N - 2;
+    int sl = 0;
+    for (int m = 0; m < h->N; ++m) {
+      if (m == n || m == q0) continue;
+      ig.sdim[sl] = (int)h->dims[m];
+      ig.Us[sl] = Uall[m];
+      ++sl;
+    }
+    for (; sl < kMaxModes - 2; ++sl) {
+      ig.sdim[sl] = 1;
+      ig.Us[sl] = nullptr;
+    }
+    ig.ldu = h->ldu;
+    ig.eT = h->ptr<int>(h->off.i8eT[n]);
+    ig.eU = eU;
+    mttkrp_i8_kernel<kI8Stages><<<p.G, kI8Threads, kI8Smem, h->es>>>(h->tmA8[n], h->tmB8[n], ig, ti, parts);
+  } else if (h->tf32) {
     TfGeom tg;
     tg.C = h->C;
     tg.ldu = h->ldu;
@@ -1051,7 +1165,7 @@ static bool pool_geo(const jkcals_config* c, PoolGeo* g) {
   const int64_t* dims = c->dims;
   const int64_t d = c->d;
   if (dims[0] < 2 || d < 0 || (d > 1 && 2 * d > dims[0]) || c->spare < 0 || c->hist_cap < 1) return false;
-  if (c->prec != JKCALS_FP64 && c->prec != JKCALS_FP32) return false;
+  if (c->prec != JKCALS_FP64 && c->prec != JKCALS_FP32 && c->prec != JKCALS_FP64_I8) return false;
   for (int m = 0; m < c->nmodels; ++m)
     if (c->ranks[m] < 1 || c->ranks[m] > kLgRMax) return false;
   // d = 0: plain CALS (§3.3): one model per id, nothing left out
@@ -1081,7 +1195,8 @@ size_t jkcals_config_workspace_bytes(const jkcals_config* c) {
   KernelInfo* ki = kernel_info(c->device, nullptr);
   if (!ki) return 0;
   Offsets o;
-  compute_offsets(c->ndims, c->dims, g.Rs, g.nslot, c->hist_cap, *ki, &o, c->prec == JKCALS_FP32, g.sumRm);
+  compute_offsets(c->ndims, c->dims, g.Rs, g.nslot, c->hist_cap, *ki, &o, c->prec == JKCALS_FP32, g.sumRm,
+                  c->prec == JKCALS_FP64_I8);
   return o.total;
 }
 
@@ -1207,7 +1322,8 @@ jkcals_status jkcals_create_config(jkcals_t* out, const jkcals_config* cfg, cons
   h->es = h->stream;
   h->ki = ki;
   h->tf32 = (prec == JKCALS_FP32) ? 1 : 0;
-  compute_offsets(ndims, dims, h->R, h->nsub, hist_cap, *ki, &h->off, h->tf32 != 0, pg0.sumRm);
+  h->i8 = (prec == JKCALS_FP64_I8) ? 1 : 0;
+  compute_offsets(ndims, dims, h->R, h->nsub, hist_cap, *ki, &h->off, h->tf32 != 0, pg0.sumRm, h->i8 != 0);
   // align the caller's pointer
   uintptr_t base = reinterpret_cast<uintptr_t>(workspace);
   uintptr_t aligned = (base + kAlign - 1) & ~(uintptr_t)(kAlign - 1);
@@ -1275,6 +1391,30 @@ jkcals_status jkcals_create_config(jkcals_t* out, const jkcals_config* cfg, cons
     split_tf32_kernel<<<nbk, 256, 0, h->stream>>>(h->ptr<double>(h->off.T), dims[0], h->I0p, I1, rest, 1, ld1,
                                                   h->ptr<float>(h->off.T1hi), h->ptr<float>(h->off.T1lo));
     CKH(h, cudaGetLastError());
+  }
+  if (h->i8) {  // per-mode INT8 digits of T with per-row scales (fixed for the handle's life)
+    int64_t stv[kMaxModes];
+    int dv[kMaxModes];
+    stv[0] = 1;
+    stv[1] = h->I0p;
+    for (int m = 2; m < ndims; ++m) stv[m] = stv[m - 1] * dims[m - 1];
+    for (int m = 0; m < ndims; ++m) dv[m] = (int)dims[m];
+    int64_t* st_d = h->ptr<int64_t>(h->off.i8st);
+    int* dims_d = h->ptr<int>(h->off.i8dims);
+    CKH(h, cudaMemcpyAsync(st_d, stv, 8 * ndims, cudaMemcpyHostToDevice, h->stream));
+    CKH(h, cudaMemcpyAsync(dims_d, dv, 4 * ndims, cudaMemcpyHostToDevice, h->stream));
+    for (int n = 0; n < ndims; ++n) {
+      const I8Plan q = make_i8_plan(ndims, dims, n, h->C, *ki);
+      int* eT = h->ptr<int>(h->off.i8eT[n]);
+      CKH(h, cudaMemsetAsync(eT, 0, q.InP * 4, h->stream));
+      row_exp_t_kernel<<<(int)q.In, 256, 0, h->stream>>>(h->ptr<double>(h->off.T), ndims, st_d, dims_d, n,
+                                                          h->P / dims[n], eT);
+      slice_t_i8_kernel<<<(int)cdiv(q.Jp * q.InP * q.KP, 256), 256, 0, h->stream>>>(
+          h->ptr<double>(h->off.T), ndims, st_d, dims_d, n, (n == 0) ? 1 : 0, (int)q.In, (int)q.InP, (int)q.Iq0,
+          (int)q.KP, q.Jp, eT, h->ptr<int8_t>(h->off.i8B[n]));
+      CKH(h, cudaGetLastError());
+    }
+    CKH(h, cudaStreamSynchronize(h->stream));  // stv / dv are host temporaries
   }
   jkcals_status st = replan(h);
   if (st != JKCALS_OK) return st;
@@ -2005,7 +2145,7 @@ int jkcals_launches_per_sweep(jkcals_t h) {
   if (!h) return 0;
   int n_red = 0;
   for (int n = 0; n < h->N; ++n) n_red += h->red_on[n] ? 1 : 0;
-  return 2 * h->N + n_red;
+  return 2 * h->N + n_red + (h->i8 ? 2 * h->N : 0);  // (+ the two U_q0-digit kernels per mode)
 }
 
 const char* jkcals_last_error(jkcals_t h) { return h ? h->err.c_str() : "null handle"; }
@@ -2103,33 +2243,6 @@ jkcals_status jkcals_mttkrp(int ndims, const int64_t* dims, int n, const double*
 
 // ---------------------------------------------------------------- EXPERIMENTAL: INT8-sliced MTTKRP
 namespace {
-struct I8Plan {
-  int64_t In, Iq0, Jp, InP, KP, CP;
-  int nMt, nNt;
-  ModePlan p;
-};
-I8Plan make_i8_plan(int ndims, const int64_t* dims, int n, int64_t C, const KernelInfo& ki) {
-  I8Plan q;
-  const ModeGeo mg = mode_geo(ndims, dims, n);
-  q.In = mg.In;
-  q.Iq0 = mg.Iq0;
-  q.Jp = mg.Jp;
-  q.InP = rup(q.In, kI8N);
-  q.KP = rup(q.Iq0, kI8K);
-  q.CP = rup(C, 128);
-  q.nMt = (int)(q.CP / 128);
-  q.nNt = (int)(q.InP / kI8N);
-  ModePlan& p = q.p;
-  p.nMt = q.nMt;
-  p.nNt = q.nNt;
-  p.BN = kI8N;
-  p.KT = (int)q.Jp;
-  p.ntiles = p.nMt * p.nNt;
-  p.units = (int64_t)p.ntiles * p.KT;
-  p.G = (int)std::min<int64_t>(p.units, (int64_t)ki.nsm);
-  finish_plan(p, mg);
-  return q;
-}
 struct I8Scratch {
   TileInfo* ti;
   double* parts;
@@ -2159,17 +2272,6 @@ I8Scratch i8_layout(uintptr_t base0, int ndims, const int64_t* dims, const I8Pla
   for (int m = 0; m < ndims; ++m) x.Up[m] = reinterpret_cast<double*>(take((size_t)dims[m] * q.CP * 8));
   x.total = (size_t)(base - start) + kAlign;
   return x;
-}
-bool make_tmap_i8(CUtensorMap* tm, const int8_t* base, int64_t kp, int64_t rows, int box_rows) {
-  auto enc = encode_fn();
-  if (!enc) return false;
-  cuuint64_t gdim[3] = {(cuuint64_t)kp, (cuuint64_t)rows, (cuuint64_t)kI8S};
-  cuuint64_t gstr[2] = {(cuuint64_t)kp, (cuuint64_t)(kp * rows)};
-  cuuint32_t box[3] = {(cuuint32_t)kI8K, (cuuint32_t)box_rows, (cuuint32_t)kI8S}, est[3] = {1, 1, 1};
-  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), gdim, gstr, box, est,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
 }
 }  // namespace
 

@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _build
 
-FP64, FP32 = 0, 1
+FP64, FP32, FP64_I8 = 0, 1, 2  # FP64_I8: experimental INT8-sliced MTTKRP
 F_CONVERGED, F_PINV_FALLBACK, F_NONFINITE, F_BREAKDOWN = 1, 2, 4, 8
 DEFAULT_TOL, DEFAULT_MAX_ITERS = 1e-6, 1000  # PAPER.md:596, 608 (§5.2 protocol)
 

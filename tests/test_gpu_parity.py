@@ -329,3 +329,18 @@ def test_experimental_int8_sliced_mttkrp(dims, C):
         M = mttkrp_i8(Td, dims, n, Ud, C).cpu().numpy()
         ref = O.mttkrp(T, U, n)
         assert rel(M, ref) <= 1e-13, (dims, C, n, rel(M, ref))
+
+
+@pytest.mark.parametrize("name,ps", [("tiny", range(10)), ("syn50_r3", range(50)), ("4way", [0, 1, 50, 99]),
+                                     ("eem_r5", [0, 133, 267])])
+def test_experimental_int8_sliced_fp64_path(name, ps):
+    # precision JKCALS_FP64_I8: the whole JK-CALS loop with the INT8-sliced MTTKRP
+    # held to the FP64 bar (1e-10) against the oracle
+    from paper_2112_03985_b200 import JKCals
+    w = make_workload(name)
+    h = JKCals(w.T, w.R, hist_cap=w.sweeps, precision=2)
+    h.set_init(w.P)
+    h.iterate(w.sweeps, 0.0)
+    ps = list(ps)
+    res = O.jk_als(w.T, w.P, p_list=ps, max_iters=w.sweeps, nthreads=NCPU)
+    check_against_oracle(h, res, ps, nt2p_of(w.T))
