@@ -9,7 +9,7 @@ from paper_2112_03985_b200 import JKCals
 from synth import make_workload
 
 name = sys.argv[1]
-prec = 1 if (len(sys.argv) > 2 and sys.argv[2] == "fp32") else 0
+prec = {"fp32": 1, "fp64_i8": 2}.get(sys.argv[2], 0) if len(sys.argv) > 2 else 0
 w = make_workload(name)
 t0 = time.time()
 h = JKCals(w.T, w.R, hist_cap=w.sweeps, precision=prec)
@@ -27,8 +27,8 @@ for p in range(w.dims[0]):
     worst_lam = max(worst_lam, float(np.linalg.norm(lam - res.lam[p]) / np.linalg.norm(res.lam[p])))
     hg, ho = h.history(p), res.history(p)
     worst_err = max(worst_err, float(np.max(np.abs(hg - ho) / np.abs(ho))))
-bar = 1e-4 if prec else 1e-10
-print(json.dumps({"config": name, "precision": "fp32" if prec else "fp64", "submodels": w.dims[0],
+bar = 1e-4 if prec == 1 else 1e-10
+print(json.dumps({"config": name, "precision": ["fp64", "fp32", "fp64_i8"][prec], "submodels": w.dims[0],
                   "sweeps": w.sweeps, "worst_rel_factor_error_per_mode": worst, "worst_rel_lambda_error": worst_lam,
                   "worst_rel_error_history": worst_err, "bar": bar, "pass": max(worst + [worst_lam]) <= bar,
                   "gpu_s": round(t1 - t0, 2), "oracle_s": round(t2 - t1, 1), "oracle_threads": os.cpu_count()}))
