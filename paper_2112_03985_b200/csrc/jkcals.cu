@@ -445,6 +445,11 @@ I8Plan make_i8_plan(int ndims, const int64_t* dims, int n, int64_t C, const Kern
   finish_plan(p, mg);
   return q;
 }
+// exact int32 accumulation: a diagonal sums <= 7 digit products of magnitude <= 64 * 64 per k, so
+// the contraction length K = I_q0 (padded) must stay below 2^31 / (7 * 4096) = 74898
+bool i8_k_ok(int ndims, const int64_t* dims) {
+  return rup(dims[1], kI8K) <= kI8MaxK && rup(dims[0], kI8K) <= kI8MaxK && ndims >= 3;
+}
 bool make_tmap_i8(CUtensorMap* tm, const int8_t* base, int64_t kp, int64_t rows, int box_rows) {
   auto enc = encode_fn();
   if (!enc) return false;
@@ -1168,6 +1173,7 @@ static bool pool_geo(const jkcals_config* c, PoolGeo* g) {
   if (c->prec != JKCALS_FP64 && c->prec != JKCALS_FP32 && c->prec != JKCALS_FP64_I8) return false;
   for (int m = 0; m < c->nmodels; ++m)
     if (c->ranks[m] < 1 || c->ranks[m] > kLgRMax) return false;
+  if (c->prec == JKCALS_FP64_I8 && !i8_k_ok(c->ndims, dims)) return false;
   // d = 0: plain CALS (§3.3): one model per id, nothing left out
   g->ngroups = d == 0 ? 1 : (dims[0] + d - 1) / d;
   if (c->sub_begin < 0 || c->sub_end <= c->sub_begin || c->sub_end > (int64_t)c->nmodels * g->ngroups) return false;
@@ -2286,7 +2292,8 @@ size_t jkcals_mttkrp_i8_scratch_bytes(int ndims, const int64_t* dims, int n, int
 jkcals_status jkcals_mttkrp_i8(int ndims, const int64_t* dims, int n, const double* T, const double* const* U,
                                int64_t C, int64_t ldu, double* M, int64_t ldm, void* scratch, size_t scratch_bytes,
                                void* stream) {
-  if (!valid_dims(ndims, dims, 1) || n < 0 || n >= ndims || !T || !U || !M || C < 1 || ldu < C || ldm < C)
+  if (!valid_dims(ndims, dims, 1) || n < 0 || n >= ndims || !T || !U || !M || C < 1 || ldu < C || ldm < C ||
+      !i8_k_ok(ndims, dims))
     return JKCALS_E_ARG;
   int dev = 0;
   cudaGetDevice(&dev);

@@ -1,5 +1,5 @@
 // mttkrp_i8.cuh — EXPERIMENTAL stand-alone FP64-accurate MTTKRP from INT8 tcgen05 MMAs
-// (not on the JK-CALS path yet).
+// (the JK-CALS path under precision JKCALS_FP64_I8, and jkcals_mttkrp_i8).
 //
 //   M(i, c) = sum_j' S(j', c) * sum_iq0 T(i, iq0, j') U_q0(iq0, c)          (the KRP factorisation)
 //
@@ -27,6 +27,7 @@ constexpr int kI8K = 32;         // K per step (32-byte SWIZZLE_32B rows)
 constexpr int kI8Stages = 4;
 constexpr int kI8Threads = 10 * 32;  // warp 0 TMA, warp 1 MMA, warps 2-9 drain (lane quadrant x column half)
 constexpr int kI8DWarps = 8;
+constexpr int64_t kI8MaxK = 65536;  // I_q0 bound for exact int32 diagonal sums (7 * 4096 * K < 2^31)
 constexpr size_t kI8ABytes = (size_t)kI8S * 128 * kI8K;    // 28 KB
 constexpr size_t kI8BBytes = (size_t)kI8S * kI8N * kI8K;   // 14 KB
 constexpr size_t kI8StageBytes = kI8ABytes + kI8BBytes;
@@ -52,10 +53,41 @@ __device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t saddr) {
 __device__ __forceinline__ uint32_t umma_idesc_i8(int N) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
 }
+// kCol: A-operand collector usage (0 none, 1 fill, 2 use, 3 lastuse) -- one A digit slice is read
+// from shared memory once and reused by the MMAs of its 7 - a diagonals (halves the smem reads)
+template <int kCol>
 __device__ __forceinline__ void umma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-               "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(a), "l"(b), "r"(idesc),
-               "r"(acc));
+  if constexpr (kCol == 1)
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                 "tcgen05.mma.cta_group::1.kind::i8.collector::a::fill [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(a),
+                 "l"(b), "r"(idesc), "r"(acc));
+  else if constexpr (kCol == 2)
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                 "tcgen05.mma.cta_group::1.kind::i8.collector::a::use [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(a),
+                 "l"(b), "r"(idesc), "r"(acc));
+  else if constexpr (kCol == 3)
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                 "tcgen05.mma.cta_group::1.kind::i8.collector::a::lastuse [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(a),
+                 "l"(b), "r"(idesc), "r"(acc));
+  else
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                 "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(a), "l"(b), "r"(idesc),
+                 "r"(acc));
+}
+// the 28 digit products of one K32 step, A slice a outer: D_{a+b} += A_a B_b
+template <int a, int bb>
+__device__ __forceinline__ void i8_products(uint32_t tmem, uint32_t a0, uint32_t b0, uint32_t idesc, bool first_k) {
+  if constexpr (a < kI8S) {
+    if constexpr (bb <= kI8S - 1 - a) {
+      constexpr int last = kI8S - 1 - a;
+      constexpr int col = last == 0 ? 0 : (bb == 0 ? 1 : (bb == last ? 3 : 2));
+      umma_i8<col>(tmem + (a + bb) * kI8N, umma_desc_sw32(a0 + a * 128 * kI8K), umma_desc_sw32(b0 + bb * kI8N * kI8K),
+                   idesc, (!first_k || a > 0) ? 1u : 0u);
+      i8_products<a, bb + 1>(tmem, a0, b0, idesc, first_k);
+    } else {
+      i8_products<a + 1, 0>(tmem, a0, b0, idesc, first_k);
+    }
+  }
 }
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
   asm volatile(
@@ -150,12 +182,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
         const uint32_t a0 = smem_u32(stages + slot * kI8StageBytes);
         const uint32_t b0 = a0 + (uint32_t)kI8ABytes;
         if (elect_one()) {
-#pragma unroll
-          for (int dg = 0; dg < kI8S; ++dg)
-#pragma unroll
-            for (int a = 0; a <= dg; ++a)
-              umma_i8(tmem + dg * kI8N, umma_desc_sw32(a0 + a * 128 * kI8K), umma_desc_sw32(b0 + (dg - a) * kI8N * kI8K),
-                      idesc, (ks > 0 || a > 0) ? 1u : 0u);
+          i8_products<0, 0>(tmem, a0, b0, idesc, ks == 0);
           umma_commit(&empty[slot]);
           if (ks == g.KS - 1) umma_commit(acc_full);
         }
@@ -219,11 +246,16 @@ __global__ void __launch_bounds__(kI8Threads, 1)
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          double v = 0.0;
-#pragma unroll
-          for (int dg = kI8S - 1; dg >= 0; --dg)  // small terms first, fixed order
-            v += (double)(int)r[dg][i] * ldexp(1.0, -14 - 7 * dg);
-          acc[cg + i] += s * v;
+          // exact integer recombination of the diagonals (|D_dg| < 2^31, K <= kI8MaxK):
+          //   hi = D0 2^21 + D1 2^14 + D2 2^7 + D3 (< 2^50),  lo = D4 2^14 + D5 2^7 + D6 (< 2^46),
+          // each converted exactly by the 1.5 * 2^52 bias trick (no I2F), one rounding in the fma
+          const int64_t hi = (int64_t)(int)r[0][i] * (1 << 21) + (int64_t)(int)r[1][i] * (1 << 14) +
+                             (int64_t)(int)r[2][i] * (1 << 7) + (int64_t)(int)r[3][i];
+          const int64_t lo = (int64_t)(int)r[4][i] * (1 << 14) + (int64_t)(int)r[5][i] * (1 << 7) + (int64_t)(int)r[6][i];
+          const double hd = __longlong_as_double(hi + 0x4338000000000000LL) - 6755399441055744.0;
+          const double ld = __longlong_as_double(lo + 0x4338000000000000LL) - 6755399441055744.0;
+          const double v = fma(ld, 0x1p-56, hd * 0x1p-35);  // D_dg carries 2^(-14 - 7 dg)
+          acc[cg + i] = fma(s, v, acc[cg + i]);
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
