@@ -865,6 +865,7 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
       ig.Us[sl] = nullptr;
     }
     ig.ldu = h->ldu;
+    ig.probe = 0;
     ig.eT = h->ptr<int>(h->off.i8eT[n]);
     ig.eU = eU;
     mttkrp_i8_kernel<kI8Stages><<<p.G, kI8Threads, kI8Smem, h->es>>>(h->tmA8[n], h->tmB8[n], ig, ti, parts);
@@ -2366,6 +2367,10 @@ jkcals_status jkcals_mttkrp_i8(int ndims, const int64_t* dims, int n, const doub
   g.ldu = q.CP;
   g.eT = x.eT;
   g.eU = x.eU;
+  {  // dev timing probe only (results are wrong when set): 1 = drain skipped, 2 = one product per K32 step
+    static const int probe = getenv("JKCALS_I8_PROBE") ? atoi(getenv("JKCALS_I8_PROBE")) : 0;
+    g.probe = probe;
+  }
   mttkrp_i8_kernel<kI8Stages><<<q.p.G, kI8Threads, kI8Smem, s>>>(tmA, tmB, g, x.ti, x.parts);
   if (cudaGetLastError() != cudaSuccess) return JKCALS_E_CUDA;
   const int64_t tot = q.In * C;

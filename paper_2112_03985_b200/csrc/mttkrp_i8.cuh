@@ -44,6 +44,7 @@ struct I8Geom {
   int64_t ldu;
   const int* eT;     // [InP] row exponents of T
   const int* eU;     // [CP] column exponents of U_q0
+  int probe;         // 0 (dev timing probes: see jkcals_mttkrp_i8)
 };
 
 __device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t saddr) {
@@ -182,7 +183,10 @@ __global__ void __launch_bounds__(kI8Threads, 1)
         const uint32_t a0 = smem_u32(stages + slot * kI8StageBytes);
         const uint32_t b0 = a0 + (uint32_t)kI8ABytes;
         if (elect_one()) {
-          i8_products<0, 0>(tmem, a0, b0, idesc, ks == 0);
+          if (g.probe == 2)
+            umma_i8<0>(tmem, umma_desc_sw32(a0), umma_desc_sw32(b0), idesc, ks > 0 ? 1u : 0u);
+          else
+            i8_products<0, 0>(tmem, a0, b0, idesc, ks == 0);
           umma_commit(&empty[slot]);
           if (ks == g.KS - 1) umma_commit(acc_full);
         }
@@ -230,6 +234,12 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       }
       mbar_wait_safe(acc_full, un & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      if (g.probe == 1) {
+        acc[0] += s;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty);
+        continue;
+      }
       const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * (kI8N / 2));
 #pragma unroll
       for (int cg = 0; cg < kI8N / 2; cg += 16) {
