@@ -85,7 +85,11 @@ KernelInfo* kernel_info(int device, std::string* err) {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(mttkrp_tf32_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTfSmemMax);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(mttkrp_i8_kernel<kI8Stages>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8Smem);
+      e = cudaFuncSetAttribute(mttkrp_i8_kernel<kI8Stages, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kI8Smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(mttkrp_i8_kernel<kI8ResStages, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kI8SmemRes);
     if (e != cudaSuccess) {
       if (err) *err = std::string("cudaFuncSetAttribute(tf32): ") + cudaGetErrorString(e);
       cudaSetDevice(prev);
@@ -447,6 +451,12 @@ I8Plan make_i8_plan(int ndims, const int64_t* dims, int n, int64_t C, const Kern
 }
 // exact int32 accumulation: a diagonal sums <= 7 digit products of magnitude <= 64 * 64 per k, so
 // the contraction length K = I_q0 (padded) must stay below 2^31 / (7 * 4096) = 74898
+// tuning knob: JKCALS_I8_RESIDENT=1 selects the resident-A variant of the INT8 kernel where it fits
+// (measured slower on syn200: its 2-stage B ring is latency-bound), default streaming
+bool i8_streaming() {
+  static const int v = getenv("JKCALS_I8_RESIDENT") ? atoi(getenv("JKCALS_I8_RESIDENT")) : 0;
+  return v == 0;
+}
 bool i8_k_ok(int ndims, const int64_t* dims) {
   return rup(dims[1], kI8K) <= kI8MaxK && rup(dims[0], kI8K) <= kI8MaxK && ndims >= 3;
 }
@@ -865,10 +875,16 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
       ig.Us[sl] = nullptr;
     }
     ig.ldu = h->ldu;
-    ig.probe = 0;
+    {  // dev timing probe only (see jkcals_mttkrp_i8); 0 in every real run
+      static const int probe = getenv("JKCALS_I8_PROBE") ? atoi(getenv("JKCALS_I8_PROBE")) : 0;
+      ig.probe = probe;
+    }
     ig.eT = h->ptr<int>(h->off.i8eT[n]);
     ig.eU = eU;
-    mttkrp_i8_kernel<kI8Stages><<<p.G, kI8Threads, kI8Smem, h->es>>>(h->tmA8[n], h->tmB8[n], ig, ti, parts);
+    if (ig.KS <= kI8ResKS && !i8_streaming())
+      mttkrp_i8_kernel<kI8ResStages, true><<<p.G, kI8Threads, kI8SmemRes, h->es>>>(h->tmA8[n], h->tmB8[n], ig, ti, parts);
+    else
+      mttkrp_i8_kernel<kI8Stages, false><<<p.G, kI8Threads, kI8Smem, h->es>>>(h->tmA8[n], h->tmB8[n], ig, ti, parts);
   } else if (h->tf32) {
     TfGeom tg;
     tg.C = h->C;
@@ -2303,8 +2319,10 @@ jkcals_status jkcals_mttkrp_i8(int ndims, const int64_t* dims, int n, const doub
   if (scratch_bytes < jkcals_mttkrp_i8_scratch_bytes(ndims, dims, n, C, dev)) return JKCALS_E_OOM;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(mttkrp_i8_kernel<kI8Stages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kI8Smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(mttkrp_i8_kernel<kI8Stages, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kI8Smem) != cudaSuccess ||
+        cudaFuncSetAttribute(mttkrp_i8_kernel<kI8ResStages, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kI8SmemRes) != cudaSuccess)
       return JKCALS_E_CUDA;
     attr = true;
   }
@@ -2371,7 +2389,10 @@ jkcals_status jkcals_mttkrp_i8(int ndims, const int64_t* dims, int n, const doub
     static const int probe = getenv("JKCALS_I8_PROBE") ? atoi(getenv("JKCALS_I8_PROBE")) : 0;
     g.probe = probe;
   }
-  mttkrp_i8_kernel<kI8Stages><<<q.p.G, kI8Threads, kI8Smem, s>>>(tmA, tmB, g, x.ti, x.parts);
+  if (g.KS <= kI8ResKS && !i8_streaming())
+    mttkrp_i8_kernel<kI8ResStages, true><<<q.p.G, kI8Threads, kI8SmemRes, s>>>(tmA, tmB, g, x.ti, x.parts);
+  else
+    mttkrp_i8_kernel<kI8Stages, false><<<q.p.G, kI8Threads, kI8Smem, s>>>(tmA, tmB, g, x.ti, x.parts);
   if (cudaGetLastError() != cudaSuccess) return JKCALS_E_CUDA;
   const int64_t tot = q.In * C;
   reduce_parts_kernel<<<(int)cdiv(tot, 256), 256, 0, s>>>(x.parts, x.ti, (int)q.In, (int)C, kI8N, q.nMt, M, ldm);

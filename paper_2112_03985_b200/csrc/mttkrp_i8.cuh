@@ -32,6 +32,15 @@ constexpr size_t kI8ABytes = (size_t)kI8S * 128 * kI8K;    // 28 KB
 constexpr size_t kI8BBytes = (size_t)kI8S * kI8N * kI8K;   // 14 KB
 constexpr size_t kI8StageBytes = kI8ABytes + kI8BBytes;
 constexpr size_t kI8Smem = 1024 + kI8Stages * kI8StageBytes + 256;
+// resident-A variant: when K = I_q0 fits 7 K32 steps (KP <= 224), the CTA keeps the whole U_q0
+// digit tile (7 x 28 KB) in shared memory across its j' units -- it is the same for every unit of
+// an m-tile -- and streams only the T digits (B) through a 2-stage ring. This cuts the L2 -> SMEM
+// traffic per unit from 294 KB to 98 KB (syn200) -- but with only 28 KB of B in flight per SM the
+// ring is latency-bound and the variant measured ~6 % slower than streaming (opt-in).
+constexpr int kI8ResKS = 7;
+constexpr int kI8ResStages = 2;
+constexpr size_t kI8SmemRes = 1024 + kI8ResKS * kI8ABytes + kI8ResStages * kI8BBytes + 256;
+static_assert(kI8SmemRes <= 232448, "resident-A INT8 MTTKRP exceeds shared memory");
 
 struct I8Geom {
   int nMt, nNt;      // output tiles: C / 128, I_n / 64 (padded)
@@ -116,18 +125,22 @@ __device__ __forceinline__ int i8_exponent(double m) {  // e with m * 2^-e <= 1/
   return e + 1;
 }
 
-template <int kStages>
+template <int kStages, bool kResA>
 __global__ void __launch_bounds__(kI8Threads, 1)
     mttkrp_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, I8Geom g,
                      const TileInfo* __restrict__ tinfo, double* __restrict__ parts) {
   extern __shared__ __align__(1024) unsigned char ism[];
-  unsigned char* stages = ism;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kStages * kI8StageBytes);
+  constexpr size_t kStageB = kResA ? kI8BBytes : kI8StageBytes;  // bytes per ring stage
+  unsigned char* ares = ism;                                       // resident A (kResA)
+  unsigned char* stages = ism + (kResA ? kI8ResKS * kI8ABytes : 0);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kStages * kStageB);
   uint64_t* full = bars;
   uint64_t* empty = full + kStages;
   uint64_t* acc_full = empty + kStages;
   uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  uint64_t* a_full = acc_empty + 1;   // resident A loaded
+  uint64_t* a_empty = a_full + 1;     // resident A no longer read by the MMAs
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_empty + 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int b = blockIdx.x;
   const int* cta_u = reinterpret_cast<const int*>(tinfo + g.nMt * g.nNt);
@@ -139,6 +152,8 @@ __global__ void __launch_bounds__(kI8Threads, 1)
     }
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, kI8DWarps);
+    mbar_init(a_full, 1);
+    mbar_init(a_empty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 0) {
@@ -153,18 +168,29 @@ __global__ void __launch_bounds__(kI8Threads, 1)
 
   if (warp == 0) {
     // ---------------- TMA producer: per unit, KS steps of (A box, B box), each all 7 slices
-    unsigned it = 0;
+    unsigned it = 0, na = 0;
+    int cur_tm = -1;
     for (int64_t u = u0; u < u1; ++u) {
       const int t = (int)(u / KT), jp = (int)(u % KT);
       const int tm = t % g.nMt, tn = t / g.nMt;
+      if (kResA && tm != cur_tm) {  // (re)load the m-tile's U_q0 digits once
+        if (na >= 1) mbar_wait_safe(a_empty, (na - 1) & 1u);
+        if (elect_one()) {
+          mbar_expect_tx(a_full, (unsigned)(g.KS * kI8ABytes));
+          for (int ks = 0; ks < g.KS; ++ks) tma_load_3d(ares + ks * kI8ABytes, &tmA, ks * kI8K, tm * 128, 0, a_full);
+        }
+        __syncwarp();
+        ++na;
+        cur_tm = tm;
+      }
       for (int ks = 0; ks < g.KS; ++ks, ++it) {
         const int slot = (int)(it % kStages);
         if (it >= (unsigned)kStages) mbar_wait_safe(&empty[slot], ((it / kStages) - 1) & 1u);
         if (elect_one()) {
-          unsigned char* st = stages + slot * kI8StageBytes;
-          mbar_expect_tx(&full[slot], (unsigned)kI8StageBytes);
-          tma_load_3d(st, &tmA, ks * kI8K, tm * 128, 0, &full[slot]);
-          tma_load_3d(st + kI8ABytes, &tmB, ks * kI8K, jp * g.InP + tn * kI8N, 0, &full[slot]);
+          unsigned char* st = stages + slot * kStageB;
+          mbar_expect_tx(&full[slot], (unsigned)kStageB);
+          if (!kResA) tma_load_3d(st, &tmA, ks * kI8K, tm * 128, 0, &full[slot]);
+          tma_load_3d(st + (kResA ? 0 : kI8ABytes), &tmB, ks * kI8K, jp * g.InP + tn * kI8N, 0, &full[slot]);
         }
         __syncwarp();
       }
@@ -172,23 +198,35 @@ __global__ void __launch_bounds__(kI8Threads, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer: 28 digit products per K32 step into the 7 diagonal accumulators
     const uint32_t idesc = umma_idesc_i8(kI8N);
-    unsigned it = 0, un = 0;
+    unsigned it = 0, un = 0, na = 0;
+    int cur_tm = -1;
     for (int64_t u = u0; u < u1; ++u, ++un) {
+      const int tm = (int)((u / KT) % g.nMt);
       if (un >= 1) mbar_wait_safe(acc_empty, (un - 1) & 1u);  // the drain has read the previous unit
+      if (kResA && tm != cur_tm) {
+        mbar_wait_safe(a_full, na & 1u);
+        ++na;
+        cur_tm = tm;
+      }
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const bool a_last = kResA && (u + 1 == u1 || (int)(((u + 1) / KT) % g.nMt) != tm);
       for (int ks = 0; ks < g.KS; ++ks, ++it) {
         const int slot = (int)(it % kStages);
         mbar_wait_safe(&full[slot], (it / kStages) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const uint32_t a0 = smem_u32(stages + slot * kI8StageBytes);
-        const uint32_t b0 = a0 + (uint32_t)kI8ABytes;
+        const uint32_t st = smem_u32(stages + slot * kStageB);
+        const uint32_t a0 = kResA ? smem_u32(ares + ks * kI8ABytes) : st;
+        const uint32_t b0 = kResA ? st : st + (uint32_t)kI8ABytes;
         if (elect_one()) {
           if (g.probe == 2)
             umma_i8<0>(tmem, umma_desc_sw32(a0), umma_desc_sw32(b0), idesc, ks > 0 ? 1u : 0u);
           else
             i8_products<0, 0>(tmem, a0, b0, idesc, ks == 0);
           umma_commit(&empty[slot]);
-          if (ks == g.KS - 1) umma_commit(acc_full);
+          if (ks == g.KS - 1) {
+            umma_commit(acc_full);
+            if (a_last) umma_commit(a_empty);  // the next unit needs another m-tile's A
+          }
         }
         __syncwarp();
       }

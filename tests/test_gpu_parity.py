@@ -344,3 +344,36 @@ def test_experimental_int8_sliced_fp64_path(name, ps):
     ps = list(ps)
     res = O.jk_als(w.T, w.P, p_list=ps, max_iters=w.sweeps, nthreads=NCPU)
     check_against_oracle(h, res, ps, nt2p_of(w.T))
+
+
+_RESIDENT_CHECK = r"""
+import sys
+import numpy as np, torch
+sys.path.insert(0, '.')
+from oracle import oracle as O
+from paper_2112_03985_b200.jkcals import mttkrp_i8
+worst = 0.0
+for dims, C in [((37, 23, 11), 129), ((60, 50, 200), 250), ((13, 7, 5, 3), 70)]:
+    g = np.random.default_rng(sum(dims) + C)
+    T = np.asfortranarray(g.standard_normal(dims))
+    U = [g.standard_normal((I, C)) for I in dims]
+    ldu = ((C + 127) // 128) * 128
+    Ud = [torch.from_numpy(np.pad(u, ((0, 0), (0, ldu - C)))).cuda() for u in U]
+    Td = torch.from_numpy(np.ravel(T, order="F").copy()).cuda()
+    for n in range(len(dims)):
+        ref = O.mttkrp(T, U, n)
+        M = mttkrp_i8(Td, dims, n, Ud, C).cpu().numpy()
+        worst = max(worst, float(np.linalg.norm(M - ref) / np.linalg.norm(ref)))
+print(worst)
+"""
+
+
+def test_int8_resident_a_variant():
+    # the opt-in resident-A INT8 kernel (JKCALS_I8_RESIDENT=1, read once per process, so it runs in
+    # a subprocess) meets the same bar as the default streaming variant
+    import subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", _RESIDENT_CHECK], cwd=root, capture_output=True, text=True,
+                         env=dict(os.environ, JKCALS_I8_RESIDENT="1"), timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert float(out.stdout.strip().splitlines()[-1]) <= 1e-13, out.stdout
