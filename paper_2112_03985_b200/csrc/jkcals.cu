@@ -59,6 +59,7 @@ struct KernelInfo {
   SmemFn smem[2][2][kMaxNT];
   int occ[2][2][kMaxNT][kMaxModes];  // [..][nslow]
   int nsm;
+  int i8clusters;                    // co-resident 2-CTA clusters of the INT8 cluster kernel (0: none)
 };
 
 KernelInfo* kernel_info(int device, std::string* err) {
@@ -90,6 +91,27 @@ KernelInfo* kernel_info(int device, std::string* err) {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(mttkrp_i8_kernel<kI8ResStages, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)kI8SmemRes);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(mttkrp_i8_kernel<kI8Stages, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kI8SmemClu);
+    ki.i8clusters = 0;
+    if (e == cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(2 * (ki.nsm / 2));
+      cfg.blockDim = dim3(kI8Threads);
+      cfg.dynamicSmemBytes = kI8SmemClu;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, mttkrp_i8_kernel<kI8Stages, false, true>, &cfg) == cudaSuccess)
+        ki.i8clusters = ncl;
+      cudaGetLastError();  // the query is advisory: 0 falls back to the one-CTA kernel
+    }
     if (e != cudaSuccess) {
       if (err) *err = std::string("cudaFuncSetAttribute(tf32): ") + cudaGetErrorString(e);
       cudaSetDevice(prev);
@@ -425,47 +447,80 @@ int bnp_of(int NT) {
 struct I8Plan {
   int64_t In, Iq0, Jp, InP, KP, CP;
   int nMt, nNt;
+  int variant;  // 0 streaming, 1 resident A (opt-in), 2 2-CTA cluster with multicast A (default)
   ModePlan p;
 };
+int i8_variant(const KernelInfo& ki, int64_t KP);
 I8Plan make_i8_plan(int ndims, const int64_t* dims, int n, int64_t C, const KernelInfo& ki) {
   I8Plan q;
   const ModeGeo mg = mode_geo(ndims, dims, n);
   q.In = mg.In;
   q.Iq0 = mg.Iq0;
   q.Jp = mg.Jp;
-  q.InP = rup(q.In, kI8N);
   q.KP = rup(q.Iq0, kI8K);
+  q.variant = i8_variant(ki, q.KP);
+  const int bn = q.variant == 2 ? 2 * kI8N : kI8N;  // plan tile rows (a pair of n-tiles per cluster)
+  q.InP = rup(q.In, bn);
   q.CP = rup(C, 128);
   q.nMt = (int)(q.CP / 128);
-  q.nNt = (int)(q.InP / kI8N);
+  q.nNt = (int)(q.InP / bn);
   ModePlan& p = q.p;
   p.nMt = q.nMt;
   p.nNt = q.nNt;
-  p.BN = kI8N;
+  p.BN = bn;
   p.KT = (int)q.Jp;
   p.ntiles = p.nMt * p.nNt;
   p.units = (int64_t)p.ntiles * p.KT;
-  p.G = (int)std::min<int64_t>(p.units, (int64_t)ki.nsm);
+  p.G = (int)std::min<int64_t>(p.units, q.variant == 2 ? (int64_t)ki.i8clusters : (int64_t)ki.nsm);
   finish_plan(p, mg);
   return q;
 }
+// launch the variant the plan chose (the cluster kernel's grid is 2 CTAs per plan "CTA")
+cudaError_t launch_i8(const I8Plan& q, const CUtensorMap& tmA, const CUtensorMap& tmB, const I8Geom& g,
+                      const TileInfo* ti, double* parts, cudaStream_t s) {
+  if (q.variant == 1) {
+    mttkrp_i8_kernel<kI8ResStages, true><<<q.p.G, kI8Threads, kI8SmemRes, s>>>(tmA, tmB, g, ti, parts);
+    return cudaGetLastError();
+  }
+  if (q.variant == 0) {
+    mttkrp_i8_kernel<kI8Stages, false><<<q.p.G, kI8Threads, kI8Smem, s>>>(tmA, tmB, g, ti, parts);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(2 * q.p.G);
+  cfg.blockDim = dim3(kI8Threads);
+  cfg.dynamicSmemBytes = kI8SmemClu;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, mttkrp_i8_kernel<kI8Stages, false, true>, tmA, tmB, g, ti, parts);
+}
 // exact int32 accumulation: a diagonal sums <= 7 digit products of magnitude <= 64 * 64 per k, so
 // the contraction length K = I_q0 (padded) must stay below 2^31 / (7 * 4096) = 74898
-// tuning knob: JKCALS_I8_RESIDENT=1 selects the resident-A variant of the INT8 kernel where it fits
-// (measured slower on syn200: its 2-stage B ring is latency-bound), default streaming
-bool i8_streaming() {
-  static const int v = getenv("JKCALS_I8_RESIDENT") ? atoi(getenv("JKCALS_I8_RESIDENT")) : 0;
-  return v == 0;
+// INT8 kernel variant: the 2-CTA cluster kernel with multicast A by default;
+// tuning knobs JKCALS_I8_RESIDENT=1 (resident A where I_q0 <= 224; latency-bound, slower) and
+// JKCALS_I8_CLUSTER=0 (the one-CTA streaming kernel)
+int i8_variant(const KernelInfo& ki, int64_t KP) {
+  static const int res = getenv("JKCALS_I8_RESIDENT") ? atoi(getenv("JKCALS_I8_RESIDENT")) : 0;
+  static const int clu = getenv("JKCALS_I8_CLUSTER") ? atoi(getenv("JKCALS_I8_CLUSTER")) : 1;
+  if (res && KP / kI8K <= kI8ResKS) return 1;
+  if (clu && ki.i8clusters >= 1) return 2;
+  return 0;
 }
 bool i8_k_ok(int ndims, const int64_t* dims) {
   return rup(dims[1], kI8K) <= kI8MaxK && rup(dims[0], kI8K) <= kI8MaxK && ndims >= 3;
 }
-bool make_tmap_i8(CUtensorMap* tm, const int8_t* base, int64_t kp, int64_t rows, int box_rows) {
+bool make_tmap_i8(CUtensorMap* tm, const int8_t* base, int64_t kp, int64_t rows, int box_rows, int box_slices = kI8S) {
   auto enc = encode_fn();
   if (!enc) return false;
   cuuint64_t gdim[3] = {(cuuint64_t)kp, (cuuint64_t)rows, (cuuint64_t)kI8S};
   cuuint64_t gstr[2] = {(cuuint64_t)kp, (cuuint64_t)(kp * rows)};
-  cuuint32_t box[3] = {(cuuint32_t)kI8K, (cuuint32_t)box_rows, (cuuint32_t)kI8S}, est[3] = {1, 1, 1};
+  cuuint32_t box[3] = {(cuuint32_t)kI8K, (cuuint32_t)box_rows, (cuuint32_t)box_slices}, est[3] = {1, 1, 1};
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), gdim, gstr, box, est,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -524,7 +579,7 @@ bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_c
     int tc;
     if (i8) {
       const I8Plan q = make_i8_plan(N, dims, n, C, ki);
-      pc = (std::max<int64_t>(q.p.G, ki.nsm) + q.p.ntiles) * kI8N * kBM;
+      pc = (std::max<int64_t>(q.p.G, ki.nsm) + q.p.ntiles) * q.p.BN * kBM;
       tc = q.p.ntiles;
     } else {
       plan_bounds(mode_geo(N, dims, n), n, C, ki, &pc, &tc, tf32);
@@ -747,7 +802,7 @@ jkcals_status replan(jkcals_t h) {
                            cudaMemcpyHostToDevice, h->stream));
     if (h->i8) {  // 3-D boxes over the U_q0 digits (rebuilt each mode) and this mode's T digits
       const I8Plan& q = h->i8q[n];
-      if (!make_tmap_i8(&h->tmA8[n], h->ptr<int8_t>(h->off.i8A), q.KP, q.CP, 128) ||
+      if (!make_tmap_i8(&h->tmA8[n], h->ptr<int8_t>(h->off.i8A), q.KP, q.CP, 128, q.variant == 2 ? 4 : kI8S) ||
           !make_tmap_i8(&h->tmB8[n], h->ptr<int8_t>(h->off.i8B[n]), q.KP, q.Jp * q.InP, kI8N))
         return fail(h, JKCALS_E_CUDA, "cuTensorMapEncodeTiled failed for the int8 digits of mode %d", n);
       continue;
@@ -850,7 +905,7 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     const int q0 = (n == 0) ? 1 : 0;
     int* eU = h->ptr<int>(h->off.i8eU);
     int8_t* A = h->ptr<int8_t>(h->off.i8A);
-    col_exp_u_kernel<<<(int)cdiv(q.CP, 128), 128, 0, h->es>>>(Uall[q0], h->ldu, (int)q.Iq0, h->C, (int)q.CP, eU);
+    col_exp_u_kernel<<<(int)cdiv(q.CP, 32), 256, 0, h->es>>>(Uall[q0], h->ldu, (int)q.Iq0, h->C, (int)q.CP, eU);
     CKH(h, cudaGetLastError());
     slice_u_i8_kernel<<<(int)cdiv(q.CP * q.KP, 256), 256, 0, h->es>>>(Uall[q0], h->ldu, (int)q.Iq0, h->C, (int)q.CP,
                                                                      (int)q.KP, eU, A);
@@ -881,10 +936,7 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     }
     ig.eT = h->ptr<int>(h->off.i8eT[n]);
     ig.eU = eU;
-    if (ig.KS <= kI8ResKS && !i8_streaming())
-      mttkrp_i8_kernel<kI8ResStages, true><<<p.G, kI8Threads, kI8SmemRes, h->es>>>(h->tmA8[n], h->tmB8[n], ig, ti, parts);
-    else
-      mttkrp_i8_kernel<kI8Stages, false><<<p.G, kI8Threads, kI8Smem, h->es>>>(h->tmA8[n], h->tmB8[n], ig, ti, parts);
+    CKH(h, launch_i8(q, h->tmA8[n], h->tmB8[n], ig, ti, parts, h->es));
   } else if (h->tf32) {
     TfGeom tg;
     tg.C = h->C;
@@ -2285,7 +2337,7 @@ I8Scratch i8_layout(uintptr_t base0, int ndims, const int64_t* dims, const I8Pla
     return o;
   };
   x.ti = reinterpret_cast<TileInfo*>(take(plan_table_bytes(q.p.ntiles, q.p.G)));
-  x.parts = reinterpret_cast<double*>(take((size_t)(q.p.G + q.p.ntiles) * kI8N * 128 * 8));
+  x.parts = reinterpret_cast<double*>(take((size_t)(q.p.G + q.p.ntiles) * q.p.BN * 128 * 8));
   x.A = reinterpret_cast<int8_t*>(take((size_t)kI8S * q.CP * q.KP));
   x.B = reinterpret_cast<int8_t*>(take((size_t)kI8S * q.Jp * q.InP * q.KP));
   x.eT = reinterpret_cast<int*>(take((size_t)q.InP * 4));
@@ -2353,7 +2405,7 @@ jkcals_status jkcals_mttkrp_i8(int ndims, const int64_t* dims, int n, const doub
   slice_t_i8_kernel<<<(int)cdiv(q.Jp * q.InP * q.KP, 256), 256, 0, s>>>(T, ndims, x.st_d, x.dims_d, n, q0, (int)q.In,
                                                                         (int)q.InP, (int)q.Iq0, (int)q.KP, q.Jp,
                                                                         x.eT, x.B);
-  col_exp_u_kernel<<<(int)cdiv(q.CP, 128), 128, 0, s>>>(x.Up[q0], q.CP, (int)q.Iq0, (int)C, (int)q.CP, x.eU);
+  col_exp_u_kernel<<<(int)cdiv(q.CP, 32), 256, 0, s>>>(x.Up[q0], q.CP, (int)q.Iq0, (int)C, (int)q.CP, x.eU);
   slice_u_i8_kernel<<<(int)cdiv(q.CP * q.KP, 256), 256, 0, s>>>(x.Up[q0], q.CP, (int)q.Iq0, (int)C, (int)q.CP,
                                                                 (int)q.KP, x.eU, x.A);
   if (cudaGetLastError() != cudaSuccess) return JKCALS_E_CUDA;
@@ -2361,7 +2413,8 @@ jkcals_status jkcals_mttkrp_i8(int ndims, const int64_t* dims, int n, const doub
   if (cudaMemcpyAsync(x.ti, table.data(), table.size(), cudaMemcpyHostToDevice, s) != cudaSuccess)
     return JKCALS_E_CUDA;
   CUtensorMap tmA, tmB;
-  if (!make_tmap_i8(&tmA, x.A, q.KP, q.CP, 128) || !make_tmap_i8(&tmB, x.B, q.KP, q.Jp * q.InP, kI8N))
+  if (!make_tmap_i8(&tmA, x.A, q.KP, q.CP, 128, q.variant == 2 ? 4 : kI8S) ||
+      !make_tmap_i8(&tmB, x.B, q.KP, q.Jp * q.InP, kI8N))
     return JKCALS_E_CUDA;
   I8Geom g;
   g.nMt = q.nMt;
@@ -2389,13 +2442,9 @@ jkcals_status jkcals_mttkrp_i8(int ndims, const int64_t* dims, int n, const doub
     static const int probe = getenv("JKCALS_I8_PROBE") ? atoi(getenv("JKCALS_I8_PROBE")) : 0;
     g.probe = probe;
   }
-  if (g.KS <= kI8ResKS && !i8_streaming())
-    mttkrp_i8_kernel<kI8ResStages, true><<<q.p.G, kI8Threads, kI8SmemRes, s>>>(tmA, tmB, g, x.ti, x.parts);
-  else
-    mttkrp_i8_kernel<kI8Stages, false><<<q.p.G, kI8Threads, kI8Smem, s>>>(tmA, tmB, g, x.ti, x.parts);
-  if (cudaGetLastError() != cudaSuccess) return JKCALS_E_CUDA;
+  if (launch_i8(q, tmA, tmB, g, x.ti, x.parts, s) != cudaSuccess) return JKCALS_E_CUDA;
   const int64_t tot = q.In * C;
-  reduce_parts_kernel<<<(int)cdiv(tot, 256), 256, 0, s>>>(x.parts, x.ti, (int)q.In, (int)C, kI8N, q.nMt, M, ldm);
+  reduce_parts_kernel<<<(int)cdiv(tot, 256), 256, 0, s>>>(x.parts, x.ti, (int)q.In, (int)C, q.p.BN, q.nMt, M, ldm);
   if (cudaGetLastError() != cudaSuccess) return JKCALS_E_CUDA;
   if (cudaStreamSynchronize(s) != cudaSuccess) return JKCALS_E_CUDA;
   return JKCALS_OK;

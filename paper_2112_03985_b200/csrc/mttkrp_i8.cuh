@@ -41,6 +41,37 @@ constexpr int kI8ResKS = 7;
 constexpr int kI8ResStages = 2;
 constexpr size_t kI8SmemRes = 1024 + kI8ResKS * kI8ABytes + kI8ResStages * kI8BBytes + 256;
 static_assert(kI8SmemRes <= 232448, "resident-A INT8 MTTKRP exceeds shared memory");
+// cluster variant: a pair of CTAs (one thread-block cluster) works on the same (m-tile, j') units
+// for two adjacent 64-row n-tiles (a 128-row "pair tile"); each CTA TMA-loads 4 of the (padded to
+// 8) U_q0 digit slices and multicasts them into both CTAs' stages, so the A operand crosses L2
+// once per pair: 56 KB instead of 84 KB of L2 -> SMEM traffic per pair and K32 step
+constexpr size_t kI8ABytesClu = (size_t)8 * 128 * kI8K;  // 8 slice slots (slot 7: TMA zero fill)
+constexpr size_t kI8StageBytesClu = kI8ABytesClu + kI8BBytes;
+constexpr size_t kI8SmemClu = 1024 + kI8Stages * kI8StageBytesClu + 256;
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
 
 struct I8Geom {
   int nMt, nNt;      // output tiles: C / 128, I_n / 64 (padded)
@@ -125,12 +156,13 @@ __device__ __forceinline__ int i8_exponent(double m) {  // e with m * 2^-e <= 1/
   return e + 1;
 }
 
-template <int kStages, bool kResA>
+template <int kStages, bool kResA, bool kClu = false>
 __global__ void __launch_bounds__(kI8Threads, 1)
     mttkrp_i8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, I8Geom g,
                      const TileInfo* __restrict__ tinfo, double* __restrict__ parts) {
   extern __shared__ __align__(1024) unsigned char ism[];
-  constexpr size_t kStageB = kResA ? kI8BBytes : kI8StageBytes;  // bytes per ring stage
+  constexpr size_t kStageB = kResA ? kI8BBytes : (kClu ? kI8StageBytesClu : kI8StageBytes);  // per ring stage
+  constexpr size_t kAOff = kClu ? kI8ABytesClu : kI8ABytes;  // B offset inside a streaming stage
   unsigned char* ares = ism;                                       // resident A (kResA)
   unsigned char* stages = ism + (kResA ? kI8ResKS * kI8ABytes : 0);
   uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kStages * kStageB);
@@ -142,13 +174,15 @@ __global__ void __launch_bounds__(kI8Threads, 1)
   uint64_t* a_empty = a_full + 1;     // resident A no longer read by the MMAs
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_empty + 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int b = blockIdx.x;
+  // kClu: the plan's "CTA" is the cluster (pair tile rows = 2 x kI8N); crk = this CTA's half
+  const int crk = kClu ? (int)cluster_ctarank() : 0;
+  const int b = kClu ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   const int* cta_u = reinterpret_cast<const int*>(tinfo + g.nMt * g.nNt);
   const int64_t u0 = cta_u[b], u1 = cta_u[b + 1];
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], kClu ? 2 : 1);  // kClu: both CTAs' MMAs must be done with the stage
     }
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, kI8DWarps);
@@ -161,7 +195,10 @@ __global__ void __launch_bounds__(kI8Threads, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
+  if (kClu)
+    cluster_sync_all();  // the peer's barriers are initialised before any multicast reaches them
+  else
+    __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   const int KT = g.Jp;  // units per tile
@@ -189,8 +226,13 @@ __global__ void __launch_bounds__(kI8Threads, 1)
         if (elect_one()) {
           unsigned char* st = stages + slot * kStageB;
           mbar_expect_tx(&full[slot], (unsigned)kStageB);
-          if (!kResA) tma_load_3d(st, &tmA, ks * kI8K, tm * 128, 0, &full[slot]);
-          tma_load_3d(st + (kResA ? 0 : kI8ABytes), &tmB, ks * kI8K, jp * g.InP + tn * kI8N, 0, &full[slot]);
+          if (kClu) {  // my 4 slice slots of A to both CTAs, my own n-tile of B
+            tma_load_3d_mc(st + crk * 4 * 128 * kI8K, &tmA, ks * kI8K, tm * 128, crk * 4, &full[slot], (uint16_t)3);
+            tma_load_3d(st + kAOff, &tmB, ks * kI8K, jp * g.InP + (2 * tn + crk) * kI8N, 0, &full[slot]);
+          } else {
+            if (!kResA) tma_load_3d(st, &tmA, ks * kI8K, tm * 128, 0, &full[slot]);
+            tma_load_3d(st + (kResA ? 0 : kI8ABytes), &tmB, ks * kI8K, jp * g.InP + tn * kI8N, 0, &full[slot]);
+          }
         }
         __syncwarp();
       }
@@ -216,13 +258,16 @@ __global__ void __launch_bounds__(kI8Threads, 1)
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t st = smem_u32(stages + slot * kStageB);
         const uint32_t a0 = kResA ? smem_u32(ares + ks * kI8ABytes) : st;
-        const uint32_t b0 = kResA ? st : st + (uint32_t)kI8ABytes;
+        const uint32_t b0 = kResA ? st : st + (uint32_t)kAOff;
         if (elect_one()) {
           if (g.probe == 2)
             umma_i8<0>(tmem, umma_desc_sw32(a0), umma_desc_sw32(b0), idesc, ks > 0 ? 1u : 0u);
           else
             i8_products<0, 0>(tmem, a0, b0, idesc, ks == 0);
-          umma_commit(&empty[slot]);
+          if (kClu)
+            umma_commit_mc(&empty[slot], (uint16_t)3);  // frees the stage in both CTAs
+          else
+            umma_commit(&empty[slot]);
           if (ks == g.KS - 1) {
             umma_commit(acc_full);
             if (a_last) umma_commit(a_empty);  // the next unit needs another m-tile's A
@@ -245,12 +290,13 @@ __global__ void __launch_bounds__(kI8Threads, 1)
     auto flush = [&](int64_t t) {  // write this CTA's piece of tile t (its column half), with the scales
       const int tm = (int)(t % g.nMt), tn = (int)(t / g.nMt);
       const TileInfo ti = tinfo[t];
-      double* P = parts + ((int64_t)ti.piece_base + (b - ti.first_cta)) * (int64_t)(kI8N * 128) + cl;
+      constexpr int kBN = kClu ? 2 * kI8N : kI8N;  // rows of a plan tile
+      double* P = parts + ((int64_t)ti.piece_base + (b - ti.first_cta)) * (int64_t)(kBN * 128) + cl;
       const int eu = g.eU[tm * 128 + cl];
 #pragma unroll
       for (int i = 0; i < kI8N / 2; ++i) {
-        const int il = h * (kI8N / 2) + i;
-        P[(int64_t)il * 128] = ldexp(acc[i], eu + g.eT[tn * kI8N + il]);
+        const int il = crk * kI8N + h * (kI8N / 2) + i;
+        P[(int64_t)il * 128] = ldexp(acc[i], eu + g.eT[tn * kBN + il]);
         acc[i] = 0.0;
       }
     };
@@ -318,6 +364,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
   }
+  if (kClu) cluster_sync_all();  // no multicast or remote arrive may target an exited peer
 }
 
 // ---- operand preparation -----------------------------------------------------------------
@@ -371,14 +418,22 @@ __global__ void slice_t_i8_kernel(const double* __restrict__ T, int N, const int
 }
 
 // column exponents of U_q0 and Asl[s][c][k] = digit s of U_q0(k, c) * 2^-e_U(c)
-__global__ void col_exp_u_kernel(const double* __restrict__ U, int64_t ldu, int rows, int C, int CP,
-                                 int* __restrict__ eU) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= CP) return;
+// 32 columns x 8 row groups per 256-thread block: coalesced along c, max-reduced across the groups
+__global__ void __launch_bounds__(256) col_exp_u_kernel(const double* __restrict__ U, int64_t ldu, int rows, int C,
+                                                        int CP, int* __restrict__ eU) {
+  __shared__ double red[8][32];
+  const int cx = threadIdx.x & 31, ry = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + cx;
   double m = 0.0;
   if (c < C)
-    for (int k = 0; k < rows; ++k) m = fmax(m, fabs(U[(int64_t)k * ldu + c]));
-  eU[c] = i8_exponent(m);
+    for (int k = ry; k < rows; k += 8) m = fmax(m, fabs(U[(int64_t)k * ldu + c]));
+  red[ry][cx] = m;
+  __syncthreads();
+  if (ry == 0 && c < CP) {
+#pragma unroll
+    for (int r = 1; r < 8; ++r) m = fmax(m, red[r][cx]);
+    eU[c] = i8_exponent(m);
+  }
 }
 __global__ void slice_u_i8_kernel(const double* __restrict__ U, int64_t ldu, int rows, int C, int CP, int KP,
                                   const int* __restrict__ eU, int8_t* __restrict__ A) {

@@ -368,12 +368,14 @@ print(worst)
 """
 
 
-def test_int8_resident_a_variant():
-    # the opt-in resident-A INT8 kernel (JKCALS_I8_RESIDENT=1, read once per process, so it runs in
-    # a subprocess) meets the same bar as the default streaming variant
+@pytest.mark.parametrize("env", [{"JKCALS_I8_RESIDENT": "1"}, {"JKCALS_I8_CLUSTER": "0"}])
+def test_int8_kernel_variants(env):
+    # the opt-in INT8 kernel variants -- resident A (JKCALS_I8_RESIDENT=1) and the one-CTA streaming
+    # kernel (JKCALS_I8_CLUSTER=0); the knobs are read once per process, so each runs in a
+    # subprocess -- meet the same bar as the default 2-CTA cluster kernel
     import subprocess, sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", _RESIDENT_CHECK], cwd=root, capture_output=True, text=True,
-                         env=dict(os.environ, JKCALS_I8_RESIDENT="1"), timeout=600)
+                         env=dict(os.environ, **env), timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     assert float(out.stdout.strip().splitlines()[-1]) <= 1e-13, out.stdout
