@@ -522,7 +522,8 @@ bool make_tmap_i8(CUtensorMap* tm, const int8_t* base, int64_t kp, int64_t rows,
   cuuint64_t gstr[2] = {(cuuint64_t)kp, (cuuint64_t)(kp * rows)};
   cuuint32_t box[3] = {(cuuint32_t)kI8K, (cuuint32_t)box_rows, (cuuint32_t)box_slices}, est[3] = {1, 1, 1};
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), gdim, gstr, box, est,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, kI8K == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }

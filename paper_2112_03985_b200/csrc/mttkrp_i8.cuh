@@ -8,10 +8,10 @@
 // Products of digits a, b with a + b = dg accumulate exactly (int32) in TMEM accumulator D_dg; per
 // j' the drain warps fold sum_dg D_dg 2^(-14-7 dg) times S(j', c) into FP64 registers, and the
 // scales 2^(e_T(i) + e_U(c)) are applied when the CTA's partial piece is written. One stream-K
-// unit = (output tile, j'); K = I_q0 padded to 32 per unit (7 K32 steps for I_q0 = 200).
+// unit = (output tile, j'); K = I_q0 padded to 64 per unit (4 K64 ring steps for I_q0 = 200).
 // Operands are precomputed by slice_t_i8_kernel / slice_u_i8_kernel into GEMM-friendly layouts:
 //   Bsl[s][j'][i (InP)][k (KP)]  and  Asl[s][c (CP)][k (KP)]   (int8, k contiguous)
-// and loaded per K32 step by 3-D TMA boxes (32 B, rows, 7 slices) with SWIZZLE_32B.
+// and loaded per K64 ring step by 3-D TMA boxes (64 B, rows, 7 slices) with SWIZZLE_64B.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -23,8 +23,8 @@ namespace jk {
 
 constexpr int kI8S = 7;          // digits (slices) per operand
 constexpr int kI8N = 64;         // UMMA N = rows i of an output tile (7 accumulators x 64 <= 512)
-constexpr int kI8K = 32;         // K per step (32-byte SWIZZLE_32B rows)
-constexpr int kI8Stages = 4;
+constexpr int kI8K = 64;         // K per ring step (64-byte SWIZZLE_64B rows; 2 UMMA K32 sub-steps)
+constexpr int kI8Stages = 2;
 constexpr int kI8Threads = 10 * 32;  // warp 0 TMA, warp 1 MMA, warps 2-9 drain (lane quadrant x column half)
 constexpr int kI8DWarps = 8;
 constexpr int64_t kI8MaxK = 65536;  // I_q0 bound for exact int32 diagonal sums (7 * 4096 * K < 2^31)
@@ -37,7 +37,7 @@ constexpr size_t kI8Smem = 1024 + kI8Stages * kI8StageBytes + 256;
 // an m-tile -- and streams only the T digits (B) through a 2-stage ring. This cuts the L2 -> SMEM
 // traffic per unit from 294 KB to 98 KB (syn200) -- but with only 28 KB of B in flight per SM the
 // ring is latency-bound and the variant measured ~6 % slower than streaming (opt-in).
-constexpr int kI8ResKS = 7;
+constexpr int kI8ResKS = 3;
 constexpr int kI8ResStages = 2;
 constexpr size_t kI8SmemRes = 1024 + kI8ResKS * kI8ABytes + kI8ResStages * kI8BBytes + 256;
 static_assert(kI8SmemRes <= 232448, "resident-A INT8 MTTKRP exceeds shared memory");
@@ -91,6 +91,12 @@ __device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1u << 16) | ((uint64_t)(256u >> 4) << 32) |
          ((uint64_t)1u << 46) | ((uint64_t)6u << 61);
 }
+__device__ __forceinline__ uint64_t umma_desc_i8(uint32_t saddr) {
+  if constexpr (kI8K == 64)
+    return umma_desc_sw64(saddr);
+  else
+    return umma_desc_sw32(saddr);
+}
 __device__ __forceinline__ uint32_t umma_idesc_i8(int N) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
 }
@@ -118,11 +124,12 @@ __device__ __forceinline__ void umma_i8(uint32_t d, uint64_t a, uint64_t b, uint
 // the 28 digit products of one K32 step, A slice a outer: D_{a+b} += A_a B_b
 template <int a, int bb>
 __device__ __forceinline__ void i8_products(uint32_t tmem, uint32_t a0, uint32_t b0, uint32_t idesc, bool first_k) {
+  // a0 / b0 already include the K32 sub-step's byte offset inside the swizzle atom
   if constexpr (a < kI8S) {
     if constexpr (bb <= kI8S - 1 - a) {
       constexpr int last = kI8S - 1 - a;
       constexpr int col = last == 0 ? 0 : (bb == 0 ? 1 : (bb == last ? 3 : 2));
-      umma_i8<col>(tmem + (a + bb) * kI8N, umma_desc_sw32(a0 + a * 128 * kI8K), umma_desc_sw32(b0 + bb * kI8N * kI8K),
+      umma_i8<col>(tmem + (a + bb) * kI8N, umma_desc_i8(a0 + a * 128 * kI8K), umma_desc_i8(b0 + bb * kI8N * kI8K),
                    idesc, (!first_k || a > 0) ? 1u : 0u);
       i8_products<a, bb + 1>(tmem, a0, b0, idesc, first_k);
     } else {
@@ -260,10 +267,13 @@ __global__ void __launch_bounds__(kI8Threads, 1)
         const uint32_t a0 = kResA ? smem_u32(ares + ks * kI8ABytes) : st;
         const uint32_t b0 = kResA ? st : st + (uint32_t)kAOff;
         if (elect_one()) {
-          if (g.probe == 2)
-            umma_i8<0>(tmem, umma_desc_sw32(a0), umma_desc_sw32(b0), idesc, ks > 0 ? 1u : 0u);
-          else
-            i8_products<0, 0>(tmem, a0, b0, idesc, ks == 0);
+#pragma unroll
+          for (int kk = 0; kk < kI8K / 32; ++kk) {
+            if (g.probe == 2)
+              umma_i8<0>(tmem, umma_desc_i8(a0 + kk * 32), umma_desc_i8(b0 + kk * 32), idesc, (ks | kk) ? 1u : 0u);
+            else
+              i8_products<0, 0>(tmem, a0 + kk * 32, b0 + kk * 32, idesc, ks == 0 && kk == 0);
+          }
           if (kClu)
             umma_commit_mc(&empty[slot], (uint16_t)3);  // frees the stage in both CTAs
           else
