@@ -503,7 +503,7 @@ cudaError_t launch_i8(const I8Plan& q, const CUtensorMap& tmA, const CUtensorMap
 // exact int32 accumulation: a diagonal sums <= 7 digit products of magnitude <= 64 * 64 per k, so
 // the contraction length K = I_q0 (padded) must stay below 2^31 / (7 * 4096) = 74898
 // INT8 kernel variant: the 2-CTA cluster kernel with multicast A by default;
-// tuning knobs JKCALS_I8_RESIDENT=1 (resident A where I_q0 <= 224; latency-bound, slower) and
+// tuning knobs JKCALS_I8_RESIDENT=1 (resident A where I_q0 <= 192; latency-bound, slower) and
 // JKCALS_I8_CLUSTER=0 (the one-CTA streaming kernel)
 int i8_variant(const KernelInfo& ki, int64_t KP) {
   static const int res = getenv("JKCALS_I8_RESIDENT") ? atoi(getenv("JKCALS_I8_RESIDENT")) : 0;

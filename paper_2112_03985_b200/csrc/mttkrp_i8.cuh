@@ -32,8 +32,8 @@ constexpr size_t kI8ABytes = (size_t)kI8S * 128 * kI8K;    // 28 KB
 constexpr size_t kI8BBytes = (size_t)kI8S * kI8N * kI8K;   // 14 KB
 constexpr size_t kI8StageBytes = kI8ABytes + kI8BBytes;
 constexpr size_t kI8Smem = 1024 + kI8Stages * kI8StageBytes + 256;
-// resident-A variant: when K = I_q0 fits 7 K32 steps (KP <= 224), the CTA keeps the whole U_q0
-// digit tile (7 x 28 KB) in shared memory across its j' units -- it is the same for every unit of
+// resident-A variant: when K = I_q0 fits kI8ResKS ring steps (KP <= 192), the CTA keeps the whole U_q0
+// digit tile (KS x 56 KB) in shared memory across its j' units -- it is the same for every unit of
 // an m-tile -- and streams only the T digits (B) through a 2-stage ring. This cuts the L2 -> SMEM
 // traffic per unit from 294 KB to 98 KB (syn200) -- but with only 28 KB of B in flight per SM the
 // ring is latency-bound and the variant measured ~6 % slower than streaming (opt-in).
@@ -44,7 +44,7 @@ static_assert(kI8SmemRes <= 232448, "resident-A INT8 MTTKRP exceeds shared memor
 // cluster variant: a pair of CTAs (one thread-block cluster) works on the same (m-tile, j') units
 // for two adjacent 64-row n-tiles (a 128-row "pair tile"); each CTA TMA-loads 4 of the (padded to
 // 8) U_q0 digit slices and multicasts them into both CTAs' stages, so the A operand crosses L2
-// once per pair: 56 KB instead of 84 KB of L2 -> SMEM traffic per pair and K32 step
+// once per pair: 56 KB instead of 84 KB of L2 -> SMEM traffic per pair and K step
 constexpr size_t kI8ABytesClu = (size_t)8 * 128 * kI8K;  // 8 slice slots (slot 7: TMA zero fill)
 constexpr size_t kI8StageBytesClu = kI8ABytesClu + kI8BBytes;
 constexpr size_t kI8SmemClu = 1024 + kI8Stages * kI8StageBytesClu + 256;
@@ -75,7 +75,7 @@ __device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
 
 struct I8Geom {
   int nMt, nNt;      // output tiles: C / 128, I_n / 64 (padded)
-  int Jp, KS;        // j' count, K32 steps per unit (KP / 32)
+  int Jp, KS;        // j' count, ring steps per unit (KP / kI8K)
   int64_t units;     // nMt * nNt * Jp
   int InP;           // padded I_n (rows of a j' block of Bsl)
   int nslow;
