@@ -61,7 +61,10 @@ typedef enum {
 } jkcals_status;
 
 /* JKCALS_FP64_I8 (experimental): FP64 factors and epilogue, the MTTKRP from INT8
- * tcgen05 MMAs on 7-digit operand slices with exact integer accumulation (FP64-accurate). */
+ * tcgen05 MMAs on 7-digit operand slices with exact integer accumulation (FP64-accurate, held to
+ * the FP64 parity bar). Requires dims[0], dims[1] <= 65536 (padded to 64: exact int32 sums);
+ * otherwise creation fails with JKCALS_E_ARG. Extra workspace: the T digits of every mode
+ * (7 x prod(dims) bytes per mode, padded). */
 typedef enum { JKCALS_FP64 = 0, JKCALS_FP32 = 1, JKCALS_FP64_I8 = 2 } jkcals_precision;
 
 enum {
@@ -301,8 +304,8 @@ jkcals_status jkcals_mttkrp(int ndims, const int64_t *dims, int n, const double 
  * operands of the per-j' inner products (T per mode-n row, U_q0 per column) split into 7 balanced
  * base-128 digits with power-of-two scales, digit products accumulated exactly in int32 TMEM
  * accumulators per significance, the slow-mode row product S(j', c) applied in FP64. Same
- * arguments as jkcals_mttkrp (ldu >= C); scratch from jkcals_mttkrp_i8_scratch_bytes. Not yet on
- * the JK-CALS path. */
+ * arguments as jkcals_mttkrp (ldu >= C); scratch from jkcals_mttkrp_i8_scratch_bytes. The
+ * JK-CALS sweep uses the same kernel under JKCALS_FP64_I8. JKCALS_E_ARG if I_q0 > 65536. */
 size_t jkcals_mttkrp_i8_scratch_bytes(int ndims, const int64_t *dims, int n, int64_t C, int device);
 jkcals_status jkcals_mttkrp_i8(int ndims, const int64_t *dims, int n, const double *T,
                                const double *const *U, int64_t C, int64_t ldu, double *M, int64_t ldm,
