@@ -348,6 +348,13 @@ __global__ void __launch_bounds__(kI8Threads, 1)
                 "=r"(r[dg][12]), "=r"(r[dg][13]), "=r"(r[dg][14]), "=r"(r[dg][15])
               : "r"(lb + (uint32_t)(dg * kI8N + cg)));
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (cg + 16 == kI8N / 2) {
+          // the accumulators are all in registers: release TMEM to the next unit's MMAs before the
+          // last chunk's recombination (overlaps it with the MMA stream)
+          asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(acc_empty);
+        }
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           // exact integer recombination of the diagonals (|D_dg| < 2^31, K <= kI8MaxK):
@@ -362,9 +369,6 @@ __global__ void __launch_bounds__(kI8Threads, 1)
           acc[cg + i] = fma(s, v, acc[cg + i]);
         }
       }
-      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(acc_empty);
     }
     if (seg_t >= 0) flush(seg_t);
   }
