@@ -916,6 +916,7 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     ig.nNt = q.nNt;
     ig.Jp = (int)q.Jp;
     ig.KS = (int)(q.KP / kI8K);
+    ig.Kq = (int)q.Iq0;
     ig.units = p.units;
     ig.InP = (int)q.InP;
     ig.nslow = h->N - 2;
@@ -2422,6 +2423,7 @@ jkcals_status jkcals_mttkrp_i8(int ndims, const int64_t* dims, int n, const doub
   g.nNt = q.nNt;
   g.Jp = (int)q.Jp;
   g.KS = (int)(q.KP / kI8K);
+  g.Kq = (int)q.Iq0;
   g.units = q.p.units;
   g.InP = (int)q.InP;
   g.nslow = ndims - 2;

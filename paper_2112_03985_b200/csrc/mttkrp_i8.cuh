@@ -76,6 +76,7 @@ __device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
 struct I8Geom {
   int nMt, nNt;      // output tiles: C / 128, I_n / 64 (padded)
   int Jp, KS;        // j' count, ring steps per unit (KP / kI8K)
+  int Kq;            // real K = I_q0 (the K32 sub-steps wholly in the zero padding are skipped)
   int64_t units;     // nMt * nNt * Jp
   int InP;           // padded I_n (rows of a j' block of Bsl)
   int nslow;
@@ -269,6 +270,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < kI8K / 32; ++kk) {
+            if (kk > 0 && ks * kI8K + kk * 32 >= g.Kq) break;  // all-zero K32 sub-step of the padding
             if (g.probe == 2)
               umma_i8<0>(tmem, umma_desc_i8(a0 + kk * 32), umma_desc_i8(b0 + kk * 32), idesc, (ks | kk) ? 1u : 0u);
             else
