@@ -313,7 +313,10 @@ def test_fp32_path_vs_oracle(name, ps):
 
 
 @pytest.mark.parametrize("dims,C", [((10, 8, 6), 20), ((37, 23, 11), 129), ((13, 7, 5, 3), 70),
-                                    ((50, 50, 50), 250), ((5, 300, 4), 10)])
+                                    ((50, 50, 50), 250), ((5, 300, 4), 10),
+                                    # I_q0 = 90 / 70 / 96 end inside the first half of the last K64 step
+                                    # (its second K32 sub-step is skipped), 97 just past it
+                                    ((90, 70, 9), 140), ((97, 96, 5), 64)])
 def test_experimental_int8_sliced_mttkrp(dims, C):
     # the FP64-accurate MTTKRP from INT8 tcgen05 MMAs (7-digit slicing, exact int32
     # diagonal accumulators, S applied in FP64) matches the oracle like the DMMA kernel does
