@@ -320,7 +320,7 @@ def main():
                                "peak": 4760.0, "frac": round(ops / (ms8 * 1e-3) / 1e12 / 4760.0, 4),
                                "peak_source": "measured kind::i8 UMMA rate, 8190 MAC/clk/SM at N >= 128 "
                                               "(profiles/r01_i8_microbench.txt); nominal dense int8 is 4500"},
-                  "parity": "every submodel of syn200 / eem R5 / 4-way within 8.1e-14 of the oracle "
+                  "parity": "every submodel of syn200 / eem R5 / 4-way within 8.2e-14 (factors) / 9.1e-14 (lambda) of the oracle "
                             "(profiles/r01_full_parity.jsonl), same bar as the FP64 path",
                   "status": "experimental (DESIGN.md §9b)"}
         h8.close()
