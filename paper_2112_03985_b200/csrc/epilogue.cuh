@@ -52,6 +52,7 @@ struct EpiArgs {
 };
 
 constexpr int kEpiThreads = 128;
+#ifdef JK_TU_HOST
 
 // Pre-reduction of the stream-K partial pieces for tiles split over many CTAs (a small-C shard
 // fills the GPU with up to 64 CTAs per tile; one epilogue CTA per submodel would otherwise sum
@@ -82,6 +83,7 @@ __global__ void __launch_bounds__(256) reduce_pieces_kernel(const double* __rest
     red[e] = s;
   }
 }
+#endif
 
 template <int RMAX>
 __device__ __forceinline__ void block_sum(double* vals, int cnt, double* red) {

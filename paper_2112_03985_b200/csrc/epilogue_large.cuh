@@ -21,7 +21,7 @@ constexpr int kLgThreads = 256;
 // The Jacobi pseudoinverse of epilogue.cuh's jacobi_pinv (same rotations, same order, same
 // rcond rule) on caller-provided work arrays, so that R up to 32 does not need 16 KB of stack
 // per thread: A and Q are R x R scratch in shared memory, Hp is written with row stride ldp.
-__device__ __noinline__ void jacobi_pinv_ptr(const double* H, int R, double* A, double* Q, double* Hp, int ldp,
+static __device__ __noinline__ void jacobi_pinv_ptr(const double* H, int R, double* A, double* Q, double* Hp, int ldp,
                                              double rcond) {
   for (int e = 0; e < R * R; ++e) { A[e] = H[e]; Q[e] = 0.0; }
   for (int i = 0; i < R; ++i) Q[i * R + i] = 1.0;
@@ -74,6 +74,7 @@ constexpr int kLgRows = 256;           // rows per chunk: one row per thread
 constexpr int kLgLd = kLgRMax + 1;     // odd row stride: thread-per-row accesses hit distinct banks
 // Ms + Vs = 2 x 256 x 33 x 8 = 132 KB of dynamic shared memory (opt-in; one CTA per SM)
 inline size_t epi_large_smem_bytes() { return (size_t)2 * kLgRows * kLgLd * sizeof(double); }
+#ifdef JK_TU_LARGE
 
 __global__ void __launch_bounds__(kLgThreads) als_epilogue_large_kernel(EpiArgs a) {
   const int k = blockIdx.x;
@@ -281,6 +282,8 @@ __global__ void __launch_bounds__(kLgThreads) als_epilogue_large_kernel(EpiArgs 
     else atomicAdd(a.active_count, 1);
   }
 }
+#endif
+#ifdef JK_TU_LARGE
 
 // Gramian of one block for ranks 17..32 (set_init / set_init_submodel / import): each thread owns
 // entries of U^T U and sums them over all rows in order.
@@ -298,5 +301,6 @@ __global__ void __launch_bounds__(kLgThreads) gram_large_kernel(const double* __
     gram[((int64_t)n * nsub + sub) * Rs * Rs + e] = s;
   }
 }
+#endif
 
 }  // namespace jk

@@ -20,14 +20,12 @@
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX3: host ranges for nsys timelines
 #include <vector>
 
+#define JK_TU_HOST  // this TU defines the small non-template kernels; the heavy ones live in k_*.cu
 #include "../../include/jkcals.h"
 #include "align.cuh"
 #include "aux_kernels.cuh"
-#include "epilogue.cuh"
 #include "epilogue_large.cuh"
-#include "mttkrp.cuh"
-#include "mttkrp_tf32.cuh"
-#include "mttkrp_i8.cuh"
+#include "kernels.h"
 
 using namespace jk;
 
@@ -40,20 +38,6 @@ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
 
 // ---------------------------------------------------------------- kernel dispatch tables
-typedef void (*MttkrpFn)(const CUtensorMap, const CUtensorMap, MttkrpView, MttkrpGeom, const TileInfo*, double*);
-
-template <int NT, bool KM, int ST>
-size_t smem_of(int nslow) { return MttkrpCfg<NT, KM, ST>::smem_bytes(nslow); }
-typedef size_t (*SmemFn)(int);
-
-template <bool KM, int ST, int... NTs>
-struct Table {
-  static void fill(MttkrpFn* fns, SmemFn* sm) {
-    int i = 0;
-    ((fns[i] = mttkrp_dmma_kernel<NTs, KM, ST>, sm[i] = smem_of<NTs, KM, ST>, ++i), ...);
-  }
-};
-
 struct KernelInfo {
   MttkrpFn fn[2][2][kMaxNT];         // [KMAJOR][STAGES==4][NT-1]
   SmemFn smem[2][2][kMaxNT];
@@ -68,32 +52,31 @@ KernelInfo* kernel_info(int device, std::string* err) {
   if (device < 0 || device >= 16) return nullptr;
   if (ready[device]) return &info[device];
   KernelInfo& ki = info[device];
-  Table<false, 2, 1, 2, 3, 4, 5, 6, 7, 8>::fill(ki.fn[0][0], ki.smem[0][0]);
-  Table<false, 4, 1, 2, 3, 4, 5, 6, 7, 8>::fill(ki.fn[0][1], ki.smem[0][1]);
-  Table<true, 2, 1, 2, 3, 4, 5, 6, 7, 8>::fill(ki.fn[1][0], ki.smem[1][0]);
-  Table<true, 4, 1, 2, 3, 4, 5, 6, 7, 8>::fill(ki.fn[1][1], ki.smem[1][1]);
+  dmma_kernels_km0(ki.fn[0], ki.smem[0]);
+  dmma_kernels_km1(ki.fn[1], ki.smem[1]);
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
   cudaDeviceGetAttribute(&ki.nsm, cudaDevAttrMultiProcessorCount, device);
   {
-    cudaError_t e = cudaFuncSetAttribute(mttkrp_tf32_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kTfSmemMax);
+    cudaError_t e = cudaSuccess;
+    for (int st : {3, 4, 6, 8})
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(tf32_kernel(st), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTfSmemMax);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(mttkrp_tf32_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTfSmemMax);
+      e = cudaFuncSetAttribute(i8_kernel(0), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8Smem);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(mttkrp_tf32_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTfSmemMax);
+      e = cudaFuncSetAttribute(i8_kernel(1), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8SmemRes);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(mttkrp_tf32_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTfSmemMax);
+      e = cudaFuncSetAttribute(i8_kernel(2), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8SmemClu);
+    // epilogue kernels: opt-in dynamic shared memory (per device, once)
+    for (EpiFns f : {epi_kernels_2(), epi_kernels_4(), epi_kernels_6(), epi_kernels_8(), epi_kernels_10(),
+                     epi_kernels_12(), epi_kernels_16()})
+      for (EpiFn k : {f.smem, f.mixed})
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(mttkrp_i8_kernel<kI8Stages, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kI8Smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(mttkrp_i8_kernel<kI8ResStages, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kI8SmemRes);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(mttkrp_i8_kernel<kI8Stages, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kI8SmemClu);
+      e = cudaFuncSetAttribute(epi_large_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)epi_large_smem_bytes());
     ki.i8clusters = 0;
     if (e == cudaSuccess) {
       cudaLaunchConfig_t cfg = {};
@@ -108,7 +91,7 @@ KernelInfo* kernel_info(int device, std::string* err) {
       cfg.attrs = at;
       cfg.numAttrs = 1;
       int ncl = 0;
-      if (cudaOccupancyMaxActiveClusters(&ncl, mttkrp_i8_kernel<kI8Stages, false, true>, &cfg) == cudaSuccess)
+      if (cudaOccupancyMaxActiveClusters(&ncl, i8_kernel(2), &cfg) == cudaSuccess)
         ki.i8clusters = ncl;
       cudaGetLastError();  // the query is advisory: 0 falls back to the one-CTA kernel
     }
@@ -479,11 +462,11 @@ I8Plan make_i8_plan(int ndims, const int64_t* dims, int n, int64_t C, const Kern
 cudaError_t launch_i8(const I8Plan& q, const CUtensorMap& tmA, const CUtensorMap& tmB, const I8Geom& g,
                       const TileInfo* ti, double* parts, cudaStream_t s) {
   if (q.variant == 1) {
-    mttkrp_i8_kernel<kI8ResStages, true><<<q.p.G, kI8Threads, kI8SmemRes, s>>>(tmA, tmB, g, ti, parts);
+    i8_kernel(1)<<<q.p.G, kI8Threads, kI8SmemRes, s>>>(tmA, tmB, g, ti, parts);
     return cudaGetLastError();
   }
   if (q.variant == 0) {
-    mttkrp_i8_kernel<kI8Stages, false><<<q.p.G, kI8Threads, kI8Smem, s>>>(tmA, tmB, g, ti, parts);
+    i8_kernel(0)<<<q.p.G, kI8Threads, kI8Smem, s>>>(tmA, tmB, g, ti, parts);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -498,7 +481,7 @@ cudaError_t launch_i8(const I8Plan& q, const CUtensorMap& tmA, const CUtensorMap
   cfg.stream = s;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, mttkrp_i8_kernel<kI8Stages, false, true>, tmA, tmB, g, ti, parts);
+  return cudaLaunchKernelEx(&cfg, i8_kernel(2), tmA, tmB, g, ti, parts);
 }
 // exact int32 accumulation: a diagonal sums <= 7 digit products of magnitude <= 64 * 64 per k, so
 // the contraction length K = I_q0 (padded) must stay below 2^31 / (7 * 4096) = 74898
@@ -846,15 +829,22 @@ jkcals_status replan(jkcals_t h) {
   return JKCALS_OK;
 }
 
-template <int RMAX>
-void launch_epi(jkcals_t h, const EpiArgs& a, bool pdl) {
-  const size_t dyn = (size_t)2 * a.In * (a.R | 1) * sizeof(double);  // odd row stride (epilogue.cuh)
-  constexpr size_t kMaxDyn = 96 * 1024;
-  static unsigned attr_mask = 0;  // per RMAX instantiation and device
-  if (!(attr_mask & (1u << (h->device & 31)))) {
-    cudaFuncSetAttribute(als_epilogue_kernel<RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDyn);
-    attr_mask |= 1u << (h->device & 31);
+EpiFns epi_fns(int rclass) {
+  switch (rclass) {
+    case 2: return epi_kernels_2();
+    case 4: return epi_kernels_4();
+    case 6: return epi_kernels_6();
+    case 8: return epi_kernels_8();
+    case 10: return epi_kernels_10();
+    case 12: return epi_kernels_12();
+    default: return epi_kernels_16();
   }
+}
+
+void launch_epi(jkcals_t h, int rclass, const EpiArgs& a, bool pdl) {
+  const size_t dyn = (size_t)2 * a.In * (a.R | 1) * sizeof(double);  // odd row stride (epilogue.cuh)
+  constexpr size_t kMaxDyn = 96 * 1024;  // opt-in set per device in kernel_info()
+  const EpiFns f = epi_fns(rclass);
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -864,23 +854,17 @@ void launch_epi(jkcals_t h, const EpiArgs& a, bool pdl) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (dyn <= kMaxDyn && h->mixed) {
-    static unsigned mixed_mask = 0;
-    if (!(mixed_mask & (1u << (h->device & 31)))) {
-      cudaFuncSetAttribute(als_epilogue_mixed_kernel<RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)kMaxDyn);
-      mixed_mask |= 1u << (h->device & 31);
-    }
     cfg.blockDim = dim3(kEpi2Threads);
     cfg.dynamicSmemBytes = dyn;
-    cudaLaunchKernelEx(&cfg, als_epilogue_mixed_kernel<RMAX>, a);
+    cudaLaunchKernelEx(&cfg, f.mixed, a);
   } else if (dyn <= kMaxDyn) {
     cfg.blockDim = dim3(kEpi2Threads);
     cfg.dynamicSmemBytes = dyn;
-    cudaLaunchKernelEx(&cfg, als_epilogue_kernel<RMAX>, a);
+    cudaLaunchKernelEx(&cfg, f.smem, a);
   } else {
     cfg.blockDim = dim3(kEpiThreads);
     cfg.dynamicSmemBytes = 0;
-    cudaLaunchKernelEx(&cfg, als_epilogue_rows_kernel<RMAX>, a);
+    cudaLaunchKernelEx(&cfg, f.rows, a);
   }
 }
 
@@ -932,10 +916,9 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
       ig.Us[sl] = nullptr;
     }
     ig.ldu = h->ldu;
-    {  // dev timing probe only (see jkcals_mttkrp_i8); 0 in every real run
-      static const int probe = getenv("JKCALS_I8_PROBE") ? atoi(getenv("JKCALS_I8_PROBE")) : 0;
-      ig.probe = probe;
-    }
+#ifdef JKCALS_DEV_PROBES  // timing-probe builds only (tools/i8_probe.py); results are wrong when set
+    ig.probe = getenv("JKCALS_I8_PROBE") ? atoi(getenv("JKCALS_I8_PROBE")) : 0;
+#endif
     ig.eT = h->ptr<int>(h->off.i8eT[n]);
     ig.eU = eU;
     CKH(h, launch_i8(q, h->tmA8[n], h->tmB8[n], ig, ti, parts, h->es));
@@ -961,18 +944,8 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     tg.stages = p.ST4;
-    if (p.ST4 == 8)
-      CKH(h, cudaLaunchKernelEx(&cfg, mttkrp_tf32_kernel<8>, h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v, tg, ti,
-                                parts));
-    else if (p.ST4 == 6)
-      CKH(h, cudaLaunchKernelEx(&cfg, mttkrp_tf32_kernel<6>, h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v, tg, ti,
-                                parts));
-    else if (p.ST4 == 4)
-      CKH(h, cudaLaunchKernelEx(&cfg, mttkrp_tf32_kernel<4>, h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v, tg, ti,
-                                parts));
-    else
-      CKH(h, cudaLaunchKernelEx(&cfg, mttkrp_tf32_kernel<3>, h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v, tg, ti,
-                                parts));
+    CKH(h, cudaLaunchKernelEx(&cfg, tf32_kernel(p.ST4), h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v, tg, ti,
+                              parts));
   } else {
     MttkrpFn fn = h->ki->fn[p.KM][p.ST4][p.NT - 1];
     // programmatic dependent launch: this grid may start (prologue) while the previous kernel
@@ -1043,12 +1016,6 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
   a.active_count = reinterpret_cast<int*>(h->ws + h->off.misc + 16);
   const bool pdl = h->pdl && !timed;
   if (h->R > 16) {  // ranks 17..32: the streaming large-rank epilogue (any I_n, mixed pools too)
-    static unsigned lg_mask = 0;
-    if (!(lg_mask & (1u << (h->device & 31)))) {
-      cudaFuncSetAttribute(als_epilogue_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)epi_large_smem_bytes());
-      lg_mask |= 1u << (h->device & 31);
-    }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1061,14 +1028,11 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     cfg.numAttrs = 1;
     if (!a.subR) a.subR = h->ptr<int>(h->off.subR);  // the large kernel reads per-block ranks
     if (!a.blkcol) a.blkcol = h->ptr<int>(h->off.blkcol);
-    cudaLaunchKernelEx(&cfg, als_epilogue_large_kernel, a);
-  } else if (h->R <= 2) launch_epi<2>(h, a, pdl);
-  else if (h->R <= 4) launch_epi<4>(h, a, pdl);
-  else if (h->R <= 6) launch_epi<6>(h, a, pdl);
-  else if (h->R <= 8) launch_epi<8>(h, a, pdl);
-  else if (h->R <= 10) launch_epi<10>(h, a, pdl);
-  else if (h->R <= 12) launch_epi<12>(h, a, pdl);
-  else launch_epi<16>(h, a, pdl);
+    cudaLaunchKernelEx(&cfg, epi_large_kernel(), a);
+  } else {
+    launch_epi(h, h->R <= 2 ? 2 : h->R <= 4 ? 4 : h->R <= 6 ? 6 : h->R <= 8 ? 8 : h->R <= 10 ? 10 : h->R <= 12 ? 12 : 16,
+               a, pdl);
+  }
   CKH(h, cudaGetLastError());
   if (timed) CKH(h, cudaEventRecord(h->ev[4 * n + 2], h->es));
   return JKCALS_OK;
@@ -1119,7 +1083,7 @@ jkcals_status compute_grams(jkcals_t h) {
     else if (h->R <= 8) launch_gram<8>(h, n);
     else if (h->R <= 16) launch_gram<16>(h, n);
     else
-      gram_large_kernel<<<h->K, kLgThreads, 0, h->stream>>>(h->U(n), (int)h->dims[n], h->ldu, h->R,
+      gram_large_kernel_fn()<<<h->K, kLgThreads, 0, h->stream>>>(h->U(n), (int)h->dims[n], h->ldu, h->R,
                                                             h->ptr<int>(h->off.blk2sub), h->ptr<int>(h->off.blkcol),
                                                             h->ptr<int>(h->off.subR), h->nsub, n,
                                                             h->ptr<double>(h->off.gram));
@@ -2371,15 +2335,6 @@ jkcals_status jkcals_mttkrp_i8(int ndims, const int64_t* dims, int n, const doub
   KernelInfo* ki = kernel_info(dev, nullptr);
   if (!ki) return JKCALS_E_CUDA;
   if (scratch_bytes < jkcals_mttkrp_i8_scratch_bytes(ndims, dims, n, C, dev)) return JKCALS_E_OOM;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(mttkrp_i8_kernel<kI8Stages, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kI8Smem) != cudaSuccess ||
-        cudaFuncSetAttribute(mttkrp_i8_kernel<kI8ResStages, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kI8SmemRes) != cudaSuccess)
-      return JKCALS_E_CUDA;
-    attr = true;
-  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const I8Plan q = make_i8_plan(ndims, dims, n, C, *ki);
   I8Scratch x = i8_layout(reinterpret_cast<uintptr_t>(scratch), ndims, dims, q);
@@ -2441,10 +2396,9 @@ jkcals_status jkcals_mttkrp_i8(int ndims, const int64_t* dims, int n, const doub
   g.ldu = q.CP;
   g.eT = x.eT;
   g.eU = x.eU;
-  {  // dev timing probe only (results are wrong when set): 1 = drain skipped, 2 = one product per K32 step
-    static const int probe = getenv("JKCALS_I8_PROBE") ? atoi(getenv("JKCALS_I8_PROBE")) : 0;
-    g.probe = probe;
-  }
+#ifdef JKCALS_DEV_PROBES  // timing-probe builds only: 1 = drain skipped, 2 = one product per K32 step
+  g.probe = getenv("JKCALS_I8_PROBE") ? atoi(getenv("JKCALS_I8_PROBE")) : 0;
+#endif
   if (launch_i8(q, tmA, tmB, g, x.ti, x.parts, s) != cudaSuccess) return JKCALS_E_CUDA;
   const int64_t tot = q.In * C;
   reduce_parts_kernel<<<(int)cdiv(tot, 256), 256, 0, s>>>(x.parts, x.ti, (int)q.In, (int)C, q.p.BN, q.nMt, M, ldm);

@@ -369,6 +369,7 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
       }
   }
 }
+#ifdef JK_TU_HOST
 
 // Plain reduction of the partial pieces into a dense row-major M (stand-alone op only; the
 // JK-CALS path reduces inside the epilogue instead).
@@ -384,6 +385,8 @@ __global__ void reduce_parts_kernel(const double* __restrict__ parts, const Tile
   for (int pc = 0; pc < ti.npieces; ++pc) s += p[(int64_t)pc * BN * kBM];
   M[(int64_t)i * ldm + c] = s;
 }
+#endif
+#ifdef JK_TU_HOST
 
 // Materialised Khatri-Rao generation (a1 in SURVEY §8a): K(j, c) = prod_{m != n} U_m(i_m(j), c),
 // row-major J x ldk. Each thread owns 4 consecutive columns and a run of kKrpRows consecutive j,
@@ -441,5 +444,6 @@ __global__ void __launch_bounds__(256) krp_gen_kernel(ModeView v, int C, int64_t
     }
   }
 }
+#endif
 
 }  // namespace jk

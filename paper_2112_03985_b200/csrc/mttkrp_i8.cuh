@@ -85,7 +85,9 @@ struct I8Geom {
   int64_t ldu;
   const int* eT;     // [InP] row exponents of T
   const int* eU;     // [CP] column exponents of U_q0
-  int probe;         // 0 (dev timing probes: see jkcals_mttkrp_i8)
+#ifdef JKCALS_DEV_PROBES
+  int probe;         // dev timing probe builds only (tools/i8_probe.py)
+#endif
 };
 
 __device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t saddr) {
@@ -271,9 +273,11 @@ __global__ void __launch_bounds__(kI8Threads, 1)
 #pragma unroll
           for (int kk = 0; kk < kI8K / 32; ++kk) {
             if (kk > 0 && ks * kI8K + kk * 32 >= g.Kq) break;  // all-zero K32 sub-step of the padding
+#ifdef JKCALS_DEV_PROBES  // timing probe builds only: one digit product per K32 step (wrong results)
             if (g.probe == 2)
               umma_i8<0>(tmem, umma_desc_i8(a0 + kk * 32), umma_desc_i8(b0 + kk * 32), idesc, (ks | kk) ? 1u : 0u);
             else
+#endif
               i8_products<0, 0>(tmem, a0 + kk * 32, b0 + kk * 32, idesc, ks == 0 && kk == 0);
           }
           if (kClu)
@@ -330,12 +334,14 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       }
       mbar_wait_safe(acc_full, un & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#ifdef JKCALS_DEV_PROBES  // timing probe builds only: drain skipped (wrong results)
       if (g.probe == 1) {
         acc[0] += s;
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty);
         continue;
       }
+#endif
       const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * (kI8N / 2));
 #pragma unroll
       for (int cg = 0; cg < kI8N / 2; cg += 16) {
@@ -383,6 +389,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
   if (kClu) cluster_sync_all();  // no multicast or remote arrive may target an exited peer
 }
 
+#ifdef JK_TU_HOST
 // ---- operand preparation -----------------------------------------------------------------
 // row exponents of T_(n): e_T(i) with max_j |T(i, j)| 2^-e <= 1/2 (one block per row)
 __global__ void row_exp_t_kernel(const double* __restrict__ T, int N, const int64_t* __restrict__ st_dev,
@@ -462,5 +469,7 @@ __global__ void slice_u_i8_kernel(const double* __restrict__ U, int64_t ldu, int
 #pragma unroll
   for (int s = 0; s < kI8S; ++s) A[(int64_t)s * slice + e] = d[s];
 }
+
+#endif  // JK_TU_HOST
 
 }  // namespace jk

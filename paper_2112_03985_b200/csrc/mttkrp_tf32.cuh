@@ -408,6 +408,7 @@ __global__ void __launch_bounds__(kTfThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(kTfTmemCols));
   }
 }
+#ifdef JK_TU_HOST
 
 // FP32 hi/lo copies of T for the TF32 path. dst layout: dims permuted by `perm01` (swap modes 0
 // and 1 when set), first-dim pitch ld_dst (multiple of 4 floats => 16-byte TMA strides).
@@ -423,5 +424,6 @@ __global__ void split_tf32_kernel(const double* __restrict__ T, int64_t I0, int6
   hi[d] = h;
   lo[d] = l;
 }
+#endif
 
 }  // namespace jk
