@@ -65,6 +65,12 @@ typedef enum {
  * the FP64 parity bar). Requires dims[0], dims[1] <= 65536 (padded to 64: exact int32 sums);
  * otherwise creation fails with JKCALS_E_ARG. Extra workspace: the T digits of every mode
  * (7 x prod(dims) bytes per mode, padded). */
+/* JKCALS_FP32 (north_star's "optional FP32 path", parity bar 1e-4): the MTTKRP in 3xTF32 on the
+ * tcgen05 tensor cores (FP32-accurate), the epilogue in FP64. The error e is a difference of
+ * O(||T||^2) terms, so an FP32-accurate M makes it unusable for a convergence test (r01: up to
+ * 31 % relative error at 4-way full size). Therefore, when iterate() runs with tol > 0, the LAST
+ * mode's MTTKRP of every sweep runs on the FP64 kernel: its update and the error/fit behind the
+ * stop rule are FP64-accurate (reading A24). With tol <= 0 every mode runs in FP32. */
 typedef enum { JKCALS_FP64 = 0, JKCALS_FP32 = 1, JKCALS_FP64_I8 = 2 } jkcals_precision;
 
 enum {
@@ -216,6 +222,16 @@ jkcals_status jkcals_get_jackknife_stats(jkcals_t h, int mode, double *mean, dou
  * mean and sum of squared deviations M2 over this handle's submodels. mode >= 1. */
 jkcals_status jkcals_get_local_moments(jkcals_t h, int mode, double *count, double *mean,
                                        double *m2);
+
+/* Merge shard moments into the job's (the end-of-run step of a sharded jackknife, SURVEY §8e;
+ * Alg. 2 alg:jk:std): folds nparts (count, mean, M2) sets of n elements each, in
+ * part order, with Chan, Golub & LeVeque's pairwise update (n = n_a + n_b, d = mean_b - mean_a,
+ * mean = mean_a + d n_b / n, M2 = M2_a + M2_b + d^2 n_a n_b / n; empty parts are skipped).
+ * Inputs are host arrays laid out part-major (counts[k * n + e], ...); outputs count, mean, m2
+ * (n each, host) may not alias them. Host computation only (no GPU needed); the std is then
+ * sqrt(((g-1)/g) M2) with g the merged count. Errors: E_ARG (null pointers, nparts < 1, n < 0). */
+jkcals_status jkcals_merge_moments(int nparts, int64_t n, const double *counts, const double *means,
+                                   const double *m2s, double *count, double *mean, double *m2);
 
 /* The same two calls for model `model` of a pool (over this handle's submodels of that model;
  * g = their count; dims[mode] x ranks[model]). The single-model calls above are model 0 and

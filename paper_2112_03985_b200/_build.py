@@ -16,8 +16,8 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libjkcals.so")
-OBJ = os.path.join(HERE, "build")
+LIB = os.environ.get("JKCALS_BUILD_LIB") or os.path.join(HERE, "libjkcals.so")  # dev variants elsewhere
+OBJ = os.path.join(HERE, "build", os.path.basename(LIB).replace(".so", ""))
 SRCS = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh"))
               + glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "jkcals.h")])
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

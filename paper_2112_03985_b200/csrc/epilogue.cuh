@@ -482,17 +482,16 @@ __device__ __forceinline__ void epi_smem_body(const EpiArgs& a, const int k, con
   const int ldm = R | 1;
   double* Vs = dyn + In * ldm;  // [In][ldm]
 
-  // (a3) Hadamard of the cached Gramians of every other mode
+  // (a3) Hadamard of the cached Gramians of every other mode. H depends only on the other modes'
+  // Gramians, written by earlier epilogues that completed before this grid was launched, so it
+  // and its Cholesky factor are formed BEFORE waiting for the MTTKRP grid (programmatic
+  // dependent launch: this prologue overlaps the MTTKRP's tail; L2 loads, not L1)
   if (tid < R * R) {
     double h = 1.0;
     for (int m = 0; m < N; ++m)
-      if (m != n) h *= a.gram[((int64_t)m * a.nsub + sub) * Rs * Rs + tid];
+      if (m != n) h *= __ldcg(a.gram + ((int64_t)m * a.nsub + sub) * Rs * Rs + tid);
     H[tid] = h;
   }
-  // (a2) fixed-order sum of the partial pieces of this submodel's R columns: J elements per
-  // thread x Q pieces = 16 independent loads in flight; the adds of each element stay in order
-  if (In * R <= kEpi2Threads) sum_pieces<1, 16>(a, cb, R, In, Ms, ldm);
-  else sum_pieces<4, 4>(a, cb, R, In, Ms, ldm);
   __syncthreads();
   EPI_PROBE(2);
   // (a4) Cholesky H = L L^T (textbook, no pivoting) in registers of thread 0; pinv fallback
@@ -535,6 +534,14 @@ __device__ __forceinline__ void epi_smem_body(const EpiArgs& a, const int k, con
       a.flags[sub] |= F_PINV;
     }
   }
+  // the MTTKRP of this mode has completed: its reduced tiles are visible from here on
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" :::);
+  if (n == 0 && k == 0 && tid == 0) *a.active_count = 0;  // per-sweep counter reset
+  // (a2) fixed-order sum of the partial pieces of this submodel's R columns (one reduced piece per
+  // tile on the FP64 path): J elements per thread x Q pieces = 16 independent loads in flight
+  if (In * R <= kEpi2Threads) sum_pieces<1, 16>(a, cb, R, In, Ms, ldm);
+  else sum_pieces<4, 4>(a, cb, R, In, Ms, ldm);
   __syncthreads();
   EPI_PROBE(3);
   const bool pinv = use_pinv != 0;
@@ -664,15 +671,22 @@ __device__ __forceinline__ void epi_smem_body(const EpiArgs& a, const int k, con
   EPI_PROBE_DUMP();
 }
 
+// frozen block (converged or failed): nothing to update, but block 0 still resets the per-sweep
+// active counter at mode 0 (after the previous grid, which may still read it, has completed)
+__device__ __forceinline__ void epi_frozen(const EpiArgs& a, int k) {
+  if (a.n == 0 && k == 0 && threadIdx.x == 0) {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    *a.active_count = 0;
+  }
+}
+
 template <int RMAX>
 __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
   const int k = blockIdx.x;
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the MTTKRP grid has completed
-  asm volatile("griddepcontrol.launch_dependents;\n" :::);
-  if (a.n == 0 && k == 0 && threadIdx.x == 0) *a.active_count = 0;  // per-sweep counter reset
+  // (block table and masks are only changed by the host between sweeps: safe before the wait)
   const int sub = a.blk2sub[k];
-  if (!a.active[sub]) return;  // frozen (converged or failed)
-  epi_smem_body<RMAX>(a, k, sub, a.subR ? a.subR[sub] : a.R);
+  if (!a.active[sub]) return epi_frozen(a, k);
+  epi_smem_body<RMAX>(a, k, sub, a.subR ? a.subR[sub] : a.R);  // waits for the MTTKRP inside
 }
 
 // Mixed-rank pool: one launch for every block; each block runs the body instantiated for the
@@ -682,11 +696,8 @@ __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_kernel(EpiArgs a) {
 template <int RMAXC>
 __global__ void __launch_bounds__(kEpi2Threads) als_epilogue_mixed_kernel(EpiArgs a) {
   const int k = blockIdx.x;
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;\n" :::);
-  if (a.n == 0 && k == 0 && threadIdx.x == 0) *a.active_count = 0;
   const int sub = a.blk2sub[k];
-  if (!a.active[sub]) return;
+  if (!a.active[sub]) return epi_frozen(a, k);
   const int R = a.subR[sub];
   if (R <= 2) epi_smem_body<2>(a, k, sub, R);
   else if (RMAXC >= 4 && R <= 4) epi_smem_body<(RMAXC >= 4 ? 4 : 2)>(a, k, sub, R);

@@ -523,6 +523,7 @@ struct Layout {
 
 struct Offsets {
   size_t T, T32hi, T32lo, T1hi, T1lo, U[2][kMaxModes], Ures, parts, tinfo[kMaxModes], tinfo1[kMaxModes], red, gram,
+      tinfo64, tinfo164,
       lambda, normT2p, fit, fit_prev, err, hist,
       slice, slice_part, stage, iters, flags, active, blk2sub, map, pglob, misc, srcoff, srcld, subR, subRc, blkcol,
       dstoff, pref[kMaxModes], aln, aperm, asign, acong, asrc, asld, srcpg;
@@ -571,6 +572,13 @@ bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_c
     o->parts_cap = std::max(o->parts_cap, pc);
     o->tiles_cap = std::max(o->tiles_cap, tc);
   }
+  if (tf32) {  // the FP32 path runs its last mode on the FP64 kernel when tol > 0 (reading A24)
+    int64_t pc;
+    int tc;
+    plan_bounds(mode_geo(N, dims, N - 1), N - 1, C, ki, &pc, &tc, false);
+    o->parts_cap = std::max(o->parts_cap, pc);
+    o->tiles_cap = std::max(o->tiles_cap, tc);
+  }
   o->parts = L.take(o->parts_cap * 8);
   for (int n = 0; n < N; ++n) o->tinfo[n] = L.take(plan_table_bytes(o->tiles_cap, ki.nsm * 8));
   // pre-reduced pieces (one per tile) for tiles split over many CTAs, and their 1-piece tables
@@ -579,6 +587,12 @@ bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_c
     const ModePlan q = i8 ? make_i8_plan(N, dims, n, C, ki).p : make_plan(mode_geo(N, dims, n), n, C, ki, tf32);
     red_cap = std::max<int64_t>(red_cap, (int64_t)q.ntiles * q.BN * kBM);
   }
+  if (tf32) {
+    const ModePlan q = make_plan(mode_geo(N, dims, N - 1), N - 1, C, ki, false);
+    red_cap = std::max<int64_t>(red_cap, (int64_t)q.ntiles * q.BN * kBM);
+  }
+  o->tinfo64 = L.take(plan_table_bytes(o->tiles_cap, ki.nsm * 8));
+  o->tinfo164 = L.take(o->tiles_cap * sizeof(TileInfo));
   o->red = L.take(red_cap * 8);
   for (int n = 0; n < N; ++n) o->tinfo1[n] = L.take(o->tiles_cap * sizeof(TileInfo));
   o->gram = L.take((size_t)N * nsub * R * R * 8);
@@ -692,6 +706,14 @@ struct jkcals_s {
   bool red_on[kMaxModes] = {false};    // pieces of this mode pre-reduced before the epilogue
   std::vector<TileInfo> table1[kMaxModes];
   int tf32 = 0;                        // precision JKCALS_FP32: 3xTF32 tcgen05 MTTKRP
+  // JKCALS_FP32 with tol > 0: the last mode's MTTKRP runs on the FP64 kernel so that the error and
+  // fit behind the convergence test are FP64-accurate (reading A24)
+  bool f64last = false;
+  ModePlan plan64;
+  CUtensorMap tmT64;
+  bool red64 = false;
+  std::vector<char> table64;
+  std::vector<TileInfo> table164;
   int i8 = 0;                          // precision JKCALS_FP64_I8: INT8-sliced FP64-accurate MTTKRP
   I8Plan i8q[kMaxModes];
   CUtensorMap tmA8[kMaxModes], tmB8[kMaxModes];
@@ -820,6 +842,25 @@ jkcals_status replan(jkcals_t h) {
       }
     }
   }
+  if (h->tf32) {  // the FP64 plan of the last mode (used when tol > 0)
+    const int n = h->N - 1;
+    h->plan64 = make_plan(mode_geo(h->N, h->dims, n), n, h->C, *h->ki, false);
+    const ModePlan& p = h->plan64;
+    if (plan_parts_doubles(p) > h->off.parts_cap || p.ntiles > h->off.tiles_cap)
+      return fail(h, JKCALS_E_OOM, "internal: plan exceeds workspace bounds");
+    h->table64 = pack_plan(p);
+    CKH(h, cudaMemcpyAsync(h->ptr<TileInfo>(h->off.tinfo64), h->table64.data(), h->table64.size(),
+                           cudaMemcpyHostToDevice, h->stream));
+    int maxp = 0;
+    for (const TileInfo& ti : p.tinfo) maxp = std::max(maxp, ti.npieces);
+    h->red64 = maxp > kRedPieces && h->dims[n] * maxp > 8192;
+    h->table164.assign(p.ntiles, TileInfo{});
+    for (int t = 0; t < p.ntiles; ++t) h->table164[t] = TileInfo{0, 1, t, 0};
+    CKH(h, cudaMemcpyAsync(h->ptr<TileInfo>(h->off.tinfo164), h->table164.data(), p.ntiles * sizeof(TileInfo),
+                           cudaMemcpyHostToDevice, h->stream));
+    if (!make_tmap_T(&h->tmT64, h->ptr<double>(h->off.T), h->N, h->dims, h->I0p, n, p.BN, bnp_of(p.NT)))
+      return fail(h, JKCALS_E_CUDA, "cuTensorMapEncodeTiled failed for the FP64 view of mode %d", n);
+  }
   CKH(h, cudaStreamSynchronize(h->stream));  // tinfo host vectors may change on the next replan
   if (h->gexec) {
     cudaGraphExecDestroy(h->gexec);
@@ -871,7 +912,8 @@ void launch_epi(jkcals_t h, int rclass, const EpiArgs& a, bool pdl) {
 jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
   double* Uall[kMaxModes];
   for (int m = 0; m < h->N; ++m) Uall[m] = h->U(m);
-  const ModePlan& p = h->plan[n];
+  const bool f64 = h->tf32 && h->f64last && n == h->N - 1;  // FP32 path, tol > 0: last mode in FP64
+  const ModePlan& p = f64 ? h->plan64 : h->plan[n];
   MttkrpView v = make_mview(h->N, h->dims, n, Uall);
   MttkrpGeom g;
   g.C = h->C;
@@ -881,7 +923,7 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
   g.KT = p.KT;
   g.units = p.units;
   g.G = p.G;
-  const TileInfo* ti = h->ptr<TileInfo>(h->off.tinfo[n]);
+  const TileInfo* ti = h->ptr<TileInfo>(f64 ? h->off.tinfo64 : h->off.tinfo[n]);
   double* parts = h->ptr<double>(h->off.parts);
   if (timed) CKH(h, cudaEventRecord(h->ev[4 * n + 0], h->es));
   if (h->i8) {
@@ -922,7 +964,7 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     ig.eT = h->ptr<int>(h->off.i8eT[n]);
     ig.eU = eU;
     CKH(h, launch_i8(q, h->tmA8[n], h->tmB8[n], ig, ti, parts, h->es));
-  } else if (h->tf32) {
+  } else if (h->tf32 && !f64) {
     TfGeom tg;
     tg.C = h->C;
     tg.ldu = h->ldu;
@@ -960,13 +1002,13 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     cfg.stream = h->es;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CKH(h, cudaLaunchKernelEx(&cfg, fn, h->tmT[n], h->tmU[h->cur][n], v, g, ti, parts));
+    CKH(h, cudaLaunchKernelEx(&cfg, fn, f64 ? h->tmT64 : h->tmT[n], h->tmU[h->cur][n], v, g, ti, parts));
   }
   CKH(h, cudaGetLastError());
   if (timed) CKH(h, cudaEventRecord(h->ev[4 * n + 1], h->es));
   const double* epi_parts = parts;
   const TileInfo* epi_ti = ti;
-  if (h->red_on[n]) {  // pre-reduce the pieces across the whole GPU (PDL-chained)
+  if (f64 ? h->red64 : h->red_on[n]) {  // pre-reduce the pieces across the whole GPU (PDL-chained)
     const int tile_elems = p.BN * kBM;
     const int64_t tot = (int64_t)p.ntiles * tile_elems;
     cudaLaunchConfig_t cfg = {};
@@ -981,7 +1023,7 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     double* red = h->ptr<double>(h->off.red);
     CKH(h, cudaLaunchKernelEx(&cfg, reduce_pieces_kernel, (const double*)parts, ti, p.ntiles, tile_elems, red));
     epi_parts = red;
-    epi_ti = h->ptr<TileInfo>(h->off.tinfo1[n]);
+    epi_ti = h->ptr<TileInfo>(f64 ? h->off.tinfo164 : h->off.tinfo1[n]);
   }
   EpiArgs a;
   a.N = h->N;
@@ -1595,6 +1637,12 @@ jkcals_status jkcals_iterate(jkcals_t h, int max_iters, double tol, int* sweeps_
   if (!h->inited) return fail(h, JKCALS_E_STATE, "iterate before set_init");
   DeviceGuard dg(h->device);
   h->aligned = false;
+  if (h->tf32 && (tol > 0.0) != h->f64last) {  // switch the last mode's MTTKRP kernel: re-capture
+    h->f64last = tol > 0.0;
+    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+    h->graph_ok = false;
+  }
   h->tol_host = tol;
   CKH(h, cudaMemcpyAsync(h->ws + h->off.misc + 8, &h->tol_host, sizeof(double), cudaMemcpyHostToDevice, h->stream));
   int it = 0;
@@ -1997,6 +2045,33 @@ jkcals_status jkcals_get_aligned_stats(jkcals_t h, int model, int mode, double* 
 jkcals_status jkcals_get_local_moments(jkcals_t h, int mode, double* count, double* mean, double* m2) {
   if (h && h->nmodels != 1) return fail(h, JKCALS_E_ARG, "pooled handle: use jkcals_get_model_moments");
   return jkcals_get_model_moments(h, 0, mode, count, mean, m2);
+}
+
+jkcals_status jkcals_merge_moments(int nparts, int64_t n, const double* counts, const double* means,
+                                   const double* m2s, double* count, double* mean, double* m2) {
+  if (nparts < 1 || n < 0 || !counts || !means || !m2s || !count || !mean || !m2) return JKCALS_E_ARG;
+  for (int64_t e = 0; e < n; ++e) {
+    double na = 0.0, ma = 0.0, sa = 0.0;
+    for (int k = 0; k < nparts; ++k) {
+      const double nb = counts[(int64_t)k * n + e];
+      if (!(nb > 0.0)) continue;
+      const double mb = means[(int64_t)k * n + e], sb = m2s[(int64_t)k * n + e];
+      if (na == 0.0) {
+        na = nb;
+        ma = mb;
+        sa = sb;
+        continue;
+      }
+      const double nn = na + nb, d = mb - ma, wb = nb / nn;
+      ma = ma + d * wb;
+      sa = sa + sb + d * d * na * wb;
+      na = nn;
+    }
+    count[e] = na;
+    mean[e] = ma;
+    m2[e] = sa;
+  }
+  return JKCALS_OK;
 }
 
 jkcals_status jkcals_get_jackknife_stats(jkcals_t h, int mode, double* mean, double* std_out) {

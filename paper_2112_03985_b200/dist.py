@@ -20,22 +20,15 @@ def shard(I0, world, rank):
 
 
 def chan_merge(count_a, mean_a, m2_a, count_b, mean_b, m2_b):
-    """Merge two moment sets (Chan, Golub, LeVeque 1979): exact for any split."""
-    n = count_a + count_b
-    with np.errstate(invalid="ignore", divide="ignore"):
-        delta = mean_b - mean_a
-        wb = np.where(n > 0, count_b / np.where(n > 0, n, 1), 0.0)
-        mean = mean_a + delta * wb
-        m2 = m2_a + m2_b + delta * delta * count_a * wb
-    return n, mean, m2
+    """Merge two moment sets (Chan, Golub, LeVeque 1979; exact for any split) -- the library's
+    jkcals_merge_moments (C ABI)."""
+    return merge_moments([(count_a, mean_a, m2_a), (count_b, mean_b, m2_b)])
 
 
 def merge_moments(parts):
-    """Fold a list of (count, mean, M2) in rank order."""
-    c, m, s = parts[0]
-    for cb, mb, sb in parts[1:]:
-        c, m, s = chan_merge(c, m, s, cb, mb, sb)
-    return c, m, s
+    """Fold a list of (count, mean, M2) in rank order (jkcals_merge_moments)."""
+    from .jkcals import merge_moments as _merge
+    return _merge(parts)
 
 
 def jackknife_std(count, m2):

@@ -37,9 +37,11 @@ def lib():
     """Load libjkcals.so (building it first if the sources are newer)."""
     global _lib
     if _lib is None:
-        path = _build.LIB
-        if _build.stale():
-            path = _build.build()
+        path = os.environ.get("JKCALS_LIB")  # dev A/B timing of another build of the same ABI
+        if not path:
+            path = _build.LIB
+            if _build.stale():
+                path = _build.build()
         L = ctypes.CDLL(path)
         P, I, I64, D, SZ = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_size_t
         sigs = {
@@ -84,6 +86,7 @@ def lib():
             "jkcals_mttkrp_i8_scratch_bytes": (SZ, [I, P, I, I64, I]),
             "jkcals_mttkrp_i8": (I, [I, P, I, P, P, I64, I64, P, I64, P, SZ, P]),
             "jkcals_krp": (I, [I, P, I, P, I64, I64, P, I64, P]),
+            "jkcals_merge_moments": (I, [I, I64, P, P, P, P, P, P]),
         }
         for name, (res, args) in sigs.items():
             fn = getattr(L, name)
@@ -103,7 +106,7 @@ EXPORTED = [
     "jkcals_get_factors", "jkcals_get_all_factors", "jkcals_get_block", "jkcals_get_status", "jkcals_get_history", "jkcals_get_jackknife_stats",
     "jkcals_get_local_moments", "jkcals_set_instrument", "jkcals_get_kernel_times", "jkcals_sweep_flops",
     "jkcals_launches_per_sweep", "jkcals_last_error", "jkcals_destroy", "jkcals_mttkrp_scratch_bytes",
-    "jkcals_mttkrp", "jkcals_krp",
+    "jkcals_mttkrp", "jkcals_krp", "jkcals_merge_moments",
 ]
 
 
@@ -461,6 +464,20 @@ def mttkrp_i8(T_flat, dims, n, U, C):
     if st != 0:
         raise JKCalsError(st, "jkcals_mttkrp_i8 failed")
     return M
+
+
+def merge_moments(parts):
+    """Fold per-shard (count, mean, M2) arrays in part order with the library's Chan merge
+    (jkcals_merge_moments; host computation, no GPU needed). Returns (count, mean, M2)."""
+    shape = np.shape(parts[0][1])
+    cs, ms, ss = (np.ascontiguousarray(np.stack([np.ravel(np.asarray(p[i], dtype=np.float64), order="F")
+                                                 for p in parts])) for i in range(3))
+    n = cs.shape[1]
+    c, m, s = np.zeros(n), np.zeros(n), np.zeros(n)
+    st = lib().jkcals_merge_moments(len(parts), n, _p(cs), _p(ms), _p(ss), _p(c), _p(m), _p(s))
+    if st != 0:
+        raise JKCalsError(st, "jkcals_merge_moments failed")
+    return tuple(np.reshape(x, shape, order="F") for x in (c, m, s))
 
 
 def krp(dims, n, U, C, out=None):

@@ -312,6 +312,38 @@ def test_fp32_path_vs_oracle(name, ps):
     check32(h, res, p_list)
 
 
+@pytest.mark.parametrize("name,ps,max_iters", [("syn50_r3", None, 1000), ("4way", [0, 57], 60)])
+def test_fp32_tol_mode_vs_oracle(name, ps, max_iters):
+    """FP32 path in tol mode (the paper's tol = 1e-6): the last mode runs on the
+    FP64 kernel (reading A24), so the error history is FP64-accurate for the FP32-path model and
+    the stop decisions match the FP64 oracle's; factors within the FP32 bar."""
+    from paper_2112_03985_b200 import JKCals
+    from paper_2112_03985_b200.jkcals import FP32
+    w = make_workload(name)
+    p_list = list(range(w.dims[0])) if ps is None else ps
+    h = JKCals(w.T, w.R, hist_cap=max_iters, precision=FP32)
+    h.set_init(w.P)
+    h.iterate(max_iters, 1e-6)
+    res = O.jk_als(w.T, w.P, p_list=p_list, max_iters=max_iters, tol=1e-6, nthreads=NCPU)
+    st = h.status()
+    same = 0
+    for q, p in enumerate(p_list):
+        it_g, it_o = int(st["iters"][p]), int(res.iters[q])
+        assert abs(it_g - it_o) <= 1, (p, it_g, it_o)  # the stop rule may flip at the threshold
+        same += it_g == it_o
+        hg, ho = h.history(p), res.history(q)
+        k = min(len(hg), len(ho))
+        # FP64-accurate errors of a model that is FP32-close to the oracle's (r01, all-FP32: 31 %)
+        assert np.all(np.abs(hg[:k] - ho[:k]) <= 1e-3 * np.abs(ho[:k])), (p, np.abs(hg[:k] / ho[:k] - 1).max())
+        if it_g == it_o:
+            fac, lam = h.factors(p)
+            for a_, b_ in zip(fac, res.factors[q]):
+                assert rel(a_, b_) <= FTOL32, (p, rel(a_, b_))
+    assert same >= 0.9 * len(p_list), (same, len(p_list))
+    if ps is None:
+        assert len(set(res.iters.tolist())) > 1
+
+
 @pytest.mark.parametrize("dims,C", [((10, 8, 6), 20), ((37, 23, 11), 129), ((13, 7, 5, 3), 70),
                                     ((50, 50, 50), 250), ((5, 300, 4), 10),
                                     # I_q0 = 90 / 70 / 96 end inside the first half of the last K64 step
