@@ -31,7 +31,8 @@ UNITS = [("jkcals.cu", [], "jkcals"),
          ("k_dmma.cu", ["-DJK_KMAJOR=1"], "k_dmma_km1"),
          ("k_tf32.cu", [], "k_tf32"),
          ("k_i8.cu", [], "k_i8"),
-         ("k_large.cu", [], "k_large")]
+         ("k_large.cu", [], "k_large"),
+         ("k_resident.cu", [], "k_resident")]
 UNITS += [("k_epi.cu", [f"-DJK_RMAX={r}"], f"k_epi_r{r}") for r in (2, 4, 6, 8, 10, 12, 16)]
 
 

@@ -646,7 +646,7 @@ bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_c
   o->asrc = L.take(nsub * N * 8);
   o->asld = L.take(nsub * N * 8);
   o->srcpg = L.take(nsub * 8);
-  o->misc = L.take(256);  // [0] normT2 (double), [8] tol (double), [16] active_count (int)
+  o->misc = L.take(256);  // [0] normT2 (double), [8] tol (double), [16] active_count (int), [24] sweeps (int)
   o->total = L.off + kAlign;  // slack for re-alignment of the caller's pointer
   return true;
 }
@@ -714,6 +714,13 @@ struct jkcals_s {
   bool red64 = false;
   std::vector<char> table64;
   std::vector<TileInfo> table164;
+  // small tensors: the whole iterate as one cluster-resident launch (resident.cuh)
+  struct {
+    bool on = false, dirty = true;
+    int cs = 1, Q = 1, kpc = 1, Cp = 4, slab = 1, rclass = 2;
+    size_t smem = 0;
+    ResArgs a;
+  } res;
   int i8 = 0;                          // precision JKCALS_FP64_I8: INT8-sliced FP64-accurate MTTKRP
   I8Plan i8q[kMaxModes];
   CUtensorMap tmA8[kMaxModes], tmB8[kMaxModes];
@@ -777,6 +784,7 @@ struct DeviceGuard {
 
 jkcals_status replan(jkcals_t h) {
   NvtxRange nv("jkcals replan");
+  h->res.dirty = true;
   for (int n = 0; n < h->N; ++n) {
     if (h->i8) {
       h->i8q[n] = make_i8_plan(h->N, h->dims, n, h->C, *h->ki);
@@ -1630,6 +1638,189 @@ jkcals_status jkcals_set_init_all(jkcals_t h, int mode, const double* U) {
   return JKCALS_OK;
 }
 
+// ------------------------------------------------------------ resident whole-iterate path
+// Shared-memory layout of one resident CTA for cluster size cs and Cp fused columns per group
+// (fills the offsets / pitches of `a`); returns the dynamic bytes.
+static size_t res_layout(const jkcals_s* h, int cs, int Cp, int kpc, ResArgs* a) {
+  const int N = h->N, last = N - 1, R = h->R;
+  // T strides: mode 0 contiguous, every other stride = 4 mod 16 doubles (conflict-free DMMA
+  // fragment loads of 4 k x 8 rows, resident.cuh)
+  int64_t pitch = 1;
+  for (int m = 0; m < N; ++m) {
+    a->pitch[m] = (int)pitch;
+    pitch = pitch * h->dims[m];
+    pitch = rup(pitch - 4, 16) + 4;
+  }
+  const int slab = (int)cdiv(h->dims[last], cs);
+  const int Cpi = res_cpitch(Cp);
+  a->Cpi = Cpi;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = (size_t)rup((int64_t)(off + bytes), 16);
+    return (int)o;
+  };
+  a->o_T = take((size_t)slab * a->pitch[last] * 8);
+  for (int m = 0; m < N; ++m) a->o_U[m] = take((size_t)h->dims[m] * Cpi * 8);
+  size_t mbytes = 0;
+  int64_t maxI = 0;
+  for (int n = 0; n < N; ++n) {
+    const int rows = n == last ? slab : (int)h->dims[n];
+    const int KG = kResWarps / res_tgroups(rows);
+    mbytes = std::max(mbytes, (size_t)KG * rows * Cpi * 8);
+    maxI = std::max<int64_t>(maxI, h->dims[n]);
+  }
+  a->o_M = take(mbytes);
+  a->o_E = take((size_t)cdiv(kpc, cs) * 2 * maxI * (R | 1) * 8);  // per owned slot
+  a->o_G = take((size_t)cdiv(kpc, cs) * N * R * R * 8);
+  a->o_X = take((size_t)kpc * 4);
+  a->o_S = take(sizeof(ResScr));
+  return off;
+}
+
+// choose the cluster size / grouping (or decide the standard path); sets h->res
+static void res_plan(jkcals_t h) {
+  h->res.dirty = false;
+  h->res.on = false;
+  const char* env = getenv("JKCALS_RESIDENT");  // "0": never; "1": whenever it fits; unset: small tensors
+  const int mode = env ? atoi(env) : -1;
+  if (mode == 0 || h->tf32 || h->i8 || h->mixed || h->R > 8 || h->K < 1) return;
+  double work = (double)h->C * (double)h->P;
+  if (mode < 0 && work > (double)(1 << 27)) return;  // large problems: the streamed path is efficient
+  const int N = h->N, last = N - 1;
+  for (int m = 0; m < N; ++m)
+    if (h->dims[m] > 4096) return;
+  const ResFn fn = resident_kernel(h->R);
+  double best = 1e300;
+  for (int cs : {1, 2, 4, 8, 16}) {
+    const int slab = (int)cdiv(h->dims[last], cs);
+    if ((int64_t)(cs - 1) * slab >= h->dims[last]) continue;  // every CTA holds a non-empty slab
+    // size with one submodel per group, then regroup by how many clusters of this size fit at
+    // once (groups are independent: clusters need not all be resident, but a second wave doubles time)
+    ResArgs a = {};
+    int kpc = 1;
+    int Cp = (int)rup((int64_t)kpc * h->R, 8);
+    size_t smem = res_layout(h, cs, Cp, kpc, &a);
+    if (smem > 200 * 1024) continue;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(226 * 1024)) != cudaSuccess ||
+        (cs > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
+      cudaGetLastError();
+      continue;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(cs * std::max(1, h->ki->nsm / cs));
+    cfg.blockDim = dim3(kResThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int qmax = 0;
+    if (cudaOccupancyMaxActiveClusters(&qmax, fn, &cfg) != cudaSuccess || qmax < 1) {
+      cudaGetLastError();
+      continue;
+    }
+    const int Q0 = std::min(h->K, qmax);
+    kpc = (int)cdiv(h->K, Q0);
+    Cp = (int)rup((int64_t)kpc * h->R, 8);
+    if (Cp > kResMaxCp || cdiv(kpc, cs) > kResMaxOwn) continue;
+    smem = res_layout(h, cs, Cp, kpc, &a);
+    if (smem > 226 * 1024) continue;
+    // per-CTA MTTKRP work ~ slab x Cp; a cluster adds DSMEM gathers and barriers
+    const double cost = (double)slab * Cp * (double)(h->P / h->dims[last]) / 1e4 + (cs > 1 ? 2.0 : 0.0) +
+                        0.5 * (double)cdiv(kpc, cs);
+    // automatic use only where r02 measured a win over the streamed path: groups of <= 8 fused
+    // columns over a multi-CTA cluster (syn50 R1-R2: 33-37 vs 39-43 us per sweep); tiny was even
+    // (18.8 vs 18.6) and wider groups slower (syn50 R3-R5) -- JKCALS_RESIDENT=1 forces it
+    if (mode < 0 && (Cp > 8 || cs < 2)) continue;
+    if (cost < best) {
+      best = cost;
+      h->res.on = true;
+      h->res.cs = cs;
+      h->res.kpc = kpc;
+      h->res.Q = (int)cdiv(h->K, kpc);
+      h->res.Cp = Cp;
+      h->res.slab = slab;
+      h->res.smem = smem;
+      h->res.rclass = h->R <= 2 ? 2 : h->R <= 4 ? 4 : 8;
+      h->res.a = a;
+    }
+  }
+  if (h->res.on)
+    cudaFuncSetAttribute(resident_kernel(h->res.rclass), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)h->res.smem);
+}
+
+static jkcals_status res_launch(jkcals_t h, int max_iters) {
+  ResArgs a = h->res.a;
+  a.N = h->N;
+  a.R = h->R;
+  a.cs = h->res.cs;
+  a.kpc = h->res.kpc;
+  a.Cp = h->res.Cp;
+  a.Cpi = res_cpitch(h->res.Cp);
+  a.slab = h->res.slab;
+  a.d = (int)h->d;
+  a.hist_cap = h->hist_cap;
+  a.max_iters = max_iters;
+  a.nsub = h->nsub;
+  a.K = h->K;
+  for (int m = 0; m < h->N; ++m) {
+    a.dims[m] = (int)h->dims[m];
+    a.U[m] = h->U(m);
+  }
+  a.gst[0] = 1;
+  a.gst[1] = h->I0p;
+  for (int m = 2; m < h->N; ++m) a.gst[m] = a.gst[m - 1] * h->dims[m - 1];
+  a.ldu = h->ldu;
+  a.T = h->ptr<double>(h->off.T);
+  a.blk2sub = h->ptr<int>(h->off.blk2sub);
+  a.pglob = h->ptr<int64_t>(h->off.pglob);
+  a.gram = h->ptr<double>(h->off.gram);
+  a.lambda = h->ptr<double>(h->off.lambda);
+  a.normT2p = h->ptr<double>(h->off.normT2p);
+  a.fit = h->ptr<double>(h->off.fit);
+  a.fit_prev = h->ptr<double>(h->off.fit_prev);
+  a.err = h->ptr<double>(h->off.err);
+  a.iters = h->ptr<int>(h->off.iters);
+  a.flags = h->ptr<int>(h->off.flags);
+  a.active = h->ptr<int>(h->off.active);
+  a.hist = h->ptr<double>(h->off.hist);
+  a.tol = reinterpret_cast<const double*>(h->ws + h->off.misc + 8);
+  a.sweeps_out = reinterpret_cast<int*>(h->ws + h->off.misc + 24);
+#ifdef JK_RES_PROF
+  a.prof = reinterpret_cast<long long*>(h->ws + h->off.misc + 64);  // 8 counters (dev builds)
+#endif
+  CKH(h, cudaMemsetAsync(a.sweeps_out, 0, sizeof(int), h->stream));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = h->res.cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(h->res.Q * h->res.cs);
+  cfg.blockDim = dim3(kResThreads);
+  cfg.dynamicSmemBytes = h->res.smem;
+  cfg.stream = h->stream;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (h->instrument) CKH(h, cudaEventRecord(h->ev[0], h->stream));
+  CKH(h, cudaLaunchKernelEx(&cfg, resident_kernel(h->res.rclass), a));
+  if (h->instrument) {
+    CKH(h, cudaEventRecord(h->ev[1], h->stream));
+    CKH(h, cudaEventSynchronize(h->ev[1]));
+    float ms = 0;
+    CKH(h, cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
+    h->t_mttkrp[0] += ms;  // the whole launch (MTTKRP and updates are fused)
+    h->launches += 1;
+  }
+  CKH(h, cudaMemcpyAsync(h->pinned_count, a.sweeps_out, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  return JKCALS_OK;
+}
+
 jkcals_status jkcals_iterate(jkcals_t h, int max_iters, double tol, int* sweeps_done) {
   NvtxRange nv("jkcals_iterate");
   if (!h || max_iters < 0) return JKCALS_E_ARG;
@@ -1645,6 +1836,15 @@ jkcals_status jkcals_iterate(jkcals_t h, int max_iters, double tol, int* sweeps_
   }
   h->tol_host = tol;
   CKH(h, cudaMemcpyAsync(h->ws + h->off.misc + 8, &h->tol_host, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  if (h->res.dirty) res_plan(h);
+  if (h->res.on && max_iters > 0 && h->K > 0) {  // one launch runs every sweep (device-side stop)
+    jkcals_status st = res_launch(h, max_iters);
+    if (st != JKCALS_OK) return st;
+    CKH(h, cudaStreamSynchronize(h->stream));
+    if (sweeps_done) *sweeps_done = *h->pinned_count;
+    h->ran = true;
+    return JKCALS_OK;
+  }
   int it = 0;
   for (; it < max_iters && h->K > 0; ++it) {
     if (h->instrument) {
@@ -2263,6 +2463,13 @@ int jkcals_launches_per_sweep(jkcals_t h) {
   for (int n = 0; n < h->N; ++n) n_red += h->red_on[n] ? 1 : 0;
   return 2 * h->N + n_red + (h->i8 ? 2 * h->N : 0);  // (+ the two U_q0-digit kernels per mode)
 }
+
+#ifdef JK_RES_PROF
+int jkcals_dev_res_prof(jkcals_t h, long long* out) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpy(out, h->ws + h->off.misc + 64, 64, cudaMemcpyDeviceToHost);
+}
+#endif
 
 const char* jkcals_last_error(jkcals_t h) { return h ? h->err.c_str() : "null handle"; }
 

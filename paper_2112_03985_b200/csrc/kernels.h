@@ -12,6 +12,7 @@
 #include "mttkrp.cuh"
 #include "mttkrp_i8.cuh"
 #include "mttkrp_tf32.cuh"
+#include "resident.cuh"
 
 namespace jk {
 
@@ -45,5 +46,9 @@ EpiFns epi_kernels_16();
 typedef void (*GramLargeFn)(const double*, int, int64_t, int, const int*, const int*, const int*, int, int, double*);
 EpiFn epi_large_kernel();
 GramLargeFn gram_large_kernel_fn();
+
+// k_resident.cu: the cluster-resident whole-iterate kernel for small tensors (resident.cuh)
+typedef void (*ResFn)(ResArgs);
+ResFn resident_kernel(int rclass);  // rank class: 2, 4 or 8
 
 }  // namespace jk

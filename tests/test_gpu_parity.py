@@ -251,7 +251,8 @@ def test_pinv_fallback_is_per_submodel():
         assert rel(a, b) <= 1e-9
 
 
-def test_deterministic_and_graph_equals_eager():
+def test_deterministic_and_graph_equals_eager(monkeypatch):
+    monkeypatch.setenv("JKCALS_RESIDENT", "0")  # the streamed path (graph replay vs eager launches)
     w = make_workload("syn50_r2")
     h1, _ = run_gpu(w, 15)
     h2, _ = run_gpu(w, 15)
