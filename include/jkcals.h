@@ -61,10 +61,17 @@ typedef enum {
 } jkcals_status;
 
 /* JKCALS_FP64_I8 (experimental): FP64 factors and epilogue, the MTTKRP from INT8
- * tcgen05 MMAs on 7-digit operand slices with exact integer accumulation (FP64-accurate, held to
- * the FP64 parity bar). Requires dims[0], dims[1] <= 65536 (padded to 64: exact int32 sums);
- * otherwise creation fails with JKCALS_E_ARG. Extra workspace: the T digits of every mode
- * (7 x prod(dims) bytes per mode, padded). */
+ * tcgen05 MMAs on 7 balanced base-128 digits per operand with exact integer accumulation. Each
+ * (row i, slow index j') slab of T_(n) and each column c of U_q0 carries its own power-of-two scale,
+ * so an operand keeps 49 bits relative to its SLAB's / COLUMN's largest magnitude and the error is
+ * per-slab normwise, not elementwise as in FP64:
+ *   |M - M_exact|(i, c) <~ 2^-47 sum_j' max_k |T(i, k, j')| sum_k |U_q0(k, c)| |S_j'(c)|.
+ * Rows of any scale are exact to FP64 level; an entry 2^b above the rest of its slab costs those
+ * entries b bits (a 1e5 scatter spike: ~1e-9 factor drift vs 1e-13 in FP64; tests/
+ * test_gpu_parity.py::test_int8_sliced_*_wide_dynamic_range). A non-finite U_q0 column yields NaN
+ * in M, as in FP64. Requires dims[0], dims[1] <= 65536 (padded to 64: exact int32 sums); otherwise
+ * creation fails with JKCALS_E_ARG. Extra workspace: the T digits of every mode (7 x prod(dims)
+ * bytes per mode, padded) and one int8 slab exponent per (i, j'). */
 /* JKCALS_FP32 (north_star's "optional FP32 path", parity bar 1e-4): the MTTKRP in 3xTF32 on the
  * tcgen05 tensor cores (FP32-accurate), the epilogue in FP64. The error e is a difference of
  * O(||T||^2) terms, so an FP32-accurate M makes it unusable for a convergence test (r01: up to

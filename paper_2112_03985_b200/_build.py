@@ -65,6 +65,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)
         os.replace(LIB + ".tmp", LIB)
+        for o in objs:  # objects are not reused (every build is full); keep the snapshot small
+            os.remove(o)
     return LIB
 
 

@@ -39,9 +39,9 @@ inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
 
 // ---------------------------------------------------------------- kernel dispatch tables
 struct KernelInfo {
-  MttkrpFn fn[2][2][kMaxNT];         // [KMAJOR][STAGES==4][NT-1]
-  SmemFn smem[2][2][kMaxNT];
-  int occ[2][2][kMaxNT][kMaxModes];  // [..][nslow]
+  MttkrpFn fn[kNumWM][2][2][kMaxNT];         // [tile width kWMs][KMAJOR][STAGES==4][NT-1]
+  SmemFn smem[kNumWM][2][2][kMaxNT];
+  int occ[kNumWM][2][2][kMaxNT][kMaxModes];  // [..][nslow]
   int nsm;
   int i8clusters;                    // co-resident 2-CTA clusters of the INT8 cluster kernel (0: none)
 };
@@ -52,8 +52,19 @@ KernelInfo* kernel_info(int device, std::string* err) {
   if (device < 0 || device >= 16) return nullptr;
   if (ready[device]) return &info[device];
   KernelInfo& ki = info[device];
-  dmma_kernels_km0(ki.fn[0], ki.smem[0]);
-  dmma_kernels_km1(ki.fn[1], ki.smem[1]);
+  {
+    MttkrpFn f[2][kNumWM][2][kMaxNT];
+    SmemFn sm[2][kNumWM][2][kMaxNT];
+    dmma_kernels_km0(f[0], sm[0]);
+    dmma_kernels_km1(f[1], sm[1]);
+    for (int wv = 0; wv < kNumWM; ++wv)
+      for (int km = 0; km < 2; ++km)
+        for (int st = 0; st < 2; ++st)
+          for (int t = 0; t < kMaxNT; ++t) {
+            ki.fn[wv][km][st][t] = f[km][wv][st][t];
+            ki.smem[wv][km][st][t] = sm[km][wv][st][t];
+          }
+  }
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
@@ -101,23 +112,24 @@ KernelInfo* kernel_info(int device, std::string* err) {
       return nullptr;
     }
   }
-  for (int km = 0; km < 2; ++km)
-    for (int st = 0; st < 2; ++st)
-      for (int t = 0; t < kMaxNT; ++t) {
-        cudaError_t e = cudaFuncSetAttribute(ki.fn[km][st][t], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)ki.smem[km][st][t](kMaxModes - 2));
-        if (e != cudaSuccess) {
-          if (err) *err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e);
-          cudaSetDevice(prev);
-          return nullptr;
+  for (int wv = 0; wv < kNumWM; ++wv)
+    for (int km = 0; km < 2; ++km)
+      for (int st = 0; st < 2; ++st)
+        for (int t = 0; t < kMaxNT; ++t) {
+          cudaError_t e = cudaFuncSetAttribute(ki.fn[wv][km][st][t], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)ki.smem[wv][km][st][t](kMaxModes - 2));
+          if (e != cudaSuccess) {
+            if (err) *err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e);
+            cudaSetDevice(prev);
+            return nullptr;
+          }
+          for (int ns = 1; ns <= kMaxModes - 2; ++ns) {
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ki.fn[wv][km][st][t], (kWMs[wv] + 1) * 32,
+                                                          ki.smem[wv][km][st][t](ns));
+            ki.occ[wv][km][st][t][ns] = std::max(1, occ);
+          }
         }
-        for (int ns = 1; ns <= kMaxModes - 2; ++ns) {
-          int occ = 0;
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ki.fn[km][st][t], (kWarps + 1) * 32,
-                                                        ki.smem[km][st][t](ns));
-          ki.occ[km][st][t][ns] = std::max(1, occ);
-        }
-      }
   cudaSetDevice(prev);
   ready[device] = true;
   return &ki;
@@ -144,6 +156,7 @@ ModeGeo mode_geo(int N, const int64_t* dims, int n) {
 
 struct ModePlan {
   int NT = 1, KM = 0, ST4 = 1, BN = 8, nMt = 1, nNt = 1, KT = 1, G = 1;
+  int WV = 0, BM = kBM;  // FP64 kernel tile width: kWMs[WV] consumer warps x 16 = BM fused columns
   int64_t units = 1;
   int ntiles = 1, npieces = 1;
   size_t smem = 0;
@@ -168,9 +181,9 @@ void finish_plan(ModePlan& p, const ModeGeo& mg, int64_t C = 0, double alpha = 1
     std::vector<double> w(p.ntiles), cum(p.ntiles + 1, 0.0);
     for (int t = 0; t < p.ntiles; ++t) {
       const int tm = t % p.nMt, tn = t / p.nMt;
-      const int64_t lc = std::min<int64_t>(kBM, C - (int64_t)tm * kBM);
+      const int64_t lc = std::min<int64_t>(p.BM, C - (int64_t)tm * p.BM);
       const int64_t lr = std::min<int64_t>(p.BN, mg.In - (int64_t)tn * p.BN);
-      const double f = (double)rup(lc, 16) / kBM * (double)rup(lr, 8) / p.BN;
+      const double f = (double)rup(lc, 16) / p.BM * (double)rup(lr, 8) / p.BN;
       w[t] = alpha + (1.0 - alpha) * f;
       cum[t + 1] = cum[t] + w[t] * p.KT;
     }
@@ -247,7 +260,7 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
     // variants that fit 2 CTAs/SM (<= 96 regs: NT <= 6) hide the per-k-tile latency better:
     // measured +7 % on syn200 (r01), modelled as a 1.08 factor
     const int km = (n != 0) ? 1 : 0, st4 = (mg.Jp >= 3) ? 1 : 0;
-    const double occ_bonus = ki.occ[km][st4][nt - 1][mg.nslow] >= 2 ? 1.08 : 1.0;
+    const double occ_bonus = ki.occ[0][km][st4][nt - 1][mg.nslow] >= 2 ? 1.08 : 1.0;
     const double score = (double)nI8 / (double)(ntiles_n * nt) * (double)nt / (nt + 1.0) * occ_bonus;
     if (score > best + 1e-12) {
       best = score;
@@ -271,12 +284,36 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
   p.BN = p.NT * 8;
   p.KM = (n != 0) ? 1 : 0;
   p.ST4 = (mg.Jp >= 3) ? 1 : 0;  // the U_q0 slab double buffer needs J' >= STAGES - 1
-  p.nMt = (int)std::max<int64_t>(1, cdiv(C, kBM));
+  // tile width: kWMs[wv] consumer warps x 16 columns. Cost model (warp-k-tiles per k-tile row):
+  // a tile with w live warps costs max(w, 0.7 WM) -- the per-k-tile fixed share, r01's alpha --
+  // so a mostly idle last tile is charged 70 % of a full one. 4-way C = 400: 8 warps -> 3 full +
+  // 1 one-warp tile = 29.6; 5 warps -> 5 full 80-column tiles = 25 / 0.90 (r02: 370 vs 393 us on
+  // modes 1-2). The wider tile is kept unless the narrower one is >= 3 % cheaper.
+  // JKCALS_FORCE_WM=<8|5> overrides (tuning).
+  {
+    double cost[kNumWM];
+    for (int wv = 0; wv < kNumWM; ++wv) {
+      const int WM = kWMs[wv], BM = WM * 16;
+      const int64_t tiles = std::max<int64_t>(1, cdiv(C, BM));
+      const int64_t w_last = cdiv(C - (tiles - 1) * BM, 16);
+      cost[wv] = (double)(tiles - 1) * WM + std::max((double)w_last, 0.7 * WM);
+      // per-warp efficiency of the narrow tile relative to the wide one (r02 on B200): its
+      // per-k-tile fixed work is shared by fewer warps -- 0.90 with NT >= 6 n8 tiles (4-way modes
+      // 0-2), 0.75 below (syn200 NT = 5: 23.2 vs 30.7 TF/s; 4-way mode 3, NT = 4, slower too)
+      if (WM < kWMs[0]) cost[wv] /= (p.NT >= 6 ? 0.90 : 0.75);
+    }
+    p.WV = (cost[1] < 0.97 * cost[0]) ? 1 : 0;
+    static int force_wm = [] { const char* e = getenv("JKCALS_FORCE_WM"); return e ? atoi(e) : 0; }();
+    for (int wv = 0; wv < kNumWM; ++wv)
+      if (force_wm == kWMs[wv]) p.WV = wv;
+    p.BM = kWMs[p.WV] * 16;
+  }
+  p.nMt = (int)std::max<int64_t>(1, cdiv(C, p.BM));
   p.KT = (int)(cdiv(mg.Iq0, kBK) * mg.Jp);
   p.ntiles = p.nMt * p.nNt;
   p.units = (int64_t)p.ntiles * p.KT;
-  p.smem = ki.smem[p.KM][p.ST4][p.NT - 1](mg.nslow);
-  int64_t gmax = (int64_t)ki.nsm * ki.occ[p.KM][p.ST4][p.NT - 1][mg.nslow];
+  p.smem = ki.smem[p.WV][p.KM][p.ST4][p.NT - 1](mg.nslow);
+  int64_t gmax = (int64_t)ki.nsm * ki.occ[p.WV][p.KM][p.ST4][p.NT - 1][mg.nslow];
   // at most kMaxPieces partial pieces per output tile: small problems (few tiles) would
   // otherwise write and re-read a BN x BM piece per CTA for ~1 k-tile of work each
   // (only for < 4 tiles: a single 128-column M tile x 5 N tiles -- a syn200 shard at 8 GPUs --
@@ -288,7 +325,7 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
   // has 16 of 128 columns): r01 measured alpha = 0.7 +6 % there, while nearly-full ragged tiles
   // (syn200: 104 of 128) are best with the uniform split. JKCALS_SK_ALPHA overrides (tuning).
   static double env_alpha = [] { const char* e = getenv("JKCALS_SK_ALPHA"); return e ? atof(e) : -1.0; }();
-  const double live_m = (double)rup(C - (int64_t)(p.nMt - 1) * kBM, 16) / kBM;
+  const double live_m = (double)rup(C - (int64_t)(p.nMt - 1) * p.BM, 16) / p.BM;
   const double alpha = env_alpha >= 0.0 ? env_alpha : (live_m < 0.5 ? 0.7 : 1.0);
   finish_plan(p, mg, C, alpha);
   return p;
@@ -296,7 +333,7 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
 
 constexpr int kRedPieces = 16;  // pre-reduce when a tile has more partial pieces than this
 
-int64_t plan_parts_doubles(const ModePlan& p) { return (int64_t)p.npieces * p.BN * kBM; }
+int64_t plan_parts_doubles(const ModePlan& p) { return (int64_t)p.npieces * p.BN * p.BM; }
 
 // device plan table: TileInfo[ntiles] followed by int cta_u[G+1] (read by the kernel)
 size_t plan_table_bytes(int ntiles, int G) { return ntiles * sizeof(TileInfo) + (size_t)(G + 1) * sizeof(int); }
@@ -312,8 +349,9 @@ void plan_bounds(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, int6
                  bool tf32 = false) {
   ModePlan p = make_plan(mg, n, C, ki, tf32);
   // any later (compacted, smaller-C) plan has G <= 8 nsm CTAs and <= ntiles tiles
-  *parts = (int64_t)(std::max<int64_t>(p.G, 8 * (int64_t)ki.nsm) + p.ntiles) * p.BN * kBM;
-  *tiles = p.ntiles;
+  // (x kBM: the widest tile; a narrower-tile plan has more tiles, bounded by nMt(80) <= 2 nMt(128))
+  *parts = (int64_t)(std::max<int64_t>(p.G, 8 * (int64_t)ki.nsm) + 2 * p.ntiles) * p.BN * kBM;
+  *tiles = 2 * p.ntiles;
 }
 
 MttkrpView make_mview(int N, const int64_t* dims, int n, const double* const* Uall) {
@@ -410,11 +448,11 @@ bool make_tmap_T32(CUtensorMap* tm, const float* T, const int64_t gdim_in[4], co
   return r == CUDA_SUCCESS;
 }
 
-bool make_tmap_U(CUtensorMap* tm, const double* U, int64_t rows, int64_t ldu) {
+bool make_tmap_U(CUtensorMap* tm, const double* U, int64_t rows, int64_t ldu, int bmp = kBMP) {
   auto enc = encode_fn();
   if (!enc) return false;
   cuuint64_t gdim[2] = {(cuuint64_t)ldu, (cuuint64_t)rows}, gstr[1] = {(cuuint64_t)ldu * 8};
-  cuuint32_t box[2] = {(cuuint32_t)kBMP, (cuuint32_t)kBK}, est[2] = {1, 1};
+  cuuint32_t box[2] = {(cuuint32_t)bmp, (cuuint32_t)kBK}, est[2] = {1, 1};
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(U), gdim, gstr, box, est,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -527,7 +565,7 @@ struct Offsets {
       lambda, normT2p, fit, fit_prev, err, hist,
       slice, slice_part, stage, iters, flags, active, blk2sub, map, pglob, misc, srcoff, srcld, subR, subRc, blkcol,
       dstoff, pref[kMaxModes], aln, aperm, asign, acong, asrc, asld, srcpg;
-  size_t i8B[kMaxModes], i8eT[kMaxModes], i8A, i8eU, i8st, i8dims;  // INT8-sliced MTTKRP (§9b)
+  size_t i8B[kMaxModes], i8eT[kMaxModes], i8dS[kMaxModes], i8A, i8eU, i8st, i8dims;  // INT8-sliced MTTKRP (§9b)
   int64_t parts_cap;
   int tiles_cap;
   int slice_nb;
@@ -621,7 +659,7 @@ bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_c
   o->subRc = L.take(nsub * 4);
   o->blkcol = L.take(nsub * 4);
   o->dstoff = L.take(nsub * 8);
-  for (int k = 0; k < kMaxModes; ++k) o->i8B[k] = o->i8eT[k] = 0;
+  for (int k = 0; k < kMaxModes; ++k) o->i8B[k] = o->i8eT[k] = o->i8dS[k] = 0;
   o->i8A = o->i8eU = o->i8st = o->i8dims = 0;
   if (i8) {  // per-mode T digits (fixed) + the U_q0 digits of the mode being updated
     int64_t amax = 0, cpmax = 0;
@@ -629,6 +667,9 @@ bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_c
       const I8Plan q = make_i8_plan(N, dims, n, C, ki);
       o->i8B[n] = L.take((size_t)kI8S * q.Jp * q.InP * q.KP);
       o->i8eT[n] = L.take((size_t)q.InP * 4);
+      o->i8dS[n] = L.take((size_t)q.Jp * q.InP);
+      // (the slab exponents are formed at create in the pieces buffer: Jp x InP ints)
+      o->parts_cap = std::max<int64_t>(o->parts_cap, (int64_t)cdiv(q.Jp * q.InP * 4, 8));
       amax = std::max<int64_t>(amax, (int64_t)kI8S * q.CP * q.KP);
       cpmax = std::max<int64_t>(cpmax, q.CP);
     }
@@ -710,7 +751,7 @@ struct jkcals_s {
   // fit behind the convergence test are FP64-accurate (reading A24)
   bool f64last = false;
   ModePlan plan64;
-  CUtensorMap tmT64;
+  CUtensorMap tmT64, tmU64[2];  // its T view and U_q0 slab maps (box width = its tile width + 4)
   bool red64 = false;
   std::vector<char> table64;
   std::vector<TileInfo> table164;
@@ -826,7 +867,7 @@ jkcals_status replan(jkcals_t h) {
       return fail(h, JKCALS_E_CUDA, "cuTensorMapEncodeTiled failed for the tensor view of mode %d", n);
     const int q0 = (n == 0) ? 1 : 0;
     for (int set = 0; set < 2; ++set)
-      if (!make_tmap_U(&h->tmU[set][n], h->ptr<double>(h->off.U[set][q0]), h->dims[q0], h->ldu))
+      if (!make_tmap_U(&h->tmU[set][n], h->ptr<double>(h->off.U[set][q0]), h->dims[q0], h->ldu, p.BM + 4))
         return fail(h, JKCALS_E_CUDA, "cuTensorMapEncodeTiled failed for U_%d", q0);
     if (h->tf32) {
       int64_t gd[4], gs[3];
@@ -868,6 +909,9 @@ jkcals_status replan(jkcals_t h) {
                            cudaMemcpyHostToDevice, h->stream));
     if (!make_tmap_T(&h->tmT64, h->ptr<double>(h->off.T), h->N, h->dims, h->I0p, n, p.BN, bnp_of(p.NT)))
       return fail(h, JKCALS_E_CUDA, "cuTensorMapEncodeTiled failed for the FP64 view of mode %d", n);
+    for (int set = 0; set < 2; ++set)  // q0 = 0 for the last mode (N >= 3)
+      if (!make_tmap_U(&h->tmU64[set], h->ptr<double>(h->off.U[set][0]), h->dims[0], h->ldu, p.BM + 4))
+        return fail(h, JKCALS_E_CUDA, "cuTensorMapEncodeTiled failed for U_0 (FP64 last mode)");
   }
   CKH(h, cudaStreamSynchronize(h->stream));  // tinfo host vectors may change on the next replan
   if (h->gexec) {
@@ -970,6 +1014,7 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     ig.probe = getenv("JKCALS_I8_PROBE") ? atoi(getenv("JKCALS_I8_PROBE")) : 0;
 #endif
     ig.eT = h->ptr<int>(h->off.i8eT[n]);
+    ig.dS = h->ptr<int8_t>(h->off.i8dS[n]);
     ig.eU = eU;
     CKH(h, launch_i8(q, h->tmA8[n], h->tmB8[n], ig, ti, parts, h->es));
   } else if (h->tf32 && !f64) {
@@ -997,7 +1042,7 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     CKH(h, cudaLaunchKernelEx(&cfg, tf32_kernel(p.ST4), h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v, tg, ti,
                               parts));
   } else {
-    MttkrpFn fn = h->ki->fn[p.KM][p.ST4][p.NT - 1];
+    MttkrpFn fn = h->ki->fn[p.WV][p.KM][p.ST4][p.NT - 1];
     // programmatic dependent launch: this grid may start (prologue) while the previous kernel
     // drains; the kernel waits (griddepcontrol.wait) before touching its inputs
     cudaLaunchConfig_t cfg = {};
@@ -1005,19 +1050,20 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = (h->pdl && !timed) ? 1 : 0;
     cfg.gridDim = dim3(p.G);
-    cfg.blockDim = dim3((kWarps + 1) * 32);
+    cfg.blockDim = dim3((kWMs[p.WV] + 1) * 32);
     cfg.dynamicSmemBytes = p.smem;
     cfg.stream = h->es;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CKH(h, cudaLaunchKernelEx(&cfg, fn, f64 ? h->tmT64 : h->tmT[n], h->tmU[h->cur][n], v, g, ti, parts));
+    CKH(h, cudaLaunchKernelEx(&cfg, fn, f64 ? h->tmT64 : h->tmT[n], f64 ? h->tmU64[h->cur] : h->tmU[h->cur][n], v,
+                              g, ti, parts));
   }
   CKH(h, cudaGetLastError());
   if (timed) CKH(h, cudaEventRecord(h->ev[4 * n + 1], h->es));
   const double* epi_parts = parts;
   const TileInfo* epi_ti = ti;
   if (f64 ? h->red64 : h->red_on[n]) {  // pre-reduce the pieces across the whole GPU (PDL-chained)
-    const int tile_elems = p.BN * kBM;
+    const int tile_elems = p.BN * p.BM;
     const int64_t tot = (int64_t)p.ntiles * tile_elems;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
@@ -1048,7 +1094,7 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
   a.d = (int)h->d;
   a.parts = epi_parts;
   a.tinfo = epi_ti;
-  a.BM = kBM;
+  a.BM = p.BM;
   a.BN = p.BN;
   a.nMt = p.nMt;
   a.gram = h->ptr<double>(h->off.gram);
@@ -1497,12 +1543,14 @@ jkcals_status jkcals_create_config(jkcals_t* out, const jkcals_config* cfg, cons
     for (int n = 0; n < ndims; ++n) {
       const I8Plan q = make_i8_plan(ndims, dims, n, h->C, *ki);
       int* eT = h->ptr<int>(h->off.i8eT[n]);
-      CKH(h, cudaMemsetAsync(eT, 0, q.InP * 4, h->stream));
-      row_exp_t_kernel<<<(int)q.In, 256, 0, h->stream>>>(h->ptr<double>(h->off.T), ndims, st_d, dims_d, n,
-                                                          h->P / dims[n], eT);
+      int* eS = h->ptr<int>(h->off.parts);  // scratch: slab exponents of this mode
+      const int q0 = (n == 0) ? 1 : 0;
+      slab_exp_t_kernel<<<(int)cdiv(q.Jp * q.InP, 256), 256, 0, h->stream>>>(
+          h->ptr<double>(h->off.T), ndims, st_d, dims_d, n, q0, (int)q.In, (int)q.InP, (int)q.Iq0, q.Jp, eS);
+      row_ref_exp_kernel<<<(int)q.InP, 256, 0, h->stream>>>(eS, (int)q.InP, q.Jp, eT, h->ptr<int8_t>(h->off.i8dS[n]));
       slice_t_i8_kernel<<<(int)cdiv(q.Jp * q.InP * q.KP, 256), 256, 0, h->stream>>>(
-          h->ptr<double>(h->off.T), ndims, st_d, dims_d, n, (n == 0) ? 1 : 0, (int)q.In, (int)q.InP, (int)q.Iq0,
-          (int)q.KP, q.Jp, eT, h->ptr<int8_t>(h->off.i8B[n]));
+          h->ptr<double>(h->off.T), ndims, st_d, dims_d, n, q0, (int)q.In, (int)q.InP, (int)q.Iq0, (int)q.KP, q.Jp,
+          eS, h->ptr<int8_t>(h->off.i8B[n]));
       CKH(h, cudaGetLastError());
     }
     CKH(h, cudaStreamSynchronize(h->stream));  // stv / dv are host temporaries
@@ -2544,7 +2592,8 @@ jkcals_status jkcals_mttkrp(int ndims, const int64_t* dims, int n, const double*
   MttkrpView v = make_mview(ndims, dims, n, Up);
   CUtensorMap tmT, tmU;
   const int q0 = (n == 0) ? 1 : 0;
-  if (!make_tmap_T(&tmT, Tp, ndims, dims, I0p, n, p.BN, bnp_of(p.NT)) || !make_tmap_U(&tmU, Up[q0], dims[q0], ldp))
+  if (!make_tmap_T(&tmT, Tp, ndims, dims, I0p, n, p.BN, bnp_of(p.NT)) ||
+      !make_tmap_U(&tmU, Up[q0], dims[q0], ldp, p.BM + 4))
     return JKCALS_E_CUDA;
   MttkrpGeom g;
   g.C = (int)C;
@@ -2554,10 +2603,11 @@ jkcals_status jkcals_mttkrp(int ndims, const int64_t* dims, int n, const double*
   g.KT = p.KT;
   g.units = p.units;
   g.G = p.G;
-  ki->fn[p.KM][p.ST4][p.NT - 1]<<<p.G, (kWarps + 1) * 32, p.smem, s>>>(tmT, tmU, v, g, ti, parts);
+  ki->fn[p.WV][p.KM][p.ST4][p.NT - 1]<<<p.G, (kWMs[p.WV] + 1) * 32, p.smem, s>>>(tmT, tmU, v, g, ti, parts);
   if (cudaGetLastError() != cudaSuccess) return JKCALS_E_CUDA;
   int64_t tot = dims[n] * C;
-  reduce_parts_kernel<<<(int)cdiv(tot, 256), 256, 0, s>>>(parts, ti, (int)dims[n], (int)C, p.BN, p.nMt, M, ldm);
+  reduce_parts_kernel<<<(int)cdiv(tot, 256), 256, 0, s>>>(parts, ti, (int)dims[n], (int)C, p.BN, p.nMt, M, ldm,
+                                                          p.BM);
   if (cudaGetLastError() != cudaSuccess) return JKCALS_E_CUDA;
   // tinfo staging is pageable-host -> device: make sure the copy has consumed it
   if (cudaStreamSynchronize(s) != cudaSuccess) return JKCALS_E_CUDA;
@@ -2570,7 +2620,8 @@ struct I8Scratch {
   TileInfo* ti;
   double* parts;
   int8_t *A, *B;
-  int *eT, *eU, *dims_d;
+  int *eT, *eU, *dims_d, *eS;
+  int8_t* dS;
   int64_t* st_d;
   double* Up[kMaxModes];
   size_t total;
@@ -2589,6 +2640,8 @@ I8Scratch i8_layout(uintptr_t base0, int ndims, const int64_t* dims, const I8Pla
   x.A = reinterpret_cast<int8_t*>(take((size_t)kI8S * q.CP * q.KP));
   x.B = reinterpret_cast<int8_t*>(take((size_t)kI8S * q.Jp * q.InP * q.KP));
   x.eT = reinterpret_cast<int*>(take((size_t)q.InP * 4));
+  x.eS = reinterpret_cast<int*>(take((size_t)q.Jp * q.InP * 4));
+  x.dS = reinterpret_cast<int8_t*>(take((size_t)q.Jp * q.InP));
   x.eU = reinterpret_cast<int*>(take((size_t)q.CP * 4));
   x.dims_d = reinterpret_cast<int*>(take(kMaxModes * 4));
   x.st_d = reinterpret_cast<int64_t*>(take(kMaxModes * 8));
@@ -2639,11 +2692,12 @@ jkcals_status jkcals_mttkrp_i8(int ndims, const int64_t* dims, int n, const doub
       return JKCALS_E_CUDA;
   }
   // operands: T digits per mode-n row scale, U_q0 digits per column scale
-  if (cudaMemsetAsync(x.eT, 0, q.InP * 4, s) != cudaSuccess) return JKCALS_E_CUDA;
-  row_exp_t_kernel<<<(int)q.In, 256, 0, s>>>(T, ndims, x.st_d, x.dims_d, n, P / dims[n], x.eT);
+  slab_exp_t_kernel<<<(int)cdiv(q.Jp * q.InP, 256), 256, 0, s>>>(T, ndims, x.st_d, x.dims_d, n, q0, (int)q.In,
+                                                                (int)q.InP, (int)q.Iq0, q.Jp, x.eS);
+  row_ref_exp_kernel<<<(int)q.InP, 256, 0, s>>>(x.eS, (int)q.InP, q.Jp, x.eT, x.dS);
   slice_t_i8_kernel<<<(int)cdiv(q.Jp * q.InP * q.KP, 256), 256, 0, s>>>(T, ndims, x.st_d, x.dims_d, n, q0, (int)q.In,
                                                                         (int)q.InP, (int)q.Iq0, (int)q.KP, q.Jp,
-                                                                        x.eT, x.B);
+                                                                        x.eS, x.B);
   col_exp_u_kernel<<<(int)cdiv(q.CP, 32), 256, 0, s>>>(x.Up[q0], q.CP, (int)q.Iq0, (int)C, (int)q.CP, x.eU);
   slice_u_i8_kernel<<<(int)cdiv(q.CP * q.KP, 256), 256, 0, s>>>(x.Up[q0], q.CP, (int)q.Iq0, (int)C, (int)q.CP,
                                                                 (int)q.KP, x.eU, x.A);
@@ -2677,6 +2731,7 @@ jkcals_status jkcals_mttkrp_i8(int ndims, const int64_t* dims, int n, const doub
   }
   g.ldu = q.CP;
   g.eT = x.eT;
+  g.dS = x.dS;
   g.eU = x.eU;
 #ifdef JKCALS_DEV_PROBES  // timing-probe builds only: 1 = drain skipped, 2 = one product per K32 step
   g.probe = getenv("JKCALS_I8_PROBE") ? atoi(getenv("JKCALS_I8_PROBE")) : 0;

@@ -18,9 +18,12 @@ namespace jk {
 
 typedef void (*MttkrpFn)(const CUtensorMap, const CUtensorMap, MttkrpView, MttkrpGeom, const TileInfo*, double*);
 typedef size_t (*SmemFn)(int);
-// k_dmma.cu (compiled once per KMAJOR): fn[st][nt - 1], st = 0 -> 2 stages, 1 -> 4 stages
-void dmma_kernels_km0(MttkrpFn fn[2][kMaxNT], SmemFn smem[2][kMaxNT]);
-void dmma_kernels_km1(MttkrpFn fn[2][kMaxNT], SmemFn smem[2][kMaxNT]);
+// k_dmma.cu (compiled once per KMAJOR): fn[wv][st][nt - 1]: wv indexes the consumer-warp count
+// kWMs[wv] (tile width 16 x WM columns), st = 0 -> 2 stages, 1 -> 4 stages
+constexpr int kNumWM = 2;
+constexpr int kWMs[kNumWM] = {8, 5};
+void dmma_kernels_km0(MttkrpFn fn[kNumWM][2][kMaxNT], SmemFn smem[kNumWM][2][kMaxNT]);
+void dmma_kernels_km1(MttkrpFn fn[kNumWM][2][kMaxNT], SmemFn smem[kNumWM][2][kMaxNT]);
 
 typedef void (*TfFn)(const CUtensorMap, const CUtensorMap, const CUtensorMap, MttkrpView, TfGeom, const TileInfo*,
                      double*);

@@ -147,26 +147,29 @@ __device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, do
 //           KMAJOR=true  (n >= 1: i_q0 contiguous in T) -> Bt[i][BKP], box (20, BN), BKP = 20.
 // The 4-double over-fetch of each box row makes the row pitch 4 mod 16 doubles, so the 64-bit
 // fragment loads of a half-warp hit 16 distinct bank pairs.
-template <int NT, bool KMAJOR, int STAGES>
+template <int NT, bool KMAJOR, int STAGES, int WM = kWarps>
 struct MttkrpCfg {
+  static constexpr int BM = WM * 16;  // fused columns of a tile: WM consumer warps x 16
+  static constexpr int BMP = BM + 4;  // = 4 mod 16 doubles for WM in {5, 8}: conflict-free loads
   static constexpr int BN = NT * 8;
   static constexpr int BNP = BN + ((4 - BN % 16) + 16) % 16;  // BN rounded up to 4 mod 16
   static constexpr int BKP = kBK + 4;
   static constexpr int kBTile = KMAJOR ? BN * BKP : kBK * BNP;  // doubles (= TMA box volume)
   static constexpr unsigned kTBytes = kBTile * 8u;
-  static constexpr size_t kUb = 2ull * kBK * kBMP;              // doubles
-  __host__ __device__ static size_t stage_doubles(int nslow) { return (size_t)kBTile + (size_t)nslow * kBM; }
+  static constexpr size_t kUb = 2ull * kBK * BMP;               // doubles
+  __host__ __device__ static size_t stage_doubles(int nslow) { return (size_t)kBTile + (size_t)nslow * BM; }
   __host__ __device__ static size_t smem_bytes(int nslow) {
     return 128 + (kUb + (size_t)STAGES * stage_doubles(nslow)) * sizeof(double) + 2 * STAGES * sizeof(uint64_t);
   }
 };
 
-template <int NT, bool KMAJOR, int STAGES>
+template <int NT, bool KMAJOR, int STAGES, int WM = kWarps>
 __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
     mttkrp_dmma_kernel(const __grid_constant__ CUtensorMap tmT, const __grid_constant__ CUtensorMap tmU,
                        MttkrpView v, MttkrpGeom g, const TileInfo* __restrict__ tinfo, double* __restrict__ parts) {
-  using Cfg = MttkrpCfg<NT, KMAJOR, STAGES>;
+  using Cfg = MttkrpCfg<NT, KMAJOR, STAGES, WM>;
   constexpr int BN = Cfg::BN, BNP = Cfg::BNP, BKP = Cfg::BKP, BT = Cfg::kBTile;
+  constexpr int BM = Cfg::BM, BMP = Cfg::BMP;
   // (no integer round-trip on the base pointer: it must stay in the shared window so that the
   // fragment loads compile to LDS, not generic LD)
   extern __shared__ __align__(1024) double smem[];
@@ -184,7 +187,7 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kWarps);
+      mbar_init(&empty[s], WM);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -196,12 +199,12 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;\n" :::);
 
-  // =========================== producer warp (warp kWarps, one lane) ===========================
+  // =========================== producer warp (warp WM, one lane) ===========================
   // (r01: a warp-uniform loop with elect.sync measured no faster here -- the FP64 kernel is
   // DMMA-bound -- and 12 % slower on the 4-way config, so the lane-0 producer stays)
-  if (warp == kWarps) {
+  if (warp == WM) {
     if (lane != 0) return;
-    const unsigned s_bytes = (unsigned)v.nslow * kBM * 8u;
+    const unsigned s_bytes = (unsigned)v.nslow * BM * 8u;
     unsigned ld_git = 0;  // tiles issued by this CTA (ring slot + phase)
     for (int64_t u = u0; u < u1;) {
       const int t = (int)(u / g.KT);
@@ -210,7 +213,7 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
       const int kt1 = (int)(kt_end < (int64_t)g.KT ? kt_end : (int64_t)g.KT);
       u += kt1 - kt0;
       const int tm = t % g.nMt, tn = t / g.nMt;
-      const int c0 = tm * kBM, i0 = tn * BN;
+      const int c0 = tm * BM, i0 = tn * BN;
       // a new segment reloads the U_q0 slab buffers: wait until every issued tile is consumed
       for (unsigned q = (ld_git >= (unsigned)STAGES ? ld_git - STAGES + 1 : 0); q < ld_git; ++q)
         mbar_wait(&empty[q % STAGES], (q / STAGES) & 1u);
@@ -238,14 +241,14 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
           for (unsigned q = (ld_git >= (unsigned)STAGES ? ld_git - STAGES + 1 : 0); q < ld_git; ++q)
             mbar_wait(&empty[q % STAGES], (q / STAGES) & 1u);
         {
-          mbar_expect_tx(bar, Cfg::kTBytes + s_bytes + (new_slab ? (unsigned)(kBK * kBMP * 8) : 0u));
+          mbar_expect_tx(bar, Cfg::kTBytes + s_bytes + (new_slab ? (unsigned)(kBK * BMP * 8) : 0u));
           // U_q0 rows [b0*BK, b0*BK+BK) x columns [c0, c0+BMP): OOB rows are zero
-          if (new_slab) tma_load_2d(Ub + (ld_b0 & 1) * (kBK * kBMP), &tmU, c0, ld_b0 * kBK, bar);
+          if (new_slab) tma_load_2d(Ub + (ld_b0 & 1) * (kBK * BMP), &tmU, c0, ld_b0 * kBK, bar);
           if (KMAJOR) tma_load_4d(st, &tmT, ld_b0 * kBK, ld_ja, i0, ld_jb, bar);  // view (q0, runA, n, runB)
           else tma_load_4d(st, &tmT, i0, ld_b0 * kBK, ld_ja, ld_jb, bar);
 #pragma unroll
           for (int s = 0; s < kMaxModes - 2; ++s)
-            if (s < v.nslow) bulk_load(st + BT + s * kBM, v.Us[s] + (int64_t)sidx[s] * g.ldu + c0, kBM * 8u, bar);
+            if (s < v.nslow) bulk_load(st + BT + s * BM, v.Us[s] + (int64_t)sidx[s] * g.ldu + c0, BM * 8u, bar);
         }
         if (new_slab) loaded_b0 = ld_b0;
         // advance to the next k-tile (j' fastest, then the i_q0 block)
@@ -271,7 +274,7 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
     return;
   }
 
-  // =========================== consumer warps 0..kWarps-1 ===========================
+  // =========================== consumer warps 0..WM-1 ===========================
   const int gid = lane >> 2, tig = lane & 3;
   unsigned git = 0;  // tiles consumed by this CTA (ring slot + phase)
   for (int64_t u = u0; u < u1;) {
@@ -281,7 +284,7 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
     const int kt1 = (int)(kt_end < (int64_t)g.KT ? kt_end : (int64_t)g.KT);
     u += kt1 - kt0;
     const int tm = t % g.nMt, tn = t / g.nMt;
-    const int c0 = tm * kBM, i0 = tn * BN;
+    const int c0 = tm * BM, i0 = tn * BN;
     const bool warp_live = (c0 + warp * 16) < g.C;
 
     double acc[2][NT][2];
@@ -301,20 +304,20 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
         const double* st = stage0 + (size_t)slot * stage_sz;
         const double* Bt = st;
         const double* Ss = st + BT;
-        const double* ub = Ub + (cmp_b0 & 1) * (kBK * kBMP) + warp * 16 + gid;
+        const double* ub = Ub + (cmp_b0 & 1) * (kBK * BMP) + warp * 16 + gid;
         const int cl = warp * 16 + gid;
         double s0 = Ss[cl], s1 = Ss[cl + 8];
         for (int s = 1; s < v.nslow; ++s) {
-          s0 *= Ss[s * kBM + cl];
-          s1 *= Ss[s * kBM + cl + 8];
+          s0 *= Ss[s * BM + cl];
+          s1 *= Ss[s * BM + cl + 8];
         }
         // A fragments of the whole k-tile: KRP^T(c, k) = U_q0(k, c) * S_{j'}(c)
         double a[kBK / 4][2];
 #pragma unroll
         for (int kk = 0; kk < kBK / 4; ++kk) {
           const int kr = kk * 4 + tig;
-          a[kk][0] = ub[kr * kBMP] * s0;
-          a[kk][1] = ub[kr * kBMP + 8] * s1;
+          a[kk][0] = ub[kr * BMP] * s0;
+          a[kk][1] = ub[kr * BMP + 8] * s1;
         }
         const int kvalid = v.Iq0 - cmp_b0 * kBK;
         if (kvalid >= kBK && full_n) {
@@ -357,15 +360,15 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
     }
 
     const TileInfo ti = tinfo[t];
-    double* P = parts + ((int64_t)ti.piece_base + (b - ti.first_cta)) * (int64_t)(BN * kBM);
+    double* P = parts + ((int64_t)ti.piece_base + (b - ti.first_cta)) * (int64_t)(BN * BM);
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
       for (int ni = 0; ni < NT; ++ni) {
         const int cl = warp * 16 + mi * 8 + gid;
         const int il = ni * 8 + 2 * tig;
-        P[(int64_t)il * kBM + cl] = acc[mi][ni][0];
-        P[(int64_t)(il + 1) * kBM + cl] = acc[mi][ni][1];
+        P[(int64_t)il * BM + cl] = acc[mi][ni][0];
+        P[(int64_t)(il + 1) * BM + cl] = acc[mi][ni][1];
       }
   }
 }
@@ -374,15 +377,16 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
 // Plain reduction of the partial pieces into a dense row-major M (stand-alone op only; the
 // JK-CALS path reduces inside the epilogue instead).
 __global__ void reduce_parts_kernel(const double* __restrict__ parts, const TileInfo* __restrict__ tinfo,
-                                    int In, int C, int BN, int nMt, double* __restrict__ M, int64_t ldm) {
+                                    int In, int C, int BN, int nMt, double* __restrict__ M, int64_t ldm,
+                                    int BM = kBM) {
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)In * C) return;
   int i = (int)(e / C), c = (int)(e % C);
-  int tn = i / BN, tm = c / kBM;
+  int tn = i / BN, tm = c / BM;
   TileInfo ti = tinfo[tn * nMt + tm];
-  const double* p = parts + (int64_t)ti.piece_base * BN * kBM + (int64_t)(i - tn * BN) * kBM + (c - tm * kBM);
+  const double* p = parts + (int64_t)ti.piece_base * BN * BM + (int64_t)(i - tn * BN) * BM + (c - tm * BM);
   double s = 0.0;
-  for (int pc = 0; pc < ti.npieces; ++pc) s += p[(int64_t)pc * BN * kBM];
+  for (int pc = 0; pc < ti.npieces; ++pc) s += p[(int64_t)pc * BN * BM];
   M[(int64_t)i * ldm + c] = s;
 }
 #endif

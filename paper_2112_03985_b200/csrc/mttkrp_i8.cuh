@@ -83,8 +83,10 @@ struct I8Geom {
   int sdim[kMaxModes - 2];
   const double* Us[kMaxModes - 2];  // slow modes' U (row-major rows x ldu)
   int64_t ldu;
-  const int* eT;     // [InP] row exponents of T
-  const int* eU;     // [CP] column exponents of U_q0
+  const int* eT;     // [InP] reference exponent of each row of T_(n) (the largest slab exponent)
+  const int8_t* dS;  // [Jp][InP] slab exponent of (row i, j') relative to eT(i), <= 0 (T digits are
+                     // scaled per (i, j') slab: a spike costs precision only in its own slab)
+  const int* eU;     // [CP] column exponents of U_q0 (kI8Bad: the column holds a non-finite value)
 #ifdef JKCALS_DEV_PROBES
   int probe;         // dev timing probe builds only (tools/i8_probe.py)
 #endif
@@ -159,6 +161,8 @@ __device__ __forceinline__ void i8_digits(double x, int e, int8_t* d) {
     r -= q;
   }
 }
+constexpr int kI8Bad = 0x7fffffff;   // column-exponent marker of a non-finite U_q0 column
+constexpr int kI8ZeroSlab = -100000; // slab-exponent marker of an all-zero slab
 __device__ __forceinline__ int i8_exponent(double m) {  // e with m * 2^-e <= 1/2
   if (!(m > 0.0)) return 0;
   int e;
@@ -312,7 +316,9 @@ __global__ void __launch_bounds__(kI8Threads, 1)
 #pragma unroll
       for (int i = 0; i < kI8N / 2; ++i) {
         const int il = crk * kI8N + h * (kI8N / 2) + i;
-        P[(int64_t)il * 128] = ldexp(acc[i], eu + g.eT[tn * kBN + il]);
+        // a non-finite U_q0 column yields NaN, as the FP64 path would (the epilogue flags it)
+        P[(int64_t)il * 128] = (eu == kI8Bad) ? __longlong_as_double(0x7ff8000000000000LL)
+                                              : ldexp(acc[i], eu + g.eT[tn * kBN + il]);
         acc[i] = 0.0;
       }
     };
@@ -322,6 +328,16 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       if (seg_t >= 0 && t != seg_t) flush(seg_t);
       seg_t = t;
       const int c = (int)(t % g.nMt) * 128 + cl;
+      // this thread's 32 rows: their slab exponents relative to the row reference (broadcast loads)
+      uint4 dsw[2];
+      {
+        constexpr int kBNr = kClu ? 2 * kI8N : kI8N;
+        const int tn = (int)(t / g.nMt);
+        const uint4* dp = reinterpret_cast<const uint4*>(g.dS + (int64_t)jp * g.InP + tn * kBNr + crk * kI8N +
+                                                          h * (kI8N / 2));
+        dsw[0] = __ldg(dp);
+        dsw[1] = __ldg(dp + 1);
+      }
       // S(j', c) = prod of the slow modes' rows (FP64, from L2; overlaps this unit's MMAs)
       double s = 1.0;
       {
@@ -374,7 +390,13 @@ __global__ void __launch_bounds__(kI8Threads, 1)
           const double hd = __longlong_as_double(hi + 0x4338000000000000LL) - 6755399441055744.0;
           const double ld = __longlong_as_double(lo + 0x4338000000000000LL) - 6755399441055744.0;
           const double v = fma(ld, 0x1p-56, hd * 0x1p-35);  // D_dg carries 2^(-14 - 7 dg)
-          acc[cg + i] = fma(s, v, acc[cg + i]);
+          // 2^(e_S(i, j') - e_T(i)) built from its exponent bits (exact; -126 <= d <= 0)
+          const int row = cg + i;
+          const uint32_t wd = (row < 16) ? ((row < 8) ? ((row < 4) ? dsw[0].x : dsw[0].y) : ((row < 12) ? dsw[0].z : dsw[0].w))
+                                         : ((row < 24) ? ((row < 20) ? dsw[1].x : dsw[1].y) : ((row < 28) ? dsw[1].z : dsw[1].w));
+          const int dsl = (int)(int8_t)(wd >> (8 * (row & 3)));
+          const double sc = __longlong_as_double((long long)(1023 + dsl) << 52);
+          acc[cg + i] = fma(s * sc, v, acc[cg + i]);
         }
       }
     }
@@ -391,35 +413,57 @@ __global__ void __launch_bounds__(kI8Threads, 1)
 
 #ifdef JK_TU_HOST
 // ---- operand preparation -----------------------------------------------------------------
-// row exponents of T_(n): e_T(i) with max_j |T(i, j)| 2^-e <= 1/2 (one block per row)
-__global__ void row_exp_t_kernel(const double* __restrict__ T, int N, const int64_t* __restrict__ st_dev,
-                                 const int* __restrict__ dims_dev, int n, int64_t J, int* __restrict__ eT) {
-  // st_dev: element strides of T per mode; the J other indices enumerated in Eq. 3 order
-  const int i = blockIdx.x;
-  double m = 0.0;
-  for (int64_t j = threadIdx.x; j < J; j += blockDim.x) {
-    int64_t rem = j, off = (int64_t)i * st_dev[n];
-    for (int k = 0; k < N; ++k) {
-      if (k == n) continue;
-      off += (rem % dims_dev[k]) * st_dev[k];
-      rem /= dims_dev[k];
+// slab exponents of T_(n): e_S(i, j') with max_k |T(i, k, j')| 2^-e <= 1/2 (kI8ZeroSlab for an
+// all-zero slab); one thread per (j', i), k = i_q0 the contraction index
+__global__ void slab_exp_t_kernel(const double* __restrict__ T, int N, const int64_t* __restrict__ st_dev,
+                                  const int* __restrict__ dims_dev, int n, int q0, int In, int InP, int Iq0,
+                                  int64_t Jp, int* __restrict__ eS) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= Jp * InP) return;
+  const int64_t jp = e / InP;
+  const int i = (int)(e % InP);
+  int ex = kI8ZeroSlab;
+  if (i < In) {
+    int64_t rem = jp, off = (int64_t)i * st_dev[n];
+    for (int m = 0; m < N; ++m) {
+      if (m == n || m == q0) continue;
+      off += (rem % dims_dev[m]) * st_dev[m];
+      rem /= dims_dev[m];
     }
-    m = fmax(m, fabs(T[off]));
+    double mx = 0.0;
+    for (int k = 0; k < Iq0; ++k) mx = fmax(mx, fabs(T[off + (int64_t)k * st_dev[q0]]));
+    if (mx > 0.0) ex = i8_exponent(mx);
   }
-  __shared__ double red[256];
+  eS[e] = ex;
+}
+
+// row reference exponents e_T(i) = max_j' e_S(i, j') and the relative slab exponents
+// dS = e_S - e_T in [-126, 0] (an all-zero slab, or one 126+ binades below its row, is -126: its
+// digits are all zero or its contribution is below 2^-126 of the row's largest)
+__global__ void row_ref_exp_kernel(const int* __restrict__ eS, int InP, int64_t Jp, int* __restrict__ eT,
+                                   int8_t* __restrict__ dS) {
+  const int i = blockIdx.x;
+  int m = kI8ZeroSlab;
+  for (int64_t jp = threadIdx.x; jp < Jp; jp += blockDim.x) m = max(m, eS[jp * InP + i]);
+  __shared__ int red[256];
   red[threadIdx.x] = m;
   __syncthreads();
   for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
+    if ((int)threadIdx.x < o) red[threadIdx.x] = max(red[threadIdx.x], red[threadIdx.x + o]);
     __syncthreads();
   }
-  if (threadIdx.x == 0) eT[i] = i8_exponent(red[0]);
+  const int ref = red[0] == kI8ZeroSlab ? 0 : red[0];
+  if (threadIdx.x == 0) eT[i] = ref;
+  for (int64_t jp = threadIdx.x; jp < Jp; jp += blockDim.x) {
+    const int es = eS[jp * InP + i];
+    dS[jp * InP + i] = (int8_t)(es == kI8ZeroSlab ? -126 : max(-126, es - ref));
+  }
 }
 
-// Bsl[s][j'][i][k] = digit s of T(i_n = i, i_q0 = k, j') * 2^-e_T(i); zero padding outside
+// Bsl[s][j'][i][k] = digit s of T(i_n = i, i_q0 = k, j') * 2^-e_S(i, j'); zero padding outside
 __global__ void slice_t_i8_kernel(const double* __restrict__ T, int N, const int64_t* __restrict__ st_dev,
                                   const int* __restrict__ dims_dev, int n, int q0, int In, int InP, int Iq0, int KP,
-                                  int64_t Jp, const int* __restrict__ eT, int8_t* __restrict__ B) {
+                                  int64_t Jp, const int* __restrict__ eS, int8_t* __restrict__ B) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t per = (int64_t)InP * KP;
   if (e >= Jp * per) return;
@@ -433,7 +477,8 @@ __global__ void slice_t_i8_kernel(const double* __restrict__ T, int N, const int
       off += (rem % dims_dev[m]) * st_dev[m];
       rem /= dims_dev[m];
     }
-    i8_digits(T[off], eT[i], d);
+    const int es = eS[jp * InP + i];
+    if (es != kI8ZeroSlab) i8_digits(T[off], es, d);
   }
   const int64_t slice = Jp * per;
 #pragma unroll
@@ -449,13 +494,16 @@ __global__ void __launch_bounds__(256) col_exp_u_kernel(const double* __restrict
   const int c = blockIdx.x * 32 + cx;
   double m = 0.0;
   if (c < C)
-    for (int k = ry; k < rows; k += 8) m = fmax(m, fabs(U[(int64_t)k * ldu + c]));
+    for (int k = ry; k < rows; k += 8) {
+      const double x = fabs(U[(int64_t)k * ldu + c]);
+      m = (x <= 1.7976931348623157e308) ? fmax(m, x) : __longlong_as_double(0x7ff0000000000000LL);  // NaN/Inf -> Inf
+    }
   red[ry][cx] = m;
   __syncthreads();
   if (ry == 0 && c < CP) {
 #pragma unroll
     for (int r = 1; r < 8; ++r) m = fmax(m, red[r][cx]);
-    eU[c] = i8_exponent(m);
+    eU[c] = isinf(m) ? kI8Bad : i8_exponent(m);
   }
 }
 __global__ void slice_u_i8_kernel(const double* __restrict__ U, int64_t ldu, int rows, int C, int CP, int KP,
@@ -464,7 +512,7 @@ __global__ void slice_u_i8_kernel(const double* __restrict__ U, int64_t ldu, int
   if (e >= (int64_t)CP * KP) return;
   const int c = (int)(e / KP), k = (int)(e % KP);
   int8_t d[kI8S] = {0, 0, 0, 0, 0, 0, 0};
-  if (c < C && k < rows) i8_digits(U[(int64_t)k * ldu + c], eU[c], d);
+  if (c < C && k < rows && eU[c] != kI8Bad) i8_digits(U[(int64_t)k * ldu + c], eU[c], d);
   const int64_t slice = (int64_t)CP * KP;
 #pragma unroll
   for (int s = 0; s < kI8S; ++s) A[(int64_t)s * slice + e] = d[s];

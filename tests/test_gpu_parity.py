@@ -367,6 +367,99 @@ def test_experimental_int8_sliced_mttkrp(dims, C):
         assert rel(M, ref) <= 1e-13, (dims, C, n, rel(M, ref))
 
 
+def _spiky_tensor(g, dims):
+    """Wide dynamic range: rows of T_(0) scaled over 1e-12 .. 1 and isolated spikes of
+    1e4 .. 1e8 times their neighbours -- the scatter-like outliers of fluorescence data."""
+    T = g.standard_normal(dims)
+    T *= (10.0 ** g.uniform(-12, 0, dims[0])).reshape((-1,) + (1,) * (len(dims) - 1))
+    flat = T.reshape(-1)
+    for amp in (1e4, 1e6, 1e8):
+        idx = g.choice(flat.size, 3, replace=False)
+        flat[idx] *= amp
+    return np.asfortranarray(T)
+
+
+@pytest.mark.parametrize("dims,C", [((40, 30, 20), 64), ((13, 9, 7, 5), 40)])
+def test_int8_sliced_mttkrp_wide_dynamic_range(dims, C):
+    """FP64_I8 with per-(row, j') slab scaling of T: every row's MTTKRP matches the oracle to FP64
+    accuracy relative to that row's own magnitude, spikes and 1e-12-scaled rows included."""
+    import torch
+    from paper_2112_03985_b200.jkcals import mttkrp_i8
+    g = np.random.default_rng(11 + sum(dims))
+    T = _spiky_tensor(g, dims)
+    U = [g.standard_normal((I, C)) for I in dims]
+    ldu = ((C + 127) // 128) * 128
+    Ud = [torch.from_numpy(np.pad(u, ((0, 0), (0, ldu - C)))).cuda() for u in U]
+    Td = torch.from_numpy(np.ravel(T, order="F").copy()).cuda()
+    for n in range(len(dims)):
+        M = mttkrp_i8(Td, dims, n, Ud, C).cpu().numpy()
+        ref = O.mttkrp(T, U, n)
+        absU = [np.abs(u) for u in U]
+        absref = O.mttkrp(np.abs(T), absU, n)
+        # the documented bound (include/jkcals.h): 49-bit digits relative to each (row i, j') slab's
+        # largest |T| and each U_q0 column's largest |U| -> per slab normwise. Tb replaces every
+        # entry of a slab (the contraction axis q0) by the slab's max |T|.
+        q0 = 1 if n == 0 else 0
+        Tb = np.broadcast_to(np.abs(T).max(axis=q0, keepdims=True), T.shape)
+        bound = 2.0 ** -44 * O.mttkrp(np.asfortranarray(Tb), absU, n) + 1e-14 * absref
+        assert np.all(np.abs(M - ref) <= bound), (dims, n, (np.abs(M - ref) / bound).max())
+        # and relative to each element's own |T| x |KRP| magnitude it stays far below the FP64 parity
+        # bar even with 1e8 spikes and rows scaled down to 1e-12 (r01's per-row scaling: ~1e-8)
+        assert (np.abs(M - ref) / np.maximum(absref, 1e-300)).max() <= 1e-9
+
+
+@pytest.mark.parametrize("spike", [None, 1e5])
+def test_int8_sliced_fp64_path_wide_dynamic_range(spike):
+    """The whole FP64_I8 JK-CALS loop on a tensor whose mode-0 slices span 1e-8 .. 1 is held to the
+    FP64 bar (the per-(row, j') scales absorb any row scaling exactly). With a scatter-like 1e5 spike
+    the per-slab normwise bound shows: the spike's slab keeps ~32 of 49 bits, so the FP64_I8 factors
+    drift to ~1e-9 while the DMMA path stays at the bar -- the documented contract (include/jkcals.h)
+    that keeps FP64_I8 supplementary."""
+    from paper_2112_03985_b200 import JKCals
+    g = np.random.default_rng(5)
+    dims, R = (24, 18, 14), 3
+    A = [g.uniform(0, 1, (I, R)) for I in dims]
+    A[0] *= (10.0 ** g.uniform(-8, 0, dims[0]))[:, None]  # samples of very different magnitude
+    T = np.einsum("ir,jr,kr->ijk", *A)
+    T = T * (1 + 0.01 * g.standard_normal(dims))
+    if spike:
+        T[g.integers(0, 24), g.integers(0, 18), g.integers(0, 14)] *= spike
+    T = np.asfortranarray(T)
+    P = [np.asfortranarray(a + 0.05 * g.standard_normal(a.shape)) for a in A]
+    res = O.jk_als(T, P, max_iters=30, nthreads=NCPU)
+    worst = {}
+    for prec in (0, 2):
+        h = JKCals(T, R, hist_cap=30, precision=prec)
+        h.set_init(P)
+        h.iterate(30, 0.0)
+        w_ = 0.0
+        for p in range(dims[0]):
+            fac, lam = h.factors(p)
+            for a_, b_ in zip(fac, res.factors[p]):
+                w_ = max(w_, rel(a_, b_))
+        worst[prec] = w_
+    assert worst[0] <= FTOL, worst
+    assert worst[2] <= (FTOL if spike is None else 1e-7), worst
+
+
+def test_int8_nonfinite_column_propagates():
+    """A non-finite U_q0 entry reaches M as NaN (it used to be sliced into finite digits)."""
+    import torch
+    from paper_2112_03985_b200.jkcals import mttkrp_i8
+    g = np.random.default_rng(3)
+    dims, C = (12, 10, 8), 16
+    T = np.asfortranarray(g.standard_normal(dims))
+    U = [g.standard_normal((I, C)) for I in dims]
+    U[1][3, 5] = np.nan  # q0 = mode 1 for n = 0
+    U[0][2, 7] = np.inf  # q0 = mode 0 for n = 1, 2
+    Ud = [torch.from_numpy(np.pad(u, ((0, 0), (0, 128 - C)))).cuda() for u in U]
+    Td = torch.from_numpy(np.ravel(T, order="F").copy()).cuda()
+    M0 = mttkrp_i8(Td, dims, 0, Ud, C).cpu().numpy()
+    assert np.all(np.isnan(M0[:, 5])) and np.all(np.isfinite(np.delete(M0, 5, axis=1)))
+    M1 = mttkrp_i8(Td, dims, 1, Ud, C).cpu().numpy()
+    assert np.all(np.isnan(M1[:, 7]))
+
+
 @pytest.mark.parametrize("name,ps", [("tiny", range(10)), ("syn50_r3", range(50)), ("4way", [0, 1, 50, 99]),
                                      ("eem_r5", [0, 133, 267])])
 def test_experimental_int8_sliced_fp64_path(name, ps):
