@@ -333,7 +333,7 @@ def main():
     dgemm = live_dgemm_tflops(torch) if rank == 0 else None
     fp64_peak = max(FP64_DMMA_PIPE_TFLOPS, dgemm or 0.0)
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "r01_mttkrp_ncu_summary.json")
+    tp = os.path.join(ROOT, "profiles", "r02_mttkrp_ncu_summary.json")
     if os.path.exists(tp):
         try:
             traffic = json.load(open(tp)).get("dram_bytes_per_launch")
