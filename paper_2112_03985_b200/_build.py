@@ -27,8 +27,10 @@ EXTRA = os.environ.get("JKCALS_NVCC_EXTRA", "").split()  # e.g. -DJKCALS_DEV_PRO
 
 # (source, defines, object name)
 UNITS = [("jkcals.cu", [], "jkcals"),
-         ("k_dmma.cu", ["-DJK_KMAJOR=0"], "k_dmma_km0"),
-         ("k_dmma.cu", ["-DJK_KMAJOR=1"], "k_dmma_km1"),
+         ("k_dmma.cu", ["-DJK_KMAJOR=0", "-DJK_KB=16"], "k_dmma_km0_kb16"),
+         ("k_dmma.cu", ["-DJK_KMAJOR=1", "-DJK_KB=16"], "k_dmma_km1_kb16"),
+         ("k_dmma.cu", ["-DJK_KMAJOR=0", "-DJK_KB=20"], "k_dmma_km0_kb20"),
+         ("k_dmma.cu", ["-DJK_KMAJOR=1", "-DJK_KB=20"], "k_dmma_km1_kb20"),
          ("k_tf32.cu", [], "k_tf32"),
          ("k_i8.cu", [], "k_i8"),
          ("k_large.cu", [], "k_large"),

@@ -39,9 +39,9 @@ inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
 
 // ---------------------------------------------------------------- kernel dispatch tables
 struct KernelInfo {
-  MttkrpFn fn[kNumWM][2][2][kMaxNT];         // [tile width kWMs][KMAJOR][STAGES==4][NT-1]
-  SmemFn smem[kNumWM][2][2][kMaxNT];
-  int occ[kNumWM][2][2][kMaxNT][kMaxModes];  // [..][nslow]
+  MttkrpFn fn[kNumKB][kNumWM][2][2][kMaxNT];         // [k depth kKBs][tile width kWMs][KMAJOR][STAGES==4][NT-1]
+  SmemFn smem[kNumKB][kNumWM][2][2][kMaxNT];
+  int occ[kNumKB][kNumWM][2][2][kMaxNT][kMaxModes];  // [..][nslow]
   int nsm;
   int i8clusters;                    // co-resident 2-CTA clusters of the INT8 cluster kernel (0: none)
 };
@@ -53,17 +53,20 @@ KernelInfo* kernel_info(int device, std::string* err) {
   if (ready[device]) return &info[device];
   KernelInfo& ki = info[device];
   {
-    MttkrpFn f[2][kNumWM][2][kMaxNT];
-    SmemFn sm[2][kNumWM][2][kMaxNT];
-    dmma_kernels_km0(f[0], sm[0]);
-    dmma_kernels_km1(f[1], sm[1]);
-    for (int wv = 0; wv < kNumWM; ++wv)
-      for (int km = 0; km < 2; ++km)
-        for (int st = 0; st < 2; ++st)
-          for (int t = 0; t < kMaxNT; ++t) {
-            ki.fn[wv][km][st][t] = f[km][wv][st][t];
-            ki.smem[wv][km][st][t] = sm[km][wv][st][t];
-          }
+    MttkrpFn f[kNumKB][2][kNumWM][2][kMaxNT];
+    SmemFn sm[kNumKB][2][kNumWM][2][kMaxNT];
+    dmma_kernels_km0_kb16(f[0][0], sm[0][0]);
+    dmma_kernels_km1_kb16(f[0][1], sm[0][1]);
+    dmma_kernels_km0_kb20(f[1][0], sm[1][0]);
+    dmma_kernels_km1_kb20(f[1][1], sm[1][1]);
+    for (int kv = 0; kv < kNumKB; ++kv)
+      for (int wv = 0; wv < kNumWM; ++wv)
+        for (int km = 0; km < 2; ++km)
+          for (int st = 0; st < 2; ++st)
+            for (int t = 0; t < kMaxNT; ++t) {
+              ki.fn[kv][wv][km][st][t] = f[kv][km][wv][st][t];
+              ki.smem[kv][wv][km][st][t] = sm[kv][km][wv][st][t];
+            }
   }
   int prev = 0;
   cudaGetDevice(&prev);
@@ -112,24 +115,25 @@ KernelInfo* kernel_info(int device, std::string* err) {
       return nullptr;
     }
   }
-  for (int wv = 0; wv < kNumWM; ++wv)
-    for (int km = 0; km < 2; ++km)
-      for (int st = 0; st < 2; ++st)
-        for (int t = 0; t < kMaxNT; ++t) {
-          cudaError_t e = cudaFuncSetAttribute(ki.fn[wv][km][st][t], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)ki.smem[wv][km][st][t](kMaxModes - 2));
-          if (e != cudaSuccess) {
-            if (err) *err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e);
-            cudaSetDevice(prev);
-            return nullptr;
+  for (int kv = 0; kv < kNumKB; ++kv)
+    for (int wv = 0; wv < kNumWM; ++wv)
+      for (int km = 0; km < 2; ++km)
+        for (int st = 0; st < 2; ++st)
+          for (int t = 0; t < kMaxNT; ++t) {
+            cudaError_t e = cudaFuncSetAttribute(ki.fn[kv][wv][km][st][t], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)ki.smem[kv][wv][km][st][t](kMaxModes - 2));
+            if (e != cudaSuccess) {
+              if (err) *err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e);
+              cudaSetDevice(prev);
+              return nullptr;
+            }
+            for (int ns = 1; ns <= kMaxModes - 2; ++ns) {
+              int occ = 0;
+              cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ki.fn[kv][wv][km][st][t], (kWMs[wv] + 1) * 32,
+                                                            ki.smem[kv][wv][km][st][t](ns));
+              ki.occ[kv][wv][km][st][t][ns] = std::max(1, occ);
+            }
           }
-          for (int ns = 1; ns <= kMaxModes - 2; ++ns) {
-            int occ = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ki.fn[wv][km][st][t], (kWMs[wv] + 1) * 32,
-                                                          ki.smem[wv][km][st][t](ns));
-            ki.occ[wv][km][st][t][ns] = std::max(1, occ);
-          }
-        }
   cudaSetDevice(prev);
   ready[device] = true;
   return &ki;
@@ -157,6 +161,7 @@ ModeGeo mode_geo(int N, const int64_t* dims, int n) {
 struct ModePlan {
   int NT = 1, KM = 0, ST4 = 1, BN = 8, nMt = 1, nNt = 1, KT = 1, G = 1;
   int WV = 0, BM = kBM;  // FP64 kernel tile width: kWMs[WV] consumer warps x 16 = BM fused columns
+  int KV = 0, KB = kBK;  // FP64 kernel k-tile depth kKBs[KV] (i_q0 values per k-tile)
   int64_t units = 1;
   int ntiles = 1, npieces = 1;
   size_t smem = 0;
@@ -260,7 +265,7 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
     // variants that fit 2 CTAs/SM (<= 96 regs: NT <= 6) hide the per-k-tile latency better:
     // measured +7 % on syn200 (r01), modelled as a 1.08 factor
     const int km = (n != 0) ? 1 : 0, st4 = (mg.Jp >= 3) ? 1 : 0;
-    const double occ_bonus = ki.occ[0][km][st4][nt - 1][mg.nslow] >= 2 ? 1.08 : 1.0;
+    const double occ_bonus = ki.occ[0][0][km][st4][nt - 1][mg.nslow] >= 2 ? 1.08 : 1.0;
     const double score = (double)nI8 / (double)(ntiles_n * nt) * (double)nt / (nt + 1.0) * occ_bonus;
     if (score > best + 1e-12) {
       best = score;
@@ -309,11 +314,33 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
     p.BM = kWMs[p.WV] * 16;
   }
   p.nMt = (int)std::max<int64_t>(1, cdiv(C, p.BM));
-  p.KT = (int)(cdiv(mg.Iq0, kBK) * mg.Jp);
+  // k-tile depth: 16 or 20 i_q0 values. A k-tile costs phi (its fixed share: barriers, TMA, the
+  // A-fragment build) + its live depth / 16; a ragged last block pays phi for a partial depth.
+  // Calibrated on B200 (r02, phi = 0.12, 2 % margin): I_q0 = 200 / 100 / 50 take 20 (syn200
+  // 157.2 -> 149.9 ms, 4-way modes 1-3 -8 to -13 %, the "All" pool -5 %), I_q0 = 201 / 268 keep 16
+  // (eem R6 was 4 % slower with 20). The 20-deep variant is also skipped when it fits fewer CTAs per
+  // SM. JKCALS_FORCE_KB=<16|20> overrides (tuning).
+  {
+    constexpr double phi = 0.12;
+    double cost[kNumKB];
+    for (int kv = 0; kv < kNumKB; ++kv) {
+      const int KB = kKBs[kv];
+      const int64_t full = mg.Iq0 / KB, rem = mg.Iq0 % KB;
+      cost[kv] = (double)full * (phi + KB / 16.0) + (rem ? phi + rem / 16.0 : 0.0);
+    }
+    p.KV = (mg.Jp >= 3 && cost[1] < 0.98 * cost[0] &&
+            ki.occ[1][p.WV][p.KM][1][p.NT - 1][mg.nslow] >= ki.occ[0][p.WV][p.KM][1][p.NT - 1][mg.nslow])
+               ? 1 : 0;  // (the 20-deep variants need STAGES = 4: J' >= 3)
+    static int force_kb = [] { const char* e = getenv("JKCALS_FORCE_KB"); return e ? atoi(e) : 0; }();
+    for (int kv = 0; kv < kNumKB; ++kv)
+      if (force_kb == kKBs[kv] && (kv == 0 || mg.Jp >= 3)) p.KV = kv;
+    p.KB = kKBs[p.KV];
+  }
+  p.KT = (int)(cdiv(mg.Iq0, p.KB) * mg.Jp);
   p.ntiles = p.nMt * p.nNt;
   p.units = (int64_t)p.ntiles * p.KT;
-  p.smem = ki.smem[p.WV][p.KM][p.ST4][p.NT - 1](mg.nslow);
-  int64_t gmax = (int64_t)ki.nsm * ki.occ[p.WV][p.KM][p.ST4][p.NT - 1][mg.nslow];
+  p.smem = ki.smem[p.KV][p.WV][p.KM][p.ST4][p.NT - 1](mg.nslow);
+  int64_t gmax = (int64_t)ki.nsm * ki.occ[p.KV][p.WV][p.KM][p.ST4][p.NT - 1][mg.nslow];
   // at most kMaxPieces partial pieces per output tile: small problems (few tiles) would
   // otherwise write and re-read a BN x BM piece per CTA for ~1 k-tile of work each
   // (only for < 4 tiles: a single 128-column M tile x 5 N tiles -- a syn200 shard at 8 GPUs --
@@ -354,12 +381,12 @@ void plan_bounds(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, int6
   *tiles = 2 * p.ntiles;
 }
 
-MttkrpView make_mview(int N, const int64_t* dims, int n, const double* const* Uall) {
+MttkrpView make_mview(int N, const int64_t* dims, int n, const double* const* Uall, int KB = kBK) {
   ModeGeo mg = mode_geo(N, dims, n);
   MttkrpView v;
   v.In = (int)mg.In;
   v.Iq0 = (int)mg.Iq0;
-  v.nb0 = (int)cdiv(mg.Iq0, kBK);
+  v.nb0 = (int)cdiv(mg.Iq0, KB);
   v.Jp = (int)mg.Jp;
   // slow modes merged into <= 2 runs: n == 0 -> one run (modes 2..N-1);
   // n >= 1 -> run A = modes 1..n-1, run B = modes n+1..N-1 (j' = jA + runA * jB, Eq. 3 order)
@@ -402,7 +429,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // viewed for mode n as a 4-D box source with non-decreasing strides:
 //   n == 0: (i_0 [In], i_1 [q0], modes 2.. [run], 1)       box (BNP, 16, 1, 1)
 //   n >= 1: (i_0 [q0], modes 1..n-1 [runA], i_n, modes n+1.. [runB])   box (20, 1, BN, 1)
-bool make_tmap_T(CUtensorMap* tm, const double* T, int N, const int64_t* dims, int64_t I0p, int n, int BN, int BNP) {
+bool make_tmap_T(CUtensorMap* tm, const double* T, int N, const int64_t* dims, int64_t I0p, int n, int BN, int BNP,
+                 int KB = kBK) {
   auto enc = encode_fn();
   if (!enc) return false;
   int64_t st[kMaxModes + 1];
@@ -417,14 +445,14 @@ bool make_tmap_T(CUtensorMap* tm, const double* T, int N, const int64_t* dims, i
     for (int m = 2; m < N; ++m) run *= dims[m];
     gdim[0] = dims[0]; gdim[1] = dims[1]; gdim[2] = run; gdim[3] = 1;
     gstr[0] = st[1] * 8; gstr[1] = st[2] * 8; gstr[2] = total * 8;
-    box[0] = BNP; box[1] = kBK; box[2] = 1; box[3] = 1;
+    box[0] = BNP; box[1] = KB; box[2] = 1; box[3] = 1;
   } else {
     int64_t runA = 1, runB = 1;
     for (int m = 1; m < n; ++m) runA *= dims[m];
     for (int m = n + 1; m < N; ++m) runB *= dims[m];
     gdim[0] = dims[0]; gdim[1] = runA; gdim[2] = dims[n]; gdim[3] = runB;
     gstr[0] = st[1] * 8; gstr[1] = st[n] * 8; gstr[2] = (n + 1 < N ? st[n + 1] : total) * 8;
-    box[0] = kBK + 4; box[1] = 1; box[2] = BN; box[3] = 1;
+    box[0] = KB + ((4 - KB % 16) + 16) % 16; box[1] = 1; box[2] = BN; box[3] = 1;  // row pitch 4 mod 16
   }
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(T), gdim, gstr, box, est,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -448,11 +476,11 @@ bool make_tmap_T32(CUtensorMap* tm, const float* T, const int64_t gdim_in[4], co
   return r == CUDA_SUCCESS;
 }
 
-bool make_tmap_U(CUtensorMap* tm, const double* U, int64_t rows, int64_t ldu, int bmp = kBMP) {
+bool make_tmap_U(CUtensorMap* tm, const double* U, int64_t rows, int64_t ldu, int bmp = kBMP, int KB = kBK) {
   auto enc = encode_fn();
   if (!enc) return false;
   cuuint64_t gdim[2] = {(cuuint64_t)ldu, (cuuint64_t)rows}, gstr[1] = {(cuuint64_t)ldu * 8};
-  cuuint32_t box[2] = {(cuuint32_t)bmp, (cuuint32_t)kBK}, est[2] = {1, 1};
+  cuuint32_t box[2] = {(cuuint32_t)bmp, (cuuint32_t)KB}, est[2] = {1, 1};
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(U), gdim, gstr, box, est,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -863,11 +891,11 @@ jkcals_status replan(jkcals_t h) {
       continue;
     }
     // TMA descriptors: the tensor view of mode n and the U_q0 slab source of both U buffer sets
-    if (!make_tmap_T(&h->tmT[n], h->ptr<double>(h->off.T), h->N, h->dims, h->I0p, n, p.BN, bnp_of(p.NT)))
+    if (!make_tmap_T(&h->tmT[n], h->ptr<double>(h->off.T), h->N, h->dims, h->I0p, n, p.BN, bnp_of(p.NT), p.KB))
       return fail(h, JKCALS_E_CUDA, "cuTensorMapEncodeTiled failed for the tensor view of mode %d", n);
     const int q0 = (n == 0) ? 1 : 0;
     for (int set = 0; set < 2; ++set)
-      if (!make_tmap_U(&h->tmU[set][n], h->ptr<double>(h->off.U[set][q0]), h->dims[q0], h->ldu, p.BM + 4))
+      if (!make_tmap_U(&h->tmU[set][n], h->ptr<double>(h->off.U[set][q0]), h->dims[q0], h->ldu, p.BM + 4, p.KB))
         return fail(h, JKCALS_E_CUDA, "cuTensorMapEncodeTiled failed for U_%d", q0);
     if (h->tf32) {
       int64_t gd[4], gs[3];
@@ -907,10 +935,10 @@ jkcals_status replan(jkcals_t h) {
     for (int t = 0; t < p.ntiles; ++t) h->table164[t] = TileInfo{0, 1, t, 0};
     CKH(h, cudaMemcpyAsync(h->ptr<TileInfo>(h->off.tinfo164), h->table164.data(), p.ntiles * sizeof(TileInfo),
                            cudaMemcpyHostToDevice, h->stream));
-    if (!make_tmap_T(&h->tmT64, h->ptr<double>(h->off.T), h->N, h->dims, h->I0p, n, p.BN, bnp_of(p.NT)))
+    if (!make_tmap_T(&h->tmT64, h->ptr<double>(h->off.T), h->N, h->dims, h->I0p, n, p.BN, bnp_of(p.NT), p.KB))
       return fail(h, JKCALS_E_CUDA, "cuTensorMapEncodeTiled failed for the FP64 view of mode %d", n);
     for (int set = 0; set < 2; ++set)  // q0 = 0 for the last mode (N >= 3)
-      if (!make_tmap_U(&h->tmU64[set], h->ptr<double>(h->off.U[set][0]), h->dims[0], h->ldu, p.BM + 4))
+      if (!make_tmap_U(&h->tmU64[set], h->ptr<double>(h->off.U[set][0]), h->dims[0], h->ldu, p.BM + 4, p.KB))
         return fail(h, JKCALS_E_CUDA, "cuTensorMapEncodeTiled failed for U_0 (FP64 last mode)");
   }
   CKH(h, cudaStreamSynchronize(h->stream));  // tinfo host vectors may change on the next replan
@@ -966,7 +994,7 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
   for (int m = 0; m < h->N; ++m) Uall[m] = h->U(m);
   const bool f64 = h->tf32 && h->f64last && n == h->N - 1;  // FP32 path, tol > 0: last mode in FP64
   const ModePlan& p = f64 ? h->plan64 : h->plan[n];
-  MttkrpView v = make_mview(h->N, h->dims, n, Uall);
+  MttkrpView v = make_mview(h->N, h->dims, n, Uall, p.KB);
   MttkrpGeom g;
   g.C = h->C;
   g.ldu = h->ldu;
@@ -1042,7 +1070,7 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     CKH(h, cudaLaunchKernelEx(&cfg, tf32_kernel(p.ST4), h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v, tg, ti,
                               parts));
   } else {
-    MttkrpFn fn = h->ki->fn[p.WV][p.KM][p.ST4][p.NT - 1];
+    MttkrpFn fn = h->ki->fn[p.KV][p.WV][p.KM][p.ST4][p.NT - 1];
     // programmatic dependent launch: this grid may start (prologue) while the previous kernel
     // drains; the kernel waits (griddepcontrol.wait) before touching its inputs
     cudaLaunchConfig_t cfg = {};
@@ -2589,11 +2617,11 @@ jkcals_status jkcals_mttkrp(int ndims, const int64_t* dims, int n, const double*
   std::vector<char> table = pack_plan(p);
   if (cudaMemcpyAsync(ti, table.data(), table.size(), cudaMemcpyHostToDevice, s) != cudaSuccess)
     return JKCALS_E_CUDA;
-  MttkrpView v = make_mview(ndims, dims, n, Up);
+  MttkrpView v = make_mview(ndims, dims, n, Up, p.KB);
   CUtensorMap tmT, tmU;
   const int q0 = (n == 0) ? 1 : 0;
-  if (!make_tmap_T(&tmT, Tp, ndims, dims, I0p, n, p.BN, bnp_of(p.NT)) ||
-      !make_tmap_U(&tmU, Up[q0], dims[q0], ldp, p.BM + 4))
+  if (!make_tmap_T(&tmT, Tp, ndims, dims, I0p, n, p.BN, bnp_of(p.NT), p.KB) ||
+      !make_tmap_U(&tmU, Up[q0], dims[q0], ldp, p.BM + 4, p.KB))
     return JKCALS_E_CUDA;
   MttkrpGeom g;
   g.C = (int)C;
@@ -2603,7 +2631,7 @@ jkcals_status jkcals_mttkrp(int ndims, const int64_t* dims, int n, const double*
   g.KT = p.KT;
   g.units = p.units;
   g.G = p.G;
-  ki->fn[p.WV][p.KM][p.ST4][p.NT - 1]<<<p.G, (kWMs[p.WV] + 1) * 32, p.smem, s>>>(tmT, tmU, v, g, ti, parts);
+  ki->fn[p.KV][p.WV][p.KM][p.ST4][p.NT - 1]<<<p.G, (kWMs[p.WV] + 1) * 32, p.smem, s>>>(tmT, tmU, v, g, ti, parts);
   if (cudaGetLastError() != cudaSuccess) return JKCALS_E_CUDA;
   int64_t tot = dims[n] * C;
   reduce_parts_kernel<<<(int)cdiv(tot, 256), 256, 0, s>>>(parts, ti, (int)dims[n], (int)C, p.BN, p.nMt, M, ldm,

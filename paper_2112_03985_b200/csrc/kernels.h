@@ -22,8 +22,13 @@ typedef size_t (*SmemFn)(int);
 // kWMs[wv] (tile width 16 x WM columns), st = 0 -> 2 stages, 1 -> 4 stages
 constexpr int kNumWM = 2;
 constexpr int kWMs[kNumWM] = {8, 5};
-void dmma_kernels_km0(MttkrpFn fn[kNumWM][2][kMaxNT], SmemFn smem[kNumWM][2][kMaxNT]);
-void dmma_kernels_km1(MttkrpFn fn[kNumWM][2][kMaxNT], SmemFn smem[kNumWM][2][kMaxNT]);
+// and k-tile depth kKBs[kv] (i_q0 values per k-tile: 16, or 20 when it divides I_q0 better)
+constexpr int kNumKB = 2;
+constexpr int kKBs[kNumKB] = {16, 20};
+void dmma_kernels_km0_kb16(MttkrpFn fn[kNumWM][2][kMaxNT], SmemFn smem[kNumWM][2][kMaxNT]);
+void dmma_kernels_km1_kb16(MttkrpFn fn[kNumWM][2][kMaxNT], SmemFn smem[kNumWM][2][kMaxNT]);
+void dmma_kernels_km0_kb20(MttkrpFn fn[kNumWM][2][kMaxNT], SmemFn smem[kNumWM][2][kMaxNT]);
+void dmma_kernels_km1_kb20(MttkrpFn fn[kNumWM][2][kMaxNT], SmemFn smem[kNumWM][2][kMaxNT]);
 
 typedef void (*TfFn)(const CUtensorMap, const CUtensorMap, const CUtensorMap, MttkrpView, TfGeom, const TileInfo*,
                      double*);

@@ -147,27 +147,27 @@ __device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, do
 //           KMAJOR=true  (n >= 1: i_q0 contiguous in T) -> Bt[i][BKP], box (20, BN), BKP = 20.
 // The 4-double over-fetch of each box row makes the row pitch 4 mod 16 doubles, so the 64-bit
 // fragment loads of a half-warp hit 16 distinct bank pairs.
-template <int NT, bool KMAJOR, int STAGES, int WM = kWarps>
+template <int NT, bool KMAJOR, int STAGES, int WM = kWarps, int KB = kBK>
 struct MttkrpCfg {
   static constexpr int BM = WM * 16;  // fused columns of a tile: WM consumer warps x 16
   static constexpr int BMP = BM + 4;  // = 4 mod 16 doubles for WM in {5, 8}: conflict-free loads
   static constexpr int BN = NT * 8;
   static constexpr int BNP = BN + ((4 - BN % 16) + 16) % 16;  // BN rounded up to 4 mod 16
-  static constexpr int BKP = kBK + 4;
-  static constexpr int kBTile = KMAJOR ? BN * BKP : kBK * BNP;  // doubles (= TMA box volume)
+  static constexpr int BKP = KB + ((4 - KB % 16) + 16) % 16;  // KB rounded up to 4 mod 16 (16 -> 20, 20 -> 20)
+  static constexpr int kBTile = KMAJOR ? BN * BKP : KB * BNP;   // doubles (= TMA box volume)
   static constexpr unsigned kTBytes = kBTile * 8u;
-  static constexpr size_t kUb = 2ull * kBK * BMP;               // doubles
+  static constexpr size_t kUb = 2ull * KB * BMP;                // doubles
   __host__ __device__ static size_t stage_doubles(int nslow) { return (size_t)kBTile + (size_t)nslow * BM; }
   __host__ __device__ static size_t smem_bytes(int nslow) {
     return 128 + (kUb + (size_t)STAGES * stage_doubles(nslow)) * sizeof(double) + 2 * STAGES * sizeof(uint64_t);
   }
 };
 
-template <int NT, bool KMAJOR, int STAGES, int WM = kWarps>
+template <int NT, bool KMAJOR, int STAGES, int WM = kWarps, int KB = kBK>
 __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
     mttkrp_dmma_kernel(const __grid_constant__ CUtensorMap tmT, const __grid_constant__ CUtensorMap tmU,
                        MttkrpView v, MttkrpGeom g, const TileInfo* __restrict__ tinfo, double* __restrict__ parts) {
-  using Cfg = MttkrpCfg<NT, KMAJOR, STAGES, WM>;
+  using Cfg = MttkrpCfg<NT, KMAJOR, STAGES, WM, KB>;
   constexpr int BN = Cfg::BN, BNP = Cfg::BNP, BKP = Cfg::BKP, BT = Cfg::kBTile;
   constexpr int BM = Cfg::BM, BMP = Cfg::BMP;
   // (no integer round-trip on the base pointer: it must stay in the shared window so that the
@@ -241,11 +241,11 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
           for (unsigned q = (ld_git >= (unsigned)STAGES ? ld_git - STAGES + 1 : 0); q < ld_git; ++q)
             mbar_wait(&empty[q % STAGES], (q / STAGES) & 1u);
         {
-          mbar_expect_tx(bar, Cfg::kTBytes + s_bytes + (new_slab ? (unsigned)(kBK * BMP * 8) : 0u));
+          mbar_expect_tx(bar, Cfg::kTBytes + s_bytes + (new_slab ? (unsigned)(KB * BMP * 8) : 0u));
           // U_q0 rows [b0*BK, b0*BK+BK) x columns [c0, c0+BMP): OOB rows are zero
-          if (new_slab) tma_load_2d(Ub + (ld_b0 & 1) * (kBK * BMP), &tmU, c0, ld_b0 * kBK, bar);
-          if (KMAJOR) tma_load_4d(st, &tmT, ld_b0 * kBK, ld_ja, i0, ld_jb, bar);  // view (q0, runA, n, runB)
-          else tma_load_4d(st, &tmT, i0, ld_b0 * kBK, ld_ja, ld_jb, bar);
+          if (new_slab) tma_load_2d(Ub + (ld_b0 & 1) * (KB * BMP), &tmU, c0, ld_b0 * KB, bar);
+          if (KMAJOR) tma_load_4d(st, &tmT, ld_b0 * KB, ld_ja, i0, ld_jb, bar);  // view (q0, runA, n, runB)
+          else tma_load_4d(st, &tmT, i0, ld_b0 * KB, ld_ja, ld_jb, bar);
 #pragma unroll
           for (int s = 0; s < kMaxModes - 2; ++s)
             if (s < v.nslow) bulk_load(st + BT + s * BM, v.Us[s] + (int64_t)sidx[s] * g.ldu + c0, BM * 8u, bar);
@@ -304,7 +304,7 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
         const double* st = stage0 + (size_t)slot * stage_sz;
         const double* Bt = st;
         const double* Ss = st + BT;
-        const double* ub = Ub + (cmp_b0 & 1) * (kBK * BMP) + warp * 16 + gid;
+        const double* ub = Ub + (cmp_b0 & 1) * (KB * BMP) + warp * 16 + gid;
         const int cl = warp * 16 + gid;
         double s0 = Ss[cl], s1 = Ss[cl + 8];
         for (int s = 1; s < v.nslow; ++s) {
@@ -312,18 +312,18 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
           s1 *= Ss[s * BM + cl + 8];
         }
         // A fragments of the whole k-tile: KRP^T(c, k) = U_q0(k, c) * S_{j'}(c)
-        double a[kBK / 4][2];
+        double a[KB / 4][2];
 #pragma unroll
-        for (int kk = 0; kk < kBK / 4; ++kk) {
+        for (int kk = 0; kk < KB / 4; ++kk) {
           const int kr = kk * 4 + tig;
           a[kk][0] = ub[kr * BMP] * s0;
           a[kk][1] = ub[kr * BMP + 8] * s1;
         }
-        const int kvalid = v.Iq0 - cmp_b0 * kBK;
-        if (kvalid >= kBK && full_n) {
+        const int kvalid = v.Iq0 - cmp_b0 * KB;
+        if (kvalid >= KB && full_n) {
           // interior tile: no predicates around the MMAs
 #pragma unroll
-          for (int kk = 0; kk < kBK / 4; ++kk) {
+          for (int kk = 0; kk < KB / 4; ++kk) {
             const int kr = kk * 4 + tig;
 #pragma unroll
             for (int ni = 0; ni < NT; ++ni) {
@@ -335,7 +335,7 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
         } else {
           // ragged edge: skip whole k4 steps / n8 tiles outside the tensor (warp-uniform)
 #pragma unroll
-          for (int kk = 0; kk < kBK / 4; ++kk) {
+          for (int kk = 0; kk < KB / 4; ++kk) {
             if (kk * 4 < kvalid) {
               const int kr = kk * 4 + tig;
 #pragma unroll
