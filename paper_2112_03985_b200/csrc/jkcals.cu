@@ -789,6 +789,7 @@ struct jkcals_s {
     int cs = 1, Q = 1, kpc = 1, Cp = 4, slab = 1, rclass = 2;
     size_t smem = 0;
     ResArgs a;
+    bool warp = false;  // tiny tensors: the warp-per-submodel kernel instead (warp_resident.cuh)
   } res;
   int i8 = 0;                          // precision JKCALS_FP64_I8: INT8-sliced FP64-accurate MTTKRP
   I8Plan i8q[kMaxModes];
@@ -1758,9 +1759,28 @@ static size_t res_layout(const jkcals_s* h, int cs, int Cp, int kpc, ResArgs* a)
 static void res_plan(jkcals_t h) {
   h->res.dirty = false;
   h->res.on = false;
-  const char* env = getenv("JKCALS_RESIDENT");  // "0": never; "1": whenever it fits; unset: small tensors
+  h->res.warp = false;
+  // "0": never; "1": the cluster kernel whenever it fits; "2": the warp kernel whenever it fits;
+  // unset: the warp kernel for tiny tensors, the cluster kernel where r02 measured it faster
+  const char* env = getenv("JKCALS_RESIDENT");
   const int mode = env ? atoi(env) : -1;
   if (mode == 0 || h->tf32 || h->i8 || h->mixed || h->R > 8 || h->K < 1) return;
+  if (mode == 2 || mode < 0) {  // tiny tensors: T in one CTA's shared memory, a warp per submodel
+    int dv[kMaxModes];
+    for (int m = 0; m < h->N; ++m) dv[m] = (int)h->dims[m];
+    const size_t wsm = ((size_t)((h->P + 1) & ~1) + (size_t)kWrWarps * wr_warp_doubles(h->N, dv, h->R)) * 8;
+    // (r02: tiny 10x8x6 -- 480 entries; the MTTKRP is lanes-over-rows FMA, so only for small J)
+    if (h->P <= 4096 && wsm <= 200 * 1024 && warp_resident_kernel(2, h->N)) {
+      h->res.on = true;
+      h->res.warp = true;
+      h->res.smem = wsm;
+      h->res.rclass = h->R <= 2 ? 2 : h->R <= 4 ? 4 : 8;
+      cudaFuncSetAttribute(warp_resident_kernel(h->res.rclass, h->N), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)wsm);
+      return;
+    }
+    if (mode == 2) return;
+  }
   double work = (double)h->C * (double)h->P;
   if (mode < 0 && work > (double)(1 << 27)) return;  // large problems: the streamed path is efficient
   const int N = h->N, last = N - 1;
@@ -1830,7 +1850,58 @@ static void res_plan(jkcals_t h) {
                          (int)h->res.smem);
 }
 
+static jkcals_status wr_launch(jkcals_t h, int max_iters) {
+  WrArgs a = {};
+  a.N = h->N;
+  a.R = h->R;
+  a.d = (int)h->d;
+  a.hist_cap = h->hist_cap;
+  a.max_iters = max_iters;
+  a.nsub = h->nsub;
+  a.K = h->K;
+  for (int m = 0; m < h->N; ++m) {
+    a.dims[m] = (int)h->dims[m];
+    a.U[m] = h->U(m);
+  }
+  a.gst[0] = 1;
+  a.gst[1] = h->I0p;
+  for (int m = 2; m < h->N; ++m) a.gst[m] = a.gst[m - 1] * h->dims[m - 1];
+  a.ldu = h->ldu;
+  a.Pel = (int)h->P;
+  a.warp_doubles = wr_warp_doubles(h->N, a.dims, h->R);
+  a.T = h->ptr<double>(h->off.T);
+  a.blk2sub = h->ptr<int>(h->off.blk2sub);
+  a.pglob = h->ptr<int64_t>(h->off.pglob);
+  a.gram = h->ptr<double>(h->off.gram);
+  a.lambda = h->ptr<double>(h->off.lambda);
+  a.normT2p = h->ptr<double>(h->off.normT2p);
+  a.fit = h->ptr<double>(h->off.fit);
+  a.fit_prev = h->ptr<double>(h->off.fit_prev);
+  a.err = h->ptr<double>(h->off.err);
+  a.iters = h->ptr<int>(h->off.iters);
+  a.flags = h->ptr<int>(h->off.flags);
+  a.active = h->ptr<int>(h->off.active);
+  a.hist = h->ptr<double>(h->off.hist);
+  a.tol = reinterpret_cast<const double*>(h->ws + h->off.misc + 8);
+  a.sweeps_out = reinterpret_cast<int*>(h->ws + h->off.misc + 24);
+  CKH(h, cudaMemsetAsync(a.sweeps_out, 0, sizeof(int), h->stream));
+  if (h->instrument) CKH(h, cudaEventRecord(h->ev[0], h->stream));
+  warp_resident_kernel(h->res.rclass, h->N)<<<(unsigned)cdiv(h->K, kWrWarps), kWrWarps * 32, h->res.smem, h->stream>>>(a);
+  CKH(h, cudaGetLastError());
+  if (h->instrument) {
+    CKH(h, cudaEventRecord(h->ev[1], h->stream));
+    CKH(h, cudaEventSynchronize(h->ev[1]));
+    float ms = 0;
+    CKH(h, cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]));
+    h->t_mttkrp[0] += ms;
+    h->launches += 1;
+  }
+  CKH(h, cudaMemcpyAsync(h->pinned_count, a.sweeps_out, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  return JKCALS_OK;
+}
+
 static jkcals_status res_launch(jkcals_t h, int max_iters) {
+  if (h->res.warp) return wr_launch(h, max_iters);
   ResArgs a = h->res.a;
   a.N = h->N;
   a.R = h->R;

@@ -13,6 +13,7 @@
 #include "mttkrp_i8.cuh"
 #include "mttkrp_tf32.cuh"
 #include "resident.cuh"
+#include "warp_resident.cuh"
 
 namespace jk {
 
@@ -58,5 +59,7 @@ GramLargeFn gram_large_kernel_fn();
 // k_resident.cu: the cluster-resident whole-iterate kernel for small tensors (resident.cuh)
 typedef void (*ResFn)(ResArgs);
 ResFn resident_kernel(int rclass);  // rank class: 2, 4 or 8
+typedef void (*WrFn)(WrArgs);
+WrFn warp_resident_kernel(int rclass, int N);  // tiny tensors, N <= 5 (nullptr otherwise): one warp per submodel
 
 }  // namespace jk

@@ -133,3 +133,46 @@ def test_resident_and_standard_paths_continue_each_other(monkeypatch):
         fac, _ = h2.factors(p)
         for a, b in zip(fac, res.factors[p]):
             assert rel(a, b) <= 1e-9, (p, rel(a, b))
+
+
+# ---------------------------------------------------------------- warp-per-submodel kernel (tiny)
+@pytest.fixture
+def warp_path(monkeypatch):
+    monkeypatch.setenv("JKCALS_RESIDENT", "2")
+
+
+def _planted(dims, R, seed):
+    g = np.random.default_rng(seed)
+    A = [g.uniform(0, 1, (I, R)) for I in dims]
+    T = np.zeros(dims)
+    for r in range(R):
+        t = A[0][:, r]
+        for a_ in A[1:]:
+            t = np.multiply.outer(t, a_[:, r])
+        T += t
+    T = np.asfortranarray(T + 0.01 * g.standard_normal(dims))
+    P = [np.asfortranarray(a_ + 0.05 * g.standard_normal(a_.shape)) for a_ in A]
+    return T, P
+
+
+def test_warp_tiny_all_submodels(warp_path):
+    w = make_workload("tiny")
+    h, done = fit(w.T, w.P, w.R, w.sweeps, instrument=True)
+    assert done == w.sweeps and h.kernel_times()[2] == 1
+    res = O.jk_als(w.T, w.P, max_iters=w.sweeps, nthreads=NCPU)
+    check(h, res, range(w.dims[0]), w.T)
+
+
+@pytest.mark.parametrize("dims,R,d,tol", [((12, 9, 7), 3, 1, 0.0), ((7, 5, 6, 4), 2, 1, 0.0), ((9, 6, 5), 4, 2, 0.0),
+                                          ((11, 8, 6), 2, 1, 1e-6), ((6, 5, 4, 3, 2), 3, 1, 0.0)])
+def test_warp_shapes_delete_d_tol(warp_path, dims, R, d, tol):
+    T, P = _planted(dims, R, sum(dims) + R)
+    sweeps = 200 if tol > 0 else 40
+    h, done = fit(T, P, R, sweeps, tol=tol, d=d, hist=sweeps)
+    if d == 1:
+        res = O.jk_als(T, P, max_iters=sweeps, tol=tol, nthreads=NCPU)
+    else:
+        res = O.jk_als_d(T, P, d, max_iters=sweeps, tol=tol, nthreads=NCPU)
+    if tol > 0:
+        assert done == res.iters.max()
+    check(h, res, range(len(O.delete_d_groups(dims[0], d))), T, d=d)
