@@ -214,4 +214,15 @@ __global__ void gather_blocks_kernel(const double* __restrict__ Uold, double* __
   Unew[e] = (c < Cnew) ? Uold[(int64_t)i * ldu + colmap[c]] : 0.0;
 }
 
+// Tolerance-mode loop condition (body tail of the WHILE graph node, jkcals.cu ensure_tol_graph):
+// misc ints [4] active submodels after this sweep (the N-1 epilogue's count), [6] sweeps run by
+// this launch, [8] sweep budget, [9] compaction threshold. Continue while the budget lasts, some
+// submodel is active and fewer than 64 fused columns have converged (Alg. 3 stop / a8 compaction).
+__global__ void tol_decide_kernel(int* __restrict__ misc_i, cudaGraphConditionalHandle hnd) {
+  const int nact = misc_i[4];
+  const int sw = misc_i[6] + 1;
+  misc_i[6] = sw;
+  cudaGraphSetConditional(hnd, (sw < misc_i[8] && nact > misc_i[9]) ? 1u : 0u);
+}
+
 }  // namespace jk

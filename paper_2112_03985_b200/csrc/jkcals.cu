@@ -37,6 +37,51 @@ constexpr size_t kTfSmemMax = 227 * 1024;  // opt-in dynamic shared memory per C
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
 
+// ---------------------------------------------------------------- tuning overrides
+// Every environment knob the library reads, parsed once per process. None changes results (each
+// selects among kernels / tilings that are all parity-tested) and none is needed in production: the
+// defaults are the calibrated cost models below. They exist for the tuning sweeps recorded in
+// DESIGN.md §9c (tools/*.py) and for the tests that pin one kernel path.
+//   JKCALS_FORCE_NT=<mode>:<NT>[,...]  N tile (n8 tiles) per mode        JKCALS_FORCE_WM=<8|5>  tile width
+//   JKCALS_FORCE_KB=<16|20>            k-tile depth                       JKCALS_SK_ALPHA=<a>    stream-K weight
+//   JKCALS_RED_PIECES=<n>              pre-reduce threshold (0: never)
+//   JKCALS_RESIDENT=<0|1|2>            0 streamed only, 1 cluster-resident, 2 warp-resident (unset: auto);
+//                                      read at each plan (tests pin the path per handle), see resident_mode()
+//   JKCALS_TF32_MIN_NNT / JKCALS_TF32_MAX_STAGES   FP32 path N tiles / ring depth
+//   JKCALS_I8_RESIDENT / JKCALS_I8_CLUSTER         FP64_I8 kernel variant
+//   JKCALS_I8_PROBE                    timing-probe builds only (-DJKCALS_DEV_PROBES; wrong results)
+//   JKCALS_TOL_HOST_LOOP=1             tol mode: host check after every sweep (no WHILE graph node)
+struct Tuning {
+  std::string force_nt;
+  int force_wm = 0, force_kb = 0, red_pieces = -1;
+  double sk_alpha = -1.0;
+  int tf32_min_nnt = 0, tf32_max_stages = 8, i8_resident = 0, i8_cluster = 1, i8_probe = 0;
+  int tol_host_loop = 0;
+};
+const Tuning& tuning() {
+  static const Tuning t = [] {
+    Tuning v;
+    auto geti = [](const char* k, int d) { const char* e = getenv(k); return e ? atoi(e) : d; };
+    if (const char* e = getenv("JKCALS_FORCE_NT")) v.force_nt = e;
+    v.force_wm = geti("JKCALS_FORCE_WM", 0);
+    v.force_kb = geti("JKCALS_FORCE_KB", 0);
+    v.red_pieces = geti("JKCALS_RED_PIECES", -1);
+    if (const char* e = getenv("JKCALS_SK_ALPHA")) v.sk_alpha = atof(e);
+    v.tf32_min_nnt = geti("JKCALS_TF32_MIN_NNT", 0);
+    v.tf32_max_stages = geti("JKCALS_TF32_MAX_STAGES", 8);
+    v.i8_resident = geti("JKCALS_I8_RESIDENT", 0);
+    v.i8_cluster = geti("JKCALS_I8_CLUSTER", 1);
+    v.i8_probe = geti("JKCALS_I8_PROBE", 0);
+    v.tol_host_loop = geti("JKCALS_TOL_HOST_LOOP", 0);
+    return v;
+  }();
+  return t;
+}
+int resident_mode() {
+  const char* e = getenv("JKCALS_RESIDENT");
+  return e ? atoi(e) : -1;
+}
+
 // ---------------------------------------------------------------- kernel dispatch tables
 struct KernelInfo {
   MttkrpFn fn[kNumKB][kNumWM][2][2][kMaxNT];         // [k depth kKBs][tile width kWMs][KMAJOR][STAGES==4][NT-1]
@@ -237,7 +282,7 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
     // FP32 (3xTF32 tcgen05) path: UMMA M = 128 fused columns, N = whole I_n up to 256 per tile
     p.tf32 = 1;
     p.nNt = (int)cdiv(mg.In, kTfMaxN);
-    if (const char* e = getenv("JKCALS_TF32_MIN_NNT")) p.nNt = std::max<int>(p.nNt, atoi(e));  // tuning only
+    p.nNt = std::max<int>(p.nNt, tuning().tf32_min_nnt);
     p.BN = (int)rup(cdiv(mg.In, p.nNt), 16);
     p.NT = p.BN / 8;
     p.KM = 1;
@@ -245,8 +290,8 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
     p.KT = (int)(cdiv(mg.Iq0, kTfBK) * mg.Jp);
     p.ntiles = p.nMt * p.nNt;
     p.units = (int64_t)p.ntiles * p.KT;
-    // deepest ring of {8, 6, 4, 3} stages that fits (env JKCALS_TF32_MAX_STAGES caps it, for tuning)
-    static int cap = [] { const char* e = getenv("JKCALS_TF32_MAX_STAGES"); return e ? atoi(e) : 8; }();
+    // deepest ring of {8, 6, 4, 3} stages that fits (JKCALS_TF32_MAX_STAGES caps it, for tuning)
+    const int cap = tuning().tf32_max_stages;
     p.ST4 = 3;
     for (int st : {8, 6, 4})
       if (st <= cap && tf_smem_bytes(p.BN, mg.nslow, st) <= kTfSmemMax) { p.ST4 = st; break; }
@@ -274,8 +319,8 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
     }
   }
   // JKCALS_FORCE_NT=<mode>:<NT>[,<mode>:<NT>...] overrides the model (tuning experiments only)
-  if (const char* e = getenv("JKCALS_FORCE_NT")) {
-    for (const char* q = e; *q;) {
+  if (!tuning().force_nt.empty()) {
+    for (const char* q = tuning().force_nt.c_str(); *q;) {
       int mm = -1, nt = 0, used = 0;
       if (sscanf(q, "%d:%d%n", &mm, &nt, &used) != 2) break;
       if (mm == n && nt >= 1 && nt <= kMaxNT) {
@@ -308,7 +353,7 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
       if (WM < kWMs[0]) cost[wv] /= (p.NT >= 6 ? 0.90 : 0.75);
     }
     p.WV = (cost[1] < 0.97 * cost[0]) ? 1 : 0;
-    static int force_wm = [] { const char* e = getenv("JKCALS_FORCE_WM"); return e ? atoi(e) : 0; }();
+    const int force_wm = tuning().force_wm;
     for (int wv = 0; wv < kNumWM; ++wv)
       if (force_wm == kWMs[wv]) p.WV = wv;
     p.BM = kWMs[p.WV] * 16;
@@ -331,7 +376,7 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
     p.KV = (mg.Jp >= 3 && cost[1] < 0.98 * cost[0] &&
             ki.occ[1][p.WV][p.KM][1][p.NT - 1][mg.nslow] >= ki.occ[0][p.WV][p.KM][1][p.NT - 1][mg.nslow])
                ? 1 : 0;  // (the 20-deep variants need STAGES = 4: J' >= 3)
-    static int force_kb = [] { const char* e = getenv("JKCALS_FORCE_KB"); return e ? atoi(e) : 0; }();
+    const int force_kb = tuning().force_kb;
     for (int kv = 0; kv < kNumKB; ++kv)
       if (force_kb == kKBs[kv] && (kv == 0 || mg.Jp >= 3)) p.KV = kv;
     p.KB = kKBs[p.KV];
@@ -351,7 +396,7 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
   // cost-weighted split only when a tile is mostly idle (e.g. 4-way C = 400: the last M tile
   // has 16 of 128 columns): r01 measured alpha = 0.7 +6 % there, while nearly-full ragged tiles
   // (syn200: 104 of 128) are best with the uniform split. JKCALS_SK_ALPHA overrides (tuning).
-  static double env_alpha = [] { const char* e = getenv("JKCALS_SK_ALPHA"); return e ? atof(e) : -1.0; }();
+  const double env_alpha = tuning().sk_alpha;
   const double live_m = (double)rup(C - (int64_t)(p.nMt - 1) * p.BM, 16) / p.BM;
   const double alpha = env_alpha >= 0.0 ? env_alpha : (live_m < 0.5 ? 0.7 : 1.0);
   finish_plan(p, mg, C, alpha);
@@ -555,8 +600,7 @@ cudaError_t launch_i8(const I8Plan& q, const CUtensorMap& tmA, const CUtensorMap
 // tuning knobs JKCALS_I8_RESIDENT=1 (resident A where I_q0 <= 192; latency-bound, slower) and
 // JKCALS_I8_CLUSTER=0 (the one-CTA streaming kernel)
 int i8_variant(const KernelInfo& ki, int64_t KP) {
-  static const int res = getenv("JKCALS_I8_RESIDENT") ? atoi(getenv("JKCALS_I8_RESIDENT")) : 0;
-  static const int clu = getenv("JKCALS_I8_CLUSTER") ? atoi(getenv("JKCALS_I8_CLUSTER")) : 1;
+  const int res = tuning().i8_resident, clu = tuning().i8_cluster;
   if (res && KP / kI8K <= kI8ResKS) return 1;
   if (clu && ki.i8clusters >= 1) return 2;
   return 0;
@@ -797,6 +841,10 @@ struct jkcals_s {
   CUtensorMap tmThi[kMaxModes], tmTlo[kMaxModes];
   cudaGraphExec_t gexec = nullptr;
   bool graph_ok = false;
+  // tolerance mode: a CUDA-graph WHILE node repeats the sweep until the device-side trigger
+  // (tol_decide_kernel) sees the call's sweep budget spent or enough convergence to compact
+  cudaGraphExec_t gexec_tol = nullptr;
+  bool tol_graph_bad = false;  // conditional nodes unavailable: per-sweep host check
   bool inited = false;
   bool ran = false;
   double tol_host = 0.0;
@@ -871,7 +919,7 @@ jkcals_status replan(jkcals_t h) {
     // many pieces per tile: pre-reduce them with the whole GPU (kRedPieces, r01: G = 8 shard)
     int maxp = 0;
     for (const TileInfo& ti : p.tinfo) maxp = std::max(maxp, ti.npieces);
-    static int red_thr = [] { const char* e = getenv("JKCALS_RED_PIECES"); return e ? atoi(e) : kRedPieces; }();
+    const int red_thr = tuning().red_pieces >= 0 ? tuning().red_pieces : kRedPieces;
     // ... and only when each epilogue CTA would sum many pieces over many rows (r01: a syn200 shard
     // at G = 8, I_n x pieces = 200 x 59, gains 14 %; syn50, 50 x 48, loses 20 % to the extra launch)
     h->red_on[n] = red_thr > 0 && maxp > red_thr && h->dims[n] * maxp > 8192;
@@ -946,6 +994,10 @@ jkcals_status replan(jkcals_t h) {
   if (h->gexec) {
     cudaGraphExecDestroy(h->gexec);
     h->gexec = nullptr;
+  }
+  if (h->gexec_tol) {
+    cudaGraphExecDestroy(h->gexec_tol);
+    h->gexec_tol = nullptr;
   }
   h->graph_ok = false;
   return JKCALS_OK;
@@ -1040,7 +1092,7 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     }
     ig.ldu = h->ldu;
 #ifdef JKCALS_DEV_PROBES  // timing-probe builds only (tools/i8_probe.py); results are wrong when set
-    ig.probe = getenv("JKCALS_I8_PROBE") ? atoi(getenv("JKCALS_I8_PROBE")) : 0;
+    ig.probe = tuning().i8_probe;
 #endif
     ig.eT = h->ptr<int>(h->off.i8eT[n]);
     ig.dS = h->ptr<int8_t>(h->off.i8dS[n]);
@@ -1191,6 +1243,56 @@ jkcals_status ensure_graph(jkcals_t h) {
   cudaGraphDestroy(graph);
   if (e != cudaSuccess) return fail(h, JKCALS_E_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
   h->graph_ok = true;
+  return JKCALS_OK;
+}
+
+// Tolerance mode without a host round trip per sweep: graph = WHILE(cond) { sweep; tol_decide },
+// the condition set on the device from the active-submodel count (misc+16) against the compaction
+// threshold and this call's sweep budget (misc+32 / +36, written by the host before each launch).
+// The host wakes only when the loop exits: to compact (a8), or at the end of the call.
+jkcals_status ensure_tol_graph(jkcals_t h) {
+  if (h->gexec_tol || h->tol_graph_bad || tuning().tol_host_loop) return JKCALS_OK;
+  cudaGraph_t graph = nullptr;
+  cudaGraphConditionalHandle hnd;
+  auto bad = [&](cudaError_t e) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    h->tol_graph_bad = true;  // (logged in last_error; iterate falls back to the per-sweep check)
+    h->err = std::string("conditional graph unavailable: ") + cudaGetErrorString(e);
+    return JKCALS_OK;
+  };
+  cudaError_t e = cudaGraphCreate(&graph, 0);
+  if (e != cudaSuccess) return bad(e);
+  e = cudaGraphConditionalHandleCreate(&hnd, graph, 1, cudaGraphCondAssignDefault);
+  if (e != cudaSuccess) return bad(e);
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = hnd;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  e = cudaGraphAddNode(&node, graph, nullptr, 0, &cp);
+  if (e != cudaSuccess) return bad(e);
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  e = cudaStreamBeginCaptureToGraph(h->cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return bad(e);
+  h->es = h->cap;
+  jkcals_status st = enqueue_sweep(h, false);
+  tol_decide_kernel<<<1, 1, 0, h->cap>>>(reinterpret_cast<int*>(h->ws + h->off.misc), hnd);
+  h->es = h->stream;
+  cudaGraph_t got = nullptr;
+  e = cudaStreamEndCapture(h->cap, &got);
+  if (st != JKCALS_OK) {
+    cudaGraphDestroy(graph);
+    return st;
+  }
+  if (e != cudaSuccess) return bad(e);
+  e = cudaGraphInstantiate(&h->gexec_tol, graph, 0);
+  if (e != cudaSuccess) {
+    h->gexec_tol = nullptr;
+    return bad(e);
+  }
+  cudaGraphDestroy(graph);
   return JKCALS_OK;
 }
 
@@ -1501,7 +1603,7 @@ jkcals_status jkcals_create_config(jkcals_t* out, const jkcals_config* cfg, cons
   h->ws_bytes = workspace_bytes - (aligned - base);
   *out = h;
 
-  CKH(h, cudaMallocHost(&h->pinned_count, sizeof(int)));
+  CKH(h, cudaMallocHost(&h->pinned_count, 4 * sizeof(int)));
   CKH(h, cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
   for (auto& e : h->ev) CKH(h, cudaEventCreate(&e));
   // T into the workspace with its mode-0 pitch padded to I0p (zero pad row when I0 is odd)
@@ -1762,8 +1864,7 @@ static void res_plan(jkcals_t h) {
   h->res.warp = false;
   // "0": never; "1": the cluster kernel whenever it fits; "2": the warp kernel whenever it fits;
   // unset: the warp kernel for tiny tensors, the cluster kernel where r02 measured it faster
-  const char* env = getenv("JKCALS_RESIDENT");
-  const int mode = env ? atoi(env) : -1;
+  const int mode = resident_mode();
   if (mode == 0 || h->tf32 || h->i8 || h->mixed || h->R > 8 || h->K < 1) return;
   if (mode == 2 || mode < 0) {  // tiny tensors: T in one CTA's shared memory, a warp per submodel
     int dv[kMaxModes];
@@ -1978,7 +2079,8 @@ jkcals_status jkcals_iterate(jkcals_t h, int max_iters, double tol, int* sweeps_
   if (h->tf32 && (tol > 0.0) != h->f64last) {  // switch the last mode's MTTKRP kernel: re-capture
     h->f64last = tol > 0.0;
     if (h->gexec) cudaGraphExecDestroy(h->gexec);
-    h->gexec = nullptr;
+    if (h->gexec_tol) cudaGraphExecDestroy(h->gexec_tol);
+    h->gexec = h->gexec_tol = nullptr;
     h->graph_ok = false;
   }
   h->tol_host = tol;
@@ -1993,6 +2095,31 @@ jkcals_status jkcals_iterate(jkcals_t h, int max_iters, double tol, int* sweeps_
     return JKCALS_OK;
   }
   int it = 0;
+  if (tol > 0.0 && !h->instrument) {
+    jkcals_status st = ensure_tol_graph(h);
+    if (st != JKCALS_OK) return st;
+  }
+  while (tol > 0.0 && !h->instrument && h->gexec_tol && it < max_iters && h->K > 0) {
+    // device-side trigger: one graph launch runs sweeps until compaction is due or the budget ends
+    const int cs = (64 + h->R - 1) / h->R;  // compact once >= 64 fused columns have converged
+    int* pin = h->pinned_count;
+    pin[0] = 0;                                  // misc+24: sweeps run by this launch
+    pin[1] = 0;
+    pin[2] = max_iters - it;                     // misc+32: sweep budget
+    pin[3] = std::max(0, h->K - cs);             // misc+36: continue while active > this
+    CKH(h, cudaMemcpyAsync(h->ws + h->off.misc + 24, pin, 4 * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+    CKH(h, cudaGraphLaunch(h->gexec_tol, h->stream));
+    CKH(h, cudaMemcpyAsync(pin, h->ws + h->off.misc + 16, 4 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CKH(h, cudaStreamSynchronize(h->stream));
+    const int nact = pin[0], ran = pin[2];
+    it += ran;
+    if (nact == 0 || (int64_t)(h->K - nact) * h->R >= 64) {
+      jkcals_status st2 = compact(h);
+      if (st2 != JKCALS_OK) return st2;
+      st2 = ensure_tol_graph(h);
+      if (st2 != JKCALS_OK) return st2;
+    }
+  }
   for (; it < max_iters && h->K > 0; ++it) {
     if (h->instrument) {
       jkcals_status st = enqueue_sweep(h, true);
@@ -2624,6 +2751,7 @@ void jkcals_destroy(jkcals_t h) {
   if (!h) return;
   DeviceGuard dg(h->device);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  if (h->gexec_tol) cudaGraphExecDestroy(h->gexec_tol);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
   if (h->pinned_count) cudaFreeHost(h->pinned_count);
@@ -2833,7 +2961,7 @@ jkcals_status jkcals_mttkrp_i8(int ndims, const int64_t* dims, int n, const doub
   g.dS = x.dS;
   g.eU = x.eU;
 #ifdef JKCALS_DEV_PROBES  // timing-probe builds only: 1 = drain skipped, 2 = one product per K32 step
-  g.probe = getenv("JKCALS_I8_PROBE") ? atoi(getenv("JKCALS_I8_PROBE")) : 0;
+  g.probe = tuning().i8_probe;
 #endif
   if (launch_i8(q, tmA, tmB, g, x.ti, x.parts, s) != cudaSuccess) return JKCALS_E_CUDA;
   const int64_t tot = q.In * C;

@@ -189,6 +189,28 @@ def test_tolerance_mode_and_compaction():
     check_against_oracle(h, res, range(50), nt2p_of(w.T))
 
 
+def test_tol_device_trigger_equals_host_loop(monkeypatch):
+    # tolerance mode runs as a CUDA-graph WHILE loop whose condition a device kernel sets (no host
+    # round trip per sweep; the host wakes only to compact). The instrumented path checks on the
+    # host after every sweep; both must stop at the same sweep with bit-identical factors, across
+    # several compactions (syn50 R3: 64 fused columns converge -> compact).
+    from paper_2112_03985_b200.jkcals import lib
+    monkeypatch.setenv("JKCALS_RESIDENT", "0")
+    w = make_workload("syn50_r3")
+    h1, d1 = run_gpu(w, 1000, tol=1e-6, hist_cap=1000)
+    assert "conditional graph" not in lib().jkcals_last_error(h1._h).decode()
+    h2, d2 = run_gpu(w, 1000, tol=1e-6, hist_cap=1000, instrument=True)
+    assert d1 == d2
+    s1, s2 = h1.status(), h2.status()
+    assert np.array_equal(s1["iters"], s2["iters"]) and np.array_equal(s1["flags"], s2["flags"])
+    for p in range(50):
+        for a, b in zip(h1.factors(p)[0], h2.factors(p)[0]):
+            assert np.array_equal(a, b), p
+    # a sweep budget that ends mid-run is honoured exactly
+    h3, d3 = run_gpu(w, 7, tol=1e-6, hist_cap=1000)
+    assert d3 == 7 and np.all(h3.status()["iters"] <= 7)
+
+
 def test_shards_equal_full_and_merge():
     from paper_2112_03985_b200.dist import jackknife_std, merge_moments
     w = make_workload("syn50_r2")

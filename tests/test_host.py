@@ -45,7 +45,8 @@ def test_library_is_sm100a():
                           text=True).stdout
     funcs = sass.split("Function : ")
     hot = [f for f in funcs if f.startswith("_ZN2jk18mttkrp_dmma_kernel")]
-    assert len(hot) == 32  # NT 1..8 x {n == 0, n >= 1} x {2, 4} stages
+    # NT 1..8 x {n == 0, n >= 1} x {2, 4} stages x {128, 80}-column tiles x {16, 20}-deep k-tiles
+    assert len(hot) == 128
     for f in hot:
         assert "DMMA" in f     # FP64 tensor-pipe instruction in the hot kernel
         assert "UTMALDG" in f  # TMA (cp.async.bulk.tensor) staging of the tensor tiles
