@@ -12,6 +12,9 @@
 //           convergence mask (|fit - fit_prev| < tol from sweep 2)          (a7)
 // Everything is summed in a fixed order, so results are run-to-run deterministic.
 #pragma once
+#ifdef JK_EPI_PROF
+#include <cstdio>
+#endif
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -56,32 +59,52 @@ constexpr int kEpiThreads = 128;
 
 // Pre-reduction of the stream-K partial pieces for tiles split over many CTAs (a small-C shard
 // fills the GPU with up to 64 CTAs per tile; one epilogue CTA per submodel would otherwise sum
-// them alone). Element e of tile t: red[t][e] = ((0 + p_0) + p_1) + ... in piece order -- the
-// very sum the epilogue forms itself, so results are bitwise those of the direct path. The
-// epilogue then reads one piece per tile.
-__global__ void __launch_bounds__(256) reduce_pieces_kernel(const double* __restrict__ parts,
-                                                            const TileInfo* __restrict__ tinfo, int ntiles,
-                                                            int tile_elems, double* __restrict__ red) {
+// them alone). One CTA per 32 consecutive elements of a tile (tile_elems = BN x BM is a multiple
+// of 128): warp w sums the w-th contiguous eighth of the piece range with all of its loads in
+// flight (coalesced 256 B rows), then warp 0 adds the eight partials in warp order. The order is
+// fixed, so results are deterministic; a one-thread-per-element loop was latency-bound (r02: a
+// syn200 shard at G = 8, 59 pieces per tile: 13.5 us per mode). The epilogue then reads one piece
+// per tile.
+constexpr int kRedWarps = 8;
+__global__ void __launch_bounds__(32 * kRedWarps) reduce_pieces_kernel(const double* __restrict__ parts,
+                                                                       const TileInfo* __restrict__ tinfo, int ntiles,
+                                                                       int tile_elems, double* __restrict__ red) {
+  __shared__ double part[kRedWarps][32];
   asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the MTTKRP grid has completed
   asm volatile("griddepcontrol.launch_dependents;\n" :::);
-  const int64_t total = (int64_t)ntiles * tile_elems;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int t = (int)(e / tile_elems);
-    const int64_t o = e - (int64_t)t * tile_elems;
-    const TileInfo ti = tinfo[t];
-    const double* p = parts + (int64_t)ti.piece_base * tile_elems + o;
-    double s = 0.0;
-    int pc = 0;
-    for (; pc + 8 <= ti.npieces; pc += 8) {
-      double x[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t e = (int64_t)blockIdx.x * 32 + lane;
+  const int t = (int)((int64_t)blockIdx.x * 32 / tile_elems);
+  const TileInfo ti = tinfo[t];
+  const int64_t o = e - (int64_t)t * tile_elems;
+  const double* p = parts + (int64_t)ti.piece_base * tile_elems + o;
+  const int lo = (int)((int64_t)ti.npieces * w / kRedWarps), hi = (int)((int64_t)ti.npieces * (w + 1) / kRedWarps);
+  double s = 0.0;
+  int pc = lo;
+  for (; pc + 8 <= hi; pc += 8) {
+    double x[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) x[q] = __ldcg(p + (int64_t)(pc + q) * tile_elems);
+    for (int q = 0; q < 8; ++q) x[q] = __ldcg(p + (int64_t)(pc + q) * tile_elems);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) s += x[q];
-    }
-    for (; pc < ti.npieces; ++pc) s += __ldcg(p + (int64_t)pc * tile_elems);
-    red[e] = s;
+    for (int q = 0; q < 8; ++q) s += x[q];
   }
+  {
+    double x[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = (pc + q < hi) ? __ldcg(p + (int64_t)(pc + q) * tile_elems) : 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (pc + q < hi) s += x[q];
+  }
+  part[w][lane] = s;
+  __syncthreads();
+  if (w == 0) {
+    double r = part[0][lane];
+#pragma unroll
+    for (int q = 1; q < kRedWarps; ++q) r += part[q][lane];
+    red[e] = r;
+  }
+  (void)ntiles;
 }
 #endif
 

@@ -48,6 +48,7 @@ inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
 //   JKCALS_RESIDENT=<0|1|2>            0 streamed only, 1 cluster-resident, 2 warp-resident (unset: auto);
 //                                      read at each plan (tests pin the path per handle), see resident_mode()
 //   JKCALS_TF32_MIN_NNT / JKCALS_TF32_MAX_STAGES   FP32 path N tiles / ring depth
+//   JKCALS_TF32_PAIR=0                 FP32 path: one-CTA kernel only (no cta_group::2 pairs)
 //   JKCALS_I8_RESIDENT / JKCALS_I8_CLUSTER         FP64_I8 kernel variant
 //   JKCALS_I8_PROBE                    timing-probe builds only (-DJKCALS_DEV_PROBES; wrong results)
 //   JKCALS_TOL_HOST_LOOP=1             tol mode: host check after every sweep (no WHILE graph node)
@@ -56,7 +57,7 @@ struct Tuning {
   int force_wm = 0, force_kb = 0, red_pieces = -1;
   double sk_alpha = -1.0;
   int tf32_min_nnt = 0, tf32_max_stages = 8, i8_resident = 0, i8_cluster = 1, i8_probe = 0;
-  int tol_host_loop = 0;
+  int tol_host_loop = 0, tf32_pair = 1;
 };
 const Tuning& tuning() {
   static const Tuning t = [] {
@@ -73,6 +74,7 @@ const Tuning& tuning() {
     v.i8_cluster = geti("JKCALS_I8_CLUSTER", 1);
     v.i8_probe = geti("JKCALS_I8_PROBE", 0);
     v.tol_host_loop = geti("JKCALS_TOL_HOST_LOOP", 0);
+    v.tf32_pair = geti("JKCALS_TF32_PAIR", 1);
     return v;
   }();
   return t;
@@ -89,6 +91,7 @@ struct KernelInfo {
   int occ[kNumKB][kNumWM][2][2][kMaxNT][kMaxModes];  // [..][nslow]
   int nsm;
   int i8clusters;                    // co-resident 2-CTA clusters of the INT8 cluster kernel (0: none)
+  int tfpairs = 0;                   // co-resident CTA pairs of the FP32 cta_group::2 kernel (0: none)
 };
 
 KernelInfo* kernel_info(int device, std::string* err) {
@@ -119,9 +122,11 @@ KernelInfo* kernel_info(int device, std::string* err) {
   cudaDeviceGetAttribute(&ki.nsm, cudaDevAttrMultiProcessorCount, device);
   {
     cudaError_t e = cudaSuccess;
-    for (int st : {3, 4, 6, 8})
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(tf32_kernel(st), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTfSmemMax);
+    for (bool pair : {false, true})
+      for (int st : {3, 4, 6, 8})
+        if (e == cudaSuccess)
+          e = cudaFuncSetAttribute(tf32_kernel(st, pair), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kTfSmemMax);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(i8_kernel(0), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8Smem);
     if (e == cudaSuccess)
@@ -153,6 +158,13 @@ KernelInfo* kernel_info(int device, std::string* err) {
       if (cudaOccupancyMaxActiveClusters(&ncl, i8_kernel(2), &cfg) == cudaSuccess)
         ki.i8clusters = ncl;
       cudaGetLastError();  // the query is advisory: 0 falls back to the one-CTA kernel
+      // CTA pairs of the FP32 path (one CTA per SM): co-resident pairs at the largest ring
+      cfg.blockDim = dim3(kTfThreads);
+      cfg.dynamicSmemBytes = kTfSmemMax;
+      ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, tf32_kernel(8, true), &cfg) == cudaSuccess)
+        ki.tfpairs = ncl;
+      cudaGetLastError();
     }
     if (e != cudaSuccess) {
       if (err) *err = std::string("cudaFuncSetAttribute(tf32): ") + cudaGetErrorString(e);
@@ -213,6 +225,7 @@ struct ModePlan {
   std::vector<TileInfo> tinfo;
   std::vector<int> cta_u;  // CTA b processes units [cta_u[b], cta_u[b+1])
   int tf32 = 0;
+  int pair = 0, nMt2 = 1;  // FP32 path: CTA-pair kernel on 256-column super tiles (nMt2 per tile row)
 };
 
 // stream-K CTA ranges, per-tile piece bookkeeping (shared by the FP64 and TF32 plans).
@@ -288,16 +301,49 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
     p.KM = 1;
     p.nMt = (int)std::max<int64_t>(1, cdiv(C, kBM));
     p.KT = (int)(cdiv(mg.Iq0, kTfBK) * mg.Jp);
-    p.ntiles = p.nMt * p.nNt;
-    p.units = (int64_t)p.ntiles * p.KT;
+    // CTA pairs (cta_group::2, UMMA M = 256) whenever there are two 128-column tiles to pair:
+    // each SM then reads A + B/2 instead of A + B from shared memory per MMA
+    p.pair = (p.nMt >= 2 && ki.tfpairs > 0 && tuning().tf32_pair) ? 1 : 0;
+    const int BNl = p.pair ? p.BN / 2 : p.BN;
     // deepest ring of {8, 6, 4, 3} stages that fits (JKCALS_TF32_MAX_STAGES caps it, for tuning)
     const int cap = tuning().tf32_max_stages;
     p.ST4 = 3;
     for (int st : {8, 6, 4})
-      if (st <= cap && tf_smem_bytes(p.BN, mg.nslow, st) <= kTfSmemMax) { p.ST4 = st; break; }
-    p.smem = tf_smem_bytes(p.BN, mg.nslow, p.ST4);
-    p.G = (int)std::min<int64_t>(p.units, std::min<int64_t>((int64_t)ki.nsm, 48 * (int64_t)p.ntiles));
-    finish_plan(p, mg);
+      if (st <= cap && tf_smem_bytes(BNl, mg.nslow, st) <= kTfSmemMax) { p.ST4 = st; break; }
+    p.smem = tf_smem_bytes(BNl, mg.nslow, p.ST4);
+    if (!p.pair) {
+      p.ntiles = p.nMt * p.nNt;
+      p.units = (int64_t)p.ntiles * p.KT;
+      p.G = (int)std::min<int64_t>(p.units, std::min<int64_t>((int64_t)ki.nsm, 48 * (int64_t)p.ntiles));
+      finish_plan(p, mg);
+      return p;
+    }
+    // stream-K over super tiles (pairs are the plan's CTAs), then one piece table entry per
+    // 128-column tile: both halves of a super tile share its CTA range and piece count
+    ModePlan q = p;
+    q.nMt = (int)cdiv(p.nMt, 2);
+    q.ntiles = q.nMt * q.nNt;
+    q.units = (int64_t)q.ntiles * q.KT;
+    q.G = (int)std::min<int64_t>(q.units, std::min<int64_t>((int64_t)ki.tfpairs, 48 * (int64_t)q.ntiles));
+    finish_plan(q, mg);
+    p.nMt2 = q.nMt;
+    p.units = q.units;
+    p.G = q.G;
+    p.cta_u = q.cta_u;
+    p.ntiles = p.nMt * p.nNt;
+    p.tinfo.resize(p.ntiles);
+    int base = 0;
+    for (int tn = 0; tn < p.nNt; ++tn)
+      for (int tm = 0; tm < p.nMt; ++tm) {
+        const TileInfo& st = q.tinfo[tn * q.nMt + tm / 2];
+        TileInfo& ti = p.tinfo[tn * p.nMt + tm];
+        ti.first_cta = st.first_cta;
+        ti.npieces = st.npieces;
+        ti.piece_base = base;
+        ti.pad_ = 0;
+        base += st.npieces;
+      }
+    p.npieces = base;
     return p;
   }
   // N tiling: NT n8 tiles per CTA tile. Score = useful/issued n8 slots x NT/(NT + 1), the second
@@ -952,8 +998,8 @@ jkcals_status replan(jkcals_t h) {
         const int64_t ld1 = rup(h->dims[1], 4), rest = h->P / (h->dims[0] * h->dims[1]);
         gd[0] = h->dims[1]; gd[1] = 1; gd[2] = h->dims[0]; gd[3] = rest;
         gs[0] = ld1; gs[1] = ld1; gs[2] = ld1 * h->dims[0];
-        if (!make_tmap_T32(&h->tmThi[n], h->ptr<float>(h->off.T1hi), gd, gs, p.BN) ||
-            !make_tmap_T32(&h->tmTlo[n], h->ptr<float>(h->off.T1lo), gd, gs, p.BN))
+        if (!make_tmap_T32(&h->tmThi[n], h->ptr<float>(h->off.T1hi), gd, gs, p.pair ? p.BN / 2 : p.BN) ||
+            !make_tmap_T32(&h->tmTlo[n], h->ptr<float>(h->off.T1lo), gd, gs, p.pair ? p.BN / 2 : p.BN))
           return fail(h, JKCALS_E_CUDA, "cuTensorMapEncodeTiled failed for the fp32 view of mode 0");
       } else {
         const int64_t ld0 = rup(h->dims[0], 4);
@@ -962,8 +1008,8 @@ jkcals_status replan(jkcals_t h) {
         for (int m = n + 1; m < h->N; ++m) runB *= h->dims[m];
         gd[0] = h->dims[0]; gd[1] = runA; gd[2] = h->dims[n]; gd[3] = runB;
         gs[0] = ld0; gs[1] = st_n; gs[2] = st_n * h->dims[n];
-        if (!make_tmap_T32(&h->tmThi[n], h->ptr<float>(h->off.T32hi), gd, gs, p.BN) ||
-            !make_tmap_T32(&h->tmTlo[n], h->ptr<float>(h->off.T32lo), gd, gs, p.BN))
+        if (!make_tmap_T32(&h->tmThi[n], h->ptr<float>(h->off.T32hi), gd, gs, p.pair ? p.BN / 2 : p.BN) ||
+            !make_tmap_T32(&h->tmTlo[n], h->ptr<float>(h->off.T32lo), gd, gs, p.pair ? p.BN / 2 : p.BN))
           return fail(h, JKCALS_E_CUDA, "cuTensorMapEncodeTiled failed for the fp32 view of mode %d", n);
       }
     }
@@ -1102,7 +1148,8 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     TfGeom tg;
     tg.C = h->C;
     tg.ldu = h->ldu;
-    tg.nMt = p.nMt;
+    tg.nMt = p.pair ? p.nMt2 : p.nMt;
+    tg.nMt1 = p.nMt;
     tg.nNt = p.nNt;
     tg.BN = p.BN;
     tg.KT = p.KT;
@@ -1110,18 +1157,22 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     tg.G = p.G;
     if (n == 0) v.runA = 1;  // the n = 0 fp32 view carries j' in its runB coordinate
     cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = (h->pdl && !timed) ? 1 : 0;
-    cfg.gridDim = dim3(p.G);
+    attr[1].id = cudaLaunchAttributeClusterDimension;  // (PAIR: 2-CTA clusters)
+    attr[1].val.clusterDim.x = 2;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(p.pair ? 2 * p.G : p.G);
     cfg.blockDim = dim3(kTfThreads);
     cfg.dynamicSmemBytes = p.smem;
     cfg.stream = h->es;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = p.pair ? 2 : 1;
     tg.stages = p.ST4;
-    CKH(h, cudaLaunchKernelEx(&cfg, tf32_kernel(p.ST4), h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v, tg, ti,
-                              parts));
+    CKH(h, cudaLaunchKernelEx(&cfg, tf32_kernel(p.ST4, p.pair != 0), h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v,
+                              tg, ti, parts));
   } else {
     MttkrpFn fn = h->ki->fn[p.KV][p.WV][p.KM][p.ST4][p.NT - 1];
     // programmatic dependent launch: this grid may start (prologue) while the previous kernel
@@ -1150,8 +1201,8 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = (h->pdl && !timed) ? 1 : 0;
-    cfg.gridDim = dim3((unsigned)std::min<int64_t>(cdiv(tot, 256), 4 * (int64_t)h->ki->nsm));
-    cfg.blockDim = dim3(256);
+    cfg.gridDim = dim3((unsigned)(tot / 32));  // one CTA per 32 elements (tile_elems % 32 == 0)
+    cfg.blockDim = dim3(32 * kRedWarps);
     cfg.stream = h->es;
     cfg.attrs = attr;
     cfg.numAttrs = 1;

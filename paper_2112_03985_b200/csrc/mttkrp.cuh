@@ -193,11 +193,6 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   }
   __syncthreads();
-  // programmatic dependent launch: everything above overlapped the previous kernel's tail;
-  // U and the partial buffer are only touched after the previous grid has fully completed.
-  // The dependent epilogue grid may be scheduled right away (its CTAs wait likewise).
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;\n" :::);
 
   // =========================== producer warp (warp WM, one lane) ===========================
   // (r01: a warp-uniform loop with elect.sync measured no faster here -- the FP64 kernel is
@@ -205,6 +200,39 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
   if (warp == WM) {
     if (lane != 0) return;
     const unsigned s_bytes = (unsigned)v.nslow * BM * 8u;
+    // programmatic dependent launch: T is constant, so the T tiles of the first STAGES k-tiles
+    // are requested BEFORE waiting for the previous grid (the previous mode's epilogue, which
+    // writes U); their barriers expect the full tile bytes and complete once the U rows issued
+    // after the wait land too. U and the partial buffer are only touched after the wait.
+    int npre = 0;
+    if (u0 < u1) {
+      const int t = (int)(u0 / g.KT);
+      const int kt0 = (int)(u0 % g.KT);
+      const int64_t kt_end = (int64_t)kt0 + (u1 - u0);
+      const int kt1 = (int)(kt_end < (int64_t)g.KT ? kt_end : (int64_t)g.KT);
+      npre = kt1 - kt0 < STAGES ? kt1 - kt0 : STAGES;
+      const int i0 = (t / g.nMt) * BN;
+      int b0 = kt0 / v.Jp, jp = kt0 % v.Jp, ja = jp % v.runA, jb = jp / v.runA, lb0 = -1;
+      for (int q = 0; q < npre; ++q) {
+        double* st = stage0 + (size_t)q * stage_sz;
+        const bool new_slab = (b0 != lb0);
+        mbar_expect_tx(&full[q], Cfg::kTBytes + s_bytes + (new_slab ? (unsigned)(KB * BMP * 8) : 0u));
+        if (KMAJOR) tma_load_4d(st, &tmT, b0 * KB, ja, i0, jb, &full[q]);
+        else tma_load_4d(st, &tmT, i0, b0 * KB, ja, jb, &full[q]);
+        lb0 = b0;
+        if (++jp == v.Jp) {
+          jp = 0;
+          ++b0;
+        }
+        if (++ja == v.runA) {
+          ja = 0;
+          ++jb;
+        }
+        if (jp == 0) jb = 0;
+      }
+    }
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" :::);
     unsigned ld_git = 0;  // tiles issued by this CTA (ring slot + phase)
     for (int64_t u = u0; u < u1;) {
       const int t = (int)(u / g.KT);
@@ -241,11 +269,14 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
           for (unsigned q = (ld_git >= (unsigned)STAGES ? ld_git - STAGES + 1 : 0); q < ld_git; ++q)
             mbar_wait(&empty[q % STAGES], (q / STAGES) & 1u);
         {
-          mbar_expect_tx(bar, Cfg::kTBytes + s_bytes + (new_slab ? (unsigned)(KB * BMP * 8) : 0u));
+          const bool pre = ld_git < (unsigned)npre;  // T already requested before the wait
+          if (!pre) mbar_expect_tx(bar, Cfg::kTBytes + s_bytes + (new_slab ? (unsigned)(KB * BMP * 8) : 0u));
           // U_q0 rows [b0*BK, b0*BK+BK) x columns [c0, c0+BMP): OOB rows are zero
           if (new_slab) tma_load_2d(Ub + (ld_b0 & 1) * (KB * BMP), &tmU, c0, ld_b0 * KB, bar);
-          if (KMAJOR) tma_load_4d(st, &tmT, ld_b0 * KB, ld_ja, i0, ld_jb, bar);  // view (q0, runA, n, runB)
-          else tma_load_4d(st, &tmT, i0, ld_b0 * KB, ld_ja, ld_jb, bar);
+          if (!pre) {
+            if (KMAJOR) tma_load_4d(st, &tmT, ld_b0 * KB, ld_ja, i0, ld_jb, bar);  // view (q0, runA, n, runB)
+            else tma_load_4d(st, &tmT, i0, ld_b0 * KB, ld_ja, ld_jb, bar);
+          }
 #pragma unroll
           for (int s = 0; s < kMaxModes - 2; ++s)
             if (s < v.nslow) bulk_load(st + BT + s * BM, v.Us[s] + (int64_t)sidx[s] * g.ldu + c0, BM * 8u, bar);
@@ -273,6 +304,9 @@ __global__ void __maxnreg__(NT <= 6 ? 96 : 112)
     }
     return;
   }
+  // consumers: the parts buffer (written at the end) may still be read by the previous grid
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" :::);
 
   // =========================== consumer warps 0..WM-1 ===========================
   const int gid = lane >> 2, tig = lane & 3;

@@ -49,14 +49,6 @@ constexpr size_t kI8ABytesClu = (size_t)8 * 128 * kI8K;  // 8 slice slots (slot 
 constexpr size_t kI8StageBytesClu = kI8ABytesClu + kI8BBytes;
 constexpr size_t kI8SmemClu = 1024 + kI8Stages * kI8StageBytesClu + 256;
 
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
 __device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar,
                                                uint16_t mask) {
   asm volatile(

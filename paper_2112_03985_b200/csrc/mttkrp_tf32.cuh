@@ -43,7 +43,8 @@ constexpr int kTfMaxStages = 8;
 struct TfGeom {
   int C;          // fused width in use
   int64_t ldu;    // pitch of the FP64 multi-factors (multiple of 128)
-  int nMt, nNt;   // output tiles (C / 128, I_n / BN)
+  int nMt, nNt;   // output tiles (C / 128 -- C / 256 super tiles when paired --, I_n / BN)
+  int nMt1;       // 128-column tiles per tile row (the piece table; = nMt unless paired)
   int BN;         // UMMA N of an output tile (multiple of 16, <= 256)
   int KT;         // k-tiles per output tile (nb0 * J')
   int64_t units;
@@ -66,8 +67,8 @@ __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
          ((uint64_t)1u << 46) | ((uint64_t)4u << 61);
 }
 // instruction descriptor: D fp32, A/B tf32, both K-major, M = 128, N = BN
-__device__ __forceinline__ uint32_t umma_idesc_tf32(int BN) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((128u >> 4) << 24);
+__device__ __forceinline__ uint32_t umma_idesc_tf32(int BN, uint32_t M = 128) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((M >> 4) << 24);
 }
 __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -94,6 +95,53 @@ __device__ __forceinline__ void mbar_wait_safe(uint64_t* bar, unsigned parity) {
   __trap();
 }
 
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// ---- CTA-pair (cta_group::2) helpers
+// shared::cluster address of the same shared variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t smem_peer(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+// arrive on an mbarrier given by its shared::cluster address (default .release.cta semantics: the
+// data it publishes -- A tiles after fence.proxy.async, drained TMEM -- is consumed by the tensor
+// core through the async proxy, not by generic loads of the peer, so no cluster-scope release is
+// needed; r02: .release.cluster compiled to MEMBAR.ALL.GPU per arrive and the acquire.cluster wait
+// to CCTL.IVALL, making the pair kernel 1.8x slower than the one-CTA kernel)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cbar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(cbar) : "memory");
+}
+// TMA of one CTA's half of a paired operand; completion is counted on the LEADER's barrier
+__device__ __forceinline__ void tma_load_4d_pair(void* dst, const CUtensorMap* tm, int x0, int x1, int x2, int x3,
+                                                 uint32_t leader_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4, %5}], [%6];\n" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(x0), "r"(x1), "r"(x2), "r"(x3), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void umma_tf32_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+// commit the pair's MMAs to the barrier at the same offset in both CTAs
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
 __device__ __forceinline__ uint32_t tf32_trunc(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
 
 template <int NSTEP>  // 32 lanes x NSTEP fp32 columns
@@ -110,7 +158,12 @@ __device__ __forceinline__ void tmem_ld_32x32b(uint32_t taddr, float* v) {
   for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(r[q]);
 }
 
-template <int kTfStages>
+// PAIR: a CTA pair (2-CTA cluster, cta_group::2) computes a 256-column super tile -- UMMA M = 256,
+// each CTA builds its own 128 columns of A and TMA-loads HALF of the T tile's rows (B), and the
+// leader's single MMA thread reads both halves: the shared-memory operand traffic per SM drops
+// from (A + B) to (A + B/2) per MMA. Pieces stay per 128-column tile (CTA rank r writes tile
+// 2 * tm2 + r), so the epilogue is unchanged.
+template <int kTfStages, bool PAIR = false>
 __global__ void __launch_bounds__(kTfThreads, 1)
     mttkrp_tf32_kernel(const __grid_constant__ CUtensorMap tmThi, const __grid_constant__ CUtensorMap tmTlo,
                        const __grid_constant__ CUtensorMap tmU, MttkrpView v, TfGeom g,
@@ -119,7 +172,8 @@ __global__ void __launch_bounds__(kTfThreads, 1)
   unsigned char* base = tsm;  // dynamic smem is 1 KB aligned (__align__(1024) on the declaration)
   double* Ub = reinterpret_cast<double*>(base);                                   // [2][BK][BMP] fp64
   unsigned char* stages = base + tf_slab_bytes();
-  const size_t stage_sz = tf_stage_bytes(g.BN, v.nslow);
+  const int BNl = PAIR ? g.BN / 2 : g.BN;  // rows of the T tile held by this CTA
+  const size_t stage_sz = tf_stage_bytes(BNl, v.nslow);
   uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kTfStages * stage_sz);
   uint64_t* fullB = bars;                      // TMA data landed (count 1 + tx)
   uint64_t* fullA = bars + kTfStages;          // A tile written (count kTfAWarps)
@@ -130,35 +184,48 @@ __global__ void __launch_bounds__(kTfThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fullS + kTfStages);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int b = blockIdx.x;
-  const int* cta_u = reinterpret_cast<const int*>(tinfo + g.nMt * g.nNt);
+  const int crk = PAIR ? (int)cluster_ctarank() : 0;
+  const bool leader = crk == 0;
+  const int b = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // the plan's CTA (a pair when PAIR)
+  const int nMt1 = PAIR ? g.nMt1 : g.nMt;  // 128-column tiles per tile row (the piece table)
+  const int* cta_u = reinterpret_cast<const int*>(tinfo + nMt1 * g.nNt);
   const int64_t u0 = cta_u[b], u1 = cta_u[b + 1];
   const int BN = g.BN;
 
   auto stA_hi = [&](int s) { return stages + s * stage_sz; };
   auto stA_lo = [&](int s) { return stages + s * stage_sz + 128 * 64; };
   auto stB_hi = [&](int s) { return stages + s * stage_sz + 2 * 128 * 64; };
-  auto stB_lo = [&](int s) { return stages + s * stage_sz + 2 * 128 * 64 + (size_t)BN * 64; };
-  auto stS = [&](int s) { return reinterpret_cast<double*>(stages + s * stage_sz + 2 * 128 * 64 + 2 * (size_t)BN * 64); };
+  auto stB_lo = [&](int s) { return stages + s * stage_sz + 2 * 128 * 64 + (size_t)BNl * 64; };
+  auto stS = [&](int s) { return reinterpret_cast<double*>(stages + s * stage_sz + 2 * 128 * 64 + 2 * (size_t)BNl * 64); };
 
   if (tid == 0) {
     for (int s = 0; s < kTfStages; ++s) {
       mbar_init(&fullB[s], 1);
       mbar_init(&fullS[s], 1);
-      mbar_init(&fullA[s], kTfAWarps);
+      mbar_init(&fullA[s], PAIR ? 2 * kTfAWarps : kTfAWarps);  // (PAIR: both CTAs' A warps)
       mbar_init(&empty[s], 1);
     }
     for (int q = 0; q < 2; ++q) {
       mbar_init(&acc_full[q], 1);
-      mbar_init(&acc_empty[q], kTfDWarps);
+      mbar_init(&acc_empty[q], PAIR ? 2 * kTfDWarps : kTfDWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   }
-  if (warp == 0) {  // TMEM accumulator: 128 lanes x 256 fp32 columns
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
-                 "n"(kTfTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  if (PAIR) {
+    __syncthreads();
+    cluster_sync_all();  // the peer's barriers are initialised before any remote arrive / commit
+  }
+  if (warp == 0) {  // TMEM accumulator: 128 lanes x 256 fp32 columns (x 2 CTAs when PAIR)
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                   "n"(kTfTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                   "n"(kTfTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
@@ -171,7 +238,7 @@ __global__ void __launch_bounds__(kTfThreads, 1)
     // ======================= TMA producer (whole warp walks the loop, one elected lane issues) ===
     {
       const unsigned s_bytes = (unsigned)v.nslow * kBM * 8u;
-      const unsigned t_bytes = 2u * (unsigned)BN * 64u;
+      const unsigned t_bytes = 2u * (unsigned)BNl * 64u;  // this CTA's B bytes per stage
       unsigned ld_git = 0;
       for (int64_t u = u0; u < u1;) {
         const int t = (int)(u / g.KT);
@@ -180,7 +247,7 @@ __global__ void __launch_bounds__(kTfThreads, 1)
         const int kt1 = (int)(kt_end < (int64_t)g.KT ? kt_end : (int64_t)g.KT);
         u += kt1 - kt0;
         const int tm = t % g.nMt, tn = t / g.nMt;
-        const int c0 = tm * kBM, i0 = tn * BN;
+        const int c0 = (PAIR ? 2 * tm + crk : tm) * kBM, i0 = tn * BN + crk * BNl;
         for (unsigned q = (ld_git >= (unsigned)kTfStages ? ld_git - kTfStages + 1 : 0); q < ld_git; ++q)
           mbar_wait_safe(&empty[q % kTfStages], (q / kTfStages) & 1u);
         int ld_b0 = kt0 / v.Jp, ld_jp = kt0 % v.Jp, loaded_b0 = -1;
@@ -207,14 +274,23 @@ __global__ void __launch_bounds__(kTfThreads, 1)
             // the A producers only need the slow-mode rows and the U_q0 slab: their own barrier
             mbar_expect_tx(sbar, s_bytes + (new_slab ? (unsigned)(kBK * kBMP * 8) : 0u));
             if (new_slab) tma_load_2d(Ub + (ld_b0 & 1) * (kBK * kBMP), &tmU, c0, ld_b0 * kBK, sbar);
+            // (c0s: the dead second half of an odd last super tile reads a valid row; unused)
+            const int c0s = c0 < nMt1 * kBM ? c0 : c0 - kBM;
 #pragma unroll
             for (int s = 0; s < kMaxModes - 2; ++s)
               if (s < v.nslow)
-                bulk_load(stS(slot) + s * kBM, v.Us[s] + (int64_t)sidx[s] * g.ldu + c0, kBM * 8u, sbar);
-            mbar_expect_tx(bar, t_bytes);
+                bulk_load(stS(slot) + s * kBM, v.Us[s] + (int64_t)sidx[s] * g.ldu + c0s, kBM * 8u, sbar);
             // view (q0, runA, n, runB) for every mode (the n = 0 view is the permuted copy)
-            tma_load_4d(stB_hi(slot), &tmThi, ld_b0 * kTfBK, ld_ja, i0, ld_jb, bar);
-            tma_load_4d(stB_lo(slot), &tmTlo, ld_b0 * kTfBK, ld_ja, i0, ld_jb, bar);
+            if (PAIR) {  // both halves complete on the leader's barrier; the leader expects both
+              if (leader) mbar_expect_tx(bar, 2 * t_bytes);
+              const uint32_t lb = smem_peer(bar, 0);
+              tma_load_4d_pair(stB_hi(slot), &tmThi, ld_b0 * kTfBK, ld_ja, i0, ld_jb, lb);
+              tma_load_4d_pair(stB_lo(slot), &tmTlo, ld_b0 * kTfBK, ld_ja, i0, ld_jb, lb);
+            } else {
+              mbar_expect_tx(bar, t_bytes);
+              tma_load_4d(stB_hi(slot), &tmThi, ld_b0 * kTfBK, ld_ja, i0, ld_jb, bar);
+              tma_load_4d(stB_lo(slot), &tmTlo, ld_b0 * kTfBK, ld_ja, i0, ld_jb, bar);
+            }
           }
           __syncwarp();
           if (new_slab) loaded_b0 = ld_b0;
@@ -240,8 +316,9 @@ __global__ void __launch_bounds__(kTfThreads, 1)
     }
   } else if (warp == kTfMmaWarp) {
     // ======================= MMA issuer (whole warp walks the loop, one elected lane issues) ===
-    {
-      const uint32_t idesc = umma_idesc_tf32(BN);
+    // (PAIR: the leader CTA's warp issues for both; the peer's MMA warp idles)
+    if (leader) {
+      const uint32_t idesc = umma_idesc_tf32(BN, PAIR ? 256u : 128u);
       unsigned git = 0, gc = 0;  // k-tiles consumed, chunks issued (accumulator buffer = gc & 1)
       for (int64_t u = u0; u < u1;) {
         const int kt0 = (int)(u % g.KT);
@@ -254,7 +331,9 @@ __global__ void __launch_bounds__(kTfThreads, 1)
         for (int kt = kt0; kt < kt1; ++kt) {
           const int cpos = (kt - kt0) % kTfChunk;
           if (cpos == 0) {  // new chunk: its accumulator buffer must have been drained
-            if (gc >= 2) mbar_wait_safe(&acc_empty[gc & 1], ((gc >> 1) - 1) & 1u);
+            if (gc >= 2) {
+              mbar_wait_safe(&acc_empty[gc & 1], ((gc >> 1) - 1) & 1u);
+            }
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             dacc = tmem + (gc & 1) * kTfMaxN;
             first = true;
@@ -270,13 +349,24 @@ __global__ void __launch_bounds__(kTfThreads, 1)
           if (elect_one()) {
             for (int kk = 0; kk < nks; ++kk) {
               const uint32_t ko = kk * 32;  // 8 tf32 = 32 bytes along K inside the 64-byte atom
-              umma_tf32(dacc, umma_desc_sw64(alo + ko), umma_desc_sw64(bhi + ko), idesc, first ? 0u : 1u);
+              if (PAIR) {
+                umma_tf32_pair(dacc, umma_desc_sw64(alo + ko), umma_desc_sw64(bhi + ko), idesc, first ? 0u : 1u);
+                umma_tf32_pair(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(blo + ko), idesc, 1u);
+                umma_tf32_pair(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(bhi + ko), idesc, 1u);
+              } else {
+                umma_tf32(dacc, umma_desc_sw64(alo + ko), umma_desc_sw64(bhi + ko), idesc, first ? 0u : 1u);
+                umma_tf32(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(blo + ko), idesc, 1u);
+                umma_tf32(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(bhi + ko), idesc, 1u);
+              }
               first = false;
-              umma_tf32(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(blo + ko), idesc, 1u);
-              umma_tf32(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(bhi + ko), idesc, 1u);
             }
-            umma_commit(&empty[slot]);  // frees the stage once these MMAs have read it
-            if (cpos == kTfChunk - 1 || kt == kt1 - 1) umma_commit(&acc_full[gc & 1]);  // -> drain warps
+            // frees the stage (in both CTAs when PAIR) once these MMAs have read it
+            if (PAIR) umma_commit_pair(&empty[slot]);
+            else umma_commit(&empty[slot]);
+            if (cpos == kTfChunk - 1 || kt == kt1 - 1) {  // -> drain warps
+              if (PAIR) umma_commit_pair(&acc_full[gc & 1]);
+              else umma_commit(&acc_full[gc & 1]);
+            }
           }
           __syncwarp();
           first = false;
@@ -300,7 +390,9 @@ __global__ void __launch_bounds__(kTfThreads, 1)
       const int64_t kt_end = (int64_t)kt0 + (u1 - u);
       const int kt1 = (int)(kt_end < (int64_t)g.KT ? kt_end : (int64_t)g.KT);
       u += kt1 - kt0;
-      const TileInfo ti = tinfo[t];
+      const int tm1 = PAIR ? 2 * (t % g.nMt) + crk : t % g.nMt;  // this CTA's 128-column tile
+      const bool wr = tm1 < nMt1;  // (PAIR: the second half of an odd last super tile is dead)
+      const TileInfo ti = tinfo[(t / g.nMt) * nMt1 + (wr ? tm1 : 0)];
       double* P = parts + ((int64_t)ti.piece_base + (b - ti.first_cta)) * (int64_t)(BN * kBM) + row;
       const int nch = (kt1 - kt0 + kTfChunk - 1) / kTfChunk;
       for (int ch = 0; ch < nch; ++ch, ++gc) {
@@ -308,7 +400,7 @@ __global__ void __launch_bounds__(kTfThreads, 1)
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16) + (gc & 1) * kTfMaxN;
         // BN is a multiple of 16; 32 columns per round keep 32 independent loads in flight
-        for (int col = 0; col < BN; col += 32) {
+        for (int col = 0; col < (wr ? BN : 0); col += 32) {
           const bool two = col + 16 < BN;
           float vals[32];
           tmem_ld_32x32b<16>(lane_base + (uint32_t)col, vals);
@@ -329,7 +421,10 @@ __global__ void __launch_bounds__(kTfThreads, 1)
         }
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[gc & 1]);
+        if (lane == 0) {
+          if (PAIR) mbar_arrive_cluster(smem_peer(&acc_empty[gc & 1], 0));
+          else mbar_arrive(&acc_empty[gc & 1]);
+        }
       }
     }
   } else {
@@ -344,7 +439,7 @@ __global__ void __launch_bounds__(kTfThreads, 1)
       const int kt1 = (int)(kt_end < (int64_t)g.KT ? kt_end : (int64_t)g.KT);
       u += kt1 - kt0;
       const int tm = t % g.nMt;
-      const int c0 = tm * kBM;
+      const int c0 = (PAIR ? 2 * tm + crk : tm) * kBM;
       const bool live = (c0 + row) < g.C;
       int cmp_b0 = kt0 / v.Jp, cmp_jp = kt0 % v.Jp;
       // swizzled (SWIZZLE_64B, K-major) byte offset of this row's 16-byte chunk ch
@@ -392,7 +487,10 @@ __global__ void __launch_bounds__(kTfThreads, 1)
         }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> tensor core
         __syncwarp();
-        if (lane == 0) mbar_arrive(&fullA[slot]);
+        if (lane == 0) {
+          if (PAIR) mbar_arrive_cluster(smem_peer(&fullA[slot], 0));
+          else mbar_arrive(&fullA[slot]);
+        }
         ++git;
         if (++cmp_jp == v.Jp) {
           cmp_jp = 0;
@@ -403,9 +501,11 @@ __global__ void __launch_bounds__(kTfThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
+  if (PAIR) cluster_sync_all();  // no remote arrive / commit / operand read may target an exited peer
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(kTfTmemCols));
+    if (PAIR) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(kTfTmemCols));
+    else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(kTfTmemCols));
   }
 }
 #ifdef JK_TU_HOST
