@@ -49,6 +49,7 @@ inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
 //                                      read at each plan (tests pin the path per handle), see resident_mode()
 //   JKCALS_TF32_MIN_NNT / JKCALS_TF32_MAX_STAGES   FP32 path N tiles / ring depth
 //   JKCALS_TF32_PAIR=0                 FP32 path: one-CTA kernel only (no cta_group::2 pairs)
+//   JKCALS_TF32_CHUNK=<k>              FP32 path: k-tiles per FP32 accumulation chain (accuracy!)
 //   JKCALS_I8_RESIDENT / JKCALS_I8_CLUSTER         FP64_I8 kernel variant
 //   JKCALS_I8_PROBE                    timing-probe builds only (-DJKCALS_DEV_PROBES; wrong results)
 //   JKCALS_TOL_HOST_LOOP=1             tol mode: host check after every sweep (no WHILE graph node)
@@ -57,7 +58,7 @@ struct Tuning {
   int force_wm = 0, force_kb = 0, red_pieces = -1;
   double sk_alpha = -1.0;
   int tf32_min_nnt = 0, tf32_max_stages = 8, i8_resident = 0, i8_cluster = 1, i8_probe = 0;
-  int tol_host_loop = 0, tf32_pair = 1;
+  int tol_host_loop = 0, tf32_pair = 1, tf32_chunk = 0;
 };
 const Tuning& tuning() {
   static const Tuning t = [] {
@@ -75,6 +76,7 @@ const Tuning& tuning() {
     v.i8_probe = geti("JKCALS_I8_PROBE", 0);
     v.tol_host_loop = geti("JKCALS_TOL_HOST_LOOP", 0);
     v.tf32_pair = geti("JKCALS_TF32_PAIR", 1);
+    v.tf32_chunk = geti("JKCALS_TF32_CHUNK", 0);
     return v;
   }();
   return t;
@@ -1171,6 +1173,7 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     cfg.attrs = attr;
     cfg.numAttrs = p.pair ? 2 : 1;
     tg.stages = p.ST4;
+    tg.chunk = tuning().tf32_chunk > 0 ? tuning().tf32_chunk : kTfChunk;
     CKH(h, cudaLaunchKernelEx(&cfg, tf32_kernel(p.ST4, p.pair != 0), h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v,
                               tg, ti, parts));
   } else {

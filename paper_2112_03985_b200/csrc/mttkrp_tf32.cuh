@@ -50,6 +50,7 @@ struct TfGeom {
   int64_t units;
   int G;
   int stages;     // shared-memory ring depth (as many as fit, <= kTfMaxStages)
+  int chunk;      // k-tiles per FP32 accumulation chain (kTfChunk unless tuned)
 };
 
 __host__ __device__ constexpr size_t tf_stage_bytes(int BN, int nslow) {
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__(kTfThreads, 1)
         bool first = true;
         uint32_t dacc = tmem;
         for (int kt = kt0; kt < kt1; ++kt) {
-          const int cpos = (kt - kt0) % kTfChunk;
+          const int cpos = (kt - kt0) % g.chunk;
           if (cpos == 0) {  // new chunk: its accumulator buffer must have been drained
             if (gc >= 2) {
               mbar_wait_safe(&acc_empty[gc & 1], ((gc >> 1) - 1) & 1u);
@@ -363,7 +364,7 @@ __global__ void __launch_bounds__(kTfThreads, 1)
             // frees the stage (in both CTAs when PAIR) once these MMAs have read it
             if (PAIR) umma_commit_pair(&empty[slot]);
             else umma_commit(&empty[slot]);
-            if (cpos == kTfChunk - 1 || kt == kt1 - 1) {  // -> drain warps
+            if (cpos == g.chunk - 1 || kt == kt1 - 1) {  // -> drain warps
               if (PAIR) umma_commit_pair(&acc_full[gc & 1]);
               else umma_commit(&acc_full[gc & 1]);
             }
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(kTfThreads, 1)
           __syncwarp();
           first = false;
           ++git;
-          if (cpos == kTfChunk - 1 || kt == kt1 - 1) ++gc;
+          if (cpos == g.chunk - 1 || kt == kt1 - 1) ++gc;
           if (++cmp_jp == v.Jp) {
             cmp_jp = 0;
             ++cmp_b0;
@@ -394,7 +395,7 @@ __global__ void __launch_bounds__(kTfThreads, 1)
       const bool wr = tm1 < nMt1;  // (PAIR: the second half of an odd last super tile is dead)
       const TileInfo ti = tinfo[(t / g.nMt) * nMt1 + (wr ? tm1 : 0)];
       double* P = parts + ((int64_t)ti.piece_base + (b - ti.first_cta)) * (int64_t)(BN * kBM) + row;
-      const int nch = (kt1 - kt0 + kTfChunk - 1) / kTfChunk;
+      const int nch = (kt1 - kt0 + g.chunk - 1) / g.chunk;
       for (int ch = 0; ch < nch; ++ch, ++gc) {
         mbar_wait_safe(&acc_full[gc & 1], (gc >> 1) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");

@@ -52,7 +52,7 @@ __host__ __device__ inline int wr_warp_doubles(int N, const int* dims, int R) {
     sumI += dims[m];
     maxI = dims[m] > maxI ? dims[m] : maxI;
   }
-  return sumI * R + 2 * maxI * R + N * R * R + 2 * R * R + R + 2;
+  return sumI * R + 2 * maxI * R + N * R * R + 2 * R * R + R + 2 + 32 * R;  // (+ MTTKRP partials)
 }
 
 template <int RMAX, int NM>  // NM: the number of modes, compile-time (index arithmetic in registers)
@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(kWrWarps * 32) warp_sweep_kernel(WrArgs a) {
   double* H = Gs + N * R * R;
   double* Lf = H + R * R;
   double* Linv = Lf + R * R;
+  double* Mp = Linv + R + 2;                       // [G][I_n][R] MTTKRP partials (I_n < 32)
   for (int m = 0; m < N; ++m)
     for (int e = lane; e < a.dims[m] * R; e += 32) {
       const int i = e / R, r = e % R;
@@ -120,7 +121,10 @@ __global__ void __launch_bounds__(kWrWarps * 32) warp_sweep_kernel(WrArgs a) {
   int sweeps = 0;
   for (int s = 0; s < a.max_iters && act; ++s) {
     ++sweeps;
-    for (int n = 0; n < N; ++n) {
+    // the mode loop is unrolled (NM is compile-time) so that q0, the slow modes and every array
+    // index below are static: with a runtime n the slow-mode tables went to local memory (r02)
+#pragma unroll
+    for (int n = 0; n < NM; ++n) {
       int In = 0;
 #pragma unroll
       for (int y = 0; y < NM; ++y)
@@ -160,62 +164,126 @@ __global__ void __launch_bounds__(kWrWarps * 32) warp_sweep_kernel(WrArgs a) {
           Iq0 = dm[y];
         }
       }
-      double acc[RMAX][2];  // [c][row slot] two rows per lane (In <= 64 typical)
-      for (int i0 = lane; i0 < In; i0 += 64) {
-        const int i1 = i0 + 32;
-        const bool two = i1 < In;
+      if (In < 32) {
+        // short modes: lanes over (row i, j'-group g), G = 32 / I_n groups taking every G-th j',
+        // the k chain split in two accumulators; the G partials of a row are then summed in g
+        // order by lane i (fixed order: deterministic). r02: tiny 10.9 -> see DESIGN.md §9c
+        const int G = 32 / In, i = lane % In, g = lane / In;
+        if (g < G) {
+          double acc[RMAX];
 #pragma unroll
-        for (int r = 0; r < RMAX; ++r) acc[r][0] = acc[r][1] = 0.0;
-        int toff = 0;
-#pragma unroll
-        for (int z = 0; z < NM - 2; ++z) sidx[z] = 0;
-        for (int jp = 0; jp < Jp; ++jp) {
-          double sv[RMAX];  // S_j'(c): the same on every lane (broadcast loads)
-#pragma unroll
-          for (int r = 0; r < RMAX; ++r) sv[r] = 1.0;
-#pragma unroll
-          for (int z = 0; z < NM - 2; ++z) {
-            const double* ur = Ub + suo[z] + sidx[z] * R;
-#pragma unroll
-            for (int r = 0; r < RMAX; ++r)
-              if (r < R) sv[r] *= ur[r];
-          }
-          double p0[RMAX], p1[RMAX];
-#pragma unroll
-          for (int r = 0; r < RMAX; ++r) p0[r] = p1[r] = 0.0;
-          const double* t0 = Ts + i0 * stn + toff;
-          const double* t1 = Ts + (two ? i1 : i0) * stn + toff;
+          for (int r = 0; r < RMAX; ++r) acc[r] = 0.0;
           const double* uq = Ub + uoq;
-#pragma unroll 4
-          for (int k = 0; k < Iq0; ++k) {
-            const double a0 = t0[k * stq], a1 = t1[k * stq];
+          for (int jp = g; jp < Jp; jp += G) {
+            int rem = jp, toff = 0;
+            double sv[RMAX];
 #pragma unroll
-            for (int r = 0; r < RMAX; ++r)
-              if (r < R) {
-                const double u = uq[k * R + r];
-                p0[r] = fma(a0, u, p0[r]);
-                p1[r] = fma(a1, u, p1[r]);
-              }
+            for (int r = 0; r < RMAX; ++r) sv[r] = 1.0;
+#pragma unroll
+            for (int z = 0; z < NM - 2; ++z) {
+              const int iz = rem % sdim[z];
+              rem /= sdim[z];
+              toff += iz * sst[z];
+              const double* ur = Ub + suo[z] + iz * R;
+#pragma unroll
+              for (int r = 0; r < RMAX; ++r)
+                if (r < R) sv[r] *= ur[r];
+            }
+            double pe[RMAX], po[RMAX];
+#pragma unroll
+            for (int r = 0; r < RMAX; ++r) pe[r] = po[r] = 0.0;
+            const double* t = Ts + i * stn + toff;
+            int kk = 0;
+            for (; kk + 2 <= Iq0; kk += 2) {
+              const double a0 = t[kk * stq], a1 = t[(kk + 1) * stq];
+#pragma unroll
+              for (int r = 0; r < RMAX; ++r)
+                if (r < R) {
+                  pe[r] = fma(a0, uq[kk * R + r], pe[r]);
+                  po[r] = fma(a1, uq[(kk + 1) * R + r], po[r]);
+                }
+            }
+            if (kk < Iq0) {
+              const double a0 = t[kk * stq];
+#pragma unroll
+              for (int r = 0; r < RMAX; ++r)
+                if (r < R) pe[r] = fma(a0, uq[kk * R + r], pe[r]);
+            }
+#pragma unroll
+            for (int r = 0; r < RMAX; ++r) acc[r] = fma(sv[r], pe[r] + po[r], acc[r]);
           }
 #pragma unroll
-          for (int r = 0; r < RMAX; ++r) {
-            acc[r][0] = fma(sv[r], p0[r], acc[r][0]);
-            acc[r][1] = fma(sv[r], p1[r], acc[r][1]);
-          }
-#pragma unroll
-          for (int z = 0; z < NM - 2; ++z) {  // next j' (mixed radix, fastest slow mode first)
-            toff += sst[z];
-            if (++sidx[z] < sdim[z]) break;
-            toff -= sst[z] * sdim[z];
-            sidx[z] = 0;
-          }
+          for (int r = 0; r < RMAX; ++r)
+            if (r < R) Mp[(g * In + i) * R + r] = acc[r];
         }
+        __syncwarp();
+        if (lane < In) {
 #pragma unroll
-        for (int r = 0; r < RMAX; ++r)
-          if (r < R) {
-            Ms[i0 * R + r] = acc[r][0];
-            if (two) Ms[i1 * R + r] = acc[r][1];
+          for (int r = 0; r < RMAX; ++r)
+            if (r < R) {
+              double sm = Mp[lane * R + r];
+              for (int q = 1; q < G; ++q) sm += Mp[(q * In + lane) * R + r];
+              Ms[lane * R + r] = sm;
+            }
+        }
+      } else {
+        double acc[RMAX][2];  // [c][row slot] two rows per lane (In <= 64 typical)
+        for (int i0 = lane; i0 < In; i0 += 64) {
+          const int i1 = i0 + 32;
+          const bool two = i1 < In;
+  #pragma unroll
+          for (int r = 0; r < RMAX; ++r) acc[r][0] = acc[r][1] = 0.0;
+          int toff = 0;
+  #pragma unroll
+          for (int z = 0; z < NM - 2; ++z) sidx[z] = 0;
+          for (int jp = 0; jp < Jp; ++jp) {
+            double sv[RMAX];  // S_j'(c): the same on every lane (broadcast loads)
+  #pragma unroll
+            for (int r = 0; r < RMAX; ++r) sv[r] = 1.0;
+  #pragma unroll
+            for (int z = 0; z < NM - 2; ++z) {
+              const double* ur = Ub + suo[z] + sidx[z] * R;
+  #pragma unroll
+              for (int r = 0; r < RMAX; ++r)
+                if (r < R) sv[r] *= ur[r];
+            }
+            double p0[RMAX], p1[RMAX];
+  #pragma unroll
+            for (int r = 0; r < RMAX; ++r) p0[r] = p1[r] = 0.0;
+            const double* t0 = Ts + i0 * stn + toff;
+            const double* t1 = Ts + (two ? i1 : i0) * stn + toff;
+            const double* uq = Ub + uoq;
+  #pragma unroll 4
+            for (int k = 0; k < Iq0; ++k) {
+              const double a0 = t0[k * stq], a1 = t1[k * stq];
+  #pragma unroll
+              for (int r = 0; r < RMAX; ++r)
+                if (r < R) {
+                  const double u = uq[k * R + r];
+                  p0[r] = fma(a0, u, p0[r]);
+                  p1[r] = fma(a1, u, p1[r]);
+                }
+            }
+  #pragma unroll
+            for (int r = 0; r < RMAX; ++r) {
+              acc[r][0] = fma(sv[r], p0[r], acc[r][0]);
+              acc[r][1] = fma(sv[r], p1[r], acc[r][1]);
+            }
+  #pragma unroll
+            for (int z = 0; z < NM - 2; ++z) {  // next j' (mixed radix, fastest slow mode first)
+              toff += sst[z];
+              if (++sidx[z] < sdim[z]) break;
+              toff -= sst[z] * sdim[z];
+              sidx[z] = 0;
+            }
           }
+  #pragma unroll
+          for (int r = 0; r < RMAX; ++r)
+            if (r < R) {
+              Ms[i0 * R + r] = acc[r][0];
+              if (two) Ms[i1 * R + r] = acc[r][1];
+            }
+        }
       }
       __syncwarp();
       // (a3) Hadamard of the cached Gramians of the other modes; (a4) Cholesky on lane 0
@@ -344,17 +412,18 @@ __global__ void __launch_bounds__(kWrWarps * 32) warp_sweep_kernel(WrArgs a) {
         il[r] = lam[r] > 0.0 ? 1.0 / lam[r] : 1.0;
       }
       __syncwarp();
-      for (int e = lane; e < In * R; e += 32) {
-        const int r = e % R;
-        double ir = 1.0;
+      for (int i = lane; i < In; i += 32) {
 #pragma unroll
-        for (int rr = 0; rr < RMAX; ++rr)
-          if (rr == r) ir = il[rr];
-        Ub[uo[n] + e] = Vs[e] * ir;
+        for (int r = 0; r < RMAX; ++r)
+          if (r < R) Ub[uo[n] + i * R + r] = Vs[i * R + r] * il[r];
       }
-      if (lane == 0)
-        for (int r = 0; r < R; ++r)
-          for (int c = 0; c < R; ++c) Gs[n * R * R + r * R + c] = vtv(r, c) * il[r] * il[c];
+      if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r)
+#pragma unroll
+          for (int c = 0; c < RMAX; ++c)
+            if (r < R && c < R) Gs[n * R * R + r * R + c] = vtv(r, c) * il[r] * il[c];
+      }
       if (n == last) {  // (a7) error, fit, history, convergence
         if (lane < R) {
 #pragma unroll
@@ -362,8 +431,11 @@ __global__ void __launch_bounds__(kWrWarps * 32) warp_sweep_kernel(WrArgs a) {
             if (r == lane) a.lambda[(int64_t)sub * R + r] = lam[r];
         }
         double quad = 0.0;
-        for (int r = 0; r < R; ++r)
-          for (int c = 0; c < R; ++c) quad += H[r * R + c] * vtv(r, c);
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r)
+#pragma unroll
+          for (int c = 0; c < RMAX; ++c)
+            if (r < R && c < R) quad += H[r * R + c] * vtv(r, c);
         const double e = nt2 + quad - 2.0 * accq[NQ];
         ++it;
         bool stay = true;
