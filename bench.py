@@ -461,7 +461,18 @@ def main():
         td = time_job(torch, hd, w.P, w.sweeps, flush, 2)
         fl_d = hd.sweep_flops() * w.sweeps
         hd.close()
+        # small configs (SURVEY §8d latency targets): whole-iterate time per sweep, auto path
+        # (warp-resident kernel for tiny, cluster-resident for syn50 R1-R2, streamed otherwise)
+        lat = {}
+        for name in ("tiny", "syn50_r1", "syn50_r2", "syn50_r3", "syn50_r5"):
+            wl = make_workload(name)
+            nsw = 1000 if name == "tiny" else 200
+            hl = JKCals(wl.T, wl.R, hist_cap=nsw)
+            tl = time_job(torch, hl, wl.P, nsw, flush, 3)
+            lat[name] = round(tl / nsw * 1e6, 2)
+            hl.close()
         supp = {
+            "latency_us_per_sweep": lat,
             "all_pool": {"workload": "all_medium: 50x200x200, models R in {3,5,7,9} jackknifed together "
                                      "(200 submodels, C = 1200), 100 sweeps", "value": round(tp, 5), "unit": "s",
                          "mttkrp_flop_rate_tflops": round(fl_p / tp / 1e12, 2)},

@@ -335,6 +335,35 @@ def test_fp32_path_vs_oracle(name, ps):
     check32(h, res, p_list)
 
 
+def test_fp32_pair_odd_tiles_and_one_cta_variant():
+    # the CTA-pair (cta_group::2) FP32 kernel with an odd number of 128-column tiles (C = 60 x 6 =
+    # 360: 3 tiles, the last super tile's second half dead) and a ragged I_n = 44, against the oracle;
+    # the one-CTA kernel (JKCALS_TF32_PAIR=0, read once per process: subprocess) meets the same bar.
+    # (R = R_true: an over-factored R = 6 > 5 model is ill-conditioned enough that BOTH FP32 kernels
+    # land near 1e-3 -- tools/pair_diag.py -- a property of FP32, not of the kernel)
+    import subprocess, sys
+    spec = ((60, 44, 36), 6, 6, 0.01, "syn", 30)
+    w = make_workload(spec)
+    h = run_gpu32(w, w.sweeps)
+    ps = [0, 31, 59]
+    res = O.jk_als(w.T, w.P, p_list=ps, max_iters=w.sweeps, nthreads=NCPU)
+    check32(h, res, ps)
+    code = ("import numpy as np\n"
+            "from synth import make_workload\n"
+            "from paper_2112_03985_b200 import JKCals\n"
+            f"w = make_workload({spec!r})\n"
+            "h = JKCals(w.T, w.R, hist_cap=w.sweeps, precision=1)\n"
+            "h.set_init(w.P); h.iterate(w.sweeps, 0.0)\n"
+            "np.save('/tmp/jk_onecta.npy', np.concatenate([np.ravel(f) for p in (0, 31, 59) for f in h.factors(p)[0]]))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         env=dict(os.environ, JKCALS_TF32_PAIR="0"), timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    one = np.load("/tmp/jk_onecta.npy")
+    pair = np.concatenate([np.ravel(f) for p in ps for f in h.factors(p)[0]])
+    assert rel(pair, one) <= FTOL32
+
+
 @pytest.mark.parametrize("name,ps,max_iters", [("syn50_r3", None, 1000), ("4way", [0, 57], 60)])
 def test_fp32_tol_mode_vs_oracle(name, ps, max_iters):
     """FP32 path in tol mode (the paper's tol = 1e-6): the last mode runs on the
