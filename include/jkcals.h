@@ -316,8 +316,9 @@ void jkcals_destroy(jkcals_t h);
  *   M(i, c) = sum_j T_(n)(i, j) * prod_{m != n} U_m(i_m(j), c),  c < C,
  * T device FP64 column-major; U[m] device row-major dims[m] x ldu, 16-byte aligned, ldu even and
  * ldu >= C (ldu >= C + 1 when C is odd); M device row-major dims[n] x ldm. scratch is device
- * memory of jkcals_mttkrp_scratch_bytes(...) bytes. Enqueued on `stream`; returns E_CUDA on a
- * launch error. */
+ * memory of jkcals_mttkrp_scratch_bytes(...) bytes. Runs on `stream` and returns after the stream
+ * has completed it (the per-call tile table is staged from pageable host memory); E_CUDA on a
+ * launch or execution error. */
 size_t jkcals_mttkrp_scratch_bytes(int ndims, const int64_t *dims, int n, int64_t C, int device);
 jkcals_status jkcals_mttkrp(int ndims, const int64_t *dims, int n, const double *T,
                             const double *const *U, int64_t C, int64_t ldu, double *M, int64_t ldm,
@@ -327,8 +328,10 @@ jkcals_status jkcals_mttkrp(int ndims, const int64_t *dims, int n, const double 
  * operands of the per-j' inner products (T per mode-n row, U_q0 per column) split into 7 balanced
  * base-128 digits with power-of-two scales, digit products accumulated exactly in int32 TMEM
  * accumulators per significance, the slow-mode row product S(j', c) applied in FP64. Same
- * arguments as jkcals_mttkrp (ldu >= C); scratch from jkcals_mttkrp_i8_scratch_bytes. The
- * JK-CALS sweep uses the same kernel under JKCALS_FP64_I8. JKCALS_E_ARG if I_q0 > 65536. */
+ * arguments and blocking behaviour as jkcals_mttkrp (ldu >= C; returns after `stream` has
+ * completed the op); scratch from jkcals_mttkrp_i8_scratch_bytes. The JK-CALS sweep uses the same
+ * kernel under JKCALS_FP64_I8. JKCALS_E_ARG if I_q0 > 65536. Accuracy: the normwise per-slab bound
+ * stated under JKCALS_FP64_I8 above. */
 size_t jkcals_mttkrp_i8_scratch_bytes(int ndims, const int64_t *dims, int n, int64_t C, int device);
 jkcals_status jkcals_mttkrp_i8(int ndims, const int64_t *dims, int n, const double *T,
                                const double *const *U, int64_t C, int64_t ldu, double *M, int64_t ldm,

@@ -1174,6 +1174,10 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     cfg.numAttrs = p.pair ? 2 : 1;
     tg.stages = p.ST4;
     tg.chunk = tuning().tf32_chunk > 0 ? tuning().tf32_chunk : kTfChunk;
+    tg.probe = 0;
+#ifdef JKCALS_DEV_PROBES  // timing-probe builds only (results are wrong when set)
+    tg.probe = tuning().i8_probe;
+#endif
     CKH(h, cudaLaunchKernelEx(&cfg, tf32_kernel(p.ST4, p.pair != 0), h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v,
                               tg, ti, parts));
   } else {

@@ -20,6 +20,9 @@
 // T is stored as FP32 hi/lo copies (built once at create): the original layout for n >= 1
 // (i_0 contiguous) and a mode-(1,0,2,..) permuted copy for n = 0 so that B is always K-major.
 #pragma once
+#ifdef JKCALS_DEV_PROBES
+#include <cstdio>
+#endif
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -51,6 +54,7 @@ struct TfGeom {
   int G;
   int stages;     // shared-memory ring depth (as many as fit, <= kTfMaxStages)
   int chunk;      // k-tiles per FP32 accumulation chain (kTfChunk unless tuned)
+  int probe;      // dev timing probe builds only (JKCALS_DEV_PROBES)
 };
 
 __host__ __device__ constexpr size_t tf_stage_bytes(int BN, int nslow) {
@@ -282,6 +286,11 @@ __global__ void __launch_bounds__(kTfThreads, 1)
               if (s < v.nslow)
                 bulk_load(stS(slot) + s * kBM, v.Us[s] + (int64_t)sidx[s] * g.ldu + c0s, kBM * 8u, sbar);
             // view (q0, runA, n, runB) for every mode (the n = 0 view is the permuted copy)
+#ifdef JKCALS_DEV_PROBES  // timing probe builds only: no T tiles (wrong results)
+            if (g.probe == 3) {
+              if (!PAIR || leader) mbar_expect_tx(bar, 0);
+            } else
+#endif
             if (PAIR) {  // both halves complete on the leader's barrier; the leader expects both
               if (leader) mbar_expect_tx(bar, 2 * t_bytes);
               const uint32_t lb = smem_peer(bar, 0);
@@ -321,6 +330,9 @@ __global__ void __launch_bounds__(kTfThreads, 1)
     if (leader) {
       const uint32_t idesc = umma_idesc_tf32(BN, PAIR ? 256u : 128u);
       unsigned git = 0, gc = 0;  // k-tiles consumed, chunks issued (accumulator buffer = gc & 1)
+#ifdef JKCALS_DEV_PROBES
+      long long pw_b = 0, pw_a = 0, pw_t0 = clock64();
+#endif
       for (int64_t u = u0; u < u1;) {
         const int kt0 = (int)(u % g.KT);
         const int64_t kt_end = (int64_t)kt0 + (u1 - u);
@@ -340,8 +352,19 @@ __global__ void __launch_bounds__(kTfThreads, 1)
             first = true;
           }
           const int slot = (int)(git % kTfStages);
+#ifdef JKCALS_DEV_PROBES  // phase clocks of the MMA warp (probe 5: printed by CTA 0 at the end)
+          long long pc0 = clock64();
+#endif
           mbar_wait_safe(&fullB[slot], (git / kTfStages) & 1u);
+#ifdef JKCALS_DEV_PROBES
+          long long pc1 = clock64();
+#endif
           mbar_wait_safe(&fullA[slot], (git / kTfStages) & 1u);
+#ifdef JKCALS_DEV_PROBES
+          long long pc2 = clock64();
+          pw_b += pc1 - pc0;
+          pw_a += pc2 - pc1;
+#endif
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
           const int kvalid = v.Iq0 - cmp_b0 * kTfBK;
           const int nks = kvalid >= kTfBK ? kTfBK / 8 : (kvalid + 7) / 8;
@@ -350,6 +373,14 @@ __global__ void __launch_bounds__(kTfThreads, 1)
           if (elect_one()) {
             for (int kk = 0; kk < nks; ++kk) {
               const uint32_t ko = kk * 32;  // 8 tf32 = 32 bytes along K inside the 64-byte atom
+#ifdef JKCALS_DEV_PROBES  // timing probe builds only: one MMA per k-tile (wrong results)
+              if (g.probe == 1 && kk > 0) break;
+              if (g.probe == 1) {
+                if (PAIR) umma_tf32_pair(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(bhi + ko), idesc, 1u);
+                else umma_tf32(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(bhi + ko), idesc, 1u);
+                continue;
+              }
+#endif
               if (PAIR) {
                 umma_tf32_pair(dacc, umma_desc_sw64(alo + ko), umma_desc_sw64(bhi + ko), idesc, first ? 0u : 1u);
                 umma_tf32_pair(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(blo + ko), idesc, 1u);
@@ -379,6 +410,10 @@ __global__ void __launch_bounds__(kTfThreads, 1)
           }
         }
       }
+#ifdef JKCALS_DEV_PROBES
+      if (g.probe == 5 && blockIdx.x == 0 && lane == 0)
+        printf("TFPROF cta0 k-tiles %u total %lld waitB %lld waitA %lld\n", git, clock64() - pw_t0, pw_b, pw_a);
+#endif
     }
   } else if (warp >= kTfAWarps) {
     // ======================= TMEM drain warps (4..7) =======================
@@ -401,7 +436,11 @@ __global__ void __launch_bounds__(kTfThreads, 1)
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16) + (gc & 1) * kTfMaxN;
         // BN is a multiple of 16; 32 columns per round keep 32 independent loads in flight
-        for (int col = 0; col < (wr ? BN : 0); col += 32) {
+        int bn_drain = wr ? BN : 0;
+#ifdef JKCALS_DEV_PROBES  // timing probe builds only: drain skipped (wrong results)
+        if (g.probe == 4) bn_drain = 0;
+#endif
+        for (int col = 0; col < bn_drain; col += 32) {
           const bool two = col + 16 < BN;
           float vals[32];
           tmem_ld_32x32b<16>(lane_base + (uint32_t)col, vals);
@@ -469,6 +508,9 @@ __global__ void __launch_bounds__(kTfThreads, 1)
         }
         unsigned char* ah = stA_hi(slot) + rbase;
         unsigned char* al = stA_lo(slot) + rbase;
+#ifdef JKCALS_DEV_PROBES  // timing probe builds only: A tile not built (wrong results)
+        if (g.probe != 2)
+#endif
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
           const int ch = kh * 2 + cc;

@@ -66,15 +66,16 @@ def test_error_history_monotone():
         assert np.all(np.diff(e) <= slack), (p, np.diff(e).max())
 
 
-def test_fault_isolated_to_one_submodel():
+@pytest.mark.parametrize("prec", [0, 2])  # FP64 DMMA, FP64_I8 (per-column U exponents + NaN marker)
+def test_fault_isolated_to_one_submodel(prec):
     # SURVEY §5 fault injection: a submodel driven to overflow (factor scaled by 1e300) is
-    # flagged non-finite and frozen; every other submodel is untouched (bitwise vs a clean run)
+    # flagged non-finite and frozen; every other submodel is untouched (vs a clean run)
     from paper_2112_03985_b200 import JKCals
     w = make_workload("syn50_r2")
-    clean = JKCals(w.T, w.R, hist_cap=30)
+    clean = JKCals(w.T, w.R, hist_cap=30, precision=prec)
     clean.set_init(w.P)
     clean.iterate(30, 0.0)
-    h = JKCals(w.T, w.R, hist_cap=30)
+    h = JKCals(w.T, w.R, hist_cap=30, precision=prec)
     h.set_init(w.P)
     bad = w.P[2] * 1e300
     h.set_init_submodel(7, 2, bad)
