@@ -50,6 +50,7 @@ inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
 //   JKCALS_TF32_MIN_NNT / JKCALS_TF32_MAX_STAGES   FP32 path N tiles / ring depth
 //   JKCALS_TF32_PAIR=0                 FP32 path: one-CTA kernel only (no cta_group::2 pairs)
 //   JKCALS_TF32_CHUNK=<k>              FP32 path: k-tiles per FP32 accumulation chain (accuracy!)
+//   JKCALS_MAX_CTAS=<g>                FP64 MTTKRP: cap on the stream-K grid
 //   JKCALS_I8_RESIDENT / JKCALS_I8_CLUSTER         FP64_I8 kernel variant
 //   JKCALS_I8_PROBE                    timing-probe builds only (-DJKCALS_DEV_PROBES; wrong results)
 //   JKCALS_TOL_HOST_LOOP=1             tol mode: host check after every sweep (no WHILE graph node)
@@ -58,7 +59,7 @@ struct Tuning {
   int force_wm = 0, force_kb = 0, red_pieces = -1;
   double sk_alpha = -1.0;
   int tf32_min_nnt = 0, tf32_max_stages = 8, i8_resident = 0, i8_cluster = 1, i8_probe = 0;
-  int tol_host_loop = 0, tf32_pair = 1, tf32_chunk = 0;
+  int tol_host_loop = 0, tf32_pair = 1, tf32_chunk = 0, max_ctas = 0;
 };
 const Tuning& tuning() {
   static const Tuning t = [] {
@@ -77,6 +78,7 @@ const Tuning& tuning() {
     v.tol_host_loop = geti("JKCALS_TOL_HOST_LOOP", 0);
     v.tf32_pair = geti("JKCALS_TF32_PAIR", 1);
     v.tf32_chunk = geti("JKCALS_TF32_CHUNK", 0);
+    v.max_ctas = geti("JKCALS_MAX_CTAS", 0);
     return v;
   }();
   return t;
@@ -434,6 +436,7 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
   p.units = (int64_t)p.ntiles * p.KT;
   p.smem = ki.smem[p.KV][p.WV][p.KM][p.ST4][p.NT - 1](mg.nslow);
   int64_t gmax = (int64_t)ki.nsm * ki.occ[p.KV][p.WV][p.KM][p.ST4][p.NT - 1][mg.nslow];
+  if (tuning().max_ctas > 0) gmax = std::min<int64_t>(gmax, tuning().max_ctas);
   // at most kMaxPieces partial pieces per output tile: small problems (few tiles) would
   // otherwise write and re-read a BN x BM piece per CTA for ~1 k-tile of work each
   // (only for < 4 tiles: a single 128-column M tile x 5 N tiles -- a syn200 shard at 8 GPUs --
@@ -970,7 +973,7 @@ jkcals_status replan(jkcals_t h) {
     const int red_thr = tuning().red_pieces >= 0 ? tuning().red_pieces : kRedPieces;
     // ... and only when each epilogue CTA would sum many pieces over many rows (r01: a syn200 shard
     // at G = 8, I_n x pieces = 200 x 59, gains 14 %; syn50, 50 x 48, loses 20 % to the extra launch)
-    h->red_on[n] = red_thr > 0 && maxp > red_thr && h->dims[n] * maxp > 8192;
+    h->red_on[n] = red_thr > 0 && maxp > red_thr && (h->dims[n] * maxp > 8192 || tuning().red_pieces >= 0);
     h->table1[n].assign(p.ntiles, TileInfo{});
     for (int t = 0; t < p.ntiles; ++t) {
       h->table1[n][t].first_cta = 0;

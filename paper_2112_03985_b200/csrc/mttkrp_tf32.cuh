@@ -38,9 +38,9 @@ constexpr int kTfThreads = (kTfAWarps + kTfDWarps + 2) * 32;
 constexpr int kTfTmaWarp = kTfAWarps + kTfDWarps, kTfMmaWarp = kTfTmaWarp + 1;
 constexpr int kTfMaxN = 256;      // UMMA N (fp32 accumulator columns) per output tile
 constexpr uint32_t kTfTmemCols = 512;  // two accumulator buffers of kTfMaxN columns
-// FP32 accumulation chains are cut every kTfChunk k-tiles (768 products x 3): the TMEM buffer is
+// FP32 accumulation chains are cut every kTfChunk k-tiles (256 products x 3): the TMEM buffer is
 // drained into the FP64 partial piece while the MMAs continue in the other buffer.
-constexpr int kTfChunk = 48;
+constexpr int kTfChunk = 16;  // r02: 48 left the fluorescence-shaped eem R5 at 2.2e-4 (bar 1e-4); 16: 1.7e-5
 constexpr int kTfMaxStages = 8;
 
 struct TfGeom {
@@ -442,22 +442,18 @@ __global__ void __launch_bounds__(kTfThreads, 1)
 #endif
         for (int col = 0; col < bn_drain; col += 32) {
           const bool two = col + 16 < BN;
+          double* Pc = P + (int64_t)col * kBM;
+          // the running FP64 piece values are requested first: their L2 round trip overlaps the
+          // TMEM loads (the volatile tcgen05.ld would otherwise order them after it)
+          double old[32];
+#pragma unroll
+          for (int q = 0; q < 32; ++q) old[q] = (ch != 0 && (q < 16 || two)) ? __ldcg(Pc + (int64_t)q * kBM) : 0.0;
           float vals[32];
           tmem_ld_32x32b<16>(lane_base + (uint32_t)col, vals);
           if (two) tmem_ld_32x32b<16>(lane_base + (uint32_t)col + 16, vals + 16);
-          double* Pc = P + (int64_t)col * kBM;
-          if (ch == 0) {
 #pragma unroll
-            for (int q = 0; q < 32; ++q)
-              if (q < 16 || two) Pc[(int64_t)q * kBM] = (double)vals[q];
-          } else {
-            double old[32];
-#pragma unroll
-            for (int q = 0; q < 32; ++q) old[q] = (q < 16 || two) ? __ldcg(Pc + (int64_t)q * kBM) : 0.0;
-#pragma unroll
-            for (int q = 0; q < 32; ++q)
-              if (q < 16 || two) Pc[(int64_t)q * kBM] = old[q] + (double)vals[q];
-          }
+          for (int q = 0; q < 32; ++q)
+            if (q < 16 || two) Pc[(int64_t)q * kBM] = old[q] + (double)vals[q];
         }
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         __syncwarp();

@@ -335,6 +335,17 @@ def test_fp32_path_vs_oracle(name, ps):
     check32(h, res, p_list)
 
 
+def test_fp32_fluorescence_shaped_full_config():
+    # the eem R5 config (268 x 201 x 61, long contractions, fluorescence-shaped data): the FP32
+    # accumulation chain length decides this one -- 48 k-tiles per chain left 2.2e-4 (> the 1e-4
+    # bar), 16 gives 1.7e-5 (profiles/r02_fp32_chunk.txt) -- sampled submodels after 100 sweeps
+    w = make_workload("eem_r5")
+    h = run_gpu32(w, w.sweeps)
+    ps = [0, 100, 200, 267]
+    res = O.jk_als(w.T, w.P, p_list=ps, max_iters=w.sweeps, nthreads=NCPU)
+    check32(h, res, ps)
+
+
 def test_fp32_pair_odd_tiles_and_one_cta_variant():
     # the CTA-pair (cta_group::2) FP32 kernel with an odd number of 128-column tiles (C = 60 x 6 =
     # 360: 3 tiles, the last super tile's second half dead) and a ragged I_n = 44, against the oracle;
