@@ -557,6 +557,17 @@ __device__ __forceinline__ void epi_smem_body(const EpiArgs& a, const int k, con
       a.flags[sub] |= F_PINV;
     }
   }
+  // (a7) the stop test's per-submodel scalars, requested before the wait (their last writers are
+  // >= 2 grids back, like the Gramians above) so thread 0's final step is not a chain of L2 loads
+  double pf_nt2 = 0.0, pf_fitp = 0.0, pf_tol = 0.0;
+  int pf_it = 0, pf_fl = 0;
+  if (last && tid == 0) {
+    pf_nt2 = a.normT2p[sub];
+    pf_fitp = a.fit_prev[sub];
+    pf_tol = *a.tol;
+    pf_it = a.iters[sub];
+    pf_fl = a.flags[sub];  // (after this thread's own F_PINV update above)
+  }
   // the MTTKRP of this mode has completed: its reduced tiles are visible from here on
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;\n" :::);
@@ -664,13 +675,13 @@ __device__ __forceinline__ void epi_smem_body(const EpiArgs& a, const int k, con
     for (int r = 0; r < R; ++r)
       for (int c = 0; c < R; ++c) quad += H[r * R + c] * vtv(r, c);
     const double crs = tot[NQ];
-    const double nt2 = a.normT2p[sub];
+    const double nt2 = pf_nt2;
     const double e = nt2 + quad - 2.0 * crs;
-    int it = a.iters[sub] + 1;
+    int it = pf_it + 1;
     a.iters[sub] = it;
     a.err[sub] = e;
     a.hist[(int64_t)sub * a.hist_cap + (it - 1) % a.hist_cap] = e;
-    int f = a.flags[sub];
+    int f = pf_fl;
     bool act = true;
     if (!isfinite(e)) {
       f |= F_NONFINITE;
@@ -678,8 +689,8 @@ __device__ __forceinline__ void epi_smem_body(const EpiArgs& a, const int k, con
     } else {
       if (e < -1e-9 * nt2) f |= F_BREAKDOWN;
       const double fit = nt2 > 0.0 ? 1.0 - sqrt(fmax(e, 0.0)) / sqrt(nt2) : 0.0;
-      const double tol = *a.tol;
-      if (tol > 0.0 && it >= 2 && fabs(fit - a.fit_prev[sub]) < tol) {
+      const double tol = pf_tol;
+      if (tol > 0.0 && it >= 2 && fabs(fit - pf_fitp) < tol) {
         f |= F_CONVERGED;
         act = false;
       }
