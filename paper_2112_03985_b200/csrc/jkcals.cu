@@ -58,7 +58,10 @@ struct Tuning {
   std::string force_nt;
   int force_wm = 0, force_kb = 0, red_pieces = -1;
   double sk_alpha = -1.0;
-  int tf32_min_nnt = 0, tf32_max_stages = 8, i8_resident = 0, i8_cluster = 1, i8_probe = 0;
+  // tf32_max_stages: 4 by default (r02: the MTTKRP is not ring-depth bound -- 3, 4, 6, 8 stages
+  // within 1 % per launch -- while a 4-stage ring leaves room for the dependent epilogue's CTAs
+  // to become resident under PDL: syn200 FP32 38.7 -> 36.3 ms, eem R5 -1.8 %, 4-way -0.4 %)
+  int tf32_min_nnt = 0, tf32_max_stages = 4, i8_resident = 0, i8_cluster = 1, i8_probe = 0;
   int tol_host_loop = 0, tf32_pair = 1, tf32_chunk = 0, max_ctas = 0;
 };
 const Tuning& tuning() {
@@ -71,7 +74,7 @@ const Tuning& tuning() {
     v.red_pieces = geti("JKCALS_RED_PIECES", -1);
     if (const char* e = getenv("JKCALS_SK_ALPHA")) v.sk_alpha = atof(e);
     v.tf32_min_nnt = geti("JKCALS_TF32_MIN_NNT", 0);
-    v.tf32_max_stages = geti("JKCALS_TF32_MAX_STAGES", 8);
+    v.tf32_max_stages = geti("JKCALS_TF32_MAX_STAGES", 4);
     v.i8_resident = geti("JKCALS_I8_RESIDENT", 0);
     v.i8_cluster = geti("JKCALS_I8_CLUSTER", 1);
     v.i8_probe = geti("JKCALS_I8_PROBE", 0);
@@ -309,7 +312,7 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
     // each SM then reads A + B/2 instead of A + B from shared memory per MMA
     p.pair = (p.nMt >= 2 && ki.tfpairs > 0 && tuning().tf32_pair) ? 1 : 0;
     const int BNl = p.pair ? p.BN / 2 : p.BN;
-    // deepest ring of {8, 6, 4, 3} stages that fits (JKCALS_TF32_MAX_STAGES caps it, for tuning)
+    // deepest ring of {8, 6, 4, 3} stages that fits under the cap (JKCALS_TF32_MAX_STAGES, default 4)
     const int cap = tuning().tf32_max_stages;
     p.ST4 = 3;
     for (int st : {8, 6, 4})
