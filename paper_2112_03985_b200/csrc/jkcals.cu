@@ -51,6 +51,7 @@ inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
 //   JKCALS_TF32_PAIR=0                 FP32 path: one-CTA kernel only (no cta_group::2 pairs)
 //   JKCALS_TF32_CHUNK=<k>              FP32 path: k-tiles per FP32 accumulation chain (accuracy!)
 //   JKCALS_MAX_CTAS=<g>                FP64 MTTKRP: cap on the stream-K grid
+//   JKCALS_TF32_JM=<1|2|4>             FP32 path: j' values per k-tile
 //   JKCALS_I8_RESIDENT / JKCALS_I8_CLUSTER         FP64_I8 kernel variant
 //   JKCALS_I8_PROBE                    timing-probe builds only (-DJKCALS_DEV_PROBES; wrong results)
 //   JKCALS_TOL_HOST_LOOP=1             tol mode: host check after every sweep (no WHILE graph node)
@@ -62,7 +63,7 @@ struct Tuning {
   // within 1 % per launch -- while a 4-stage ring leaves room for the dependent epilogue's CTAs
   // to become resident under PDL: syn200 FP32 38.7 -> 36.3 ms, eem R5 -1.8 %, 4-way -0.4 %)
   int tf32_min_nnt = 0, tf32_max_stages = 4, i8_resident = 0, i8_cluster = 1, i8_probe = 0;
-  int tol_host_loop = 0, tf32_pair = 1, tf32_chunk = 0, max_ctas = 0;
+  int tol_host_loop = 0, tf32_pair = 1, tf32_chunk = 0, max_ctas = 0, tf32_jm = 0;
 };
 const Tuning& tuning() {
   static const Tuning t = [] {
@@ -82,6 +83,7 @@ const Tuning& tuning() {
     v.tf32_pair = geti("JKCALS_TF32_PAIR", 1);
     v.tf32_chunk = geti("JKCALS_TF32_CHUNK", 0);
     v.max_ctas = geti("JKCALS_MAX_CTAS", 0);
+    v.tf32_jm = geti("JKCALS_TF32_JM", 0);
     return v;
   }();
   return t;
@@ -130,10 +132,11 @@ KernelInfo* kernel_info(int device, std::string* err) {
   {
     cudaError_t e = cudaSuccess;
     for (bool pair : {false, true})
-      for (int st : {3, 4, 6, 8})
-        if (e == cudaSuccess)
-          e = cudaFuncSetAttribute(tf32_kernel(st, pair), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kTfSmemMax);
+      for (int st : {2, 3, 4})
+        for (int jm : {1, 2, 4})
+          if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(tf32_kernel(st, pair, jm), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kTfSmemMax);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(i8_kernel(0), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kI8Smem);
     if (e == cudaSuccess)
@@ -169,7 +172,7 @@ KernelInfo* kernel_info(int device, std::string* err) {
       cfg.blockDim = dim3(kTfThreads);
       cfg.dynamicSmemBytes = kTfSmemMax;
       ncl = 0;
-      if (cudaOccupancyMaxActiveClusters(&ncl, tf32_kernel(8, true), &cfg) == cudaSuccess)
+      if (cudaOccupancyMaxActiveClusters(&ncl, tf32_kernel(4, true), &cfg) == cudaSuccess)
         ki.tfpairs = ncl;
       cudaGetLastError();
     }
@@ -233,6 +236,7 @@ struct ModePlan {
   std::vector<int> cta_u;  // CTA b processes units [cta_u[b], cta_u[b+1])
   int tf32 = 0;
   int pair = 0, nMt2 = 1;  // FP32 path: CTA-pair kernel on 256-column super tiles (nMt2 per tile row)
+  int JM = 1;              // FP32 path: j' values per k-tile
 };
 
 // stream-K CTA ranges, per-tile piece bookkeeping (shared by the FP64 and TF32 plans).
@@ -307,17 +311,25 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
     p.NT = p.BN / 8;
     p.KM = 1;
     p.nMt = (int)std::max<int64_t>(1, cdiv(C, kBM));
-    p.KT = (int)(cdiv(mg.Iq0, kTfBK) * mg.Jp);
     // CTA pairs (cta_group::2, UMMA M = 256) whenever there are two 128-column tiles to pair:
     // each SM then reads A + B/2 instead of A + B from shared memory per MMA
     p.pair = (p.nMt >= 2 && ki.tfpairs > 0 && tuning().tf32_pair) ? 1 : 0;
     const int BNl = p.pair ? p.BN / 2 : p.BN;
-    // deepest ring of {8, 6, 4, 3} stages that fits under the cap (JKCALS_TF32_MAX_STAGES, default 4)
+    // j' values per k-tile (JM): more MMA work per ring handshake (r02); at most
+    // what a 2-stage ring fits
+    // per mode (r02, profiles/r02_fp32_jm.txt): a k-tile of I_n >= 192 rows already carries enough
+    // MMA work per handshake (syn200: JM = 2 was 7 % slower), narrower tiles gain from 4 j' per
+    // k-tile (eem mode 2, I_n = 61: 172 -> 111 us; 4-way mode 3, I_n = 30: 412 -> 277 us)
+    { const int jm = tuning().tf32_jm > 0 ? tuning().tf32_jm : (p.BN >= 192 ? 1 : 4);
+      p.JM = jm >= 4 ? 4 : jm >= 2 ? 2 : 1; }
+    while (p.JM > 1 && tf_smem_bytes(BNl, mg.nslow, 2, p.JM) > kTfSmemMax) p.JM /= 2;
+    p.KT = (int)(cdiv(mg.Iq0, kTfBK) * cdiv(mg.Jp, p.JM));
+    // deepest ring of {4, 3, 2} stages that fits under the cap (JKCALS_TF32_MAX_STAGES, default 4)
     const int cap = tuning().tf32_max_stages;
-    p.ST4 = 3;
-    for (int st : {8, 6, 4})
-      if (st <= cap && tf_smem_bytes(BNl, mg.nslow, st) <= kTfSmemMax) { p.ST4 = st; break; }
-    p.smem = tf_smem_bytes(BNl, mg.nslow, p.ST4);
+    p.ST4 = 2;
+    for (int st : {4, 3})  // (deeper rings measured no faster, r02)
+      if (st <= cap && tf_smem_bytes(BNl, mg.nslow, st, p.JM) <= kTfSmemMax) { p.ST4 = st; break; }
+    p.smem = tf_smem_bytes(BNl, mg.nslow, p.ST4, p.JM);
     if (!p.pair) {
       p.ntiles = p.nMt * p.nNt;
       p.units = (int64_t)p.ntiles * p.KT;
@@ -1179,12 +1191,13 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     cfg.attrs = attr;
     cfg.numAttrs = p.pair ? 2 : 1;
     tg.stages = p.ST4;
-    tg.chunk = tuning().tf32_chunk > 0 ? tuning().tf32_chunk : kTfChunk;
+    tg.jm = p.JM;  // (the chain length stays ~256 products x 3: kTfChunk 16-k sub-tiles)
+    tg.chunk = tuning().tf32_chunk > 0 ? tuning().tf32_chunk : std::max(1, kTfChunk / p.JM);
     tg.probe = 0;
 #ifdef JKCALS_DEV_PROBES  // timing-probe builds only (results are wrong when set)
     tg.probe = tuning().i8_probe;
 #endif
-    CKH(h, cudaLaunchKernelEx(&cfg, tf32_kernel(p.ST4, p.pair != 0), h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v,
+    CKH(h, cudaLaunchKernelEx(&cfg, tf32_kernel(p.ST4, p.pair != 0, p.JM), h->tmThi[n], h->tmTlo[n], h->tmU[h->cur][n], v,
                               tg, ti, parts));
   } else {
     MttkrpFn fn = h->ki->fn[p.KV][p.WV][p.KM][p.ST4][p.NT - 1];

@@ -33,7 +33,7 @@ void dmma_kernels_km1_kb20(MttkrpFn fn[kNumWM][2][kMaxNT], SmemFn smem[kNumWM][2
 
 typedef void (*TfFn)(const CUtensorMap, const CUtensorMap, const CUtensorMap, MttkrpView, TfGeom, const TileInfo*,
                      double*);
-TfFn tf32_kernel(int stages, bool pair = false);  // k_tf32.cu: stages in {3, 4, 6, 8}; pair: cta_group::2
+TfFn tf32_kernel(int stages, bool pair = false, int jm = 1);  // k_tf32.cu: stages {2,3,4}, pair: cta_group::2, jm {1,2,4}
 
 typedef void (*I8Fn)(const CUtensorMap, const CUtensorMap, I8Geom, const TileInfo*, double*);
 I8Fn i8_kernel(int variant);  // k_i8.cu: 0 streaming, 1 resident A, 2 2-CTA cluster

@@ -53,17 +53,19 @@ struct TfGeom {
   int64_t units;
   int G;
   int stages;     // shared-memory ring depth (as many as fit, <= kTfMaxStages)
-  int chunk;      // k-tiles per FP32 accumulation chain (kTfChunk unless tuned)
+  int chunk;      // k-tiles per FP32 accumulation chain (kTfChunk / jm unless tuned)
+  int jm;         // j' values per k-tile (1, 2 or 4): a k-tile is 16 i_q0 x jm j' (r02)
   int probe;      // dev timing probe builds only (JKCALS_DEV_PROBES)
 };
 
-__host__ __device__ constexpr size_t tf_stage_bytes(int BN, int nslow) {
-  return 2u * 128u * 64u + 2u * (size_t)BN * 64u + (size_t)nslow * kBM * 8u;
+// one ring stage = jm sub-tiles of {A_hi, A_lo (128 x 64 B each), B_hi, B_lo (BN x 64 B), S rows}
+__host__ __device__ constexpr size_t tf_stage_bytes(int BN, int nslow, int jm = 1) {
+  return (size_t)jm * (2u * 128u * 64u + 2u * (size_t)BN * 64u + (size_t)nslow * kBM * 8u);
 }
 __host__ __device__ constexpr size_t tf_slab_bytes() { return 2ull * kBK * kBMP * 8ull; }
-__host__ __device__ constexpr size_t tf_smem_bytes(int BN, int nslow, int stages) {
+__host__ __device__ constexpr size_t tf_smem_bytes(int BN, int nslow, int stages, int jm = 1) {
   // 1 KB alignment slack + slab + stages + barriers (3 per stage + 4) + TMEM address
-  return 1024 + tf_slab_bytes() + stages * tf_stage_bytes(BN, nslow) + (4 * stages + 4) * 8 + 16;
+  return 1024 + tf_slab_bytes() + stages * tf_stage_bytes(BN, nslow, jm) + (4 * stages + 4) * 8 + 16;
 }
 
 // UMMA shared-memory descriptor: K-major, SWIZZLE_64B, 8-row groups of 64-byte rows (SBO 512 B)
@@ -168,7 +170,7 @@ __device__ __forceinline__ void tmem_ld_32x32b(uint32_t taddr, float* v) {
 // leader's single MMA thread reads both halves: the shared-memory operand traffic per SM drops
 // from (A + B) to (A + B/2) per MMA. Pieces stay per 128-column tile (CTA rank r writes tile
 // 2 * tm2 + r), so the epilogue is unchanged.
-template <int kTfStages, bool PAIR = false>
+template <int kTfStages, bool PAIR = false, int JMT = 1>
 __global__ void __launch_bounds__(kTfThreads, 1)
     mttkrp_tf32_kernel(const __grid_constant__ CUtensorMap tmThi, const __grid_constant__ CUtensorMap tmTlo,
                        const __grid_constant__ CUtensorMap tmU, MttkrpView v, TfGeom g,
@@ -178,7 +180,9 @@ __global__ void __launch_bounds__(kTfThreads, 1)
   double* Ub = reinterpret_cast<double*>(base);                                   // [2][BK][BMP] fp64
   unsigned char* stages = base + tf_slab_bytes();
   const int BNl = PAIR ? g.BN / 2 : g.BN;  // rows of the T tile held by this CTA
-  const size_t stage_sz = tf_stage_bytes(BNl, v.nslow);
+  constexpr int JM = JMT;                    // j' per k-tile (compile-time: loops unrolled)
+  const int KTJ = (v.Jp + JM - 1) / JM;       // k-tiles per i_q0 block
+  const size_t stage_sz = tf_stage_bytes(BNl, v.nslow, JM);
   uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kTfStages * stage_sz);
   uint64_t* fullB = bars;                      // TMA data landed (count 1 + tx)
   uint64_t* fullA = bars + kTfStages;          // A tile written (count kTfAWarps)
@@ -197,11 +201,18 @@ __global__ void __launch_bounds__(kTfThreads, 1)
   const int64_t u0 = cta_u[b], u1 = cta_u[b + 1];
   const int BN = g.BN;
 
-  auto stA_hi = [&](int s) { return stages + s * stage_sz; };
-  auto stA_lo = [&](int s) { return stages + s * stage_sz + 128 * 64; };
-  auto stB_hi = [&](int s) { return stages + s * stage_sz + 2 * 128 * 64; };
-  auto stB_lo = [&](int s) { return stages + s * stage_sz + 2 * 128 * 64 + (size_t)BNl * 64; };
-  auto stS = [&](int s) { return reinterpret_cast<double*>(stages + s * stage_sz + 2 * 128 * 64 + 2 * (size_t)BNl * 64); };
+  // stage layout: A_hi[JM] | A_lo[JM] | B_hi[JM] | B_lo[JM] | S[JM][nslow][128] (sub-tile jj of a
+  // stage is j' = jp0 + jj; every sub-tile base is a multiple of 512 B, the SWIZZLE_64B period)
+  auto stA_hi = [&](int s, int jj) { return stages + s * stage_sz + (size_t)jj * 8192; };
+  auto stA_lo = [&](int s, int jj) { return stages + s * stage_sz + (size_t)(JM + jj) * 8192; };
+  auto stB_hi = [&](int s, int jj) { return stages + s * stage_sz + (size_t)JM * 16384 + (size_t)jj * BNl * 64; };
+  auto stB_lo = [&](int s, int jj) {
+    return stages + s * stage_sz + (size_t)JM * 16384 + (size_t)(JM + jj) * BNl * 64;
+  };
+  auto stS = [&](int s, int jj) {
+    return reinterpret_cast<double*>(stages + s * stage_sz + (size_t)JM * 16384 + (size_t)2 * JM * BNl * 64 +
+                                     (size_t)jj * v.nslow * kBM * 8);
+  };
 
   if (tid == 0) {
     for (int s = 0; s < kTfStages; ++s) {
@@ -255,71 +266,104 @@ __global__ void __launch_bounds__(kTfThreads, 1)
         const int c0 = (PAIR ? 2 * tm + crk : tm) * kBM, i0 = tn * BN + crk * BNl;
         for (unsigned q = (ld_git >= (unsigned)kTfStages ? ld_git - kTfStages + 1 : 0); q < ld_git; ++q)
           mbar_wait_safe(&empty[q % kTfStages], (q / kTfStages) & 1u);
-        int ld_b0 = kt0 / v.Jp, ld_jp = kt0 % v.Jp, loaded_b0 = -1;
+        int loaded_b0 = -1;
+        // running j' state (divisions only at a segment start: a per-k-tile div/mod chain in
+        // this single issuing lane made the TMA loop the bottleneck)
+        int ld_b0 = kt0 / KTJ, ld_jp = (kt0 % KTJ) * JM;
         int ld_ja = ld_jp % v.runA, ld_jb = ld_jp / v.runA;
         int sidx[kMaxModes - 2];
         {
           int rem = ld_jp;
 #pragma unroll
-          for (int s = 0; s < kMaxModes - 2; ++s)
-            if (s < v.nslow) { sidx[s] = rem % v.sdim[s]; rem /= v.sdim[s]; }
+          for (int q = 0; q < kMaxModes - 2; ++q)
+            if (q < v.nslow) { sidx[q] = rem % v.sdim[q]; rem /= v.sdim[q]; }
         }
 #pragma unroll 1
         for (int kt = kt0; kt < kt1; ++kt) {
+          const int nv = v.Jp - ld_jp < JM ? v.Jp - ld_jp : JM;  // j' sub-tiles of this k-tile
           const int slot = (int)(ld_git % kTfStages);
           if (ld_git >= (unsigned)kTfStages) mbar_wait_safe(&empty[slot], ((ld_git / kTfStages) - 1) & 1u);
           uint64_t* bar = &fullB[slot];
           const bool new_slab = (ld_b0 != loaded_b0);
-          if (new_slab && v.Jp < kTfStages - 1) {  // short i_q0 blocks: drain before reusing a slab buffer
+          if (new_slab && KTJ < kTfStages - 1) {  // short i_q0 blocks: drain before reusing a slab buffer
             for (unsigned q = (ld_git >= (unsigned)kTfStages ? ld_git - kTfStages + 1 : 0); q < ld_git; ++q)
               mbar_wait_safe(&empty[q % kTfStages], (q / kTfStages) & 1u);
           }
           uint64_t* sbar = &fullS[slot];
           if (elect_one()) {
             // the A producers only need the slow-mode rows and the U_q0 slab: their own barrier
-            mbar_expect_tx(sbar, s_bytes + (new_slab ? (unsigned)(kBK * kBMP * 8) : 0u));
+            mbar_expect_tx(sbar, (unsigned)nv * s_bytes + (new_slab ? (unsigned)(kBK * kBMP * 8) : 0u));
             if (new_slab) tma_load_2d(Ub + (ld_b0 & 1) * (kBK * kBMP), &tmU, c0, ld_b0 * kBK, sbar);
             // (c0s: the dead second half of an odd last super tile reads a valid row; unused)
             const int c0s = c0 < nMt1 * kBM ? c0 : c0 - kBM;
+            {
+              int si[kMaxModes - 2];  // slow-mode indices of j' = ld_jp + jj (mixed radix, Eq. 3)
 #pragma unroll
-            for (int s = 0; s < kMaxModes - 2; ++s)
-              if (s < v.nslow)
-                bulk_load(stS(slot) + s * kBM, v.Us[s] + (int64_t)sidx[s] * g.ldu + c0s, kBM * 8u, sbar);
+              for (int q = 0; q < kMaxModes - 2; ++q) si[q] = sidx[q];
+              for (int jj = 0; jj < JM && jj < nv; ++jj) {
+#pragma unroll
+                for (int q = 0; q < kMaxModes - 2; ++q)
+                  if (q < v.nslow)
+                    bulk_load(stS(slot, jj) + q * kBM, v.Us[q] + (int64_t)si[q] * g.ldu + c0s, kBM * 8u, sbar);
+#pragma unroll
+                for (int q = 0; q < kMaxModes - 2; ++q) {
+                  if (q < v.nslow) {
+                    if (++si[q] < v.sdim[q]) break;
+                    si[q] = 0;
+                  }
+                }
+              }
+            }
             // view (q0, runA, n, runB) for every mode (the n = 0 view is the permuted copy)
 #ifdef JKCALS_DEV_PROBES  // timing probe builds only: no T tiles (wrong results)
-            if (g.probe == 3) {
+            if (g.probe == 3 || g.probe == 6) {
               if (!PAIR || leader) mbar_expect_tx(bar, 0);
             } else
 #endif
-            if (PAIR) {  // both halves complete on the leader's barrier; the leader expects both
-              if (leader) mbar_expect_tx(bar, 2 * t_bytes);
-              const uint32_t lb = smem_peer(bar, 0);
-              tma_load_4d_pair(stB_hi(slot), &tmThi, ld_b0 * kTfBK, ld_ja, i0, ld_jb, lb);
-              tma_load_4d_pair(stB_lo(slot), &tmTlo, ld_b0 * kTfBK, ld_ja, i0, ld_jb, lb);
-            } else {
-              mbar_expect_tx(bar, t_bytes);
-              tma_load_4d(stB_hi(slot), &tmThi, ld_b0 * kTfBK, ld_ja, i0, ld_jb, bar);
-              tma_load_4d(stB_lo(slot), &tmTlo, ld_b0 * kTfBK, ld_ja, i0, ld_jb, bar);
+            {
+              // both halves of a pair complete on the leader's barrier; the leader expects both
+              if (!PAIR || leader) mbar_expect_tx(bar, (unsigned)nv * (PAIR ? 2 * t_bytes : t_bytes));
+              const uint32_t lb = PAIR ? smem_peer(bar, 0) : 0u;
+              int ja = ld_ja, jb = ld_jb;
+              for (int jj = 0; jj < JM && jj < nv; ++jj) {
+                if (PAIR) {
+                  tma_load_4d_pair(stB_hi(slot, jj), &tmThi, ld_b0 * kTfBK, ja, i0, jb, lb);
+                  tma_load_4d_pair(stB_lo(slot, jj), &tmTlo, ld_b0 * kTfBK, ja, i0, jb, lb);
+                } else {
+                  tma_load_4d(stB_hi(slot, jj), &tmThi, ld_b0 * kTfBK, ja, i0, jb, bar);
+                  tma_load_4d(stB_lo(slot, jj), &tmTlo, ld_b0 * kTfBK, ja, i0, jb, bar);
+                }
+                if (++ja == v.runA) {
+                  ja = 0;
+                  ++jb;
+                }
+              }
             }
           }
           __syncwarp();
           if (new_slab) loaded_b0 = ld_b0;
           ++ld_git;
-          if (++ld_jp == v.Jp) {
+          // advance the running j' state by the nv j' of this k-tile (every lane, uniformly)
+          for (int jj = 0; jj < JM && jj < nv; ++jj) {
+            if (++ld_ja == v.runA) {
+              ld_ja = 0;
+              ++ld_jb;
+            }
+#pragma unroll
+            for (int q = 0; q < kMaxModes - 2; ++q) {
+              if (q < v.nslow) {
+                if (++sidx[q] < v.sdim[q]) break;
+                sidx[q] = 0;
+              }
+            }
+          }
+          ld_jp += nv;
+          if (ld_jp == v.Jp) {  // next i_q0 block: j' restarts at 0
             ld_jp = 0;
             ++ld_b0;
-          }
-          if (++ld_ja == v.runA) {
-            ld_ja = 0;
-            ++ld_jb;
-          }
-          if (ld_jp == 0) ld_jb = 0;
+            ld_ja = ld_jb = 0;
 #pragma unroll
-          for (int s = 0; s < kMaxModes - 2; ++s) {
-            if (s < v.nslow) {
-              if (++sidx[s] < v.sdim[s]) break;
-              sidx[s] = 0;
-            }
+            for (int q = 0; q < kMaxModes - 2; ++q) sidx[q] = 0;
           }
         }
       }
@@ -338,9 +382,9 @@ __global__ void __launch_bounds__(kTfThreads, 1)
         const int64_t kt_end = (int64_t)kt0 + (u1 - u);
         const int kt1 = (int)(kt_end < (int64_t)g.KT ? kt_end : (int64_t)g.KT);
         u += kt1 - kt0;
-        int cmp_b0 = kt0 / v.Jp, cmp_jp = kt0 % v.Jp;
         bool first = true;
         uint32_t dacc = tmem;
+        int cmp_b0 = kt0 / KTJ, cmp_g = kt0 % KTJ;  // running (i_q0 block, j' group)
         for (int kt = kt0; kt < kt1; ++kt) {
           const int cpos = (kt - kt0) % g.chunk;
           if (cpos == 0) {  // new chunk: its accumulator buffer must have been drained
@@ -366,31 +410,38 @@ __global__ void __launch_bounds__(kTfThreads, 1)
           pw_a += pc2 - pc1;
 #endif
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          const int nv = v.Jp - cmp_g * JM < JM ? v.Jp - cmp_g * JM : JM;
           const int kvalid = v.Iq0 - cmp_b0 * kTfBK;
           const int nks = kvalid >= kTfBK ? kTfBK / 8 : (kvalid + 7) / 8;
-          const uint32_t ahi = smem_u32(stA_hi(slot)), alo = smem_u32(stA_lo(slot));
-          const uint32_t bhi = smem_u32(stB_hi(slot)), blo = smem_u32(stB_lo(slot));
           if (elect_one()) {
-            for (int kk = 0; kk < nks; ++kk) {
-              const uint32_t ko = kk * 32;  // 8 tf32 = 32 bytes along K inside the 64-byte atom
+            // sub-tile jj of the stage sits at a fixed stride from sub-tile 0 (A: 8 KB, B: BNl x 64 B)
+            const uint32_t ahi0 = smem_u32(stA_hi(slot, 0)), alo0 = smem_u32(stA_lo(slot, 0));
+            const uint32_t bhi0 = smem_u32(stB_hi(slot, 0)), blo0 = smem_u32(stB_lo(slot, 0));
+            const uint32_t bstride = (uint32_t)BNl * 64u;
+            for (int jj = 0; jj < JM && jj < nv; ++jj) {
+              const uint32_t ahi = ahi0 + jj * 8192u, alo = alo0 + jj * 8192u;
+              const uint32_t bhi = bhi0 + jj * bstride, blo = blo0 + jj * bstride;
+              for (int kk = 0; kk < nks; ++kk) {
+                const uint32_t ko = kk * 32;  // 8 tf32 = 32 bytes along K inside the 64-byte atom
 #ifdef JKCALS_DEV_PROBES  // timing probe builds only: one MMA per k-tile (wrong results)
-              if (g.probe == 1 && kk > 0) break;
-              if (g.probe == 1) {
-                if (PAIR) umma_tf32_pair(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(bhi + ko), idesc, 1u);
-                else umma_tf32(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(bhi + ko), idesc, 1u);
-                continue;
-              }
+                if ((g.probe == 1 || g.probe == 6) && (jj > 0 || kk > 0)) break;
+                if (g.probe == 1 || g.probe == 6) {
+                  if (PAIR) umma_tf32_pair(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(bhi + ko), idesc, 1u);
+                  else umma_tf32(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(bhi + ko), idesc, 1u);
+                  continue;
+                }
 #endif
-              if (PAIR) {
-                umma_tf32_pair(dacc, umma_desc_sw64(alo + ko), umma_desc_sw64(bhi + ko), idesc, first ? 0u : 1u);
-                umma_tf32_pair(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(blo + ko), idesc, 1u);
-                umma_tf32_pair(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(bhi + ko), idesc, 1u);
-              } else {
-                umma_tf32(dacc, umma_desc_sw64(alo + ko), umma_desc_sw64(bhi + ko), idesc, first ? 0u : 1u);
-                umma_tf32(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(blo + ko), idesc, 1u);
-                umma_tf32(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(bhi + ko), idesc, 1u);
+                if (PAIR) {
+                  umma_tf32_pair(dacc, umma_desc_sw64(alo + ko), umma_desc_sw64(bhi + ko), idesc, first ? 0u : 1u);
+                  umma_tf32_pair(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(blo + ko), idesc, 1u);
+                  umma_tf32_pair(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(bhi + ko), idesc, 1u);
+                } else {
+                  umma_tf32(dacc, umma_desc_sw64(alo + ko), umma_desc_sw64(bhi + ko), idesc, first ? 0u : 1u);
+                  umma_tf32(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(blo + ko), idesc, 1u);
+                  umma_tf32(dacc, umma_desc_sw64(ahi + ko), umma_desc_sw64(bhi + ko), idesc, 1u);
+                }
+                first = false;
               }
-              first = false;
             }
             // frees the stage (in both CTAs when PAIR) once these MMAs have read it
             if (PAIR) umma_commit_pair(&empty[slot]);
@@ -404,8 +455,8 @@ __global__ void __launch_bounds__(kTfThreads, 1)
           first = false;
           ++git;
           if (cpos == g.chunk - 1 || kt == kt1 - 1) ++gc;
-          if (++cmp_jp == v.Jp) {
-            cmp_jp = 0;
+          if (++cmp_g == KTJ) {
+            cmp_g = 0;
             ++cmp_b0;
           }
         }
@@ -438,7 +489,7 @@ __global__ void __launch_bounds__(kTfThreads, 1)
         // BN is a multiple of 16; 32 columns per round keep 32 independent loads in flight
         int bn_drain = wr ? BN : 0;
 #ifdef JKCALS_DEV_PROBES  // timing probe builds only: drain skipped (wrong results)
-        if (g.probe == 4) bn_drain = 0;
+        if (g.probe == 4 || g.probe == 6) bn_drain = 0;
 #endif
         for (int col = 0; col < bn_drain; col += 32) {
           const bool two = col + 16 < BN;
@@ -477,7 +528,6 @@ __global__ void __launch_bounds__(kTfThreads, 1)
       const int tm = t % g.nMt;
       const int c0 = (PAIR ? 2 * tm + crk : tm) * kBM;
       const bool live = (c0 + row) < g.C;
-      int cmp_b0 = kt0 / v.Jp, cmp_jp = kt0 % v.Jp;
       // swizzled (SWIZZLE_64B, K-major) byte offset of this row's 16-byte chunk ch
       const uint32_t rbase = (uint32_t)(row >> 3) * 512u + (uint32_t)(row & 7) * 64u;
       const uint32_t sw = (uint32_t)((row & 7) >> 1) & 3u;
@@ -485,44 +535,48 @@ __global__ void __launch_bounds__(kTfThreads, 1)
       // an i_q0 block; they are re-read from the FP64 slab only when the block changes
       float uv[8];
       int uv_b0 = -1;
+      int cmp_b0 = kt0 / KTJ, cmp_g = kt0 % KTJ;  // running (i_q0 block, j' group)
       for (int kt = kt0; kt < kt1; ++kt) {
+        const int nv = v.Jp - cmp_g * JM < JM ? v.Jp - cmp_g * JM : JM;
         const int slot = (int)(git % kTfStages);
         if (git >= (unsigned)kTfStages) mbar_wait_safe(&empty[slot], ((git / kTfStages) - 1) & 1u);
         mbar_wait_safe(&fullS[slot], (git / kTfStages) & 1u);
-        const double* Ss = stS(slot);
-        float s = 0.0f;
-        if (live) {
-          double sd = Ss[row];
-          for (int q = 1; q < v.nslow; ++q) sd *= Ss[q * kBM + row];
-          s = (float)sd;
-        }
         if (uv_b0 != cmp_b0) {
           const double* ub = Ub + (cmp_b0 & 1) * (kBK * kBMP) + row;
 #pragma unroll
           for (int e = 0; e < 8; ++e) uv[e] = (float)ub[(kh * 8 + e) * kBMP];
           uv_b0 = cmp_b0;
         }
-        unsigned char* ah = stA_hi(slot) + rbase;
-        unsigned char* al = stA_lo(slot) + rbase;
+        for (int jj = 0; jj < JM && jj < nv; ++jj) {  // one A sub-tile per j' of the k-tile
+          const double* Ss = stS(slot, jj);
+          float s = 0.0f;
+          if (live) {
+            double sd = Ss[row];
+            for (int q = 1; q < v.nslow; ++q) sd *= Ss[q * kBM + row];
+            s = (float)sd;
+          }
+          unsigned char* ah = stA_hi(slot, jj) + rbase;
+          unsigned char* al = stA_lo(slot, jj) + rbase;
 #ifdef JKCALS_DEV_PROBES  // timing probe builds only: A tile not built (wrong results)
-        if (g.probe != 2)
+          if (g.probe != 2 && g.probe != 6)
 #endif
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          const int ch = kh * 2 + cc;
-          float4 h4, l4;
-          float* hp = &h4.x;
-          float* lp = &l4.x;
+          for (int cc = 0; cc < 2; ++cc) {
+            const int ch = kh * 2 + cc;
+            float4 h4, l4;
+            float* hp = &h4.x;
+            float* lp = &l4.x;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float a = uv[cc * 4 + e] * s;  // KRP^T(c, k) = U_q0(k, c) * S(c), FP32 product
-            const uint32_t hb = tf32_trunc(a);
-            hp[e] = __uint_as_float(hb);
-            lp[e] = a - __uint_as_float(hb);
+            for (int e = 0; e < 4; ++e) {
+              const float a = uv[cc * 4 + e] * s;  // KRP^T(c, k) = U_q0(k, c) * S(c), FP32 product
+              const uint32_t hb = tf32_trunc(a);
+              hp[e] = __uint_as_float(hb);
+              lp[e] = a - __uint_as_float(hb);
+            }
+            const uint32_t off = ((uint32_t)ch ^ sw) * 16u;
+            *reinterpret_cast<float4*>(ah + off) = h4;
+            *reinterpret_cast<float4*>(al + off) = l4;
           }
-          const uint32_t off = ((uint32_t)ch ^ sw) * 16u;
-          *reinterpret_cast<float4*>(ah + off) = h4;
-          *reinterpret_cast<float4*>(al + off) = l4;
         }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> tensor core
         __syncwarp();
@@ -531,8 +585,8 @@ __global__ void __launch_bounds__(kTfThreads, 1)
           else mbar_arrive(&fullA[slot]);
         }
         ++git;
-        if (++cmp_jp == v.Jp) {
-          cmp_jp = 0;
+        if (++cmp_g == KTJ) {
+          cmp_g = 0;
           ++cmp_b0;
         }
       }
