@@ -445,22 +445,44 @@ __global__ void __launch_bounds__(256) krp_gen_kernel(ModeView v, int C, int64_t
   const bool full4 = (c + 4 <= C) && ((ldu & 3) == 0) && ((ldk & 3) == 0);
   // unrolled so that the factor-row loads of several rows are in flight at once (the loop is
   // otherwise one L2 round trip per 32-byte store); streaming (.cs) stores: K is not re-read here
+  // S = product of the slower rest-mode rows (q >= 1), the same for I_fast consecutive rows:
+  // formed once per j' and kept in registers, so a row reads one factor row (the fastest mode's)
+  // instead of nrest -- half the L2 reads for 3-way tensors (r02). Same multiplication order as
+  // forming the whole product per row (slowest mode first): bitwise-identical results.
+  double s0 = 1.0, s1 = 1.0, s2 = 1.0, s3 = 1.0;
+  bool need_s = true;
 #pragma unroll 4
   for (int j = j0; j < j1; ++j) {
-    double r0 = 1.0, r1 = 1.0, r2 = 1.0, r3 = 1.0;
+    if (need_s) {
+      s0 = s1 = s2 = s3 = 1.0;
 #pragma unroll
-    for (int q = kMaxModes - 2; q >= 0; --q) {
-      if (q < v.nrest) {
-        const double* row = v.U[q] + (int64_t)idx[q] * ldu + c;
-        if (full4) {
-          double4 x = *reinterpret_cast<const double4*>(row);  // 32B-aligned (ldu % 4 == 0)
-          r0 *= x.x; r1 *= x.y; r2 *= x.z; r3 *= x.w;
-        } else {
-          r0 *= row[0];
-          if (c + 1 < C) r1 *= row[1];
-          if (c + 2 < C) r2 *= row[2];
-          if (c + 3 < C) r3 *= row[3];
+      for (int q = kMaxModes - 2; q >= 1; --q) {
+        if (q < v.nrest) {
+          const double* row = v.U[q] + (int64_t)idx[q] * ldu + c;
+          if (full4) {
+            double4 x = *reinterpret_cast<const double4*>(row);  // 32B-aligned (ldu % 4 == 0)
+            s0 *= x.x; s1 *= x.y; s2 *= x.z; s3 *= x.w;
+          } else {
+            s0 *= row[0];
+            if (c + 1 < C) s1 *= row[1];
+            if (c + 2 < C) s2 *= row[2];
+            if (c + 3 < C) s3 *= row[3];
+          }
         }
+      }
+      need_s = false;
+    }
+    double r0 = s0, r1 = s1, r2 = s2, r3 = s3;
+    {
+      const double* row = v.U[0] + (int64_t)idx[0] * ldu + c;
+      if (full4) {
+        double4 x = *reinterpret_cast<const double4*>(row);
+        r0 *= x.x; r1 *= x.y; r2 *= x.z; r3 *= x.w;
+      } else {
+        r0 *= row[0];
+        if (c + 1 < C) r1 *= row[1];
+        if (c + 2 < C) r2 *= row[2];
+        if (c + 3 < C) r3 *= row[3];
       }
     }
     double* dst = K + (int64_t)j * ldk + c;
@@ -478,6 +500,7 @@ __global__ void __launch_bounds__(256) krp_gen_kernel(ModeView v, int C, int64_t
       if (q < v.nrest) {
         if (++idx[q] < v.rdim[q]) break;
         idx[q] = 0;
+        need_s = true;  // a slower index moves: new S
       }
     }
   }

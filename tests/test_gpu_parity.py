@@ -107,6 +107,24 @@ def test_krp_kernel_vs_khatri_rao():
         assert np.array_equal(K, ref) or np.allclose(K, ref, rtol=1e-15, atol=0)
 
 
+def test_krp_kernel_full_size_vector_path():
+    # the materialised KRP at a realistic size (50 x 200 x 200, C = 96: the 4-wide vector path,
+    # ldu % 4 == 0, and the register-cached slow-row product), every mode, bitwise vs the oracle's
+    # Khatri-Rao (same multiplication order) -- or to 1 ulp if the compiler contracts differently
+    import torch
+    from paper_2112_03985_b200 import krp
+    g = np.random.default_rng(11)
+    dims, C, ldu = (50, 200, 200), 96, 128
+    U = [g.standard_normal((I, C)) for I in dims]
+    Ud = [torch.from_numpy(np.pad(u, ((0, 0), (0, ldu - C)))).cuda() for u in U]
+    for n in range(3):
+        K = krp(dims, n, Ud, C).cpu().numpy()
+        rest = [m for m in range(3) if m != n]
+        ref = O.khatri_rao(U[rest[1]], U[rest[0]])
+        assert K.shape == ref.shape
+        assert np.allclose(K, ref, rtol=2.3e-16, atol=0), n
+
+
 # ---------------------------------------------------------------- JK-CALS vs JK-ALS
 def test_tiny_all_submodels():
     w = make_workload("tiny")
