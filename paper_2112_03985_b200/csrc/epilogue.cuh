@@ -401,10 +401,10 @@ constexpr int kEpi2Threads = 256;
 #define EPI_PROBE_DUMP()                                                                          \
   do {                                                                                            \
     if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))                     \
-      printf("EPI blk %d n %d: %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", blockIdx.x,   \
+      printf("EPI blk %d n %d: %llu %llu %llu %llu %llu %llu %llu chol %llu\n", blockIdx.x,       \
              a.n, epi_ts_[1] - epi_ts_[0], epi_ts_[2] - epi_ts_[0], epi_ts_[3] - epi_ts_[0],       \
              epi_ts_[4] - epi_ts_[0], epi_ts_[5] - epi_ts_[0], epi_ts_[6] - epi_ts_[0],            \
-             epi_ts_[7] - epi_ts_[0], 0ull, 0ull, 0ull);                                                           \
+             epi_ts_[7] - epi_ts_[0], epi_ts_[8] - epi_ts_[0]);                                    \
   } while (0)
 #else
 #define EPI_PROBE(i) do {} while (0)
@@ -557,6 +557,7 @@ __device__ __forceinline__ void epi_smem_body(const EpiArgs& a, const int k, con
       a.flags[sub] |= F_PINV;
     }
   }
+  EPI_PROBE(8);  // (after thread 0's Cholesky: barrier-free, so other threads pass earlier)
   // (a7) the stop test's per-submodel scalars, requested before the wait (their last writers are
   // >= 2 grids back, like the Gramians above) so thread 0's final step is not a chain of L2 loads
   double pf_nt2 = 0.0, pf_fitp = 0.0, pf_tol = 0.0;
