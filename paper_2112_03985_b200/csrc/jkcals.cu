@@ -52,6 +52,7 @@ inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
 //   JKCALS_TF32_CHUNK=<k>              FP32 path: k-tiles per FP32 accumulation chain (accuracy!)
 //   JKCALS_MAX_CTAS=<g>                FP64 MTTKRP: cap on the stream-K grid
 //   JKCALS_TF32_JM=<1|2|4>             FP32 path: j' values per k-tile
+//   JKCALS_MAX_PIECES=<p>              FP64 MTTKRP: stream-K pieces per tile when < 4 tiles (48)
 //   JKCALS_I8_RESIDENT / JKCALS_I8_CLUSTER         FP64_I8 kernel variant
 //   JKCALS_I8_PROBE                    timing-probe builds only (-DJKCALS_DEV_PROBES; wrong results)
 //   JKCALS_TOL_HOST_LOOP=1             tol mode: host check after every sweep (no WHILE graph node)
@@ -63,7 +64,7 @@ struct Tuning {
   // within 1 % per launch -- while a 4-stage ring leaves room for the dependent epilogue's CTAs
   // to become resident under PDL: syn200 FP32 38.7 -> 36.3 ms, eem R5 -1.8 %, 4-way -0.4 %)
   int tf32_min_nnt = 0, tf32_max_stages = 4, i8_resident = 0, i8_cluster = 1, i8_probe = 0;
-  int tol_host_loop = 0, tf32_pair = 1, tf32_chunk = 0, max_ctas = 0, tf32_jm = 0;
+  int tol_host_loop = 0, tf32_pair = 1, tf32_chunk = 0, max_ctas = 0, tf32_jm = 0, max_pieces = 0;
 };
 const Tuning& tuning() {
   static const Tuning t = [] {
@@ -84,6 +85,7 @@ const Tuning& tuning() {
     v.tf32_chunk = geti("JKCALS_TF32_CHUNK", 0);
     v.max_ctas = geti("JKCALS_MAX_CTAS", 0);
     v.tf32_jm = geti("JKCALS_TF32_JM", 0);
+    v.max_pieces = geti("JKCALS_MAX_PIECES", 0);
     return v;
   }();
   return t;
@@ -456,7 +458,7 @@ ModePlan make_plan(const ModeGeo& mg, int n, int64_t C, const KernelInfo& ki, bo
   // otherwise write and re-read a BN x BM piece per CTA for ~1 k-tile of work each
   // (only for < 4 tiles: a single 128-column M tile x 5 N tiles -- a syn200 shard at 8 GPUs --
   // must still fill both CTA slots of every SM, r01 +20 %; such tiles are pre-reduced, kRedPieces)
-  constexpr int64_t kMaxPieces = 48;
+  const int64_t kMaxPieces = tuning().max_pieces > 0 ? tuning().max_pieces : 48;
   if (p.ntiles < 4) gmax = std::min<int64_t>(gmax, kMaxPieces * p.ntiles);
   p.G = (int)std::min<int64_t>(p.units, gmax);
   // cost-weighted split only when a tile is mostly idle (e.g. 4-way C = 400: the last M tile
