@@ -7,16 +7,19 @@
 // lo = x - hi, and D += A_hi B_hi^T + A_hi B_lo^T + A_lo B_hi^T (the lo*lo term is below FP32
 // rounding) — "3xTF32", which a single TF32 pass would fail (1.5e-4 > 1e-4).
 //
-// Roles (one CTA per SM, 6 warps):
-//   warps 0-3  A producers: build the KRP^T tile of a k-step in shared memory, already split into
-//              hi/lo and laid out in the UMMA K-major SWIZZLE_64B canonical layout, from the
-//              U_q0 slab (TMA) scaled by the S_{j'} row (bulk copies) -- the KRP never hits HBM;
-//              at the end of an output tile they drain the TMEM accumulator (tcgen05.ld) into
-//              the FP64 partial-piece buffer consumed by the same epilogue as the FP64 path.
-//   warp 4     TMA producer (one lane): T_hi / T_lo boxes (4-D tensor maps, 64-B swizzle), the
-//              S rows and the U_q0 slab, all on the stage's mbarrier.
-//   warp 5     MMA issuer (one lane): 3 x (BK/8) tcgen05.mma per k-tile, tcgen05.commit to the
-//              stage's `empty` barrier and, per output tile, to `acc_full`.
+// Roles (one CTA per SM, 14 warps):
+//   warps 0-7   A producers: build the KRP^T tile of a k-tile in shared memory, already split into
+//               hi/lo and laid out in the UMMA K-major SWIZZLE_64B canonical layout, from the
+//               U_q0 slab (TMA) scaled by the S_{j'} rows (bulk copies) -- the KRP never hits HBM.
+//   warps 8-11  drain: per FP32 accumulation chain, tcgen05.ld of the TMEM accumulator (one lane
+//               quadrant each) added into the FP64 partial piece read by the FP64 path's epilogue.
+//   warp 12     TMA producer (one lane): T_hi / T_lo boxes (4-D tensor maps, 64-B swizzle), the
+//               S rows and the U_q0 slab, on the stage's mbarriers.
+//   warp 13     MMA issuer (one lane): 3 x (16/8) tcgen05.mma per j' sub-tile, tcgen05.commit to
+//               the stage's `empty` barrier and, per chain, to `acc_full`.
+// Variants (r02): PAIR -- a 2-CTA cluster on a 256-column super tile with cta_group::2 MMAs
+// (M = 256), each CTA holding half of the T tile; JM -- 1, 2 or 4 j' values per k-tile, to
+// amortise the ring handshakes on narrow tiles.
 // T is stored as FP32 hi/lo copies (built once at create): the original layout for n >= 1
 // (i_0 contiguous) and a mode-(1,0,2,..) permuted copy for n = 0 so that B is always K-major.
 #pragma once
