@@ -31,6 +31,21 @@ hp.align()
 h32 = JKCals(w.T, w.R, hist_cap=10, precision=1)
 h32.set_init(w.P)
 h32.iterate(5, 0.0)
+# r02 kernels: FP32 CTA pairs with an odd tile count + 4 j' per k-tile, the cluster-resident
+# syn50-size path, tol mode through the CUDA-graph WHILE node
+w6 = make_workload(((60, 44, 36), 6, 6, 0.01, "syn", 4))
+h6 = JKCals(w6.T, w6.R, hist_cap=4, precision=1)
+h6.set_init(w6.P)
+h6.iterate(3, 0.0)
+w1 = make_workload("syn50_r1")
+hr = JKCals(w1.T, w1.R, hist_cap=8)
+hr.set_init(w1.P)
+hr.iterate(4, 0.0)
+w3 = make_workload("syn50_r3")
+os.environ["JKCALS_RESIDENT"] = "0"
+ht = JKCals(w3.T, w3.R, hist_cap=200)
+ht.set_init(w3.P)
+ht.iterate(200, 1e-6)
 g = np.random.default_rng(0)
 dims, C = (9, 7, 5), 20
 T = torch.from_numpy(g.standard_normal(int(np.prod(dims)))).cuda()
