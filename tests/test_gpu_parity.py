@@ -197,6 +197,18 @@ def test_sampled_syn200_bench_config():
     check_against_oracle(h, res, ps, nt2p_of(w.T))
 
 
+def test_small_shard_pre_reduced_pieces():
+    # a syn200 shard at G = 8 (25 submodels, C = 125): one 128-column tile split ~59 ways, so the
+    # stream-K pieces go through the warp-split reduce_pieces_kernel before the epilogue (the
+    # r02 rewrite) -- sampled submodels of two shards against the oracle at the FP64 bar
+    w = make_workload("syn200")
+    for lo, hi, ps in ((0, 25, [0, 13, 24]), (175, 200, [175, 199])):
+        h, _ = run_gpu(w, w.sweeps, sub_range=(lo, hi))
+        res = O.jk_als(w.T, w.P, p_list=ps, max_iters=w.sweeps, nthreads=NCPU)
+        check_against_oracle(h, res, ps, nt2p_of(w.T))
+        h.close()
+
+
 # ---------------------------------------------------------------- modes of operation
 def test_tolerance_mode_and_compaction():
     w = make_workload("syn50_r3")
