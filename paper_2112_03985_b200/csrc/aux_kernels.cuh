@@ -204,6 +204,20 @@ __global__ void store_block_kernel(const double* __restrict__ U, int I, int64_t 
   dst[e] = U[(int64_t)i * ldu + col + r];
 }
 
+// (a8) the same for every block converged since the last compaction in one launch per mode:
+// tab[3 y .. 3 y + 2] = (first column, rank R, slot) of block y; its mode-n block lands at
+// Ures + slot * slot_doubles + sum_{m<n} I_m * R (the per-slot result store layout)
+__global__ void store_blocks_kernel(const double* __restrict__ U, int I, int64_t ldu, const int* __restrict__ tab,
+                                    int64_t slot_doubles, int64_t sumIprev, double* __restrict__ Ures) {
+  const int y = blockIdx.y;
+  const int col = tab[3 * y], R = tab[3 * y + 1], slot = tab[3 * y + 2];
+  double* dst = Ures + (int64_t)slot * slot_doubles + sumIprev * R;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < I * R; e += gridDim.x * blockDim.x) {
+    const int i = e / R, r = e % R;
+    dst[e] = U[(int64_t)i * ldu + col + r];
+  }
+}
+
 // (a8) masked compaction: gather the surviving blocks' columns (new column c <- old column
 // colmap[c]) to the front of the other multi-factor buffer; columns >= C_new become zero padding.
 __global__ void gather_blocks_kernel(const double* __restrict__ Uold, double* __restrict__ Unew, int I,

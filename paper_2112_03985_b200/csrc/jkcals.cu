@@ -791,7 +791,7 @@ bool compute_offsets(int N, const int64_t* dims, int R, int64_t nsub, int hist_c
   o->flags = L.take(nsub * 4);
   o->active = L.take(nsub * 4);
   o->blk2sub = L.take(nsub * 4);
-  o->map = L.take(ldu * 4);  // compaction column map
+  o->map = L.take(ldu * 12);  // compaction column map (ldu ints) / converged-block table (3 per block)
   o->pglob = L.take(nsub * 8);
   o->srcoff = L.take(nsub * 8);
   o->srcld = L.take(nsub * 8);
@@ -1462,21 +1462,29 @@ jkcals_status compact(jkcals_t h) {
                          h->stream));
   CKH(h, cudaStreamSynchronize(h->stream));
   const int64_t sumI = sum_dims(h);
-  std::vector<int> keep;
+  std::vector<int> keep, tab;  // tab: (column, rank, slot) of each block to store
+  int rmax = 1;
   for (int k = 0; k < h->K; ++k) {
     const int sub = h->h_blk2sub[k], R = h->h_subR[sub], col = h->h_blkcol[k];
     if (act[sub]) {
       keep.push_back(sub);
     } else if (!h->h_stored[sub]) {
-      int64_t o = 0;
-      for (int n = 0; n < h->N; ++n) {
-        int I = (int)h->dims[n];
-        double* dst = h->ptr<double>(h->off.Ures) + (int64_t)sub * sumI * h->R + o;
-        store_block_kernel<<<(int)cdiv((int64_t)I * R, 256), 256, 0, h->stream>>>(h->U(n), I, h->ldu, R, col, dst);
-        CKH(h, cudaGetLastError());
-        o += (int64_t)I * R;
-      }
+      tab.insert(tab.end(), {col, R, sub});
+      rmax = std::max(rmax, R);
       h->h_stored[sub] = 1;
+    }
+  }
+  if (!tab.empty()) {  // one launch per mode for all newly converged blocks (r02: was N per block)
+    const int nst = (int)tab.size() / 3;
+    int* dtab = h->ptr<int>(h->off.map);  // (free here: relayout uploads its column map after these)
+    CKH(h, cudaMemcpyAsync(dtab, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+    int64_t sumIprev = 0;
+    for (int n = 0; n < h->N; ++n) {
+      const int I = (int)h->dims[n];
+      store_blocks_kernel<<<dim3((unsigned)cdiv((int64_t)I * rmax, 256), (unsigned)nst), 256, 0, h->stream>>>(
+          h->U(n), I, h->ldu, dtab, sumI * h->R, sumIprev, h->ptr<double>(h->off.Ures));
+      CKH(h, cudaGetLastError());
+      sumIprev += I;
     }
   }
   if ((int)keep.size() == h->K) return JKCALS_OK;
