@@ -78,11 +78,11 @@ typedef enum {
  * 31 % relative error at 4-way full size). Therefore, when iterate() runs with tol > 0, the LAST
  * mode's MTTKRP of every sweep runs on the FP64 kernel: its update and the error/fit behind the
  * stop rule are FP64-accurate (reading A24). With tol <= 0 every mode runs in FP32.
- * Accuracy: FP32 accumulation chains are cut every 256 products (x 3 split terms) and summed in
+ * Accuracy: FP32 accumulation chains are cut every 128 products (x 3 split terms) and summed in
  * FP64; measured at full size (every submodel, 100 sweeps) against the FP64 oracle: syn200
- * 6.3e-6, 4-way 2.9e-6, fluorescence-shaped eem R5 5.2e-5 / 7.8e-5 (factors / lambda) -- the
- * latter's margin to the 1e-4 bar is thin: ill-conditioned models (e.g. R above the data's
- * rank) can exceed 1e-4 in FP32 and should use JKCALS_FP64. */
+ * 1.6e-6, 4-way 4.1e-7, fluorescence-shaped eem R5 1.7e-5 / 2.6e-5 (factors / lambda).
+ * Ill-conditioned models (e.g. R above the data's rank) can exceed 1e-4 in FP32 and should use
+ * JKCALS_FP64. */
 typedef enum { JKCALS_FP64 = 0, JKCALS_FP32 = 1, JKCALS_FP64_I8 = 2 } jkcals_precision;
 
 enum {

@@ -1193,7 +1193,7 @@ jkcals_status enqueue_mode(jkcals_t h, int n, bool timed) {
     cfg.attrs = attr;
     cfg.numAttrs = p.pair ? 2 : 1;
     tg.stages = p.ST4;
-    tg.jm = p.JM;  // (the chain length stays ~256 products x 3: kTfChunk 16-k sub-tiles)
+    tg.jm = p.JM;  // (the chain length stays 128 products x 3: kTfChunk 16-k sub-tiles)
     tg.chunk = tuning().tf32_chunk > 0 ? tuning().tf32_chunk : std::max(1, kTfChunk / p.JM);
     tg.probe = 0;
 #ifdef JKCALS_DEV_PROBES  // timing-probe builds only (results are wrong when set)

@@ -41,9 +41,9 @@ constexpr int kTfThreads = (kTfAWarps + kTfDWarps + 2) * 32;
 constexpr int kTfTmaWarp = kTfAWarps + kTfDWarps, kTfMmaWarp = kTfTmaWarp + 1;
 constexpr int kTfMaxN = 256;      // UMMA N (fp32 accumulator columns) per output tile
 constexpr uint32_t kTfTmemCols = 512;  // two accumulator buffers of kTfMaxN columns
-// FP32 accumulation chains are cut every kTfChunk k-tiles (256 products x 3): the TMEM buffer is
+// FP32 accumulation chains are cut every kTfChunk k-tiles (128 products x 3): the TMEM buffer is
 // drained into the FP64 partial piece while the MMAs continue in the other buffer.
-constexpr int kTfChunk = 16;  // r02: 48 left the fluorescence-shaped eem R5 at 2.2e-4 (bar 1e-4); 16: 1.7e-5
+constexpr int kTfChunk = 8;  // r02: 48 left the fluorescence-shaped eem R5 at 2.2e-4 (bar 1e-4), 16 at 1.2e-4 (lambda, full size)
 constexpr int kTfMaxStages = 8;
 
 struct TfGeom {

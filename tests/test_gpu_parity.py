@@ -367,8 +367,9 @@ def test_fp32_path_vs_oracle(name, ps):
 
 def test_fp32_fluorescence_shaped_full_config():
     # the eem R5 config (268 x 201 x 61, long contractions, fluorescence-shaped data): the FP32
-    # accumulation chain length decides this one -- 48 k-tiles per chain left 2.2e-4 (> the 1e-4
-    # bar), 16 gives 1.7e-5 (profiles/r02_fp32_chunk.txt) -- sampled submodels after 100 sweeps
+    # accumulation chain length decides this one -- 768-product chains left 2.2e-4 (> the 1e-4
+    # bar), 128-product chains 1.7e-5 at full size (profiles/r02_full_parity.jsonl) -- sampled
+    # submodels after 100 sweeps
     w = make_workload("eem_r5")
     h = run_gpu32(w, w.sweeps)
     ps = [0, 100, 200, 267]
