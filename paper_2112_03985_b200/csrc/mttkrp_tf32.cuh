@@ -66,9 +66,27 @@ __host__ __device__ constexpr size_t tf_stage_bytes(int BN, int nslow, int jm = 
   return (size_t)jm * (2u * 128u * 64u + 2u * (size_t)BN * 64u + (size_t)nslow * kBM * 8u);
 }
 __host__ __device__ constexpr size_t tf_slab_bytes() { return 2ull * kBK * kBMP * 8ull; }
+// drain staging: two buffers of 16 TMEM columns x 128 lanes in FP64 ([16 rows i][128 columns c])
+constexpr size_t kTfStgBytes = 2u * 16u * 128u * 8u;
 __host__ __device__ constexpr size_t tf_smem_bytes(int BN, int nslow, int stages, int jm = 1) {
-  // 1 KB alignment slack + slab + stages + barriers (3 per stage + 4) + TMEM address
-  return 1024 + tf_slab_bytes() + stages * tf_stage_bytes(BN, nslow, jm) + (4 * stages + 4) * 8 + 16;
+  // 1 KB alignment slack + drain staging + slab + stages + barriers (4 per stage + 4) + TMEM address
+  return 1024 + kTfStgBytes + tf_slab_bytes() + stages * tf_stage_bytes(BN, nslow, jm) + (4 * stages + 4) * 8 + 16;
+}
+// bulk (TMA-engine) moves of a drained FP64 block into the partial piece: plain copy for the first
+// chain of a segment, f64 add (UBLKRED.ADD.F64) for the next ones -- no L2 round trip on the drain
+__device__ __forceinline__ void bulk_store_f64(double* dst, const void* src, unsigned bytes, bool add) {
+  if (add)
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;\n" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+  else
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void drain_bar() {  // the 4 drain warps only (named barrier 1)
+  asm volatile("bar.sync 1, %0;\n" ::"n"(kTfDWarps * 32) : "memory");
 }
 
 // UMMA shared-memory descriptor: K-major, SWIZZLE_64B, 8-row groups of 64-byte rows (SBO 512 B)
@@ -180,8 +198,9 @@ __global__ void __launch_bounds__(kTfThreads, 1)
                        const TileInfo* __restrict__ tinfo, double* __restrict__ parts) {
   extern __shared__ __align__(1024) unsigned char tsm[];
   unsigned char* base = tsm;  // dynamic smem is 1 KB aligned (__align__(1024) on the declaration)
-  double* Ub = reinterpret_cast<double*>(base);                                   // [2][BK][BMP] fp64
-  unsigned char* stages = base + tf_slab_bytes();
+  double* stg = reinterpret_cast<double*>(base);                                  // drain staging
+  double* Ub = reinterpret_cast<double*>(base + kTfStgBytes);                      // [2][BK][BMP] fp64
+  unsigned char* stages = base + kTfStgBytes + tf_slab_bytes();
   const int BNl = PAIR ? g.BN / 2 : g.BN;  // rows of the T tile held by this CTA
   constexpr int JM = JMT;                    // j' per k-tile (compile-time: loops unrolled)
   const int KTJ = (v.Jp + JM - 1) / JM;       // k-tiles per i_q0 block
@@ -470,10 +489,15 @@ __global__ void __launch_bounds__(kTfThreads, 1)
 #endif
     }
   } else if (warp >= kTfAWarps) {
-    // ======================= TMEM drain warps (4..7) =======================
+    // ======================= TMEM drain warps (8..11) =======================
+    // per chain: tcgen05.ld 16 TMEM columns at a time -> FP64 -> a shared staging block laid out
+    // like the piece ([16 rows][128 fused columns], 16 KB contiguous) -> one bulk copy (first chain of
+    // a segment) or bulk f64 add (later chains) by one thread. r02: the former read-modify-write
+    // through L2 made the drain the bottleneck at 128-product chains.
     const int quad = warp & 3;               // TMEM lane quadrant of this warp
     const int row = quad * 32 + lane;        // fused column c0 + row <-> TMEM lane
-    unsigned gc = 0;
+    const bool issuer = (warp == kTfAWarps && lane == 0);
+    unsigned gc = 0, rnd = 0;  // chains drained, staging rounds (buffer rnd & 1)
     for (int64_t u = u0; u < u1;) {
       const int t = (int)(u / g.KT);
       const int kt0 = (int)(u % g.KT);
@@ -483,31 +507,31 @@ __global__ void __launch_bounds__(kTfThreads, 1)
       const int tm1 = PAIR ? 2 * (t % g.nMt) + crk : t % g.nMt;  // this CTA's 128-column tile
       const bool wr = tm1 < nMt1;  // (PAIR: the second half of an odd last super tile is dead)
       const TileInfo ti = tinfo[(t / g.nMt) * nMt1 + (wr ? tm1 : 0)];
-      double* P = parts + ((int64_t)ti.piece_base + (b - ti.first_cta)) * (int64_t)(BN * kBM) + row;
+      double* P = parts + ((int64_t)ti.piece_base + (b - ti.first_cta)) * (int64_t)(BN * kBM);
       const int nch = (kt1 - kt0 + g.chunk - 1) / g.chunk;
       for (int ch = 0; ch < nch; ++ch, ++gc) {
         mbar_wait_safe(&acc_full[gc & 1], (gc >> 1) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16) + (gc & 1) * kTfMaxN;
-        // BN is a multiple of 16; 32 columns per round keep 32 independent loads in flight
         int bn_drain = wr ? BN : 0;
 #ifdef JKCALS_DEV_PROBES  // timing probe builds only: drain skipped (wrong results)
         if (g.probe == 4 || g.probe == 6) bn_drain = 0;
 #endif
-        for (int col = 0; col < bn_drain; col += 32) {
-          const bool two = col + 16 < BN;
-          double* Pc = P + (int64_t)col * kBM;
-          // the running FP64 piece values are requested first: their L2 round trip overlaps the
-          // TMEM loads (the volatile tcgen05.ld would otherwise order them after it)
-          double old[32];
-#pragma unroll
-          for (int q = 0; q < 32; ++q) old[q] = (ch != 0 && (q < 16 || two)) ? __ldcg(Pc + (int64_t)q * kBM) : 0.0;
-          float vals[32];
+        // the previous chain's adds into this piece must have landed before this chain's are issued
+        if (issuer) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+        for (int col = 0; col < bn_drain; col += 16, ++rnd) {
+          double* sb = stg + (rnd & 1) * 2048;
+          if (rnd >= 2) {  // staging buffer rnd & 1 was read by the bulk op of round rnd - 2
+            if (issuer) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+            drain_bar();
+          }
+          float vals[16];
           tmem_ld_32x32b<16>(lane_base + (uint32_t)col, vals);
-          if (two) tmem_ld_32x32b<16>(lane_base + (uint32_t)col + 16, vals + 16);
 #pragma unroll
-          for (int q = 0; q < 32; ++q)
-            if (q < 16 || two) Pc[(int64_t)q * kBM] = old[q] + (double)vals[q];
+          for (int q = 0; q < 16; ++q) sb[q * 128 + row] = (double)vals[q];
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic -> bulk copy
+          drain_bar();
+          if (issuer) bulk_store_f64(P + (int64_t)col * kBM, sb, 16u * 128u * 8u, ch != 0);
         }
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         __syncwarp();
@@ -517,6 +541,7 @@ __global__ void __launch_bounds__(kTfThreads, 1)
         }
       }
     }
+    if (issuer) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");  // pieces complete
   } else {
     // ======================= A producers (warps 0-7) =======================
     const int row = tid & (kBM - 1);  // fused column c0 + row of the A tile
