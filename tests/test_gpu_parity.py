@@ -377,6 +377,17 @@ def test_fp32_fluorescence_shaped_full_config():
     check32(h, res, ps)
 
 
+def test_fp32_path_is_deterministic():
+    # the FP32 drain adds each accumulation chain into the FP64 piece with bulk f64 adds; chains of
+    # one piece are issued only after the previous chain's group completed, so two runs agree bitwise
+    w = make_workload("syn50_r5")
+    a = run_gpu32(w, 10)
+    b = run_gpu32(w, 10)
+    for p in (0, 7, 49):
+        for x, y in zip(a.factors(p)[0], b.factors(p)[0]):
+            assert np.array_equal(x, y), p
+
+
 def test_fp32_pair_odd_tiles_and_one_cta_variant():
     # the CTA-pair (cta_group::2) FP32 kernel with an odd number of 128-column tiles (C = 60 x 6 =
     # 360: 3 tiles, the last super tile's second half dead) and a ragged I_n = 44, against the oracle;
